@@ -1,0 +1,463 @@
+"""bench.py -- effective HBM GB/s of the TRIOT hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the whole hot path over the BASELINE workloads that are bandwidth
+measurements: C2 embed (f32, (384)^3 -> (512)^3), C3 expected value (f64, (16)^6),
+C4 product (f64, A (32,48,24,40,36) x B (40,32,32,32,32) over (32,32,24,32,32)) and
+C5 embed (f32, (3)^14 -> (4)^14), in that order on one stream.  C1 (75 KB, launch-bound) is
+reported separately as latency.  value = algorithmic bytes (read + written)
+of the K timed steps / device time; inputs are resident in HBM before the timed region; the
+step moves 2.6 GB, ≫ the 126 MB L2, so each op's inputs were evicted by its predecessor
+(no extra flush).  Device time = CUDA events on the launching stream, max over ranks.
+
+N > 1 (torchrun): every rank runs the full step on its own GPU (independent problem
+instances, weak scaling, no collective on the data path); value = all ranks' bytes / max time.
+
+--impl reference: the CPU oracle (oracle/, plain C, 1 thread) on a bounded slab of the same
+workload per step (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from triot_inputs import CONFIGS, make_inputs  # noqa: E402
+
+METRIC = "effective HBM GB/s and % of B200 peak per op (embed/binary/expected value)"
+UNIT = "GB/s"
+NOMINAL_HBM_GBS = 8000.0
+WORKLOAD = "C2+C3+C4+C5"
+STEP_OPS = ("C2", "C3", "C4", "C5")
+
+
+def algorithmic_bytes(name: str) -> int:
+    """Bytes read + written per op: embed reads the src elements inside dst
+    and writes all of dst; binary reads a and b over iter and writes c; EV reads p and writes
+    d doubles."""
+    c = CONFIGS[name]
+    esz = 4 if c.dtype == "f32" else 8
+    sh = c.shapes
+    if c.op == "embed":
+        rd = math.prod(min(a, b) for a, b in zip(sh["src"], sh["dst"])) * esz
+        wr = math.prod(sh["dst"]) * esz
+    elif c.op == "ev":
+        rd, wr = math.prod(sh["p"]) * esz, len(sh["p"]) * 8
+    else:
+        rd, wr = 2 * math.prod(sh["iter"]) * esz, math.prod(sh["iter"]) * esz
+    return rd + wr
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi SM clocks + throttle reasons, sampled every 50 ms while running."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append((time.time(), parts))
+
+    def mark(self):
+        self.marks.append(time.time())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        lo, hi = (self.marks[0], self.marks[-1]) if len(self.marks) >= 2 else (0, 1e30)
+        inwin = [p for t, p in self.samples if lo - 0.06 <= t <= hi + 0.06]
+        use = inwin if inwin else [p for _, p in self.samples]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[1]) for p in use if num(p[1]) is not None]
+        mx = [num(p[2]) for p in use if num(p[2]) is not None]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for p in use:
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(use),
+                "window": "timed region" if inwin else "whole run"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1608_00099_b200 as T
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- inputs resident in HBM (init excluded from timing)
+    host = {n: make_inputs(n) for n in ("C1",) + STEP_OPS}
+    g = {}
+    g["src2"] = torch.from_numpy(host["C2"]["src"]).to(dev)
+    g["dst2"] = torch.empty(host["C2"]["dst_shape"], dtype=torch.float32, device=dev)
+    g["p3"] = torch.from_numpy(host["C3"]["p"]).to(dev)
+    g["m3"] = torch.empty(6, dtype=torch.float64, device=dev)
+    g["a4"] = torch.from_numpy(host["C4"]["a"]).to(dev)
+    g["b4"] = torch.from_numpy(host["C4"]["b"]).to(dev)
+    g["c4"] = torch.empty(host["C4"]["iter_shape"], dtype=torch.float64, device=dev)
+    g["src5"] = torch.from_numpy(host["C5"]["src"]).to(dev)
+    g["dst5"] = torch.empty(host["C5"]["dst_shape"], dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        T.embed(g["dst2"], g["src2"])
+        if evs is not None:
+            evs[0].record(stream)
+        T.expected_value(g["p3"], out=g["m3"])
+        if evs is not None:
+            evs[1].record(stream)
+        T.apply_binary(g["a4"], g["b4"], "mul", out=g["c4"])
+        if evs is not None:
+            evs[2].record(stream)
+        T.embed(g["dst5"], g["src5"])
+        if evs is not None:
+            evs[3].record(stream)
+
+    sampler = ClockSampler(dev.index if dev.index is not None else 0)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: K steps, events between ops, barrier + sync on both sides
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    e_start = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.mark()
+    e_start.record(stream)
+    for k in range(K):
+        step(evs[k])
+    torch.cuda.synchronize(dev)
+    sampler.mark()
+    if world > 1:
+        dist.barrier()
+    total_ms = e_start.elapsed_time(evs[-1][3])
+    per_op_ms = {n: 0.0 for n in STEP_OPS}
+    for k in range(K):
+        prev = e_start if k == 0 else evs[k - 1][3]
+        marks = [prev] + evs[k]
+        for i, n in enumerate(STEP_OPS):
+            per_op_ms[n] += marks[i].elapsed_time(marks[i + 1])
+    per_op_ms = {n: v / K for n, v in per_op_ms.items()}
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---- C1: latency-bound; us per call over back-to-back launches
+    c1src = torch.from_numpy(host["C1"]["src"]).to(dev)
+    c1dst = torch.empty(host["C1"]["dst_shape"], dtype=torch.float64, device=dev)
+    for _ in range(10):
+        T.embed(c1dst, c1src)
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    n_c1 = 200
+    for _ in range(n_c1):
+        T.embed(c1dst, c1src)
+    eb.record(stream)
+    torch.cuda.synchronize(dev)
+    c1_us = ea.elapsed_time(eb) * 1000.0 / n_c1
+
+    # ---- e2e: same step through the public API with pinned HOST buffers; every step copies
+    # its inputs H2D and reads its results back D2H inside the timed region
+    e2e = run_e2e(args, host, dev, stream, T, world)
+    sampler.stop()
+
+    peak, peak_kind = measured_peak()
+    step_bytes = sum(algorithmic_bytes(n) for n in STEP_OPS)
+    value = world * K * step_bytes / (total_ms * 1e-3) / 1e9
+    per_op = []
+    for n in STEP_OPS:
+        b = algorithmic_bytes(n)
+        gbs = b / (per_op_ms[n] * 1e-3) / 1e9
+        per_op.append({"config": n, "op": {"C2": "embed", "C3": "expected_value",
+                                          "C4": "apply_binary", "C5": "embed"}[n],
+                       "bytes": b, "us": round(per_op_ms[n] * 1000, 2), "gbs": round(gbs, 1),
+                       "pct_of_8000": round(100 * gbs / NOMINAL_HBM_GBS, 1),
+                       "pct_of_measured": round(100 * gbs / peak, 1)})
+    dom = max(per_op, key=lambda r: r["us"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom["config"])
+    except Exception:
+        traffic = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(budget_s=args.cpu_budget)
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(total_ms / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32+f64 (embed: raw 32-bit words; binary f64; EV f64 accumulate)",
+        "data": "synthetic (numpy PCG64 seeds 1..5, BASELINE.json configs)",
+        "config": {"workload": WORKLOAD, "bytes_per_step": step_bytes,
+                   "ops": "C2 embed f32 (384)^3->(512)^3; C3 EV f64 (16)^6; C4 mul f64 "
+                          "(32,48,24,40,36)x(40,32,32,32,32)->(32,32,24,32,32); C5 embed f32 "
+                          "(3)^14->(4)^14",
+                   "l2": "no flush: 2.6 GB per step >> 126 MB L2, each op's inputs evicted "
+                         "by its predecessor",
+                   "parallelism": f"replicas x{world} (weak; no data-path collective)"},
+        "per_op": per_op,
+        "c1_latency_us": round(c1_us, 2),
+        "roofline": {"bound": "hbm", "kernel": f"{dom['op']} ({dom['config']})",
+                     "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": round(dom["gbs"] / peak, 3), "peak_kind": peak_kind,
+                     "traffic": traffic},
+        "clocks": sampler.summary(),
+        "e2e": e2e,
+        "gpu_launches": 4 * K,
+        "cpu_baseline": cpu,
+    }
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_e2e(args, host, dev, stream, T, world):
+    import torch
+    pin = {
+        "src2": torch.from_numpy(host["C2"]["src"]).pin_memory(),
+        "p3": torch.from_numpy(host["C3"]["p"]).pin_memory(),
+        "a4": torch.from_numpy(host["C4"]["a"]).pin_memory(),
+        "b4": torch.from_numpy(host["C4"]["b"]).pin_memory(),
+        "src5": torch.from_numpy(host["C5"]["src"]).pin_memory(),
+    }
+    outs = {
+        "dst2": torch.empty(host["C2"]["dst_shape"], dtype=torch.float32).pin_memory(),
+        "m3": torch.empty(6, dtype=torch.float64).pin_memory(),
+        "c4": torch.empty(host["C4"]["iter_shape"], dtype=torch.float64).pin_memory(),
+        "dst5": torch.empty(host["C5"]["dst_shape"], dtype=torch.float32).pin_memory(),
+    }
+    h2d = sum(t.numel() * t.element_size() for t in pin.values())
+    d2h = sum(t.numel() * t.element_size() for t in outs.values())
+
+    def e2e_step():
+        src2 = pin["src2"].to(dev, non_blocking=True)
+        dst2 = torch.empty(host["C2"]["dst_shape"], dtype=torch.float32, device=dev)
+        T.embed(dst2, src2)
+        outs["dst2"].copy_(dst2, non_blocking=True)
+        m3 = T.expected_value(pin["p3"].to(dev, non_blocking=True))
+        outs["m3"].copy_(m3, non_blocking=True)
+        c4 = T.apply_binary(pin["a4"].to(dev, non_blocking=True),
+                            pin["b4"].to(dev, non_blocking=True), "mul")
+        outs["c4"].copy_(c4, non_blocking=True)
+        src5 = pin["src5"].to(dev, non_blocking=True)
+        dst5 = torch.empty(host["C5"]["dst_shape"], dtype=torch.float32, device=dev)
+        T.embed(dst5, src5)
+        outs["dst5"].copy_(dst5, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    k = max(1, min(args.steps, args.e2e_steps))
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(k):
+        e2e_step()
+    eb.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = ea.elapsed_time(eb) / k
+    step_bytes = sum(algorithmic_bytes(n) for n in STEP_OPS)
+    return {"value": round(world * step_bytes / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": k,
+            "ms_per_step": round(ms, 3),
+            "note": "public API (paper_1608_00099_b200.embed/apply_binary/expected_value) from "
+                    "pinned host buffers; H2D of inputs and D2H of every result inside the "
+                    "timed region"}
+
+
+# ----------------------------------------------------------------------------- oracle arms
+
+def _slab(name: str, frac: float):
+    """A leading slab (fraction of axis 0) of config `name`: the bounded CPU sample."""
+    inp = make_inputs(name)
+    if name in ("C1", "C2", "C5"):
+        dsh = inp["dst_shape"]
+        m = max(1, int(math.ceil(frac * dsh[0])))
+        src = np.ascontiguousarray(inp["src"][:m])
+        dst_shape = (m,) + tuple(dsh[1:])
+        rd = math.prod(min(a, b) for a, b in zip(src.shape, dst_shape)) * src.itemsize
+        wr = math.prod(dst_shape) * src.itemsize
+        return ("embed", (src, dst_shape), rd + wr)
+    if name == "C3":
+        p = inp["p"]
+        m = max(1, int(math.ceil(frac * p.shape[0])))
+        ps = np.ascontiguousarray(p[:m])
+        return ("ev", (ps,), ps.nbytes + ps.ndim * 8)
+    ish = inp["iter_shape"]
+    m = max(1, int(math.ceil(frac * ish[0])))
+    a = np.ascontiguousarray(inp["a"][:m])
+    b = np.ascontiguousarray(inp["b"][:m])
+    ish = (m,) + tuple(ish[1:])
+    return ("binary", (a, b, ish), 3 * math.prod(ish) * 8)
+
+
+def _run_slab(kind, args_):
+    from oracle import oracle as O
+    if kind == "embed":
+        src, dsh = args_
+        dst = np.empty(dsh, dtype=src.dtype)
+        t = time.perf_counter()
+        O.embed(dst, src)
+        return time.perf_counter() - t
+    if kind == "ev":
+        t = time.perf_counter()
+        O.expected_value(args_[0])
+        return time.perf_counter() - t
+    a, b, ish = args_
+    t = time.perf_counter()
+    O.apply_binary(a, b, "mul", iter_shape=ish)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(budget_s: float = 20.0, frac: float | None = None):
+    """The oracle as it stands, 1 thread, on a slab of each op sized to ~budget_s seconds."""
+    if frac is None:
+        probe = [_slab(n, 1.0 / 64) for n in STEP_OPS]
+        t = sum(_run_slab(k, a) for k, a, _ in probe)
+        full_est = t * 64
+        frac = min(1.0, budget_s / max(full_est, 1e-9))
+    slabs = [_slab(n, frac) for n in STEP_OPS]
+    secs = sum(_run_slab(k, a) for k, a, _ in slabs)
+    nbytes = sum(b for _, _, b in slabs)
+    return {"value": round(nbytes / secs / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"leading {frac:.3f} of axis 0 of each of C2,C3,C4,C5 (one slab per op), "
+                      f"{nbytes} algorithmic bytes in {secs:.2f} s, single thread, "
+                      f"host {os.cpu_count()} cores",
+            "seconds": round(secs, 3)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    budget = args.ref_budget
+    probe = [_slab(n, 1.0 / 64) for n in STEP_OPS]
+    full_est = sum(_run_slab(k, a) for k, a, _ in probe) * 64
+    frac = min(1.0, budget / max(1, args.steps + args.warmup) / max(full_est, 1e-9))
+    slabs = [_slab(n, frac) for n in STEP_OPS]
+    step_bytes = sum(b for _, _, b in slabs)
+    for _ in range(args.warmup):
+        for k, a, _ in slabs:
+            _run_slab(k, a)
+    total = 0.0
+    for _ in range(args.steps):
+        total += sum(_run_slab(k, a) for k, a, _ in slabs)
+    value = args.steps * step_bytes / total / 1e9
+    sample = (f"leading {frac:.4f} of axis 0 of each of C2,C3,C4,C5 per step "
+              f"({step_bytes} algorithmic bytes), single thread")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "bytes_per_step": step_bytes,
+                   "parallelism": "CPU oracle, rank 0 only"},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=120.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        args.gpus = world
+    if world > 1 and "RANK" not in os.environ:
+        sys.exit("for --gpus > 1 launch with torch.distributed.run (one process per GPU)")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,191 @@
+/*
+ * triot.h -- C-ABI of the B200 (sm_100a) TRIOT hot path.
+ *
+ * TRIOT = "template-recursive iteration over tensors" (Heyl & Serang, arXiv 1608.00099; the
+ * paper text is cited as P:<line>).  The hot path is tuple-indexed iteration over a counter
+ * shape: for every index tuple t of the counter, each tensor's flat offset is computed by
+ * Horner's rule over that tensor's OWN shape (Alg 2, applied per tensor at
+ * P:217), then an operation that may read t is applied (Alg 10).  This library
+ * exports the three instances of that path the build targets:
+ *
+ *   triot_embed            zero-padded embedding (or crop) of one tensor into another
+ *                          (the Benchmark-1 body "xV = yV")
+ *   triot_apply_binary     c[t] = a[t] OP b[t] over tensors of different shapes
+ *                          (Alg 9 apply_tensors; PMF products P:613)
+ *   triot_expected_value   m_k = sum_t t_k * p[t], the index-weighted reduction
+ *                          (Alg 11; "expected value computation")
+ *
+ * Conventions shared by every entry point:
+ *   - Layout: every tensor is a dense, row-major ("as used in the C programming language",
+ *     P:50) contiguous buffer plus a host array `const int64_t shape[d]`.  One d per call.
+ *     Shapes are read during the call and not retained.
+ *   - Dimension: 1 <= d <= triot_max_dimension() (= 16).  The paper fixes a compile-time
+ *     maximum (MAX_TENSOR_DIMENSION) and dispatches a runtime d onto compile-time
+ *     instances (Alg 7); here the instances are sm_100a kernels for D = 1..16.
+ *   - Ownership: every data pointer (dst, src, a, b, c, p, means, workspace) is a DEVICE
+ *     pointer owned by the caller.  The library never allocates or frees device memory.
+ *   - Extents may be 0 (empty tensors).  Elements are float32 (TRIOT_F32) or float64
+ *     (TRIOT_F64); every tensor of one call has the same dtype.  Data pointers must be aligned
+ *     to the element size; wider (up to 32-byte) accesses are chosen at run time.
+ *   - Checking: one up-front check over shapes, never per element.  Validation errors
+ *     return synchronously before anything is enqueued; nothing is written.
+ *   - Asynchrony: work is enqueued on `cuda_stream` (a cudaStream_t passed as void*; NULL =
+ *     the legacy default stream) and the call returns.  Device faults surface at the caller's
+ *     next synchronisation.  Launch failures return TRIOT_ERR_CUDA.
+ *   - Errors: return codes only (never exceptions across the ABI).  triot_last_error()
+ *     returns a thread-local message naming the tensor and axis (the vocabulary of the
+ *     paper's check_tensor_pack_bounds).
+ *   - Aliasing: the written tensor must not overlap any input (the paper relies on
+ *     __restrict), except exact in-place binary ops (see triot_apply_binary).
+ *   - Thread safety: stateless apart from cached per-device attributes; callable from
+ *     several host threads on different streams.
+ *
+ * This header does not include any CUDA header.
+ */
+#ifndef TRIOT_H_
+#define TRIOT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TRIOT_API __attribute__((visibility("default")))
+#else
+#define TRIOT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { TRIOT_F32 = 0, TRIOT_F64 = 1 } triot_dtype;
+
+typedef enum { TRIOT_ADD = 0, TRIOT_SUB = 1, TRIOT_MUL = 2, TRIOT_DIV = 3 } triot_binop;
+
+enum {
+  TRIOT_EMBED_FULL = 0u,        /* write every element of dst (zeros outside src)            */
+  TRIOT_EMBED_REGION_ONLY = 1u  /* write only t < min(src_shape, dst_shape)                  */
+};
+
+typedef enum {
+  TRIOT_OK = 0,
+  TRIOT_ERR_NULL_POINTER = 1,          /* non-empty tensor with NULL data, or NULL shape/out   */
+  TRIOT_ERR_UNSUPPORTED_DIMENSION = 2, /* d < 1 || d > triot_max_dimension()                   */
+  TRIOT_ERR_BAD_SHAPE = 3,             /* negative extent, or a tensor of >= 2^62 bytes        */
+  TRIOT_ERR_AXIS_OUT_OF_BOUNDS = 4,    /* iteration shape exceeds an operand on some axis      */
+  TRIOT_ERR_BAD_DTYPE_OR_OP = 5,       /* unknown dtype, op or flag bits                       */
+  TRIOT_ERR_MISALIGNED = 6,            /* data pointer not aligned to its element size         */
+  TRIOT_ERR_ALIASING = 7,              /* output overlaps an input (other than exact in-place) */
+  TRIOT_ERR_WORKSPACE = 8,             /* workspace NULL or smaller than the queried size      */
+  TRIOT_ERR_CUDA = 9                   /* a CUDA call failed; detail in triot_last_error()     */
+} triot_status;
+
+/* 16: the largest d with a compiled instance (the paper's MAX_TENSOR_DIMENSION). */
+TRIOT_API int triot_max_dimension(void);
+
+/* Static string for a status code ("TRIOT_OK", "TRIOT_ERR_ALIASING", ...). Never NULL. */
+TRIOT_API const char* triot_status_string(int status);
+
+/* Thread-local detail of the last non-OK return on this thread (e.g. "AxisOutOfBounds: tensor
+ * 'a' axis 2: iteration extent 7 > tensor extent 5").  Empty string after success. */
+TRIOT_API const char* triot_last_error(void);
+
+/*
+ * triot_embed -- zero-padded embedding ("copying data from one tensor to another larger,
+ * zero padded tensor"; "zero padding a tensor to perform convolution via the
+ * multidimensional fast Fourier transform"), i.e. apply_tensors with body "xV = yV"
+ * iterated over dst's shape.
+ *
+ *   flags == TRIOT_EMBED_FULL:        for every t in prod[0, dst_shape[k]):
+ *                                       dst[t] = (t_k < src_shape[k] for all k) ? src[t] : +0.0
+ *   flags == TRIOT_EMBED_REGION_ONLY: for every t in prod[0, min(src_shape[k], dst_shape[k])):
+ *                                       dst[t] = src[t]; other elements of dst are not written.
+ *
+ * src may be larger than dst on any axis (a crop, the paper's Benchmark 1) and
+ * smaller on others (pad).  Elements are moved as raw bits (NaN payloads, -0.0, subnormals
+ * survive); the padding is the all-zero bit pattern (+0.0).
+ *   dst, src:   device pointers, dense row-major, dtype `dtype`; must not overlap.
+ *   dst_shape, src_shape: host arrays of d extents.
+ * Empty dst: no-op.  Empty src with FULL: dst becomes all +0.0.
+ */
+TRIOT_API int triot_embed(void* dst, const int64_t* dst_shape,
+                const void* src, const int64_t* src_shape,
+                int d, int dtype, unsigned flags, void* cuda_stream);
+
+/*
+ * triot_apply_binary -- element-wise op over tensors of different shapes (Alg 9 apply_tensors,
+ * only the destination is written; "the product of two or more probability mass
+ * functions with varying support"):
+ *
+ *   for every t in prod[0, iter_shape[k]):   c[t] = a[t] OP b[t]
+ *
+ * where each of a, b, c is indexed by its OWN shape.  OP is IEEE-754 round-to-nearest
+ * with a single rounding (no contraction, no flush-to-zero).
+ *   iter_shape == NULL: the element-wise minimum of a_shape and b_shape (the paper leaves the
+ *                       iteration shape to the caller, "assumes x has smaller shape").
+ *   c_shape == NULL:    c is dense in iter_shape.  Otherwise c_shape >= iter_shape per axis and
+ *                       the elements of c outside iter_shape are left untouched.
+ * iter_shape must not exceed a_shape, b_shape or c_shape on any axis
+ * (TRIOT_ERR_AXIS_OUT_OF_BOUNDS, naming the tensor and axis).
+ * c must not overlap a or b, except c == a (or c == b) with identical shape and iter_shape equal
+ * to that shape (pure in-place; the aliasing-safe idiom of P:601).
+ */
+TRIOT_API int triot_apply_binary(void* c, const int64_t* c_shape,
+                       const void* a, const int64_t* a_shape,
+                       const void* b, const int64_t* b_shape,
+                       const int64_t* iter_shape, int d, int dtype, int op, void* cuda_stream);
+
+/*
+ * triot_expected_value_workspace_size -- bytes of device workspace triot_expected_value needs for
+ * this shape.  The workspace must be zero-filled ONCE when allocated; every call leaves its
+ * completion ticket at zero again, so no per-call memset is needed.  One workspace per
+ * concurrently running stream.
+ */
+TRIOT_API int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, size_t* bytes);
+
+/*
+ * triot_expected_value -- Alg 11 with a single tensor:
+ *
+ *   means[k] = sum over t in prod[0, shape[j]) of  t_k * p[t],     k = 0..d-1
+ *
+ * accumulated in fp64 for both dtypes (Alg 11's Vector<double> result), with 0-based
+ * tuple coordinates as weights (counter[k]) and NO normalisation by sum(p) (Alg 11 never
+ * divides).  The result is deterministic run to run on one device (fixed grid, ordered final
+ * sum); it matches the correctly rounded sum within 1e-12 relative per component.
+ *   means:     device pointer to d doubles (written by the kernel).
+ *   p:         device pointer, dense row-major, dtype `dtype`.
+ *   workspace: device pointer of >= triot_expected_value_workspace_size bytes, zeroed once.
+ * Empty p (some extent 0): means are all 0.0.
+ */
+TRIOT_API int triot_expected_value(double* means, const void* p, const int64_t* shape, int d, int dtype,
+                         void* workspace, size_t workspace_bytes, void* cuda_stream);
+
+/* ---- diagnostics (host only; no device work, usable without a GPU) ---------------------- */
+
+/*
+ * triot_plan_describe -- writes, as one JSON object into buf (NUL-terminated, truncated to
+ * buf_len), the launch plan the library would use for an op on these shapes: canonical axes
+ * (unit axes dropped, contiguous axes merged), vector width, per-digit extents, the
+ * per-step carry increment, per-tensor strides/carry deltas, and the fast-division magics.
+ *   op: 0 = embed (shapes[0]=dst, shapes[1]=src, flags as triot_embed),
+ *       1 = binary (shapes[0]=c or NULL, shapes[1]=a, shapes[2]=b, iter or NULL; `flags`
+ *           carries the triot_binop),
+ *       2 = expected value (shapes[0]=p).
+ *   ptr_mod32: byte offsets modulo 32 of each tensor's data pointer (alignment model).
+ * Returns a triot_status (validation errors exactly as the real call would report them).
+ */
+TRIOT_API int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape, int d,
+                        int dtype, unsigned flags, const unsigned* ptr_mod32,
+                        char* buf, size_t buf_len);
+
+/* The Granlund-Montgomery round-up magic the kernels use to divide by an invariant extent
+ * (P:143 notes that division is slow; it is done once per thread with a multiply-high):
+ *   q = (umulhi(n, mul) + ((n - umulhi(n, mul)) >> (shift & 0xff))) >> (shift >> 8)
+ * equals n / divisor for every 32-bit n.  divisor must be >= 1. */
+TRIOT_API int triot_fastdiv_magic(uint32_t divisor, uint32_t* mul, uint32_t* shift);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRIOT_H_ */

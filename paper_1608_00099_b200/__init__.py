@@ -1,0 +1,30 @@
+"""paper_1608_00099_b200 -- the TRIOT hot path (arXiv 1608.00099) on B200 (sm_100a).
+
+Public API on torch CUDA tensors (torch is used for device memory and streams only; every
+step runs in libtriot.so's kernels, see include/triot.h):
+
+    embed(dst, src, region_only=False)                  -> dst      (triot_embed)
+    apply_binary(a, b, op="mul", out=None, iter_shape=None) -> out  (triot_apply_binary)
+    expected_value(p)                                   -> (d,) float64 CUDA tensor
+                                                           (triot_expected_value)
+
+The C-ABI entry points themselves are re-exported with their C names (triot_embed, ...).
+There is no CPU fallback: importing raises if libtriot.so is missing, and the tensor API
+raises for non-CUDA tensors.
+"""
+from __future__ import annotations
+
+from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED_FULL,
+                   TRIOT_EMBED_REGION_ONLY, TRIOT_F32, TRIOT_F64, TRIOT_MUL, TRIOT_SUB,
+                   TriotError, check, lib, triot_apply_binary, triot_embed,
+                   triot_expected_value, triot_expected_value_workspace_size,
+                   triot_fastdiv_magic, triot_last_error, triot_max_dimension,
+                   triot_plan_describe, triot_status_string, LIB_PATH)
+from .api import apply_binary, embed, expected_value, OPS
+
+__all__ = [
+    "embed", "apply_binary", "expected_value", "OPS", "TriotError",
+    "triot_embed", "triot_apply_binary", "triot_expected_value",
+    "triot_expected_value_workspace_size", "triot_max_dimension", "triot_status_string",
+    "triot_last_error", "triot_plan_describe", "triot_fastdiv_magic", "LIB_PATH",
+]

@@ -1,0 +1,144 @@
+"""ctypes binding of libtriot.so -- argument marshalling only.
+
+The functions here have the C-ABI's names and arguments (include/triot.h): raw device
+pointers as ints, shapes as sequences of ints, the CUDA stream as an int handle.  Every step
+of the hot path runs in the library's sm_100a kernels; there is no Python or CPU fallback:
+if the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtriot.so")
+
+TRIOT_F32, TRIOT_F64 = 0, 1
+TRIOT_ADD, TRIOT_SUB, TRIOT_MUL, TRIOT_DIV = 0, 1, 2, 3
+TRIOT_EMBED_FULL, TRIOT_EMBED_REGION_ONLY = 0, 1
+OP_EMBED, OP_BINARY, OP_EV = 0, 1, 2
+
+STATUS = {
+    0: "TRIOT_OK", 1: "TRIOT_ERR_NULL_POINTER", 2: "TRIOT_ERR_UNSUPPORTED_DIMENSION",
+    3: "TRIOT_ERR_BAD_SHAPE", 4: "TRIOT_ERR_AXIS_OUT_OF_BOUNDS", 5: "TRIOT_ERR_BAD_DTYPE_OR_OP",
+    6: "TRIOT_ERR_MISALIGNED", 7: "TRIOT_ERR_ALIASING", 8: "TRIOT_ERR_WORKSPACE",
+    9: "TRIOT_ERR_CUDA",
+}
+EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "triot_embed",
+           "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
+           "triot_plan_describe", "triot_fastdiv_magic")
+
+
+class TriotError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_1608_00099_b200.build` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_vp = ctypes.c_void_p
+
+_lib.triot_max_dimension.restype = ctypes.c_int
+_lib.triot_max_dimension.argtypes = []
+_lib.triot_status_string.restype = ctypes.c_char_p
+_lib.triot_status_string.argtypes = [ctypes.c_int]
+_lib.triot_last_error.restype = ctypes.c_char_p
+_lib.triot_last_error.argtypes = []
+_lib.triot_embed.restype = ctypes.c_int
+_lib.triot_embed.argtypes = [_vp, _i64p, _vp, _i64p, ctypes.c_int, ctypes.c_int, ctypes.c_uint,
+                             _vp]
+_lib.triot_apply_binary.restype = ctypes.c_int
+_lib.triot_apply_binary.argtypes = [_vp, _i64p, _vp, _i64p, _vp, _i64p, _i64p, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int, _vp]
+_lib.triot_expected_value_workspace_size.restype = ctypes.c_int
+_lib.triot_expected_value_workspace_size.argtypes = [_i64p, ctypes.c_int, ctypes.c_int,
+                                                     ctypes.POINTER(ctypes.c_size_t)]
+_lib.triot_expected_value.restype = ctypes.c_int
+_lib.triot_expected_value.argtypes = [_vp, _vp, _i64p, ctypes.c_int, ctypes.c_int, _vp,
+                                      ctypes.c_size_t, _vp]
+_lib.triot_plan_describe.restype = ctypes.c_int
+_lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
+                                     ctypes.c_char_p, ctypes.c_size_t]
+_lib.triot_fastdiv_magic.restype = ctypes.c_int
+_lib.triot_fastdiv_magic.argtypes = [ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
+                                     ctypes.POINTER(ctypes.c_uint32)]
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _shape(s):
+    if s is None:
+        return None
+    s = [int(x) for x in s]
+    return (ctypes.c_int64 * max(1, len(s)))(*s)
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise TriotError(status, _lib.triot_last_error().decode())
+
+
+# ---- the C-ABI, one Python function per entry point (same names) --------------------------
+
+def triot_max_dimension() -> int:
+    return _lib.triot_max_dimension()
+
+
+def triot_status_string(status: int) -> str:
+    return _lib.triot_status_string(status).decode()
+
+
+def triot_last_error() -> str:
+    return _lib.triot_last_error().decode()
+
+
+def triot_embed(dst: int, dst_shape, src: int, src_shape, d: int, dtype: int, flags: int,
+                stream: int) -> int:
+    return _lib.triot_embed(dst, _shape(dst_shape), src, _shape(src_shape), d, dtype, flags,
+                            stream)
+
+
+def triot_apply_binary(c: int, c_shape, a: int, a_shape, b: int, b_shape, iter_shape, d: int,
+                       dtype: int, op: int, stream: int) -> int:
+    return _lib.triot_apply_binary(c, _shape(c_shape), a, _shape(a_shape), b, _shape(b_shape),
+                                   _shape(iter_shape), d, dtype, op, stream)
+
+
+def triot_expected_value_workspace_size(shape, d: int, dtype: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(_lib.triot_expected_value_workspace_size(_shape(shape), d, dtype, ctypes.byref(out)))
+    return int(out.value)
+
+
+def triot_expected_value(means: int, p: int, shape, d: int, dtype: int, workspace: int,
+                         workspace_bytes: int, stream: int) -> int:
+    return _lib.triot_expected_value(means, p, _shape(shape), d, dtype, workspace,
+                                     workspace_bytes, stream)
+
+
+def triot_plan_describe(op: int, shapes, iter_shape, d: int, dtype: int, flags: int = 0,
+                        ptr_mod32=(0, 0, 0)) -> dict:
+    arrs = [_shape(s) if s is not None else None for s in shapes] + [None] * (3 - len(shapes))
+    ptrs = (_i64p * 3)(*[ctypes.cast(a, _i64p) if a is not None else _i64p() for a in arrs])
+    mods = (ctypes.c_uint * 3)(*ptr_mod32)
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(_lib.triot_plan_describe(op, ptrs, _shape(iter_shape), d, dtype, flags, mods, buf,
+                                   len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def triot_fastdiv_magic(divisor: int) -> tuple[int, int]:
+    m, s = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    check(_lib.triot_fastdiv_magic(divisor, ctypes.byref(m), ctypes.byref(s)))
+    return int(m.value), int(s.value)

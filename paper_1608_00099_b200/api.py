@@ -1,0 +1,104 @@
+"""Tensor-level wrappers: shapes from tensor.shape, pointers from data_ptr(), the stream from
+torch.cuda.current_stream().  Marshalling only -- the computation is the C-ABI call."""
+from __future__ import annotations
+
+import threading
+
+from . import _lib
+
+OPS = {"add": _lib.TRIOT_ADD, "sub": _lib.TRIOT_SUB, "mul": _lib.TRIOT_MUL,
+       "div": _lib.TRIOT_DIV}
+
+_ws_lock = threading.Lock()
+_ws_cache: dict = {}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return _lib.TRIOT_F32
+    if t.dtype == torch.float64:
+        return _lib.TRIOT_F64
+    raise TypeError(f"triot supports float32 and float64 tensors, got {t.dtype}")
+
+
+def _check_tensor(name: str, t, device=None):
+    if not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (dense row-major)")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+
+
+def _stream(device) -> int:
+    return _torch().cuda.current_stream(device).cuda_stream
+
+
+def embed(dst, src, region_only: bool = False):
+    """dst[t] = src[t] where t < src.shape, +0.0 elsewhere (or only the overlap if
+    region_only).  In place on dst; returns dst."""
+    _check_tensor("dst", dst)
+    _check_tensor("src", src, dst.device)
+    if src.dtype != dst.dtype or src.dim() != dst.dim():
+        raise ValueError("dst and src must have the same dtype and dimension")
+    flags = _lib.TRIOT_EMBED_REGION_ONLY if region_only else _lib.TRIOT_EMBED_FULL
+    _lib.check(_lib.triot_embed(dst.data_ptr(), tuple(dst.shape), src.data_ptr(),
+                                tuple(src.shape), dst.dim(), _dtype_code(dst), flags,
+                                _stream(dst.device)))
+    return dst
+
+
+def apply_binary(a, b, op: str = "mul", out=None, iter_shape=None):
+    """out[t] = a[t] OP b[t] for t in iter_shape (default: element-wise min of the shapes).
+    `out` defaults to a new tensor dense in iter_shape."""
+    torch = _torch()
+    _check_tensor("a", a)
+    _check_tensor("b", b, a.device)
+    if a.dtype != b.dtype or a.dim() != b.dim():
+        raise ValueError("a and b must have the same dtype and dimension")
+    if iter_shape is None:
+        iter_shape = tuple(min(x, y) for x, y in zip(a.shape, b.shape))
+    iter_shape = tuple(int(x) for x in iter_shape)
+    if out is None:
+        out = torch.empty(iter_shape, dtype=a.dtype, device=a.device)
+    _check_tensor("out", out, a.device)
+    if out.dtype != a.dtype:
+        raise ValueError("out must have the dtype of a and b")
+    _lib.check(_lib.triot_apply_binary(out.data_ptr(), tuple(out.shape), a.data_ptr(),
+                                       tuple(a.shape), b.data_ptr(), tuple(b.shape), iter_shape,
+                                       a.dim(), _dtype_code(a), OPS[op], _stream(a.device)))
+    return out
+
+
+def workspace(p_shape, dtype_code: int, device):
+    """The cached, once-zeroed expected-value workspace for (device, current stream)."""
+    torch = _torch()
+    need = _lib.triot_expected_value_workspace_size(tuple(p_shape), len(p_shape), dtype_code)
+    key = (device, _stream(device))
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device=device)
+            _ws_cache[key] = ws
+    return ws
+
+
+def expected_value(p, out=None):
+    """means[k] = sum_t t_k * p[t] (fp64), k = 0..d-1.  Returns a (d,) float64 CUDA tensor."""
+    torch = _torch()
+    _check_tensor("p", p)
+    code = _dtype_code(p)
+    d = p.dim()
+    if out is None:
+        out = torch.empty(d, dtype=torch.float64, device=p.device)
+    _check_tensor("out", out, p.device)
+    ws = workspace(tuple(p.shape), code, p.device)
+    _lib.check(_lib.triot_expected_value(out.data_ptr(), p.data_ptr(), tuple(p.shape), d, code,
+                                         ws.data_ptr(), ws.numel(), _stream(p.device)))
+    return out

@@ -1,0 +1,260 @@
+// capi.cu -- the extern "C" entry points of include/triot.h: validate (plan.cpp), pick the
+// compiled instance from the dispatch tables (inst.cu), size the grid from the SM count, and
+// enqueue on the caller's stream.  No device memory is allocated here.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/triot.h"
+#include "desc.h"
+#include "plan.hpp"
+
+// dispatch tables, one per compiled family (inst.cu)
+extern "C" {
+const void* triot_table_0_4_0(int, int, int);
+const void* triot_table_0_8_0(int, int, int);
+const void* triot_table_1_4_0(int, int, int);
+const void* triot_table_1_4_1(int, int, int);
+const void* triot_table_1_4_2(int, int, int);
+const void* triot_table_1_4_3(int, int, int);
+const void* triot_table_1_8_0(int, int, int);
+const void* triot_table_1_8_1(int, int, int);
+const void* triot_table_1_8_2(int, int, int);
+const void* triot_table_1_8_3(int, int, int);
+const void* triot_table_2_4_0(int, int, int);
+const void* triot_table_2_8_0(int, int, int);
+}
+
+namespace triot {
+namespace {
+
+typedef const void* (*TableFn)(int, int, int);
+
+TableFn table_for(const Geom& g) {
+  const bool e8 = g.esz == 8;
+  if (g.op == OP_EMBED) return e8 ? triot_table_0_8_0 : triot_table_0_4_0;
+  if (g.op == OP_EV) return e8 ? triot_table_2_8_0 : triot_table_2_4_0;
+  static const TableFn b4[4] = {triot_table_1_4_0, triot_table_1_4_1, triot_table_1_4_2,
+                                triot_table_1_4_3};
+  static const TableFn b8[4] = {triot_table_1_8_0, triot_table_1_8_1, triot_table_1_8_2,
+                                triot_table_1_8_3};
+  return e8 ? b8[g.binop] : b4[g.binop];
+}
+
+int vindex(const Geom& g) {
+  if (g.V == 32 / g.esz) return 0;
+  if (g.V == 16 / g.esz) return 1;
+  return 2;
+}
+
+std::mutex g_mu;
+int g_sms[64] = {0};
+std::unordered_map<const void*, int> g_occ;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(TRIOT_ERR_CUDA, "CUDA: %s: %s", what, cudaGetErrorString(e));
+}
+
+// grid sizing: enough resident warps to keep >= ~48 KB of loads in flight per SM, each warp a
+// contiguous run of >= kMinSteps steps
+int launch_geometry(const void* fn, const Geom& g, int max_grid, unsigned* grid_out,
+                    uint64_t* q_out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int sms, occ;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 0 || dev >= 64) return set_error(TRIOT_ERR_CUDA, "CUDA: device id %d", dev);
+    if (!g_sms[dev]) {
+      e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    }
+    sms = g_sms[dev];
+    auto it = g_occ.find(fn);
+    if (it == g_occ.end()) {
+      int nb = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, TRIOT_BLOCK, 0);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      if (nb < 1) nb = 1;
+      it = g_occ.emplace(fn, nb).first;
+    }
+    occ = it->second;
+  }
+  const uint64_t wpb = TRIOT_BLOCK / 32;
+  const uint64_t kMinSteps = 4;
+  uint64_t grid = (uint64_t)sms * (uint64_t)occ;
+  uint64_t need = (g.nsteps + kMinSteps * wpb - 1) / (kMinSteps * wpb);
+  if (need < grid) grid = need;
+  if (grid > (uint64_t)max_grid) grid = (uint64_t)max_grid;
+  if (grid < 1) grid = 1;
+  uint64_t q = (g.nsteps + grid * wpb - 1) / (grid * wpb);
+  if (q < 1) q = 1;
+  grid = (g.nsteps + q * wpb - 1) / (q * wpb);
+  if (grid < 1) grid = 1;
+  *grid_out = (unsigned)grid;
+  *q_out = q;
+  return TRIOT_OK;
+}
+
+template <typename IDX>
+int launch_t(const Geom& g, const void* fn, unsigned grid, uint64_t q, cudaStream_t st,
+             void* out, void* ws) {
+  Desc<IDX> d;
+  memset(&d, 0, sizeof(d));
+  fill_desc<IDX>(g, d, q);
+  d.out = out;
+  d.ws = ws;
+  void* args[1] = {&d};
+  cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(TRIOT_BLOCK), args, 0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  return TRIOT_OK;
+}
+
+int launch(const Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
+  const void* fn = table_for(g)(g.D, vindex(g), g.idx64 ? 1 : 0);
+  if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no instance for D=%d V=%d", g.D, g.V);
+  int max_grid = 1 << 30;
+  if (g.op == OP_EV) max_grid = TRIOT_EV_MAX_GRID;
+  unsigned grid;
+  uint64_t q;
+  int st = launch_geometry(fn, g, max_grid, &grid, &q);
+  if (st) return st;
+  if (g.op == OP_EV) {
+    size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 1) * sizeof(double);
+    if (!ws || ws_bytes < need)
+      return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
+                       need);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  return g.idx64 ? launch_t<uint64_t>(g, fn, grid, q, s, out, ws)
+                 : launch_t<uint32_t>(g, fn, grid, q, s, out, ws);
+}
+
+size_t ev_ws_bytes(int d) {
+  return TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * (size_t)(d + 1) * sizeof(double);
+}
+
+}  // namespace
+}  // namespace triot
+
+using namespace triot;
+
+extern "C" {
+
+int triot_max_dimension(void) { return TRIOT_MAXD; }
+
+const char* triot_status_string(int s) {
+  switch (s) {
+    case TRIOT_OK: return "TRIOT_OK";
+    case TRIOT_ERR_NULL_POINTER: return "TRIOT_ERR_NULL_POINTER";
+    case TRIOT_ERR_UNSUPPORTED_DIMENSION: return "TRIOT_ERR_UNSUPPORTED_DIMENSION";
+    case TRIOT_ERR_BAD_SHAPE: return "TRIOT_ERR_BAD_SHAPE";
+    case TRIOT_ERR_AXIS_OUT_OF_BOUNDS: return "TRIOT_ERR_AXIS_OUT_OF_BOUNDS";
+    case TRIOT_ERR_BAD_DTYPE_OR_OP: return "TRIOT_ERR_BAD_DTYPE_OR_OP";
+    case TRIOT_ERR_MISALIGNED: return "TRIOT_ERR_MISALIGNED";
+    case TRIOT_ERR_ALIASING: return "TRIOT_ERR_ALIASING";
+    case TRIOT_ERR_WORKSPACE: return "TRIOT_ERR_WORKSPACE";
+    case TRIOT_ERR_CUDA: return "TRIOT_ERR_CUDA";
+    default: return "TRIOT_ERR_UNKNOWN";
+  }
+}
+
+const char* triot_last_error(void) { return last_error(); }
+
+int triot_embed(void* dst, const int64_t* dst_shape, const void* src, const int64_t* src_shape,
+                int d, int dtype, unsigned flags, void* cuda_stream) {
+  Geom g;
+  int st = plan_embed(g, dst, dst_shape, src, src_shape, d, dtype, flags);
+  if (st || g.empty) return st;
+  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if (!st) clear_error();
+  return st;
+}
+
+int triot_apply_binary(void* c, const int64_t* c_shape, const void* a, const int64_t* a_shape,
+                       const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
+                       int dtype, int op, void* cuda_stream) {
+  Geom g;
+  int st = plan_binary(g, c, c_shape, a, a_shape, b, b_shape, iter_shape, d, dtype, op);
+  if (st || g.empty) return st;
+  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if (!st) clear_error();
+  return st;
+}
+
+int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, size_t* bytes) {
+  if (!bytes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: bytes is NULL");
+  Geom g;
+  // validate the shape exactly like the real call (pointer checks skipped: no data yet)
+  int st = plan_ev(g, (const void*)(uintptr_t)64, shape, d, dtype);
+  if (st) return st;
+  *bytes = ev_ws_bytes(d);
+  return TRIOT_OK;
+}
+
+int triot_expected_value(double* means, const void* p, const int64_t* shape, int d, int dtype,
+                         void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  Geom g;
+  int st = plan_ev(g, p, shape, d, dtype);
+  if (st) return st;
+  if (!means) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: means is NULL");
+  if (((uintptr_t)means) % 8)
+    return set_error(TRIOT_ERR_MISALIGNED, "Misaligned: means is not 8-byte aligned");
+  {
+    uintptr_t m0 = (uintptr_t)means, m1 = m0 + (uintptr_t)d * 8;
+    uintptr_t p0 = (uintptr_t)p, p1 = p0 + (uintptr_t)g.t[0].numel * (uintptr_t)g.esz;
+    if (g.t[0].numel && m0 < p1 && p0 < m1)
+      return set_error(TRIOT_ERR_ALIASING, "Aliasing: means overlaps p");
+  }
+  if (g.empty) {
+    cudaError_t e = cudaMemsetAsync(means, 0, (size_t)d * sizeof(double), (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    clear_error();
+    return TRIOT_OK;
+  }
+  st = launch(g, cuda_stream, means, workspace, workspace_bytes);
+  if (!st) clear_error();
+  return st;
+}
+
+int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape, int d,
+                        int dtype, unsigned flags, const unsigned* ptr_mod32, char* buf,
+                        size_t buf_len) {
+  if (!shapes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: shapes is NULL");
+  // synthetic, non-overlapping device addresses with the requested alignment
+  uintptr_t base[3];
+  for (int x = 0; x < 3; ++x)
+    base[x] = ((uintptr_t)(x + 1) << 44) + (ptr_mod32 ? (uintptr_t)ptr_mod32[x] : 0);
+  Geom g;
+  int st;
+  if (op == OP_EMBED)
+    st = plan_embed(g, (void*)base[0], shapes[0], (const void*)base[1], shapes[1], d, dtype, flags);
+  else if (op == OP_BINARY)
+    st = plan_binary(g, (void*)base[0], shapes[0], (const void*)base[1], shapes[1],
+                     (const void*)base[2], shapes[2], iter_shape, d, dtype, (int)flags);
+  else if (op == OP_EV)
+    st = plan_ev(g, (const void*)base[0], shapes[0], d, dtype);
+  else
+    return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
+  if (st) return st;
+  std::string s = describe(g);
+  if (buf && buf_len) {
+    size_t n = s.size() < buf_len - 1 ? s.size() : buf_len - 1;
+    memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return TRIOT_OK;
+}
+
+int triot_fastdiv_magic(uint32_t divisor, uint32_t* mul, uint32_t* shift) {
+  if (!mul || !shift) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: output is NULL");
+  if (divisor == 0) return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: divisor 0");
+  fastdiv_magic(divisor, mul, shift);
+  return TRIOT_OK;
+}
+
+}  // extern "C"

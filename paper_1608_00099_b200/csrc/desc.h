@@ -1,0 +1,71 @@
+// desc.h -- the launch descriptor: a POD built on the host (plan.cpp) and passed by value as a
+// kernel parameter (< 2 KB, lives in the constant parameter bank, so every field read in the
+// kernels is a constant-bank operand, not a load).
+//
+// Vocabulary:
+//   counter    the iteration shape (dst for embed, iter for binary, p for EV), after
+//              canonicalisation (unit axes dropped, contiguous axes merged).
+//   vector     V consecutive counter elements (32 bytes when geometry and alignment allow).
+//   digits     u[0..D-1]: the mixed-radix coordinates of a vector.  Digits 0..D-2 are counter
+//              axes; digit D-1 (the "vector digit") is either the vector index inside a counter
+//              row (R == 1) or a group of R whole rows when rows are shorter than a vector
+//              (R > 1: the inner-axis collapse for tiny innermost extents).
+//   step       +32 vectors (one warp-wide stride), pre-decoded into mixed-radix digits dlt[].
+//   sig[k]     a tensor's Horner stride of digit k (Alg 2 / P:50 applied to its own shape).
+//   kap[k]     the offset change when digit k carries out: sig[k-1] - ext[k] * sig[k].
+#pragma once
+#include <stdint.h>
+
+#define TRIOT_MAXD 16
+#define TRIOT_MAXT 3
+#define TRIOT_BLOCK 256   // threads per block of every kernel
+
+namespace triot {
+
+enum Op { OP_EMBED = 0, OP_BINARY = 1, OP_EV = 2 };
+
+template <typename IDX>
+struct TensorAcc {
+  IDX sig[TRIOT_MAXD];   // stride (elements) of each vector digit
+  IDX kap[TRIOT_MAXD];   // carry delta of each digit (kap[0] unused)
+  IDX step;              // offset change of a +32-vector step, before carries
+  IDX rho;               // stride of the row inside a collapsed vector (R > 1)
+  IDX tau;               // stride of the innermost counter axis (1 for contiguous rows)
+  uint32_t vec;          // 1: V elements are contiguous and V*esz-aligned -> one wide access
+  uint32_t pad_;
+  const void* ptr;       // device base pointer
+};
+
+template <typename IDX>
+struct Desc {
+  IDX ext[TRIOT_MAXD];   // digit extents
+  IDX dlt[TRIOT_MAXD];   // digits of the +32-vector step
+  IDX bnd[TRIOT_MAXD];   // embed: digit k (k < D-1) is in bounds iff u[k] < bnd[k]
+  uint32_t fdm[TRIOT_MAXD];  // fast-division magic multiplier per digit extent (IDX = u32)
+  uint32_t fds[TRIOT_MAXD];  // fast-division shifts: s1 | s2 << 8
+  IDX nvec;              // number of vectors W
+  IDX nsteps;            // ceil(W / 32)
+  IDX steps_per_warp;    // Q: each warp owns steps [w*Q, (w+1)*Q)
+  int32_t khi, klo;      // innermost / outermost digit with a nonzero step digit
+  // in-vector geometry
+  uint32_t lgL;          // log2(elements per row inside a vector): log2(V) if R == 1
+  uint32_t R;            // rows per vector
+  IDX rowmul, colmul;    // first row / col of a vector = u[D-1] * rowmul / colmul
+  IDX vfull, vany;       // embed: vector digit u fully in bounds iff u < vfull, any iff u < vany
+  IDX srows, scols;      // embed: per-element bounds of a partial vector
+  // expected value: weight slots -> output
+  int32_t collapsed;     // 1 iff R > 1
+  int32_t d_out;         // number of means written (the caller's d)
+  int32_t slot_of_axis[TRIOT_MAXD];  // means[j] = slot >= 0 ? total[slot] : 0
+  int32_t op;            // binary op
+  int32_t pad_;
+  TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p
+  void* out;             // EV: means (device)
+  void* ws;              // EV: workspace (device)
+};
+
+// Workspace layout of the expected value: [ticket u32 | pad to 256 B] [grid x (D+1) doubles].
+#define TRIOT_EV_MAX_GRID 2048
+#define TRIOT_EV_WS_HEADER 256
+
+}  // namespace triot

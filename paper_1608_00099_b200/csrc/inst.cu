@@ -1,0 +1,80 @@
+// inst.cu -- explicit instantiation of one kernel family and its dispatch table.
+//
+// Compiled several times with different macros (build.py), one object per (op, element size,
+// binary op), so the D = 1..16 x V x IDX matrix compiles in parallel -- the GPU analogue of the
+// paper's compile-time note (max dimension 16 compiles in 16 s).  The table replaces
+// LinearTemplateSearch (Alg 7): runtime (D, V, index width) -> kernel in O(1).
+//
+//   TRIOT_INST_OP   0 = embed, 1 = binary, 2 = expected value
+//   TRIOT_INST_ESZ  4 or 8
+//   TRIOT_INST_BOP  binary op 0..3 (binary only)
+#include "kernels.cuh"
+
+#ifndef TRIOT_INST_OP
+#error "define TRIOT_INST_OP"
+#endif
+#ifndef TRIOT_INST_ESZ
+#error "define TRIOT_INST_ESZ"
+#endif
+#ifndef TRIOT_INST_BOP
+#define TRIOT_INST_BOP 0
+#endif
+
+#define TRIOT_CAT2(a, b) a##b
+#define TRIOT_CAT(a, b) TRIOT_CAT2(a, b)
+#define TRIOT_NAME \
+  TRIOT_CAT(TRIOT_CAT(TRIOT_CAT(triot_table_, TRIOT_INST_OP), TRIOT_CAT(_, TRIOT_INST_ESZ)), \
+            TRIOT_CAT(_, TRIOT_INST_BOP))
+
+namespace triot {
+namespace {
+
+constexpr int ESZ = TRIOT_INST_ESZ;
+
+// loads in flight per lane per batch (bytes in flight, SURVEY §8(d) Little's law)
+constexpr int KEMBED = 4;
+constexpr int KBIN = 2;
+constexpr int KEV = 4;
+
+template <int D, int V, typename IDX>
+const void* kptr() {
+#if TRIOT_INST_OP == 0
+  return (const void*)&embed_kernel<D, ESZ, V, IDX, KEMBED>;
+#elif TRIOT_INST_OP == 1
+  return (const void*)&binary_kernel<D, ESZ, V, IDX, KBIN, TRIOT_INST_BOP>;
+#else
+  return (const void*)&ev_kernel<D, ESZ, V, IDX, KEV>;
+#endif
+}
+
+// table index: ((D-1) * 3 + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element
+template <int D>
+struct Fill {
+  static void run(const void** t) {
+    t[((D - 1) * 3 + 0) * 2 + 0] = kptr<D, 32 / ESZ, uint32_t>();
+    t[((D - 1) * 3 + 0) * 2 + 1] = kptr<D, 32 / ESZ, uint64_t>();
+    t[((D - 1) * 3 + 1) * 2 + 0] = kptr<D, 16 / ESZ, uint32_t>();
+    t[((D - 1) * 3 + 1) * 2 + 1] = kptr<D, 16 / ESZ, uint64_t>();
+    t[((D - 1) * 3 + 2) * 2 + 0] = kptr<D, 1, uint32_t>();
+    t[((D - 1) * 3 + 2) * 2 + 1] = kptr<D, 1, uint64_t>();
+    Fill<D - 1>::run(t);
+  }
+};
+template <>
+struct Fill<0> {
+  static void run(const void**) {}
+};
+
+struct Table {
+  const void* t[TRIOT_MAXD * 3 * 2];
+  Table() { Fill<TRIOT_MAXD>::run(t); }
+};
+
+}  // namespace
+}  // namespace triot
+
+extern "C" const void* TRIOT_NAME(int D, int vi, int idx64) {
+  static const triot::Table tab;  // thread-safe one-time init
+  if (D < 1 || D > TRIOT_MAXD || vi < 0 || vi > 2) return nullptr;
+  return tab.t[((D - 1) * 3 + vi) * 2 + (idx64 ? 1 : 0)];
+}

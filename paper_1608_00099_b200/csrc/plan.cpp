@@ -1,0 +1,582 @@
+// plan.cpp -- validation, canonicalisation and descriptor geometry (host only).
+// See plan.hpp for the mapping to the paper's Alg 6-9; DESIGN.md §Plan for the rules.
+#include "plan.hpp"
+
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/triot.h"
+
+namespace triot {
+
+// ------------------------------------------------------------------------------ errors
+
+static thread_local char g_err[512] = {0};
+
+int set_error(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+void clear_error() { g_err[0] = 0; }
+const char* last_error() { return g_err; }
+
+// ------------------------------------------------------------------------------ fast division
+
+void fastdiv_magic(uint32_t div, uint32_t* mul, uint32_t* shift) {
+  // l = ceil(log2 div); m = floor(2^32 (2^l - div) / div) + 1; s1 = min(l,1); s2 = max(l-1,0)
+  uint32_t l = 0;
+  while (l < 32 && (1ull << l) < div) ++l;
+  uint64_t m = ((((1ull << l) - div) << 32) / div) + 1;
+  uint32_t s1 = l < 1 ? l : 1;
+  uint32_t s2 = l > 0 ? l - 1 : 0;
+  *mul = (uint32_t)m;
+  *shift = s1 | (s2 << 8);
+}
+
+// ------------------------------------------------------------------------------ helpers
+
+static const uint64_t kMaxBytes = 1ull << 62;
+
+// Checks extents of one shape; sets numel.  P:48 assumes s_i >= 1; zero extents are allowed
+// (reading R15) and negative ones rejected.
+static int check_shape(const char* name, const int64_t* s, int d, int esz, uint64_t* numel) {
+  if (!s) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: shape of '%s' is NULL", name);
+  uint64_t n = 1;
+  bool zero = false;
+  for (int k = 0; k < d; ++k) {
+    if (s[k] < 0)
+      return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: tensor '%s' axis %d has extent %lld", name,
+                       k, (long long)s[k]);
+    if (s[k] == 0) zero = true;
+  }
+  if (zero) {
+    *numel = 0;
+    return TRIOT_OK;
+  }
+  for (int k = 0; k < d; ++k) {
+    uint64_t e = (uint64_t)s[k];
+    if (e != 0 && n > (kMaxBytes / (uint64_t)esz) / e)
+      return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: tensor '%s' has >= 2^62 bytes", name);
+    n *= e;
+  }
+  *numel = n;
+  return TRIOT_OK;
+}
+
+static int check_ptr(const char* name, const void* p, uint64_t numel, int esz) {
+  if (numel == 0) return TRIOT_OK;
+  if (!p) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: data of '%s' is NULL", name);
+  if (((uintptr_t)p) % (uintptr_t)esz)
+    return set_error(TRIOT_ERR_MISALIGNED,
+                     "Misaligned: data of '%s' (%p) is not aligned to its %d-byte element", name,
+                     p, esz);
+  return TRIOT_OK;
+}
+
+static bool overlap(const void* a, uint64_t na, const void* b, uint64_t nb, int esz) {
+  if (na == 0 || nb == 0) return false;
+  uintptr_t a0 = (uintptr_t)a, a1 = a0 + na * (uint64_t)esz;
+  uintptr_t b0 = (uintptr_t)b, b1 = b0 + nb * (uint64_t)esz;
+  return a0 < b1 && b0 < a1;
+}
+
+static int dtype_size(int dtype) { return dtype == TRIOT_F32 ? 4 : dtype == TRIOT_F64 ? 8 : 0; }
+
+// Horner strides of a shape (Alg 2 / P:50): sigma_k = prod_{j>k} s_j.
+static void strides_of(const int64_t* s, int d, uint64_t* sig) {
+  uint64_t acc = 1;
+  for (int k = d - 1; k >= 0; --k) {
+    sig[k] = acc;
+    acc *= (uint64_t)s[k];
+  }
+}
+
+// ------------------------------------------------------------------------------ core planner
+//
+// Input: counter extents n[0..d-1], per tensor Horner strides, embed bounds bnd (min(src, n)).
+// Output: g's canonical axes, digits and per-tensor accessors.
+
+struct Axis {
+  uint64_t n, bnd;
+  uint64_t sig[TRIOT_MAXT];
+  int orig, merged;
+};
+
+static int ilog2(uint64_t v) {
+  int l = 0;
+  while ((1ull << l) < v) ++l;
+  return l;
+}
+
+static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
+                  const uint64_t* bnd, bool allow_merge, bool bounds) {
+  const int d = g.d, nt = g.ntensor;
+  // 1. drop unit axes ("if some axes have trivial length 1, then those axes can simply
+  //    be ignored"); keep at least one axis.
+  Axis ax[TRIOT_MAXD];
+  int na = 0;
+  for (int k = 0; k < d; ++k) {
+    if (n[k] == 1) continue;
+    Axis a;
+    a.n = n[k];
+    a.bnd = bnd ? bnd[k] : n[k];
+    for (int x = 0; x < nt; ++x) a.sig[x] = sig[x][k];
+    a.orig = k;
+    a.merged = 1;
+    ax[na++] = a;
+  }
+  if (na == 0) {
+    Axis a;
+    a.n = 1;
+    a.bnd = 1;
+    for (int x = 0; x < nt; ++x) a.sig[x] = sig[x][d - 1];
+    a.orig = d - 1;
+    a.merged = 1;
+    ax[na++] = a;
+  }
+  // 2. merge adjacent axes whose strides compose in every tensor (and, for embed, whose inner
+  //    axis is never out of bounds), so that merged offsets are still Horner sums.
+  if (allow_merge) {
+    int j = na - 1;
+    while (j > 0) {
+      Axis& o = ax[j - 1];
+      Axis& i = ax[j];
+      bool ok = true;
+      for (int x = 0; x < nt; ++x)
+        if (o.sig[x] != i.n * i.sig[x]) ok = false;
+      if (bounds && i.bnd != i.n) ok = false;
+      if (ok) {
+        Axis m;
+        m.n = o.n * i.n;
+        m.bnd = o.bnd * i.n;
+        for (int x = 0; x < nt; ++x) m.sig[x] = i.sig[x];
+        m.orig = i.orig;
+        m.merged = o.merged + i.merged;
+        ax[j - 1] = m;
+        for (int q = j; q + 1 < na; ++q) ax[q] = ax[q + 1];
+        --na;
+        --j;  // the merged axis sits at j-1: next try (j-2, j-1)
+      } else {
+        --j;
+      }
+    }
+  }
+  g.Dc = na;
+  for (int k = 0; k < na; ++k) {
+    g.cn[k] = ax[k].n;
+    g.corig[k] = ax[k].orig;
+    g.cmerged[k] = ax[k].merged;
+  }
+
+  // 3. vector geometry: V in {32 B, 16 B, 1 element}; case (a) V | n_last, case (b) rows
+  //    shorter than a vector, R = V / n_last whole rows per vector.
+  const int vmax = 32 / g.esz;
+  const int cands[3] = {vmax, 16 / g.esz, 1};
+  int best = -1;
+  long best_score = -1;
+  struct Cand {
+    int V, R, D;
+    bool collapsed;
+    bool vec[TRIOT_MAXT];
+  } cc[3];
+  const uint64_t nl = ax[na - 1].n;
+  for (int ci = 0; ci < 3; ++ci) {
+    int V = cands[ci];
+    Cand c;
+    c.V = V;
+    c.R = 1;
+    c.collapsed = false;
+    if (nl % (uint64_t)V == 0) {
+      c.D = na;
+    } else if (na >= 2 && nl < (uint64_t)V && (uint64_t)V % nl == 0 &&
+               ax[na - 2].n % ((uint64_t)V / nl) == 0) {
+      c.R = V / (int)nl;
+      c.collapsed = true;
+      c.D = na - 1;
+    } else {
+      cc[ci].V = 0;
+      continue;
+    }
+    // per-tensor wide-access legality: contiguous inside the vector and V*esz aligned
+    int nvec_ok = 0;
+    for (int x = 0; x < nt; ++x) {
+      bool ok = V > 1;
+      uint64_t tau = ax[na - 1].sig[x];
+      if (tau != 1) ok = false;
+      if (c.collapsed && ax[na - 2].sig[x] != nl) ok = false;
+      if ((uintptr_t)g.t[x].ptr % (uintptr_t)(V * g.esz)) ok = false;
+      for (int k = 0; k < na - (c.collapsed ? 2 : 1); ++k)
+        if (ax[k].sig[x] % (uint64_t)V) ok = false;
+      if (c.collapsed && (ax[na - 2].sig[x] * (uint64_t)c.R) % (uint64_t)V) ok = false;
+      c.vec[x] = ok;
+      nvec_ok += ok ? 1 : 0;
+    }
+    cc[ci] = c;
+    long score = (c.vec[0] ? 1000 : 0) + nvec_ok * 100 + V;
+    if (score > best_score) {
+      best_score = score;
+      best = ci;
+    }
+  }
+  const Cand& c = cc[best];
+  g.V = c.V;
+  g.R = c.R;
+  g.collapsed = c.collapsed;
+  g.D = c.D;
+  const int D = g.D;
+  const uint64_t V = (uint64_t)c.V;
+  // digit k < D-1 is canonical axis k; the vector digit D-1 is axis na-1 (a) or na-2 (b)
+  for (int k = 0; k < D - 1; ++k) {
+    g.ext[k] = ax[k].n;
+    g.bnd[k] = ax[k].bnd;
+    for (int x = 0; x < nt; ++x) g.t[x].sig[k] = ax[k].sig[x];
+  }
+  if (!c.collapsed) {
+    const Axis& a = ax[na - 1];
+    g.ext[D - 1] = a.n / V;
+    g.bnd[D - 1] = g.ext[D - 1];
+    for (int x = 0; x < nt; ++x) {
+      g.t[x].sig[D - 1] = V * a.sig[x];
+      g.t[x].rho = 0;
+      g.t[x].tau = a.sig[x];
+    }
+    g.lgL = ilog2(V);
+    g.rowmul = 0;
+    g.colmul = V;
+    g.srows = 1;
+    g.scols = bounds ? a.bnd : a.n;
+    g.vfull = g.scols / V;
+    g.vany = (g.scols + V - 1) / V;
+  } else {
+    const Axis& r = ax[na - 2];
+    const Axis& a = ax[na - 1];
+    const uint64_t R = (uint64_t)c.R;
+    g.ext[D - 1] = r.n / R;
+    g.bnd[D - 1] = g.ext[D - 1];
+    for (int x = 0; x < nt; ++x) {
+      g.t[x].sig[D - 1] = R * r.sig[x];
+      g.t[x].rho = r.sig[x];
+      g.t[x].tau = a.sig[x];
+    }
+    g.lgL = ilog2(a.n);
+    g.rowmul = R;
+    g.colmul = 0;
+    g.srows = bounds ? r.bnd : r.n;
+    g.scols = bounds ? a.bnd : a.n;
+    g.vfull = g.scols >= a.n ? g.srows / R : 0;
+    g.vany = g.scols > 0 ? (g.srows + R - 1) / R : 0;
+  }
+  if (!bounds) {
+    g.vfull = g.vany = g.ext[D - 1];
+    for (int k = 0; k < D; ++k) g.bnd[k] = g.ext[k];
+  }
+  if (g.all_oob) {
+    g.vfull = g.vany = 0;
+  }
+  for (int x = 0; x < nt; ++x) g.t[x].vec = c.vec[x];
+
+  // 4. totals, the +32-vector step in mixed radix, carry deltas, fast-division magics
+  g.N = 1;
+  for (int k = 0; k < na; ++k) g.N *= ax[k].n;
+  g.nvec = g.N / V;
+  g.nsteps = (g.nvec + 31) / 32;
+  uint64_t rem = 32;
+  for (int k = D - 1; k >= 1; --k) {
+    g.dlt[k] = rem % g.ext[k];
+    rem /= g.ext[k];
+  }
+  g.dlt[0] = rem;
+  g.khi = -1;
+  g.klo = D;
+  for (int k = 0; k < D; ++k)
+    if (g.dlt[k]) {
+      if (k > g.khi) g.khi = k;
+      if (k < g.klo) g.klo = k;
+    }
+  for (int x = 0; x < nt; ++x) {
+    uint64_t st = 0;
+    for (int k = 0; k < D; ++k) st += g.dlt[k] * g.t[x].sig[k];
+    g.t[x].step = st;
+    g.t[x].kap[0] = 0;
+    for (int k = 1; k < D; ++k) g.t[x].kap[k] = g.t[x].sig[k - 1] - g.ext[k] * g.t[x].sig[k];
+  }
+  for (int k = 0; k < D; ++k) {
+    uint32_t e = g.ext[k] >= 1 && g.ext[k] <= 0xffffffffull ? (uint32_t)g.ext[k] : 1;
+    fastdiv_magic(e, &g.fdm[k], &g.fds[k]);
+  }
+  // 5. index width: 32-bit iff every offset, count and vector index fits
+  uint64_t mx = g.N + 64 * V;
+  for (int x = 0; x < nt; ++x)
+    if (g.t[x].numel > mx) mx = g.t[x].numel;
+  for (int k = 0; k < D; ++k)
+    if (g.ext[k] + 32 > mx) mx = g.ext[k] + 32;
+  g.idx64 = mx >= (1ull << 32) - 64;
+  // 6. expected-value weight slots: digit k<D-1 -> axis; vector digit -> last (a) or row axis (b)
+  for (int j = 0; j < TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  for (int k = 0; k < D - 1; ++k) g.slot_of_axis[ax[k].orig] = k;
+  if (!c.collapsed) {
+    g.slot_of_axis[ax[na - 1].orig] = D - 1;
+    g.nslots = D;
+  } else {
+    g.slot_of_axis[ax[na - 2].orig] = D - 1;
+    g.slot_of_axis[ax[na - 1].orig] = D;
+    g.nslots = D + 1;
+  }
+  if (g.N == 1 && n[ax[0].orig] == 1) g.slot_of_axis[ax[0].orig] = -1;  // weight 0 anyway
+}
+
+// ------------------------------------------------------------------------------ public planners
+
+int plan_embed(Geom& g, void* dst, const int64_t* dst_shape, const void* src,
+               const int64_t* src_shape, int d, int dtype, unsigned flags) {
+  g = Geom();
+  if (d < 1 || d > TRIOT_MAXD)
+    return set_error(TRIOT_ERR_UNSUPPORTED_DIMENSION,
+                     "UnsupportedDimension: d = %d, supported 1..%d", d, TRIOT_MAXD);
+  int esz = dtype_size(dtype);
+  if (!esz) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadDtype: dtype = %d", dtype);
+  if (flags & ~1u) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadFlags: flags = %u", flags);
+  uint64_t nd, ns;
+  int st;
+  if ((st = check_shape("dst", dst_shape, d, esz, &nd))) return st;
+  if ((st = check_shape("src", src_shape, d, esz, &ns))) return st;
+  bool region = (flags & TRIOT_EMBED_REGION_ONLY) != 0;
+  uint64_t n[TRIOT_MAXD], bnd[TRIOT_MAXD];
+  uint64_t N = 1;
+  for (int k = 0; k < d; ++k) {
+    uint64_t D_ = (uint64_t)dst_shape[k], S = (uint64_t)src_shape[k];
+    n[k] = region ? (D_ < S ? D_ : S) : D_;
+    bnd[k] = S < n[k] ? S : n[k];
+    N *= n[k];
+  }
+  if ((st = check_ptr("dst", dst, nd, esz))) return st;
+  // src is read only where t < src_shape inside the counter
+  bool reads_src = N > 0 && ns > 0;
+  if ((st = check_ptr("src", src, reads_src ? ns : 0, esz))) return st;
+  if (reads_src && overlap(dst, nd, src, ns, esz))
+    return set_error(TRIOT_ERR_ALIASING, "Aliasing: dst and src overlap");
+  g.op = OP_EMBED;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.flags = flags;
+  g.d = d;
+  g.ntensor = 2;
+  g.t[0].ptr = dst;
+  g.t[0].numel = nd;
+  g.t[1].ptr = src;
+  g.t[1].numel = ns;
+  if (N == 0) {
+    g.empty = true;
+    clear_error();
+    return TRIOT_OK;
+  }
+  g.all_oob = ns == 0;
+  uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
+  strides_of(dst_shape, d, sig[0]);
+  if (ns == 0) {
+    for (int k = 0; k < d; ++k) sig[1][k] = 0;
+  } else {
+    strides_of(src_shape, d, sig[1]);
+  }
+  build(g, n, sig, bnd, /*allow_merge=*/true, /*bounds=*/!region);
+  clear_error();
+  return TRIOT_OK;
+}
+
+int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const int64_t* a_shape,
+                const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
+                int dtype, int op) {
+  g = Geom();
+  if (d < 1 || d > TRIOT_MAXD)
+    return set_error(TRIOT_ERR_UNSUPPORTED_DIMENSION,
+                     "UnsupportedDimension: d = %d, supported 1..%d", d, TRIOT_MAXD);
+  int esz = dtype_size(dtype);
+  if (!esz) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadDtype: dtype = %d", dtype);
+  if (op < TRIOT_ADD || op > TRIOT_DIV)
+    return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
+  uint64_t na_, nb_, nc_, ni_;
+  int st;
+  if ((st = check_shape("a", a_shape, d, esz, &na_))) return st;
+  if ((st = check_shape("b", b_shape, d, esz, &nb_))) return st;
+  int64_t it[TRIOT_MAXD];
+  if (iter_shape) {
+    if ((st = check_shape("iter", iter_shape, d, esz, &ni_))) return st;
+    for (int k = 0; k < d; ++k) it[k] = iter_shape[k];
+  } else {
+    for (int k = 0; k < d; ++k) it[k] = a_shape[k] < b_shape[k] ? a_shape[k] : b_shape[k];
+  }
+  int64_t cs[TRIOT_MAXD];
+  if (c_shape) {
+    if ((st = check_shape("c", c_shape, d, esz, &nc_))) return st;
+    for (int k = 0; k < d; ++k) cs[k] = c_shape[k];
+  } else {
+    for (int k = 0; k < d; ++k) cs[k] = it[k];
+  }
+  check_shape("iter", it, d, esz, &ni_);
+  check_shape("c", cs, d, esz, &nc_);
+  // check_tensor_pack_bounds: the iteration shape must lie inside every operand
+  const char* names[3] = {"c", "a", "b"};
+  const int64_t* shp[3] = {cs, a_shape, b_shape};
+  for (int x = 0; x < 3; ++x)
+    for (int k = 0; k < d; ++k)
+      if (it[k] > shp[x][k])
+        return set_error(TRIOT_ERR_AXIS_OUT_OF_BOUNDS,
+                         "AxisOutOfBounds: tensor '%s' axis %d: iteration extent %lld > tensor "
+                         "extent %lld",
+                         names[x], k, (long long)it[k], (long long)shp[x][k]);
+  if ((st = check_ptr("c", c, nc_, esz))) return st;
+  if ((st = check_ptr("a", a, ni_ ? na_ : 0, esz))) return st;
+  if ((st = check_ptr("b", b, ni_ ? nb_ : 0, esz))) return st;
+  if (ni_) {
+    const void* ins[2] = {a, b};
+    const uint64_t nin[2] = {na_, nb_};
+    const int64_t* ishp[2] = {a_shape, b_shape};
+    for (int x = 0; x < 2; ++x) {
+      if (!overlap(c, nc_, ins[x], nin[x], esz)) continue;
+      bool inplace = c == ins[x];
+      for (int k = 0; k < d && inplace; ++k)
+        if (cs[k] != ishp[x][k] || it[k] != cs[k]) inplace = false;
+      if (!inplace)
+        return set_error(TRIOT_ERR_ALIASING,
+                         "Aliasing: c overlaps '%s' (only exact in-place c == %s with equal "
+                         "shapes and iteration shape is allowed)",
+                         names[x + 1], names[x + 1]);
+    }
+  }
+  g.op = OP_BINARY;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.binop = op;
+  g.d = d;
+  g.ntensor = 3;
+  g.t[0].ptr = c;
+  g.t[0].numel = nc_;
+  g.t[1].ptr = a;
+  g.t[1].numel = na_;
+  g.t[2].ptr = b;
+  g.t[2].numel = nb_;
+  if (ni_ == 0) {
+    g.empty = true;
+    clear_error();
+    return TRIOT_OK;
+  }
+  uint64_t n[TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) n[k] = (uint64_t)it[k];
+  uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
+  strides_of(cs, d, sig[0]);
+  strides_of(a_shape, d, sig[1]);
+  strides_of(b_shape, d, sig[2]);
+  build(g, n, sig, nullptr, /*allow_merge=*/true, /*bounds=*/false);
+  clear_error();
+  return TRIOT_OK;
+}
+
+int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype) {
+  g = Geom();
+  if (d < 1 || d > TRIOT_MAXD)
+    return set_error(TRIOT_ERR_UNSUPPORTED_DIMENSION,
+                     "UnsupportedDimension: d = %d, supported 1..%d", d, TRIOT_MAXD);
+  int esz = dtype_size(dtype);
+  if (!esz) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadDtype: dtype = %d", dtype);
+  uint64_t np_;
+  int st;
+  if ((st = check_shape("p", shape, d, esz, &np_))) return st;
+  if ((st = check_ptr("p", p, np_, esz))) return st;
+  g.op = OP_EV;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.d = d;
+  g.ntensor = 1;
+  g.t[0].ptr = p;
+  g.t[0].numel = np_;
+  if (np_ == 0) {
+    g.empty = true;
+    clear_error();
+    return TRIOT_OK;
+  }
+  uint64_t n[TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) n[k] = (uint64_t)shape[k];
+  uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
+  strides_of(shape, d, sig[0]);
+  // every digit is a weight (Alg 11 reads counter[k]), so axes are never merged
+  build(g, n, sig, nullptr, /*allow_merge=*/false, /*bounds=*/false);
+  clear_error();
+  return TRIOT_OK;
+}
+
+// ------------------------------------------------------------------------------ describe
+
+static void arr(std::string& s, const char* key, const uint64_t* v, int n) {
+  s += "\"";
+  s += key;
+  s += "\":[";
+  char b[32];
+  for (int i = 0; i < n; ++i) {
+    snprintf(b, sizeof(b), "%s%llu", i ? "," : "", (unsigned long long)v[i]);
+    s += b;
+  }
+  s += "],";
+}
+static void arri(std::string& s, const char* key, const int* v, int n) {
+  s += "\"";
+  s += key;
+  s += "\":[";
+  char b[32];
+  for (int i = 0; i < n; ++i) {
+    snprintf(b, sizeof(b), "%s%d", i ? "," : "", v[i]);
+    s += b;
+  }
+  s += "],";
+}
+static void arr32(std::string& s, const char* key, const uint32_t* v, int n) {
+  uint64_t w[TRIOT_MAXD];
+  for (int i = 0; i < n; ++i) w[i] = v[i];
+  arr(s, key, w, n);
+}
+
+std::string describe(const Geom& g) {
+  std::string s = "{";
+  char b[512];
+  snprintf(b, sizeof(b),
+           "\"op\":%d,\"esz\":%d,\"d\":%d,\"empty\":%s,\"idx64\":%s,\"all_oob\":%s,\"Dc\":%d,"
+           "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"N\":%llu,\"nvec\":%llu,"
+           "\"nsteps\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
+           "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,",
+           g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
+           g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
+           g.collapsed ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
+           (unsigned long long)g.nsteps, g.khi, g.klo, (unsigned long long)g.rowmul,
+           (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,
+           (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots);
+  s += b;
+  arr(s, "cn", g.cn, g.Dc);
+  arri(s, "corig", g.corig, g.Dc);
+  arri(s, "cmerged", g.cmerged, g.Dc);
+  arr(s, "ext", g.ext, g.D);
+  arr(s, "dlt", g.dlt, g.D);
+  arr(s, "bnd", g.bnd, g.D);
+  arr32(s, "fdm", g.fdm, g.D);
+  arr32(s, "fds", g.fds, g.D);
+  arri(s, "slot_of_axis", g.slot_of_axis, g.d);
+  s += "\"t\":[";
+  for (int x = 0; x < g.ntensor; ++x) {
+    s += x ? ",{" : "{";
+    arr(s, "sig", g.t[x].sig, g.D);
+    arr(s, "kap", g.t[x].kap, g.D);
+    snprintf(b, sizeof(b), "\"step\":%llu,\"rho\":%llu,\"tau\":%llu,\"vec\":%s,\"numel\":%llu}",
+             (unsigned long long)g.t[x].step, (unsigned long long)g.t[x].rho,
+             (unsigned long long)g.t[x].tau, g.t[x].vec ? "true" : "false",
+             (unsigned long long)g.t[x].numel);
+    s += b;
+  }
+  s += "]}";
+  return s;
+}
+
+}  // namespace triot

@@ -1,0 +1,114 @@
+// plan.hpp -- host side of the boundary: validation, canonicalisation and the launch plan.
+//
+// Pure host C++ (no CUDA headers), so the whole plan can be inspected without a GPU through
+// triot_plan_describe().  The paper's structure it replaces:
+//   - check_tensor_pack_bounds (Alg 8/9): one check over shapes;
+//   - LinearTemplateSearch (Alg 7): runtime d -> compile-time instance; here an O(1)
+//     table lookup on the canonical digit count (dispatch.cu);
+//   - ForEachFixedDimension (Alg 6): the per-tuple loop nest; here the descriptor that
+//     lets each GPU lane run the odometer of Alg 3 on a compile-time number of digits.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "desc.h"
+
+namespace triot {
+
+struct Geom {
+  int op = 0, esz = 0, dtype = 0, binop = 0;
+  unsigned flags = 0;
+  int d = 0;          // caller's dimension
+  int ntensor = 0;
+  bool empty = false; // nothing to launch (empty counter); EV still writes zeros
+  bool idx64 = false;
+  bool all_oob = false;
+  // canonical axes (after unit-axis drop and merge), for describe()
+  int Dc = 0;
+  uint64_t cn[TRIOT_MAXD] = {};
+  int corig[TRIOT_MAXD] = {};      // original axis of each canonical axis (innermost of a merge)
+  int cmerged[TRIOT_MAXD] = {};    // number of original axes merged into it
+  // digits
+  int D = 0, V = 1, R = 1, lgL = 0;
+  bool collapsed = false;
+  uint64_t N = 0;
+  uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
+  uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
+  uint64_t nvec = 0, nsteps = 0;
+  int khi = 0, klo = 0;
+  uint64_t rowmul = 0, colmul = 0, vfull = 0, vany = 0, srows = 0, scols = 0;
+  int slot_of_axis[TRIOT_MAXD] = {};
+  int nslots = 0;
+  struct T {
+    uint64_t sig[TRIOT_MAXD] = {}, kap[TRIOT_MAXD] = {};
+    uint64_t step = 0, rho = 0, tau = 1;
+    bool vec = false;
+    const void* ptr = nullptr;
+    uint64_t numel = 0;
+  } t[TRIOT_MAXT];
+};
+
+// Each returns a triot_status; on error the thread-local message is set.
+int plan_embed(Geom& g, void* dst, const int64_t* dst_shape, const void* src,
+               const int64_t* src_shape, int d, int dtype, unsigned flags);
+int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const int64_t* a_shape,
+                const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
+                int dtype, int op);
+int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype);
+
+// Granlund-Montgomery round-up magic for an invariant 32-bit divisor (>= 1).
+void fastdiv_magic(uint32_t div, uint32_t* mul, uint32_t* shift);
+
+std::string describe(const Geom& g);
+
+// thread-local error detail
+int set_error(int status, const char* fmt, ...);
+void clear_error();
+const char* last_error();
+
+template <typename IDX>
+void fill_desc(const Geom& g, Desc<IDX>& d, uint64_t steps_per_warp) {
+  for (int k = 0; k < TRIOT_MAXD; ++k) {
+    d.ext[k] = (IDX)g.ext[k];
+    d.dlt[k] = (IDX)g.dlt[k];
+    d.bnd[k] = (IDX)g.bnd[k];
+    d.fdm[k] = g.fdm[k];
+    d.fds[k] = g.fds[k];
+    d.slot_of_axis[k] = g.slot_of_axis[k];
+  }
+  d.nvec = (IDX)g.nvec;
+  d.nsteps = (IDX)g.nsteps;
+  d.steps_per_warp = (IDX)steps_per_warp;
+  d.khi = g.khi;
+  d.klo = g.klo;
+  d.lgL = (uint32_t)g.lgL;
+  d.R = (uint32_t)g.R;
+  d.rowmul = (IDX)g.rowmul;
+  d.colmul = (IDX)g.colmul;
+  d.vfull = (IDX)g.vfull;
+  d.vany = (IDX)g.vany;
+  d.srows = (IDX)g.srows;
+  d.scols = (IDX)g.scols;
+  d.collapsed = g.collapsed ? 1 : 0;
+  d.d_out = g.d;
+  d.op = g.binop;
+  d.pad_ = 0;
+  for (int x = 0; x < TRIOT_MAXT; ++x) {
+    for (int k = 0; k < TRIOT_MAXD; ++k) {
+      d.t[x].sig[k] = (IDX)g.t[x].sig[k];
+      d.t[x].kap[k] = (IDX)g.t[x].kap[k];
+    }
+    d.t[x].step = (IDX)g.t[x].step;
+    d.t[x].rho = (IDX)g.t[x].rho;
+    d.t[x].tau = (IDX)g.t[x].tau;
+    d.t[x].vec = g.t[x].vec ? 1u : 0u;
+    d.t[x].pad_ = 0;
+    d.t[x].ptr = g.t[x].ptr;
+  }
+  d.out = nullptr;
+  d.ws = nullptr;
+}
+
+}  // namespace triot

@@ -1,0 +1,116 @@
+"""A CPU model of the kernels' index algorithm, driven by the REAL launch descriptor.
+
+triot_plan_describe() returns the descriptor the library would pass to the sm_100a kernel
+(canonical digits, +32-vector step digits, per-tensor strides and carry deltas, bounds).
+This model runs exactly the kernel's per-lane algorithm on it -- decode the start vector,
+then advance +32 vectors with the unrolled carry loop, adding the carry deltas to each
+tensor's offset -- and applies the op on numpy buffers.  Comparing its output with the oracle
+on small random shapes checks the host plan (validation, canonicalisation, vector geometry,
+carry deltas) without a GPU.  It is a test helper: the product never runs it.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M32 = (1 << 32) - 1
+
+
+def _wrap(x, idx64):
+    return x if idx64 else (x & M32)
+
+
+def run(desc: dict, op: str, bufs: list, q: int = 3, binop: str = "mul"):
+    """bufs: flat numpy arrays in tensor order (embed: dst, src; binary: c, a, b; ev: p).
+    Writes outputs in place; for 'ev' returns the weight-slot totals (list of floats)."""
+    D, V, idx64 = desc["D"], desc["V"], desc["idx64"]
+    ext, dlt, bnd = desc["ext"], desc["dlt"], desc["bnd"]
+    khi, klo, lgL = desc["khi"], desc["klo"], desc["lgL"]
+    T = desc["t"]
+    nt = len(T)
+    L = 1 << lgL
+    nvec, nsteps = desc["nvec"], desc["nsteps"]
+    W = lambda x: _wrap(x, idx64)
+    slots = [0.0] * (D + 1)
+
+    def start(v):
+        u = [0] * D
+        for k in range(D - 1, 0, -1):
+            u[k] = v % ext[k]
+            v //= ext[k]
+        u[0] = v
+        off = [W(sum(u[k] * T[x]["sig"][k] for k in range(D))) for x in range(nt)]
+        oob = 0
+        for k in range(D - 1):
+            oob |= int(u[k] >= bnd[k]) << k
+        return u, off, oob
+
+    def step(u, off, oob):
+        off = [W(off[x] + T[x]["step"]) for x in range(nt)]
+        carry = 0
+        for k in range(D - 1, -1, -1):
+            if k > khi:
+                continue
+            nu = u[k] + dlt[k] + carry
+            carry = int(nu >= ext[k])
+            if carry:
+                nu -= ext[k]
+                off = [W(off[x] + T[x]["kap"][k]) for x in range(nt)]
+            u[k] = nu
+            if k < D - 1:
+                oob = (oob & ~(1 << k)) | (int(nu >= bnd[k]) << k)
+            if k <= klo and not carry:
+                break
+        return u, off, oob
+
+    def eoff(x, off, e):
+        r, c = e >> lgL, e & (L - 1)
+        return W(off + r * T[x]["rho"] + c * T[x]["tau"])
+
+    nwarps = (nsteps + q - 1) // q
+    for w in range(nwarps):
+        s0, s1 = w * q, min((w + 1) * q, nsteps)
+        for lane in range(32):
+            u, off, oob = start(s0 * 32 + lane)
+            for s in range(s0, s1):
+                v = s * 32 + lane
+                if v < nvec:
+                    uv = u[D - 1]
+                    if op == "embed":
+                        vals = np.zeros(V, dtype=bufs[0].dtype)
+                        anyb = oob == 0 and uv < desc["vany"]
+                        if anyb and uv < desc["vfull"]:
+                            vals = np.array([bufs[1][eoff(1, off[1], e)] for e in range(V)],
+                                            dtype=bufs[0].dtype)
+                        elif anyb:
+                            row0, col0 = uv * desc["rowmul"], uv * desc["colmul"]
+                            for e in range(V):
+                                r, c = e >> lgL, e & (L - 1)
+                                if row0 + r < desc["srows"] and col0 + c < desc["scols"]:
+                                    vals[e] = bufs[1][eoff(1, off[1], e)]
+                        for e in range(V):
+                            bufs[0][eoff(0, off[0], e)] = vals[e]
+                    elif op == "binary":
+                        fn = {"add": np.add, "sub": np.subtract, "mul": np.multiply,
+                              "div": np.divide}[binop]
+                        for e in range(V):
+                            with np.errstate(all="ignore"):
+                                bufs[0][eoff(0, off[0], e)] = fn(bufs[1][eoff(1, off[1], e)],
+                                                                 bufs[2][eoff(2, off[2], e)])
+                    else:
+                        x = [float(bufs[0][eoff(0, off[0], e)]) for e in range(V)]
+                        s_ = sum(x)
+                        for k in range(D - 1):
+                            slots[k] += u[k] * s_
+                        wr = sum((e >> lgL) * x[e] for e in range(V))
+                        wc = sum((e & (L - 1)) * x[e] for e in range(V))
+                        base = uv * (desc["rowmul"] + desc["colmul"])
+                        if desc["collapsed"]:
+                            slots[D - 1] += base * s_ + wr
+                            slots[D] += wc
+                        else:
+                            slots[D - 1] += base * s_ + wc
+                u, off, oob = step(u, off, oob)
+    if op == "ev":
+        d = len(desc["slot_of_axis"])
+        return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]
+    return None

@@ -1,0 +1,260 @@
+"""The C-ABI boundary without a GPU: the library loads, exports every symbol include/triot.h
+declares, validates exactly as the header states, and its host plan (canonicalisation, vector
+geometry, carry deltas, fast-division magics) is checked against the oracle through a CPU model
+of the kernel algorithm (tests/kernel_model.py).  No compute call reaches the device here."""
+import ctypes
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from triot_inputs import CONFIGS, random_shape, random_values
+from tests import kernel_model
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "triot.h")
+
+T = pytest.importorskip("paper_1608_00099_b200")
+L = T._lib
+
+F32, F64 = L.TRIOT_F32, L.TRIOT_F64
+FAKE = 1 << 40        # a 256-byte-aligned fake device address; validation never dereferences
+
+
+def declared_symbols():
+    with open(HEADER) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"TRIOT_API\s+[\w\s\*]+?\b(triot_\w+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol():
+    decl = declared_symbols()
+    assert len(decl) == 9, decl
+    out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))
+    assert exported == decl
+    assert tuple(sorted(L.EXPORTS)) == tuple(decl)
+    lib = ctypes.CDLL(T.LIB_PATH)
+    for name in decl:
+        assert getattr(lib, name)
+
+
+def test_no_torch_or_oracle_linkage():
+    out = subprocess.run(["ldd", T.LIB_PATH], capture_output=True, text=True).stdout
+    assert "torch" not in out and "oracle" not in out and "libcudart" not in out
+
+
+def test_constants_and_status_strings():
+    assert T.triot_max_dimension() == 16
+    for code, name in L.STATUS.items():
+        assert T.triot_status_string(code) == name
+
+
+def _embed(dst_shape, src_shape, d=None, dtype=F64, flags=0, dst=FAKE, src=FAKE * 2):
+    d = len(dst_shape) if d is None else d
+    return T.triot_embed(dst, dst_shape, src, src_shape, d, dtype, flags, 0)
+
+
+def test_validation_embed():
+    ok_cuda = L.STATUS[9]
+    assert _embed((2, 2), (2, 2), d=0) == 2
+    assert _embed((2,) * 17, (2,) * 17) == 2
+    assert "d = 17" in T.triot_last_error()
+    assert _embed((2, -1), (2, 2)) == 3
+    assert "axis 1" in T.triot_last_error()
+    assert _embed((1 << 31, 1 << 31), (2, 2)) == 3          # >= 2^62 bytes
+    assert _embed((2, 2), (2, 2), dtype=7) == 5
+    assert _embed((2, 2), (2, 2), flags=4) == 5
+    assert _embed((2, 2), (2, 2), dst=0) == 1
+    assert _embed((2, 2), (2, 2), src=0) == 1
+    assert _embed((2, 2), (2, 2), dst=FAKE + 4) == 6          # f64 needs 8-byte alignment
+    assert _embed((4, 4), (4, 4), src=FAKE + 64) == 7         # overlap
+    # empty dst: a no-op that touches nothing, so NULL pointers are fine
+    assert _embed((0, 4), (3, 4), dst=0, src=0) == 0
+    assert T.triot_embed(FAKE, None, FAKE * 2, (2, 2), 2, F64, 0, 0) == 1
+    del ok_cuda
+
+
+def test_validation_binary_check_bounds():
+    # iter (3,3) over (2,3) -> AxisOutOfBounds(tensor 0, axis 0)
+    st = T.triot_apply_binary(FAKE, None, FAKE * 2, (2, 3), FAKE * 3, (3, 3), (3, 3), 2, F64,
+                              L.TRIOT_MUL, 0)
+    assert st == 4
+    msg = T.triot_last_error()
+    assert "'a'" in msg and "axis 0" in msg
+    st = T.triot_apply_binary(FAKE, (2, 2), FAKE * 2, (3, 3), FAKE * 3, (3, 3), (2, 3), 2, F64,
+                              L.TRIOT_MUL, 0)
+    assert st == 4 and "'c'" in T.triot_last_error() and "axis 1" in T.triot_last_error()
+    assert T.triot_apply_binary(FAKE, None, FAKE * 2, (2, 2), FAKE * 3, (2, 2), None, 2, F64, 9,
+                                0) == 5
+    # aliasing: c overlapping a with different shapes is refused, exact in-place is allowed
+    assert T.triot_apply_binary(FAKE, (4, 4), FAKE + 8, (4, 4), FAKE * 3, (4, 4), None, 2, F64,
+                                L.TRIOT_ADD, 0) == 7
+    assert T.triot_apply_binary(FAKE, (4, 4), FAKE, (4, 5), FAKE * 3, (4, 4), None, 2, F64,
+                                L.TRIOT_ADD, 0) == 7
+    # empty iteration: no-op
+    assert T.triot_apply_binary(0, None, 0, (0, 3), 0, (2, 3), None, 2, F64, L.TRIOT_ADD, 0) == 0
+
+
+def test_validation_ev():
+    assert T.triot_expected_value_workspace_size((16,) * 6, 6, F64) > 256
+    with pytest.raises(T.TriotError):
+        T.triot_expected_value_workspace_size((2,) * 17, 17, F64)
+    ws = T.triot_expected_value_workspace_size((4, 4), 2, F64)
+    assert T.triot_expected_value(0, FAKE, (4, 4), 2, F64, FAKE * 3, ws, 0) == 1
+    assert T.triot_expected_value(FAKE + 4, FAKE * 2, (4, 4), 2, F64, FAKE * 3, ws, 0) == 6
+    assert T.triot_expected_value(FAKE + 8, FAKE, (4, 4), 2, F64, FAKE * 3, ws, 0) == 7
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="GPU present")
+def test_valid_call_without_gpu_reports_cuda_error():
+    st = _embed((4, 4), (2, 2))
+    assert st == 9 and "CUDA" in T.triot_last_error()
+
+
+# ------------------------------------------------------------------ fast division magics
+
+def _fastdiv(n, m, s):
+    h = (n * m) >> 32
+    return (h + ((n - h) >> (s & 0xFF))) >> (s >> 8)
+
+
+def test_fastdiv_exact():
+    rng = np.random.default_rng(3)
+    divisors = {1, 2, 3, 4, 5, 7, 8, 9, 16, 24, 32, 36, 40, 48, 64, 384, 512, 6, 12, 2 ** 31 - 1,
+                2 ** 31, 2 ** 31 + 1, 2 ** 32 - 1, 65537, 1000003}
+    divisors |= set(int(x) for x in rng.integers(1, 2 ** 32, size=40))
+    edge = [0, 1, 2, 3, 2 ** 16, 2 ** 31 - 1, 2 ** 31, 2 ** 32 - 2, 2 ** 32 - 1]
+    for dv in sorted(divisors):
+        m, s = T.triot_fastdiv_magic(dv)
+        ns = edge + [int(x) for x in rng.integers(0, 2 ** 32, size=2000)]
+        ns += [k * dv + r for k in (1, 2, 3, 1000) for r in (0, dv - 1) if k * dv + r < 2 ** 32]
+        for n in ns:
+            assert _fastdiv(n, m, s) == n // dv, (dv, n)
+        if dv & (dv - 1) == 0:          # 2^k: the magic degenerates to Alg 12's shift
+            assert all(_fastdiv(n, m, s) == n >> (dv.bit_length() - 1) for n in ns)
+    with pytest.raises(T.TriotError):
+        T.triot_fastdiv_magic(0)
+
+
+# ------------------------------------------------------------------ plans of C1..C5
+
+def _plan(name, mods=(0, 0, 0)):
+    c = CONFIGS[name]
+    sh = c.shapes
+    dt = F32 if c.dtype == "f32" else F64
+    if c.op == "embed":
+        return T.triot_plan_describe(0, [sh["dst"], sh["src"]], None, len(sh["dst"]), dt, 0, mods)
+    if c.op == "binary":
+        return T.triot_plan_describe(1, [None, sh["a"], sh["b"]], sh["iter"], len(sh["a"]), dt,
+                                     L.TRIOT_MUL, mods)
+    return T.triot_plan_describe(2, [sh["p"]], None, len(sh["p"]), dt, 0, mods)
+
+
+def test_plans_of_the_five_configs():
+    p = _plan("C1")     # dst rows 64 B -> 32-B stores; src rows 40 B -> element loads
+    assert (p["Dc"], p["D"], p["V"], p["collapsed"]) == (4, 4, 4, False)
+    assert [t["vec"] for t in p["t"]] == [True, False]
+    p = _plan("C2")     # both rows 32-B multiples, src/zero boundary at 1536 B is vector-aligned
+    assert (p["Dc"], p["D"], p["V"]) == (3, 3, 8)
+    assert [t["vec"] for t in p["t"]] == [True, True]
+    assert (p["vfull"], p["vany"]) == (48, 48)
+    p = _plan("C3")
+    assert (p["Dc"], p["D"], p["V"]) == (6, 6, 4) and p["t"][0]["vec"]
+    p = _plan("C4")     # A rows 288 B = 9 x 32 B stay aligned
+    assert (p["Dc"], p["D"], p["V"]) == (5, 5, 4)
+    assert [t["vec"] for t in p["t"]] == [True, True, True]
+    p = _plan("C5")     # innermost 4 floats < a vector: 2 dst rows per 32-B vector
+    assert (p["Dc"], p["D"], p["V"], p["R"], p["collapsed"]) == (14, 13, 8, 2, True)
+    assert [t["vec"] for t in p["t"]] == [True, False]
+    assert all(not pl["idx64"] for pl in map(_plan, CONFIGS))
+    # misaligned output pointer: the plan falls back to narrower accesses, never faults
+    p = _plan("C2", mods=(4, 0, 0))
+    assert not p["t"][0]["vec"]
+
+
+def test_canonicalisation_drops_and_merges():
+    # equal inner extents merge (P:609 style simplification); unit axes are dropped
+    p = T.triot_plan_describe(0, [(6, 1, 5, 8), (4, 1, 5, 8)], None, 4, F32, 0)
+    assert p["Dc"] == 1 and p["cn"] == [240] and p["scols"] == 160   # t < 160 <=> t0 < 4
+    p = T.triot_plan_describe(0, [(6, 5, 8), (4, 3, 8)], None, 3, F32, 0)
+    assert p["Dc"] == 2 and p["cn"] == [6, 40]        # src row stride 24 != 40: no outer merge
+    p = T.triot_plan_describe(1, [None, (3, 4, 5), (3, 4, 5)], None, 3, F64, 0)
+    assert p["Dc"] == 1 and p["cn"] == [60]
+    # expected value never merges: every digit is a weight (Alg 11)
+    p = T.triot_plan_describe(2, [(3, 4, 5)], None, 3, F64, 0)
+    assert p["Dc"] == 3
+
+
+# ------------------------------------------------------------------ kernel model vs oracle
+
+def _bits(a):
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("seed", range(12))
+def test_model_embed_vs_oracle(dtype, seed):
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.integers(1, 9))
+    src_shape = random_shape(rng, d, 1500, lo=1, hi=7 if d > 3 else 14)
+    dst_shape = tuple(max(1, s + int(rng.integers(-2, 5))) for s in src_shape)
+    if seed % 4 == 0:   # tiny innermost extents -> collapsed vectors
+        dst_shape = dst_shape[:-1] + (int(rng.choice([1, 2, 4])),)
+    if math.prod(dst_shape) > 4000:
+        dst_shape = tuple(min(a, b) for a, b in zip(dst_shape, src_shape))
+    region = seed % 5 == 4
+    src = random_values(rng, src_shape, dtype, "normal")
+    ref = np.full(dst_shape, -7.0, dtype=src.dtype)
+    O.embed(ref, src, region_only=region)
+    dt = F32 if dtype == "f32" else F64
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, dt, 1 if region else 0)
+    out = np.full(dst_shape, -7.0, dtype=src.dtype)
+    kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)], q=int(rng.integers(1, 5)))
+    np.testing.assert_array_equal(_bits(out), _bits(ref))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_model_binary_vs_oracle(seed):
+    rng = np.random.default_rng(2000 + seed)
+    d = int(rng.integers(1, 8))
+    dtype = "f32" if seed % 2 else "f64"
+    ish = random_shape(rng, d, 1500, lo=1, hi=7 if d > 3 else 14)
+    a = random_values(rng, tuple(s + int(rng.integers(0, 3)) for s in ish), dtype, "normal")
+    b = random_values(rng, tuple(s + int(rng.integers(0, 3)) for s in ish), dtype, "normal")
+    cs = tuple(s + int(rng.integers(0, 2)) for s in ish) if seed % 3 == 0 else ish
+    op = ["add", "sub", "mul", "div"][seed % 4]
+    ref = np.full(cs, 5.0, dtype=a.dtype)
+    O.apply_binary(a, b, op, iter_shape=ish, out=ref)
+    dt = F32 if dtype == "f32" else F64
+    desc = T.triot_plan_describe(1, [cs, a.shape, b.shape], ish, d, dt, T.OPS[op])
+    out = np.full(cs, 5.0, dtype=a.dtype)
+    kernel_model.run(desc, "binary", [out.reshape(-1), a.reshape(-1), b.reshape(-1)],
+                     q=int(rng.integers(1, 5)), binop=op)
+    np.testing.assert_array_equal(_bits(out), _bits(ref))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_model_ev_vs_oracle(seed):
+    rng = np.random.default_rng(3000 + seed)
+    d = int(rng.integers(1, 8))
+    shape = random_shape(rng, d, 1500, lo=1, hi=7 if d > 3 else 14)
+    if seed % 3 == 0:
+        shape = shape[:-1] + (int(rng.choice([1, 2, 4])),)
+    p = rng.integers(0, 256, size=shape).astype(np.float64)     # exact: any order agrees
+    desc = T.triot_plan_describe(2, [shape], None, d, F64, 0)
+    got = kernel_model.run(desc, "ev", [p.reshape(-1)], q=int(rng.integers(1, 5)))
+    np.testing.assert_array_equal(np.array(got), O.expected_value(p))

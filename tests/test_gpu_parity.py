@@ -1,0 +1,265 @@
+"""GPU parity: the sm_100a kernels (called through the C-ABI) against the CPU oracle.
+
+Bar: bit-exact for embed and apply_binary (memcmp of the whole output),
+<= 1e-12 relative per component for the fp64 expected value (against the Neumaier-compensated
+oracle), bit-exact for integer-valued and 2^-24-uniform PMFs, and bitwise deterministic.
+The five BASELINE configs are compared at full size, element by element, in the same launch
+configuration bench.py times (the library chooses it from the shapes and the SM count).
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1608_00099_b200 as T  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from triot_inputs import make_inputs, random_shape, random_values, special_values  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def _bits(a: np.ndarray) -> np.ndarray:
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+def _dev(a: np.ndarray, offset: int = 0):
+    """Copy to the GPU; offset > 0 places the tensor `offset` elements into a larger buffer so
+    its base pointer is only element-aligned (the alignment fallbacks)."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if offset == 0:
+        return t.to(DEV)
+    buf = torch.empty(t.numel() + offset, dtype=t.dtype, device=DEV)
+    v = buf[offset:].view(t.shape)
+    v.copy_(t.to(DEV))
+    return v
+
+
+def _poisoned(shape, dtype, offset=0):
+    x = np.full(shape, np.nan, dtype=dtype)
+    return _dev(x, offset)
+
+
+def assert_bits_equal(got, ref):
+    g = got.cpu().numpy()
+    assert g.shape == ref.shape
+    bad = np.flatnonzero(_bits(g).ravel() != _bits(ref).ravel())
+    assert bad.size == 0, f"{bad.size} mismatches, first at flat {bad[:5]}: {g.ravel()[bad[:5]]} vs {ref.ravel()[bad[:5]]}"
+
+
+# ---------------------------------------------------------------- the five configs, full size
+
+def test_C1_embed_full():
+    inp = make_inputs("C1")
+    ref = np.empty(inp["dst_shape"]); O.embed(ref, inp["src"])
+    dst = _poisoned(inp["dst_shape"], np.float64)
+    T.embed(dst, _dev(inp["src"]))
+    assert_bits_equal(dst, ref)
+
+
+def test_C2_embed_full():
+    inp = make_inputs("C2")
+    ref = np.empty(inp["dst_shape"], np.float32); O.embed(ref, inp["src"])
+    dst = _poisoned(inp["dst_shape"], np.float32)
+    T.embed(dst, _dev(inp["src"]))
+    assert_bits_equal(dst, ref)
+
+
+def test_C3_expected_value_full():
+    p = make_inputs("C3")["p"]
+    ref, plain = O.expected_value(p, with_plain=True)
+    pt = _dev(p)
+    m1 = T.expected_value(pt).cpu().numpy()
+    m2 = T.expected_value(pt).cpu().numpy()
+    assert np.all(np.abs(m1 - ref) <= 1e-12 * np.abs(ref)), (m1, ref)
+    assert _bits(m1).tolist() == _bits(m2).tolist()          # deterministic run to run
+
+
+def test_C4_binary_full():
+    inp = make_inputs("C4")
+    ref = O.apply_binary(inp["a"], inp["b"], "mul", inp["iter_shape"])
+    out = T.apply_binary(_dev(inp["a"]), _dev(inp["b"]), "mul")
+    assert tuple(out.shape) == inp["iter_shape"]
+    assert_bits_equal(out, ref)
+
+
+def test_C5_embed_full():
+    inp = make_inputs("C5")
+    ref = np.empty(inp["dst_shape"], np.float32); O.embed(ref, inp["src"])
+    dst = _poisoned(inp["dst_shape"], np.float32)
+    T.embed(dst, _dev(inp["src"]))
+    assert_bits_equal(dst, ref)
+
+
+def test_region_only_C1_C5():
+    for name in ("C1", "C5"):
+        inp = make_inputs(name)
+        src = inp["src"]
+        ref = np.full(inp["dst_shape"], 3.0, dtype=src.dtype)
+        O.embed(ref, src, region_only=True)
+        dst = _dev(np.full(inp["dst_shape"], 3.0, dtype=src.dtype))
+        T.embed(dst, _dev(src), region_only=True)
+        assert_bits_equal(dst, ref)
+
+
+# ---------------------------------------------------------------- random shapes, d = 1..16
+
+def _rand_embed_case(rng, d, dtype):
+    hi = 5 if d > 8 else (9 if d > 4 else 40)
+    src_shape = random_shape(rng, d, 60000, lo=1, hi=hi)
+    dst_shape = tuple(max(0, s + int(rng.integers(-2, 5))) for s in src_shape)
+    r = rng.random()
+    if r < 0.25:       # tiny / odd innermost extents
+        dst_shape = dst_shape[:-1] + (int(rng.choice([1, 2, 3, 4, 5, 8])),)
+    elif r < 0.35:     # zero extent somewhere
+        k = int(rng.integers(0, d))
+        dst_shape = dst_shape[:k] + (0,) + dst_shape[k + 1:]
+    if math.prod(dst_shape) > 200000:
+        dst_shape = tuple(min(a, b) for a, b in zip(dst_shape, src_shape))
+    return src_shape, dst_shape
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", list(range(1, 17)))
+def test_embed_random(d, dtype):
+    rng = np.random.default_rng(10 * d + (dtype == np.float64))
+    for rep in range(4):
+        src_shape, dst_shape = _rand_embed_case(rng, d, dtype)
+        src = rng.standard_normal(src_shape).astype(dtype)
+        off_d, off_s = (0, 0) if rep < 2 else (1 + rep % 3, rep % 2)
+        for region in (False, True):
+            ref = np.full(dst_shape, np.nan, dtype=dtype)
+            O.embed(ref, src, region_only=region)
+            dst = _poisoned(dst_shape, dtype, off_d)
+            T.embed(dst, _dev(src, off_s), region_only=region)
+            assert_bits_equal(dst, ref)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div"])
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 6, 8, 11, 14, 16])
+def test_binary_random(d, op, dtype):
+    rng = np.random.default_rng(100 * d + len(op) + (dtype == np.float64))
+    for rep in range(3):
+        hi = 5 if d > 8 else (9 if d > 4 else 40)
+        ish = random_shape(rng, d, 60000, lo=1, hi=hi)
+        if rep == 1:
+            ish = ish[:-1] + (int(rng.choice([1, 2, 3, 5])),)
+        a = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(dtype)
+        b = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(dtype)
+        cs = tuple(s + int(rng.integers(0, 2)) for s in ish) if rep == 2 else ish
+        ref = np.full(cs, 9.0, dtype=dtype)
+        O.apply_binary(a, b, op, iter_shape=ish, out=ref)
+        out = _dev(np.full(cs, 9.0, dtype=dtype), rep)
+        T.apply_binary(_dev(a, rep % 2), _dev(b), op, out=out, iter_shape=ish)
+        assert_bits_equal(out, ref)
+
+
+def test_binary_inplace_and_special_values():
+    for dtype in (np.float32, np.float64):
+        sv = special_values("f32" if dtype == np.float32 else "f64")
+        a = np.tile(sv, 8).reshape(4, 16).astype(dtype)
+        b = np.tile(sv[::-1], 8).reshape(4, 16).astype(dtype)
+        for op in ("add", "sub", "mul", "div"):
+            ref = O.apply_binary(a, b, op)
+            at = _dev(a)
+            T.apply_binary(at, _dev(b), op, out=at)          # exact in-place c == a
+            g = at.cpu().numpy()
+            nan = np.isnan(ref)
+            assert np.array_equal(np.isnan(g), nan)
+            assert_bits_equal(torch.from_numpy(np.where(nan, 0, g)), np.where(nan, 0, ref))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_embed_moves_raw_bits(dtype):
+    sv = special_values("f32" if dtype == np.float32 else "f64")
+    src = np.tile(sv, 6).reshape(3, 16)
+    ref = np.full((5, 19), np.nan, dtype=dtype); O.embed(ref, src)
+    dst = _poisoned((5, 19), dtype)
+    T.embed(dst, _dev(src))
+    assert_bits_equal(dst, ref)
+
+
+@pytest.mark.parametrize("d", list(range(1, 17)))
+def test_ev_random_integer_exact(d):
+    rng = np.random.default_rng(500 + d)
+    hi = 5 if d > 8 else (9 if d > 4 else 40)
+    for rep in range(3):
+        shape = random_shape(rng, d, 100000, lo=1, hi=hi)
+        if rep == 1:
+            shape = shape[:-1] + (int(rng.choice([1, 2, 3, 4])),)
+        for dtype in (np.float32, np.float64):
+            p = rng.integers(0, 256, size=shape).astype(dtype)
+            got = T.expected_value(_dev(p, rep)).cpu().numpy()
+            np.testing.assert_array_equal(got, O.expected_value(p))
+
+
+def test_ev_closed_forms():
+    p = np.full((16,) * 6, 2.0 ** -24)
+    assert T.expected_value(_dev(p)).cpu().tolist() == [7.5] * 6
+    q = np.zeros((4, 6, 3, 5)); q[3, 1, 2, 4] = 1.0
+    assert T.expected_value(_dev(q)).cpu().tolist() == [3.0, 1.0, 2.0, 4.0]
+    e = T.expected_value(_dev(np.zeros((3, 0, 2))))
+    assert e.cpu().tolist() == [0.0, 0.0, 0.0]
+
+
+def test_ev_signed_f32_bound():
+    rng = np.random.default_rng(77)
+    p = (rng.standard_normal((33, 17, 9, 5))).astype(np.float32)
+    ref = O.expected_value(p)
+    scale = O.expected_value_abs(p)
+    got = T.expected_value(_dev(p)).cpu().numpy()
+    assert np.all(np.abs(got - ref) <= 1e-12 * scale)
+
+
+def test_streams_and_repeated_calls():
+    """Several streams, EV workspace ticket left at zero between calls."""
+    inp = make_inputs("C1")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    src = _dev(inp["src"])
+    ref = np.empty(inp["dst_shape"]); O.embed(ref, inp["src"])
+    p = _dev(make_inputs("C3")["p"])
+    outs = []
+    for s in (s1, s2, s1):
+        with torch.cuda.stream(s):
+            dst = _poisoned(inp["dst_shape"], np.float64)
+            T.embed(dst, src)
+            outs.append((dst, T.expected_value(p)))
+    torch.cuda.synchronize()
+    for dst, m in outs:
+        assert_bits_equal(dst, ref)
+        assert torch.equal(m, outs[0][1])
+
+
+def test_errors_raise_not_fallback():
+    x = torch.zeros(4, 4, dtype=torch.float64, device=DEV)
+    with pytest.raises(T.TriotError):
+        T.apply_binary(x, torch.zeros(3, 4, dtype=torch.float64, device=DEV), "mul",
+                       iter_shape=(4, 4))
+    with pytest.raises(TypeError):
+        T.embed(x.cpu(), x.cpu())
+
+
+@pytest.mark.slow
+def test_u64_index_path():
+    """A tensor of > 2^32 elements takes the 64-bit-index instances (17.2 GB f32 dst)."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40e9:
+        pytest.skip("needs ~20 GB free")
+    dst_shape = (65537, 65536)
+    src = np.random.default_rng(9).random((5, 70001)).astype(np.float32)
+    desc = T.triot_plan_describe(0, [dst_shape, src.shape], None, 2, T.TRIOT_F32, 0)
+    assert desc["idx64"]
+    dst = torch.full(dst_shape, float("nan"), dtype=torch.float32, device=DEV)
+    T.embed(dst, _dev(src))
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:5, :], torch.from_numpy(src[:, :65536]).to(DEV))
+    assert int(torch.count_nonzero(dst[5:])) == 0
+    tail = dst[-1, -8:].cpu().numpy()
+    assert not np.any(_bits(tail))
+    del dst
+    torch.cuda.empty_cache()
