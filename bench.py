@@ -381,13 +381,20 @@ def _run_slab(kind, args_):
     return time.perf_counter() - t
 
 
+def _calibrate(seconds: float) -> float:
+    """Fraction of axis 0 whose oracle run takes about `seconds` (per-byte rate of a probe)."""
+    probe = [_slab(n, 1.0 / 64) for n in STEP_OPS]
+    t = sum(_run_slab(k, a) for k, a, _ in probe)
+    pbytes = sum(b for _, _, b in probe)
+    full = sum(algorithmic_bytes(n) for n in STEP_OPS)
+    full_s = t / max(pbytes, 1) * full
+    return min(1.0, seconds / max(full_s, 1e-9))
+
+
 def cpu_baseline(budget_s: float = 20.0, frac: float | None = None):
     """The oracle as it stands, 1 thread, on a slab of each op sized to ~budget_s seconds."""
     if frac is None:
-        probe = [_slab(n, 1.0 / 64) for n in STEP_OPS]
-        t = sum(_run_slab(k, a) for k, a, _ in probe)
-        full_est = t * 64
-        frac = min(1.0, budget_s / max(full_est, 1e-9))
+        frac = _calibrate(budget_s)
     slabs = [_slab(n, frac) for n in STEP_OPS]
     secs = sum(_run_slab(k, a) for k, a, _ in slabs)
     nbytes = sum(b for _, _, b in slabs)
@@ -403,10 +410,7 @@ def run_reference(args, rank, world):
         return
     from oracle import oracle as O
     O.build()
-    budget = args.ref_budget
-    probe = [_slab(n, 1.0 / 64) for n in STEP_OPS]
-    full_est = sum(_run_slab(k, a) for k, a, _ in probe) * 64
-    frac = min(1.0, budget / max(1, args.steps + args.warmup) / max(full_est, 1e-9))
+    frac = _calibrate(args.ref_budget / max(1, args.steps + args.warmup))
     slabs = [_slab(n, frac) for n in STEP_OPS]
     step_bytes = sum(b for _, _, b in slabs)
     for _ in range(args.warmup):

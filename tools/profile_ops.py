@@ -1,0 +1,48 @@
+"""Run each TRIOT op on its BASELINE config a few times (profiling driver for ncu).
+
+    python tools/profile_ops.py [--only C5] [--reps 3]
+
+Every launch is one of the library's kernels; inputs are built before the first launch.
+Exits 0 only if every op ran (no parity check here -- that is tests/)."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1608_00099_b200 as T  # noqa: E402
+from triot_inputs import make_inputs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    dev = torch.device("cuda:0")
+    for name in a.only.split(","):
+        inp = make_inputs(name)
+        if name in ("C1", "C2", "C5"):
+            src = torch.from_numpy(inp["src"]).to(dev)
+            dst = torch.empty(inp["dst_shape"], dtype=src.dtype, device=dev)
+            fn = lambda: T.embed(dst, src)
+        elif name == "C3":
+            p = torch.from_numpy(inp["p"]).to(dev)
+            out = torch.empty(p.dim(), dtype=torch.float64, device=dev)
+            fn = lambda: T.expected_value(p, out=out)
+        else:
+            x = torch.from_numpy(inp["a"]).to(dev)
+            y = torch.from_numpy(inp["b"]).to(dev)
+            c = torch.empty(inp["iter_shape"], dtype=torch.float64, device=dev)
+            fn = lambda: T.apply_binary(x, y, "mul", out=c)
+        for _ in range(a.reps):
+            fn()
+        torch.cuda.synchronize()
+        print(name, "ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
