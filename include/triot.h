@@ -172,11 +172,22 @@ TRIOT_API int triot_expected_value(double* means, const void* p, const int64_t* 
  *           carries the triot_binop),
  *       2 = expected value (shapes[0]=p).
  *   ptr_mod32: byte offsets modulo 32 of each tensor's data pointer (alignment model).
+ *   mode, warps: the work decomposition to describe (0 = contiguous chunk per warp, 1 = grid
+ *              stride) over `warps` warps; the real call picks them from the SM count.
  * Returns a triot_status (validation errors exactly as the real call would report them).
  */
-TRIOT_API int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape, int d,
-                        int dtype, unsigned flags, const unsigned* ptr_mod32,
-                        char* buf, size_t buf_len);
+TRIOT_API int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape,
+                                  int d, int dtype, unsigned flags, const unsigned* ptr_mod32,
+                                  int mode, uint64_t warps, char* buf, size_t buf_len);
+
+/*
+ * triot_set_launch_policy -- tuning hook (thread-local): force the work decomposition of this
+ * thread's subsequent calls.  mode: -1 = automatic (default), 0 = contiguous chunk per warp,
+ * 1 = grid stride; blocks_per_sm: 0 = as many as fit.  Results are bit-identical under every
+ * policy for embed and binary; the expected value's summation order follows the policy (it
+ * stays deterministic for a fixed policy).  Used by tools/tune.py; not needed otherwise.
+ */
+TRIOT_API int triot_set_launch_policy(int mode, int blocks_per_sm);
 
 /* The Granlund-Montgomery round-up magic the kernels use to divide by an invariant extent
  * (P:143 notes that division is slow; it is done once per thread with a multiply-high):

@@ -27,7 +27,7 @@ STATUS = {
 }
 EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "triot_embed",
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
-           "triot_plan_describe", "triot_fastdiv_magic")
+           "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
 class TriotError(RuntimeError):
@@ -39,7 +39,7 @@ class TriotError(RuntimeError):
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_1608_00099_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_1608_00099_b200/build.py` "
         "(there is no CPU fallback)")
 
 _lib = ctypes.CDLL(LIB_PATH)
@@ -67,7 +67,10 @@ _lib.triot_expected_value.argtypes = [_vp, _vp, _i64p, ctypes.c_int, ctypes.c_in
 _lib.triot_plan_describe.restype = ctypes.c_int
 _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
-                                     ctypes.c_char_p, ctypes.c_size_t]
+                                     ctypes.c_int, ctypes.c_uint64, ctypes.c_char_p,
+                                     ctypes.c_size_t]
+_lib.triot_set_launch_policy.restype = ctypes.c_int
+_lib.triot_set_launch_policy.argtypes = [ctypes.c_int, ctypes.c_int]
 _lib.triot_fastdiv_magic.restype = ctypes.c_int
 _lib.triot_fastdiv_magic.argtypes = [ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_uint32)]
@@ -127,14 +130,19 @@ def triot_expected_value(means: int, p: int, shape, d: int, dtype: int, workspac
                                      workspace_bytes, stream)
 
 
+def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:
+    """Tuning hook: -1 = automatic, 0 = chunk per warp, 1 = grid stride (thread-local)."""
+    check(_lib.triot_set_launch_policy(mode, blocks_per_sm))
+
+
 def triot_plan_describe(op: int, shapes, iter_shape, d: int, dtype: int, flags: int = 0,
-                        ptr_mod32=(0, 0, 0)) -> dict:
+                        ptr_mod32=(0, 0, 0), mode: int = 0, warps: int = 1) -> dict:
     arrs = [_shape(s) if s is not None else None for s in shapes] + [None] * (3 - len(shapes))
     ptrs = (_i64p * 3)(*[ctypes.cast(a, _i64p) if a is not None else _i64p() for a in arrs])
     mods = (ctypes.c_uint * 3)(*ptr_mod32)
     buf = ctypes.create_string_buffer(1 << 16)
-    check(_lib.triot_plan_describe(op, ptrs, _shape(iter_shape), d, dtype, flags, mods, buf,
-                                   len(buf)))
+    check(_lib.triot_plan_describe(op, ptrs, _shape(iter_shape), d, dtype, flags, mods, mode,
+                                   warps, buf, len(buf)))
     return json.loads(buf.value.decode())
 
 

@@ -1,6 +1,6 @@
 """Build libtriot.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-    python -m paper_1608_00099_b200.build [--force] [--ptxas-v]
+    python paper_1608_00099_b200/build.py [--force] [--ptxas-v]   (or __graft_entry__.build())
 
 Objects go to paper_1608_00099_b200/build/, the library to paper_1608_00099_b200/libtriot.so
 (both git-ignored; the .so travels to the GPU box with the gpurun snapshot).  The kernel

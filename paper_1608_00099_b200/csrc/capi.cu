@@ -58,10 +58,23 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_error(TRIOT_ERR_CUDA, "CUDA: %s: %s", what, cudaGetErrorString(e));
 }
 
-// grid sizing: enough resident warps to keep >= ~48 KB of loads in flight per SM, each warp a
-// contiguous run of >= kMinSteps steps
-int launch_geometry(const void* fn, const Geom& g, int max_grid, unsigned* grid_out,
-                    uint64_t* q_out) {
+// ---- work decomposition policy ----------------------------------
+// mode 0 = each warp streams a contiguous chunk; mode 1 = grid stride (all warps sweep one
+// window of the tensors together, which the B200 DRAM schedules better: tools/membench.py).
+// blocks_per_sm 0 = as many as fit (occupancy).  The automatic choice was tuned on B200
+// (tools/tune.py); triot_set_launch_policy() overrides it for the calling thread (tuning only).
+struct Policy {
+  int mode;
+  int bpsm;
+};
+thread_local Policy g_override = {-1, 0};
+
+Policy auto_policy(const Geom& g) {
+  (void)g;
+  return Policy{1, 0};
+}
+
+int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -84,28 +97,31 @@ int launch_geometry(const void* fn, const Geom& g, int max_grid, unsigned* grid_
     }
     occ = it->second;
   }
+  Policy pol = auto_policy(g);
+  if (g_override.mode >= 0) pol.mode = g_override.mode;
+  if (g_override.bpsm > 0) pol.bpsm = g_override.bpsm;
   const uint64_t wpb = TRIOT_BLOCK / 32;
-  const uint64_t kMinSteps = 4;
-  uint64_t grid = (uint64_t)sms * (uint64_t)occ;
+  const uint64_t kMinSteps = 4;  // >= 4 steps per warp amortise the start decode
+  uint64_t grid = (uint64_t)sms * (uint64_t)(pol.bpsm > 0 ? pol.bpsm : occ);
   uint64_t need = (g.nsteps + kMinSteps * wpb - 1) / (kMinSteps * wpb);
   if (need < grid) grid = need;
   if (grid > (uint64_t)max_grid) grid = (uint64_t)max_grid;
   if (grid < 1) grid = 1;
-  uint64_t q = (g.nsteps + grid * wpb - 1) / (grid * wpb);
-  if (q < 1) q = 1;
-  grid = (g.nsteps + q * wpb - 1) / (q * wpb);
-  if (grid < 1) grid = 1;
+  set_decomposition(g, pol.mode, grid * wpb);
+  if (pol.mode == 0) {  // drop blocks whose warps would get no chunk
+    uint64_t q = g.wmul / 32;
+    grid = (g.nsteps + q * wpb - 1) / (q * wpb);
+    if (grid < 1) grid = 1;
+  }
   *grid_out = (unsigned)grid;
-  *q_out = q;
   return TRIOT_OK;
 }
 
 template <typename IDX>
-int launch_t(const Geom& g, const void* fn, unsigned grid, uint64_t q, cudaStream_t st,
-             void* out, void* ws) {
+int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void* out, void* ws) {
   Desc<IDX> d;
   memset(&d, 0, sizeof(d));
-  fill_desc<IDX>(g, d, q);
+  fill_desc<IDX>(g, d);
   d.out = out;
   d.ws = ws;
   void* args[1] = {&d};
@@ -114,14 +130,13 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, uint64_t q, cudaStrea
   return TRIOT_OK;
 }
 
-int launch(const Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
+int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   const void* fn = table_for(g)(g.D, vindex(g), g.idx64 ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no instance for D=%d V=%d", g.D, g.V);
   int max_grid = 1 << 30;
   if (g.op == OP_EV) max_grid = TRIOT_EV_MAX_GRID;
   unsigned grid;
-  uint64_t q;
-  int st = launch_geometry(fn, g, max_grid, &grid, &q);
+  int st = launch_geometry(fn, g, max_grid, &grid);
   if (st) return st;
   if (g.op == OP_EV) {
     size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 1) * sizeof(double);
@@ -130,8 +145,8 @@ int launch(const Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
                        need);
   }
   cudaStream_t s = (cudaStream_t)stream;
-  return g.idx64 ? launch_t<uint64_t>(g, fn, grid, q, s, out, ws)
-                 : launch_t<uint32_t>(g, fn, grid, q, s, out, ws);
+  return g.idx64 ? launch_t<uint64_t>(g, fn, grid, s, out, ws)
+                 : launch_t<uint32_t>(g, fn, grid, s, out, ws);
 }
 
 size_t ev_ws_bytes(int d) {
@@ -222,8 +237,8 @@ int triot_expected_value(double* means, const void* p, const int64_t* shape, int
 }
 
 int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape, int d,
-                        int dtype, unsigned flags, const unsigned* ptr_mod32, char* buf,
-                        size_t buf_len) {
+                        int dtype, unsigned flags, const unsigned* ptr_mod32, int mode,
+                        uint64_t warps, char* buf, size_t buf_len) {
   if (!shapes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: shapes is NULL");
   // synthetic, non-overlapping device addresses with the requested alignment
   uintptr_t base[3];
@@ -241,12 +256,23 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
   else
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
   if (st) return st;
+  if (mode < 0 || mode > 1) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadMode: %d", mode);
+  if (!g.empty) set_decomposition(g, mode, warps ? warps : 1);
   std::string s = describe(g);
   if (buf && buf_len) {
     size_t n = s.size() < buf_len - 1 ? s.size() : buf_len - 1;
     memcpy(buf, s.data(), n);
     buf[n] = 0;
   }
+  return TRIOT_OK;
+}
+
+int triot_set_launch_policy(int mode, int blocks_per_sm) {
+  if (mode < -1 || mode > 1 || blocks_per_sm < 0 || blocks_per_sm > 32)
+    return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadPolicy: mode %d, blocks_per_sm %d", mode,
+                     blocks_per_sm);
+  g_override.mode = mode;
+  g_override.bpsm = mode < 0 ? 0 : blocks_per_sm;
   return TRIOT_OK;
 }
 

@@ -44,8 +44,11 @@ struct Desc {
   uint32_t fdm[TRIOT_MAXD];  // fast-division magic multiplier per digit extent (IDX = u32)
   uint32_t fds[TRIOT_MAXD];  // fast-division shifts: s1 | s2 << 8
   IDX nvec;              // number of vectors W
-  IDX nsteps;            // ceil(W / 32)
-  IDX steps_per_warp;    // Q: each warp owns steps [w*Q, (w+1)*Q)
+  // work decomposition: warp w starts at vector w*wmul + lane, owns
+  // the window [w*wmul, min(w*wmul + wspan, W)) and advances by dv vectors per step.
+  //   chunk mode:  wmul = wspan = Q*32, dv = 32      (each warp streams a contiguous run)
+  //   stride mode: wmul = 32, wspan = W, dv = 32*warps (all warps sweep one window together)
+  IDX wmul, wspan, dv;
   int32_t khi, klo;      // innermost / outermost digit with a nonzero step digit
   // in-vector geometry
   uint32_t lgL;          // log2(elements per row inside a vector): log2(V) if R == 1

@@ -149,6 +149,13 @@ __device__ __forceinline__ void odo_step(const Desc<IDX>& d, IDX (&u)[D], IDX (&
   }
 }
 
+// end of warp's window: min(base0 + wspan, W), guarding wrap-around of the index type
+template <typename IDX>
+__device__ __forceinline__ IDX warp_end(const Desc<IDX>& d, IDX base0) {
+  IDX e = base0 + d.wspan;
+  return (e > d.nvec || e < base0) ? d.nvec : e;
+}
+
 // element e of a vector: row r = e >> lgL, column c = e & (L-1); offset off + r*rho + c*tau
 template <typename IDX>
 __device__ __forceinline__ IDX elem_off(IDX off, int e, uint32_t lgL, IDX rho, IDX tau) {
@@ -192,20 +199,22 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   constexpr int NW = V * EW;
   const int lane = threadIdx.x & 31;
   const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
-  const IDX s0 = warp * d.steps_per_warp;
-  if (s0 >= d.nsteps) return;
-  const IDX s1 = min(s0 + d.steps_per_warp, d.nsteps);
+  const IDX base0 = warp * d.wmul;
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
   IDX u[D], off[2];
   uint32_t oob;
-  odo_start<D, 2, true, IDX>(d, s0 * 32 + (IDX)lane, u, off, oob);
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 2, true, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
-  for (IDX s = s0; s < s1; s += K) {
+  for (IDX b = base0; b < vend; b += K * d.dv) {
     uint32_t buf[K][NW];
     IDX doff[K];
     bool valid[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      valid[j] = (s + j < s1) && ((s + j) * 32 + (IDX)lane < d.nvec);
+      valid[j] = v < vend;
+      v += d.dv;
       doff[j] = off[0];
       if (valid[j]) {
         const IDX uv = u[D - 1];
@@ -286,20 +295,22 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
   constexpr int NW = V * EW;
   const int lane = threadIdx.x & 31;
   const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
-  const IDX s0 = warp * d.steps_per_warp;
-  if (s0 >= d.nsteps) return;
-  const IDX s1 = min(s0 + d.steps_per_warp, d.nsteps);
+  const IDX base0 = warp * d.wmul;
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
   IDX u[D], off[3];
   uint32_t oob;
-  odo_start<D, 3, false, IDX>(d, s0 * 32 + (IDX)lane, u, off, oob);
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 3, false, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
-  for (IDX s = s0; s < s1; s += K) {
+  for (IDX b = base0; b < vend; b += K * d.dv) {
     uint32_t ba[K][NW], bb[K][NW];
     IDX coff[K];
     bool valid[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      valid[j] = (s + j < s1) && ((s + j) * 32 + (IDX)lane < d.nvec);
+      valid[j] = v < vend;
+      v += d.dv;
       coff[j] = off[0];
       if (valid[j]) {
         load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, ba[j]);
@@ -336,25 +347,27 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
-  const IDX s0 = warp * d.steps_per_warp;
+  const IDX base0 = warp * d.wmul;
   double acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
   const uint32_t lgL = d.lgL;
-  if (s0 < d.nsteps) {
-    const IDX s1 = min(s0 + d.steps_per_warp, d.nsteps);
+  if (base0 < d.nvec) {
+    const IDX vend = warp_end(d, base0);
     IDX u[D], off[1];
     uint32_t oob;
-    odo_start<D, 1, false, IDX>(d, s0 * 32 + (IDX)lane, u, off, oob);
+    IDX v = base0 + (IDX)lane;
+    odo_start<D, 1, false, IDX>(d, v, u, off, oob);
     const IDX vmul = d.rowmul + d.colmul;  // exactly one of them is nonzero
     const bool coll = d.collapsed != 0;
-    for (IDX s = s0; s < s1; s += K) {
+    for (IDX b = base0; b < vend; b += K * d.dv) {
       uint32_t buf[K][NW];
       bool valid[K];
       IDX uu[K][D];
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        valid[j] = (s + j < s1) && ((s + j) * 32 + (IDX)lane < d.nvec);
+        valid[j] = v < vend;
+        v += d.dv;
         if (valid[j]) load_vec<ESZ, V, IDX>(d.t[0], off[0], lgL, buf[j]);
 #pragma unroll
         for (int k = 0; k < D; ++k) uu[j][k] = u[k];

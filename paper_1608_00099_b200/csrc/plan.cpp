@@ -286,32 +286,18 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   for (int k = 0; k < na; ++k) g.N *= ax[k].n;
   g.nvec = g.N / V;
   g.nsteps = (g.nvec + 31) / 32;
-  uint64_t rem = 32;
-  for (int k = D - 1; k >= 1; --k) {
-    g.dlt[k] = rem % g.ext[k];
-    rem /= g.ext[k];
-  }
-  g.dlt[0] = rem;
-  g.khi = -1;
-  g.klo = D;
-  for (int k = 0; k < D; ++k)
-    if (g.dlt[k]) {
-      if (k > g.khi) g.khi = k;
-      if (k < g.klo) g.klo = k;
-    }
   for (int x = 0; x < nt; ++x) {
-    uint64_t st = 0;
-    for (int k = 0; k < D; ++k) st += g.dlt[k] * g.t[x].sig[k];
-    g.t[x].step = st;
     g.t[x].kap[0] = 0;
     for (int k = 1; k < D; ++k) g.t[x].kap[k] = g.t[x].sig[k - 1] - g.ext[k] * g.t[x].sig[k];
   }
+  set_decomposition(g, 0, 1);
   for (int k = 0; k < D; ++k) {
     uint32_t e = g.ext[k] >= 1 && g.ext[k] <= 0xffffffffull ? (uint32_t)g.ext[k] : 1;
     fastdiv_magic(e, &g.fdm[k], &g.fds[k]);
   }
-  // 5. index width: 32-bit iff every offset, count and vector index fits
-  uint64_t mx = g.N + 64 * V;
+  // 5. index width: 32-bit iff every offset, count and vector index fits, with room for the
+  //    largest per-batch advance (K steps of up to 2^20 vectors)
+  uint64_t mx = g.N + (1ull << 24) * V;
   for (int x = 0; x < nt; ++x)
     if (g.t[x].numel > mx) mx = g.t[x].numel;
   for (int k = 0; k < D; ++k)
@@ -329,6 +315,45 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
     g.nslots = D + 1;
   }
   if (g.N == 1 && n[ax[0].orig] == 1) g.slot_of_axis[ax[0].orig] = -1;  // weight 0 anyway
+}
+
+void set_decomposition(Geom& g, int mode, uint64_t warps) {
+  if (warps < 1) warps = 1;
+  if (mode == 1) {
+    g.mode = 1;
+    g.wmul = 32;
+    g.wspan = g.nvec;
+    g.dv = 32 * warps;
+  } else {
+    g.mode = 0;
+    uint64_t q = (g.nsteps + warps - 1) / warps;
+    if (q < 1) q = 1;
+    g.wmul = g.wspan = 32 * q;
+    g.dv = 32;
+  }
+  // the step in mixed radix (digit 0 absorbs the rest; it only matters past the end)
+  const int D = g.D;
+  uint64_t rem = g.dv;
+  for (int k = D - 1; k >= 1; --k) {
+    g.dlt[k] = rem % g.ext[k];
+    rem /= g.ext[k];
+  }
+  g.dlt[0] = rem;
+  g.khi = -1;
+  g.klo = D;
+  for (int k = 0; k < D; ++k)
+    if (g.dlt[k]) {
+      if (k > g.khi) g.khi = k;
+      if (k < g.klo) g.klo = k;
+    }
+  if (g.khi < 0) {  // cannot happen for dv >= 1; keep the kernel loop well-formed
+    g.khi = g.klo = 0;
+  }
+  for (int x = 0; x < g.ntensor; ++x) {
+    uint64_t st = 0;
+    for (int k = 0; k < D; ++k) st += g.dlt[k] * g.t[x].sig[k];
+    g.t[x].step = st;
+  }
 }
 
 // ------------------------------------------------------------------------------ public planners
@@ -542,16 +567,17 @@ static void arr32(std::string& s, const char* key, const uint32_t* v, int n) {
 
 std::string describe(const Geom& g) {
   std::string s = "{";
-  char b[512];
+  char b[1024];
   snprintf(b, sizeof(b),
            "\"op\":%d,\"esz\":%d,\"d\":%d,\"empty\":%s,\"idx64\":%s,\"all_oob\":%s,\"Dc\":%d,"
            "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"N\":%llu,\"nvec\":%llu,"
-           "\"nsteps\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
+           "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
-           (unsigned long long)g.nsteps, g.khi, g.klo, (unsigned long long)g.rowmul,
+           (unsigned long long)g.nsteps, g.mode, (unsigned long long)g.wmul,
+           (unsigned long long)g.wspan, (unsigned long long)g.dv, g.khi, g.klo, (unsigned long long)g.rowmul,
            (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,
            (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots);
   s += b;

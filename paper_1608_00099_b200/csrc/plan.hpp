@@ -37,6 +37,8 @@ struct Geom {
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
   uint64_t nvec = 0, nsteps = 0;
+  uint64_t wmul = 32, wspan = 32, dv = 32;   // decomposition (set_decomposition)
+  int mode = 0;                              // 0 = chunk, 1 = stride
   int khi = 0, klo = 0;
   uint64_t rowmul = 0, colmul = 0, vfull = 0, vany = 0, srows = 0, scols = 0;
   int slot_of_axis[TRIOT_MAXD] = {};
@@ -58,6 +60,10 @@ int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const i
                 int dtype, int op);
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype);
 
+// Work decomposition over `warps` warps: mode 0 = contiguous chunk per warp, 1 = grid stride.
+// Sets wmul/wspan/dv and the mixed-radix digits of the per-step advance (dlt, khi, klo, step).
+void set_decomposition(Geom& g, int mode, uint64_t warps);
+
 // Granlund-Montgomery round-up magic for an invariant 32-bit divisor (>= 1).
 void fastdiv_magic(uint32_t div, uint32_t* mul, uint32_t* shift);
 
@@ -69,7 +75,7 @@ void clear_error();
 const char* last_error();
 
 template <typename IDX>
-void fill_desc(const Geom& g, Desc<IDX>& d, uint64_t steps_per_warp) {
+void fill_desc(const Geom& g, Desc<IDX>& d) {
   for (int k = 0; k < TRIOT_MAXD; ++k) {
     d.ext[k] = (IDX)g.ext[k];
     d.dlt[k] = (IDX)g.dlt[k];
@@ -79,8 +85,9 @@ void fill_desc(const Geom& g, Desc<IDX>& d, uint64_t steps_per_warp) {
     d.slot_of_axis[k] = g.slot_of_axis[k];
   }
   d.nvec = (IDX)g.nvec;
-  d.nsteps = (IDX)g.nsteps;
-  d.steps_per_warp = (IDX)steps_per_warp;
+  d.wmul = (IDX)g.wmul;
+  d.wspan = (IDX)g.wspan;
+  d.dv = (IDX)g.dv;
   d.khi = g.khi;
   d.klo = g.klo;
   d.lgL = (uint32_t)g.lgL;

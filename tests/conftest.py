@@ -9,3 +9,18 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU oracle case")
+
+
+def _ensure_built():
+    """A fresh checkout has no libtriot.so (git-ignored): build it once, like build() does."""
+    lib = os.path.join(ROOT, "paper_1608_00099_b200", "libtriot.so")
+    if not os.path.exists(lib):
+        import importlib.util
+        spec = importlib.util.spec_from_file_location(
+            "_triot_build", os.path.join(ROOT, "paper_1608_00099_b200", "build.py"))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        mod.build()
+
+
+_ensure_built()

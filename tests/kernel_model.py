@@ -19,7 +19,7 @@ def _wrap(x, idx64):
     return x if idx64 else (x & M32)
 
 
-def run(desc: dict, op: str, bufs: list, q: int = 3, binop: str = "mul"):
+def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
     """bufs: flat numpy arrays in tensor order (embed: dst, src; binary: c, a, b; ev: p).
     Writes outputs in place; for 'ev' returns the weight-slot totals (list of floats)."""
     D, V, idx64 = desc["D"], desc["V"], desc["idx64"]
@@ -28,7 +28,7 @@ def run(desc: dict, op: str, bufs: list, q: int = 3, binop: str = "mul"):
     T = desc["t"]
     nt = len(T)
     L = 1 << lgL
-    nvec, nsteps = desc["nvec"], desc["nsteps"]
+    nvec = desc["nvec"]
     W = lambda x: _wrap(x, idx64)
     slots = [0.0] * (D + 1)
 
@@ -66,14 +66,18 @@ def run(desc: dict, op: str, bufs: list, q: int = 3, binop: str = "mul"):
         r, c = e >> lgL, e & (L - 1)
         return W(off + r * T[x]["rho"] + c * T[x]["tau"])
 
-    nwarps = (nsteps + q - 1) // q
+    wmul, wspan, dv = desc["wmul"], desc["wspan"], desc["dv"]
+    nwarps = (nvec + wmul - 1) // wmul if desc["mode"] == 0 else dv // 32
     for w in range(nwarps):
-        s0, s1 = w * q, min((w + 1) * q, nsteps)
+        base0 = w * wmul
+        if base0 >= nvec:
+            continue
+        vend = min(base0 + wspan, nvec)
         for lane in range(32):
-            u, off, oob = start(s0 * 32 + lane)
-            for s in range(s0, s1):
-                v = s * 32 + lane
-                if v < nvec:
+            v = base0 + lane
+            u, off, oob = start(v)
+            while v < vend:
+                if True:
                     uv = u[D - 1]
                     if op == "embed":
                         vals = np.zeros(V, dtype=bufs[0].dtype)
@@ -110,6 +114,7 @@ def run(desc: dict, op: str, bufs: list, q: int = 3, binop: str = "mul"):
                         else:
                             slots[D - 1] += base * s_ + wc
                 u, off, oob = step(u, off, oob)
+                v += dv
     if op == "ev":
         d = len(desc["slot_of_axis"])
         return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]

@@ -33,7 +33,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     decl = declared_symbols()
-    assert len(decl) == 9, decl
+    assert len(decl) == 10, decl
     out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))
@@ -221,9 +221,10 @@ def test_model_embed_vs_oracle(dtype, seed):
     ref = np.full(dst_shape, -7.0, dtype=src.dtype)
     O.embed(ref, src, region_only=region)
     dt = F32 if dtype == "f32" else F64
-    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, dt, 1 if region else 0)
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, dt, 1 if region else 0,
+                                 mode=seed % 2, warps=int(rng.integers(1, 9)))
     out = np.full(dst_shape, -7.0, dtype=src.dtype)
-    kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)], q=int(rng.integers(1, 5)))
+    kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
     np.testing.assert_array_equal(_bits(out), _bits(ref))
 
 
@@ -240,10 +241,10 @@ def test_model_binary_vs_oracle(seed):
     ref = np.full(cs, 5.0, dtype=a.dtype)
     O.apply_binary(a, b, op, iter_shape=ish, out=ref)
     dt = F32 if dtype == "f32" else F64
-    desc = T.triot_plan_describe(1, [cs, a.shape, b.shape], ish, d, dt, T.OPS[op])
+    desc = T.triot_plan_describe(1, [cs, a.shape, b.shape], ish, d, dt, T.OPS[op],
+                                 mode=seed % 2, warps=int(rng.integers(1, 9)))
     out = np.full(cs, 5.0, dtype=a.dtype)
-    kernel_model.run(desc, "binary", [out.reshape(-1), a.reshape(-1), b.reshape(-1)],
-                     q=int(rng.integers(1, 5)), binop=op)
+    kernel_model.run(desc, "binary", [out.reshape(-1), a.reshape(-1), b.reshape(-1)], binop=op)
     np.testing.assert_array_equal(_bits(out), _bits(ref))
 
 
@@ -255,6 +256,7 @@ def test_model_ev_vs_oracle(seed):
     if seed % 3 == 0:
         shape = shape[:-1] + (int(rng.choice([1, 2, 4])),)
     p = rng.integers(0, 256, size=shape).astype(np.float64)     # exact: any order agrees
-    desc = T.triot_plan_describe(2, [shape], None, d, F64, 0)
-    got = kernel_model.run(desc, "ev", [p.reshape(-1)], q=int(rng.integers(1, 5)))
+    desc = T.triot_plan_describe(2, [shape], None, d, F64, 0, mode=seed % 2,
+                                 warps=int(rng.integers(1, 9)))
+    got = kernel_model.run(desc, "ev", [p.reshape(-1)])
     np.testing.assert_array_equal(np.array(got), O.expected_value(p))
