@@ -173,7 +173,8 @@ TRIOT_API int triot_expected_value(double* means, const void* p, const int64_t* 
  *       2 = expected value (shapes[0]=p).
  *   ptr_mod32: byte offsets modulo 32 of each tensor's data pointer (alignment model).
  *   mode, warps: the work decomposition to describe (0 = contiguous chunk per warp, 1 = grid
- *              stride) over `warps` warps; the real call picks them from the SM count.
+ *              stride, over `warps` warps; 2 = contiguous chunk per block of the expected-value
+ *              bulk-copy kernel, over `warps` blocks); the real call picks them from the SM count.
  * Returns a triot_status (validation errors exactly as the real call would report them).
  */
 TRIOT_API int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape,
@@ -183,7 +184,8 @@ TRIOT_API int triot_plan_describe(int op, const int64_t* const* shapes, const in
 /*
  * triot_set_launch_policy -- tuning hook (thread-local): force the work decomposition of this
  * thread's subsequent calls.  mode: -1 = automatic (default), 0 = contiguous chunk per warp,
- * 1 = grid stride; blocks_per_sm: 0 = as many as fit.  Results are bit-identical under every
+ * 1 = grid stride, 2 = the expected value's bulk-copy pipeline (block chunks; other ops treat 2
+ * as automatic); blocks_per_sm: 0 = the default for the mode.  Results are bit-identical under every
  * policy for embed and binary; the expected value's summation order follows the policy (it
  * stays deterministic for a fixed policy).  Used by tools/tune.py; not needed otherwise.
  */

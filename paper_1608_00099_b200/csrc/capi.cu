@@ -26,6 +26,8 @@ const void* triot_table_1_8_2(int, int, int);
 const void* triot_table_1_8_3(int, int, int);
 const void* triot_table_2_4_0(int, int, int);
 const void* triot_table_2_8_0(int, int, int);
+const void* triot_table_2_4_1(int, int, int);
+const void* triot_table_2_8_1(int, int, int);
 }
 
 namespace triot {
@@ -70,8 +72,8 @@ struct Policy {
 thread_local Policy g_override = {-1, 0};
 
 Policy auto_policy(const Geom& g) {
-  (void)g;
-  return Policy{1, 0};
+  if (g.op == OP_EV) return Policy{0, 0};
+  return Policy{0, 16};
 }
 
 int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
@@ -130,7 +132,65 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
   return TRIOT_OK;
 }
 
+// EV bulk-copy fast path: full 32-byte vectors, 32-B aligned p, one persistent block per SM
+int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, bool* used) {
+  *used = false;
+  if (g.op != OP_EV || g.V * g.esz != 32 || !g.t[0].vec) return TRIOT_OK;
+  if (g_override.mode >= 0 && g_override.mode != 2) return TRIOT_OK;
+  const void* fn = (g.esz == 8 ? triot_table_2_8_1 : triot_table_2_4_1)(g.D, 0, g.idx64 ? 1 : 0);
+  if (!fn) return TRIOT_OK;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int sms;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 0 || dev >= 64) return set_error(TRIOT_ERR_CUDA, "CUDA: device id %d", dev);
+    if (!g_sms[dev]) {
+      e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    }
+    sms = g_sms[dev];
+    if (g_occ.find(fn) == g_occ.end()) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIOT_EV_SMEM);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+      g_occ.emplace(fn, 1);
+    }
+  }
+  uint64_t blocks = (uint64_t)sms * (uint64_t)(g_override.bpsm > 0 ? g_override.bpsm : 1);
+  uint64_t need = (g.nvec + TRIOT_EV_SVEC - 1) / TRIOT_EV_SVEC;
+  if (need < blocks) blocks = need;
+  if (blocks > TRIOT_EV_MAX_GRID) blocks = TRIOT_EV_MAX_GRID;
+  if (blocks < 1) blocks = 1;
+  set_decomposition(g, 2, blocks);
+  uint64_t grid = (g.nvec + g.wmul - 1) / g.wmul;
+  size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 1) * sizeof(double);
+  if (!ws || ws_bytes < need_ws)
+    return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
+                     need_ws);
+  *used = true;
+  auto go = [&](auto tag) -> int {
+    using IDX = decltype(tag);
+    Desc<IDX> d;
+    memset(&d, 0, sizeof(d));
+    fill_desc<IDX>(g, d);
+    d.out = out;
+    d.ws = ws;
+    void* args[1] = {&d};
+    cudaError_t e2 = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(TRIOT_BLOCK), args,
+                                      TRIOT_EV_SMEM, (cudaStream_t)stream);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaLaunchKernel");
+    return TRIOT_OK;
+  };
+  return g.idx64 ? go(uint64_t(0)) : go(uint32_t(0));
+}
+
 int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
+  if (g.op == OP_EV) {
+    bool used = false;
+    int st = launch_ev_tma(g, stream, out, ws, ws_bytes, &used);
+    if (st || used) return st;
+  }
   const void* fn = table_for(g)(g.D, vindex(g), g.idx64 ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no instance for D=%d V=%d", g.D, g.V);
   int max_grid = 1 << 30;
@@ -256,7 +316,7 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
   else
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
   if (st) return st;
-  if (mode < 0 || mode > 1) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadMode: %d", mode);
+  if (mode < 0 || mode > 2) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadMode: %d", mode);
   if (!g.empty) set_decomposition(g, mode, warps ? warps : 1);
   std::string s = describe(g);
   if (buf && buf_len) {
@@ -268,7 +328,7 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
 }
 
 int triot_set_launch_policy(int mode, int blocks_per_sm) {
-  if (mode < -1 || mode > 1 || blocks_per_sm < 0 || blocks_per_sm > 32)
+  if (mode < -1 || mode > 2 || blocks_per_sm < 0 || blocks_per_sm > 1024)
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadPolicy: mode %d, blocks_per_sm %d", mode,
                      blocks_per_sm);
   g_override.mode = mode;

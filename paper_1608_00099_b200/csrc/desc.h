@@ -70,5 +70,9 @@ struct Desc {
 // Workspace layout of the expected value: [ticket u32 | pad to 256 B] [grid x (D+1) doubles].
 #define TRIOT_EV_MAX_GRID 2048
 #define TRIOT_EV_WS_HEADER 256
+// EV bulk-copy pipeline: NSTAGE shared-memory stages of SVEC 32-byte vectors per block
+#define TRIOT_EV_NSTAGE 8
+#define TRIOT_EV_SVEC 512
+#define TRIOT_EV_SMEM (TRIOT_EV_NSTAGE * TRIOT_EV_SVEC * 32 + 2 * TRIOT_EV_NSTAGE * 8)
 
 }  // namespace triot

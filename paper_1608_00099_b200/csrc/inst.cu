@@ -7,7 +7,7 @@
 //
 //   TRIOT_INST_OP   0 = embed, 1 = binary, 2 = expected value
 //   TRIOT_INST_ESZ  4 or 8
-//   TRIOT_INST_BOP  binary op 0..3 (binary only)
+//   TRIOT_INST_BOP  binary op 0..3 (binary); 1 = bulk-copy variant (expected value)
 #include "kernels.cuh"
 
 #ifndef TRIOT_INST_OP
@@ -42,6 +42,9 @@ const void* kptr() {
   return (const void*)&embed_kernel<D, ESZ, V, IDX, KEMBED>;
 #elif TRIOT_INST_OP == 1
   return (const void*)&binary_kernel<D, ESZ, V, IDX, KBIN, TRIOT_INST_BOP>;
+#elif TRIOT_INST_BOP == 1
+  // EV bulk-copy fast path: only the 32-byte vector width exists
+  return V == 32 / ESZ ? (const void*)&ev_tma_kernel<D, ESZ, IDX> : nullptr;
 #else
   return (const void*)&ev_kernel<D, ESZ, V, IDX, KEV>;
 #endif

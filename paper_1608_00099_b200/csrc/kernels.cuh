@@ -332,70 +332,86 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ expected value
-// m_k = sum_t t_k p[t] (Alg 11) in fp64.  Per vector the outer digits are constant,
-// so with s = sum_e p_e:  acc_k += u_k * s (outer digits) and the vector digit contributes
-// (first row/col) * s plus the small in-vector weights.  Per-lane accumulators, then a
-// fixed-order warp butterfly, fixed-order cross-warp sum, one partial per block, and the last
-// block (ticket) sums the partials in a fixed order: deterministic run to run ("each thread
-// computes its own pre-result and these pre-results are amalgamated").
+// m_k = sum_t t_k p[t] (Alg 11) in fp64.  p is the counter tensor itself (dense,
+// never merged), so vector v starts at element v*V: the loads need no odometer.  Two kernels:
+// ev_tma_kernel (the fast path: p streamed by TMA bulk copies into a ring of shared-memory
+// stages, one persistent block per SM) and ev_kernel (batched 32-byte loads; any alignment or
+// vector width).  The digits (the weights t_k) advance with the Alg 3 odometer as vectors are
+// consumed.  Per
+// vector the outer digits are constant, so with s = sum_e p_e:  acc_k += u_k * s, and the
+// vector digit contributes (first row/col) * s plus the in-vector weights.  Per-lane fp64
+// accumulators, then a fixed-order warp butterfly, a fixed-order cross-warp sum, one partial per
+// block, and the last block (ticket) sums the partials in a fixed order: deterministic run to
+// run ("each thread computes its own pre-result and these pre-results are amalgamated").
 
-template <int D, int ESZ, int V, typename IDX, int K>
-__global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc<IDX> d) {
+template <int D, typename IDX>
+__device__ __forceinline__ void digits_step(const Desc<IDX>& d, IDX (&u)[D]) {
+  bool carry = false;
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) {
+    if (k > d.khi) continue;
+    IDX nu = u[k] + d.dlt[k] + (carry ? IDX(1) : IDX(0));
+    carry = nu >= d.ext[k];
+    if (carry) nu -= d.ext[k];
+    u[k] = nu;
+    if (k <= d.klo && !carry) break;
+  }
+}
+
+template <int ESZ, int V, typename IDX>
+__device__ __forceinline__ void ev_load(const TensorAcc<IDX>& t, IDX v, uint32_t* w) {
   constexpr int EW = ESZ / 4;
-  constexpr int NW = V * EW;
-  constexpr int NS = D + 1;  // weight slots (D digits + the column slot of a collapsed vector)
+  const IDX off = v * (IDX)V;
+  if (V > 1 && t.vec) {
+    Mem<V * ESZ>::ld(addr<ESZ>(t.ptr, off), w);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) Mem<ESZ>::ld(addr<ESZ>(t.ptr, off + (IDX)e), w + e * EW);
+  }
+}
+
+template <int D, typename IDX>
+__device__ __forceinline__ void ev_decode(const Desc<IDX>& d, IDX v, IDX (&u)[D]) {
+#pragma unroll
+  for (int k = D - 1; k >= 1; --k) {
+    IDX q = divq<IDX>(v, d.ext[k], d.fdm[k], d.fds[k]);
+    u[k] = v - q * d.ext[k];
+    v = q;
+  }
+  u[0] = v;
+}
+
+// One vector's contribution: s = sum_e p_e; acc_k += u_k * s for the outer digits; the vector
+// digit adds (first row or column) * s plus the in-vector row/column weights.
+template <int D, int ESZ, int V, typename IDX>
+__device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const IDX (&u)[D],
+                                              const uint32_t* w, double (&acc)[D + 1]) {
+  constexpr int EW = ESZ / 4;
+  const uint32_t lgL = d.lgL;
+  double x[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) x[e] = (double)Elem<ESZ>::get(w + e * EW);
+  double sum = x[0];
+#pragma unroll
+  for (int e = 1; e < V; ++e) sum += x[e];
+  double wr = 0.0, wc = 0.0;
+#pragma unroll
+  for (int e = 1; e < V; ++e) {
+    wr = fma((double)((uint32_t)e >> lgL), x[e], wr);
+    wc = fma((double)((uint32_t)e & ((1u << lgL) - 1u)), x[e], wc);
+  }
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) acc[k] = fma((double)u[k], sum, acc[k]);
+  const bool coll = d.collapsed != 0;
+  acc[D - 1] += fma((double)(u[D - 1] * (d.rowmul + d.colmul)), sum, coll ? wr : wc);
+  if (coll) acc[D] += wc;
+}
+
+// Fixed-order block reduction, one partial per block, ordered final sum by the last block.
+template <int NS, typename IDX>
+__device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS]) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
-  const IDX base0 = warp * d.wmul;
-  double acc[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-  const uint32_t lgL = d.lgL;
-  if (base0 < d.nvec) {
-    const IDX vend = warp_end(d, base0);
-    IDX u[D], off[1];
-    uint32_t oob;
-    IDX v = base0 + (IDX)lane;
-    odo_start<D, 1, false, IDX>(d, v, u, off, oob);
-    const IDX vmul = d.rowmul + d.colmul;  // exactly one of them is nonzero
-    const bool coll = d.collapsed != 0;
-    for (IDX b = base0; b < vend; b += K * d.dv) {
-      uint32_t buf[K][NW];
-      bool valid[K];
-      IDX uu[K][D];
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        valid[j] = v < vend;
-        v += d.dv;
-        if (valid[j]) load_vec<ESZ, V, IDX>(d.t[0], off[0], lgL, buf[j]);
-#pragma unroll
-        for (int k = 0; k < D; ++k) uu[j][k] = u[k];
-        odo_step<D, 1, false, IDX>(d, u, off, oob);
-      }
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        if (!valid[j]) continue;
-        double x[V];
-#pragma unroll
-        for (int e = 0; e < V; ++e) x[e] = (double)Elem<ESZ>::get(buf[j] + e * EW);
-        double sum = x[0];
-#pragma unroll
-        for (int e = 1; e < V; ++e) sum += x[e];
-        double wr = 0.0, wc = 0.0;
-#pragma unroll
-        for (int e = 1; e < V; ++e) {
-          wr = fma((double)((uint32_t)e >> lgL), x[e], wr);
-          wc = fma((double)((uint32_t)e & ((1u << lgL) - 1u)), x[e], wc);
-        }
-#pragma unroll
-        for (int k = 0; k < D - 1; ++k) acc[k] = fma((double)uu[j][k], sum, acc[k]);
-        acc[D - 1] += fma((double)(uu[j][D - 1] * vmul), sum, coll ? wr : wc);
-        if (coll) acc[D] += wc;
-      }
-    }
-  }
-  // ---- deterministic reduction
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
 #pragma unroll
@@ -415,8 +431,8 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
 #pragma unroll
     for (int w = 0; w < kBlock / 32; ++w) t += sm[w][threadIdx.x];
     part[(size_t)blockIdx.x * NS + threadIdx.x] = t;
+    __threadfence();
   }
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
@@ -440,19 +456,162 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
     for (int k = 0; k < NS; ++k) sm[wib][k] = f[k];
   }
   __syncthreads();
-  __shared__ double tot[NS];
-  if (threadIdx.x < NS) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kBlock / 32; ++w) t += sm[w][threadIdx.x];
-    tot[threadIdx.x] = t;
-  }
-  __syncthreads();
   if (threadIdx.x < (unsigned)d.d_out) {
     const int sl = d.slot_of_axis[threadIdx.x];
-    ((double*)d.out)[threadIdx.x] = sl >= 0 ? tot[sl] : 0.0;
+    double t = 0.0;
+    if (sl >= 0) {
+      for (int w = 0; w < kBlock / 32; ++w) t += sm[w][sl];
+    }
+    ((double*)d.out)[threadIdx.x] = t;
   }
   if (threadIdx.x == 0) *ticket = 0u;  // leave the workspace ready for the next call
+}
+
+template <int D, int ESZ, int V, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  constexpr int NS = D + 1;  // weight slots (D digits + the column slot of a collapsed vector)
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
+  const IDX base0 = warp * d.wmul;
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+  if (base0 < d.nvec) {
+    const IDX vend = warp_end(d, base0);
+    const IDX dv = d.dv;
+    IDX v = base0 + (IDX)lane;
+    IDX u[D];
+    ev_decode<D, IDX>(d, v, u);
+    for (IDX b = base0; b < vend; b += (IDX)K * dv) {
+      uint32_t buf[K][NW];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (v + (IDX)j * dv < vend) ev_load<ESZ, V, IDX>(d.t[0], v + (IDX)j * dv, buf[j]);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (v < vend) ev_accumulate<D, ESZ, V, IDX>(d, u, buf[j], acc);
+        digits_step<D, IDX>(d, u);
+        v += dv;
+      }
+    }
+  }
+  ev_reduce<NS, IDX>(d, acc);
+}
+
+// ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// EV fast path.  Block b owns vectors [b*wmul, min((b+1)*wmul, W)) of the dense p; thread 0
+// keeps NSTAGE bulk copies of SVEC 32-byte vectors in flight (the "full" mbarriers complete on
+// the transferred bytes), all threads consume a stage from shared memory (thread t takes
+// vectors t, t+256, ...: the odometer steps +256 vectors) and each warp releases the stage on
+// its "empty" mbarrier before thread 0 refills it.  Requires V*ESZ == 32 and a 32-B aligned p.
+template <int D, int ESZ, typename IDX>
+__global__ void __launch_bounds__(kBlock, 1) ev_tma_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int V = 32 / ESZ;
+  constexpr int NS = D + 1;
+  constexpr int NSTAGE = TRIOT_EV_NSTAGE;
+  constexpr int SVEC = TRIOT_EV_SVEC;
+  constexpr int PER_THREAD = SVEC / kBlock;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)(smem + (size_t)NSTAGE * SVEC * 32);
+  uint64_t* empty = full + NSTAGE;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const IDX vb = (IDX)blockIdx.x * d.wmul;
+  IDX ve = vb + d.wmul;
+  if (ve > d.nvec || ve < vb) ve = d.nvec;
+  const IDX nst = vb < ve ? (ve - vb + SVEC - 1) / SVEC : 0;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBlock / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const char* pbase = (const char*)d.t[0].ptr;
+  if (tid == 0) {
+    for (IDX i = 0; i < nst && i < (IDX)NSTAGE; ++i) {
+      const IDX v0 = vb + i * SVEC;
+      const IDX nv = (ve - v0) < (IDX)SVEC ? (ve - v0) : (IDX)SVEC;
+      mbar_expect_tx(&full[i], (uint32_t)nv * 32u);
+      bulk_g2s(smem + (size_t)i * SVEC * 32, pbase + (uint64_t)v0 * 32, (uint32_t)nv * 32u,
+               &full[i]);
+    }
+  }
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+  IDX u[D];
+  ev_decode<D, IDX>(d, vb + (IDX)tid, u);
+  for (IDX i = 0; i < nst; ++i) {
+    const int slot = (int)(i % NSTAGE);
+    const uint32_t par = (uint32_t)((i / NSTAGE) & 1);
+    mbar_wait(&full[slot], par);
+    const unsigned char* st = smem + (size_t)slot * SVEC * 32;
+    const IDX v0 = vb + i * SVEC;
+#pragma unroll
+    for (int j = 0; j < PER_THREAD; ++j) {
+      const int q = tid + j * kBlock;
+      if (v0 + (IDX)q < ve) {
+        uint32_t w[8];
+        const uint4 lo = *(const uint4*)(st + q * 32);
+        const uint4 hi = *(const uint4*)(st + q * 32 + 16);
+        w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+        w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+        ev_accumulate<D, ESZ, V, IDX>(d, u, w, acc);
+      }
+      digits_step<D, IDX>(d, u);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (tid == 0 && i + NSTAGE < nst) {
+      mbar_wait(&empty[slot], par);
+      const IDX vn = vb + (i + NSTAGE) * SVEC;
+      const IDX nv = (ve - vn) < (IDX)SVEC ? (ve - vn) : (IDX)SVEC;
+      mbar_expect_tx(&full[slot], (uint32_t)nv * 32u);
+      bulk_g2s(smem + (size_t)slot * SVEC * 32, pbase + (uint64_t)vn * 32, (uint32_t)nv * 32u,
+               &full[slot]);
+    }
+  }
+  ev_reduce<NS, IDX>(d, acc);
 }
 
 }  // namespace triot

@@ -319,7 +319,15 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
 
 void set_decomposition(Geom& g, int mode, uint64_t warps) {
   if (warps < 1) warps = 1;
-  if (mode == 1) {
+  if (mode == 2) {
+    // block chunks for the EV bulk-copy kernel: `warps` counts blocks here; each block owns a
+    // multiple of SVEC vectors and its threads step by one block (TRIOT_BLOCK vectors)
+    g.mode = 2;
+    uint64_t per = (g.nvec + warps - 1) / warps;
+    per = (per + TRIOT_EV_SVEC - 1) / TRIOT_EV_SVEC * TRIOT_EV_SVEC;
+    g.wmul = g.wspan = per;
+    g.dv = TRIOT_BLOCK;
+  } else if (mode == 1) {
     g.mode = 1;
     g.wmul = 32;
     g.wspan = g.nvec;

@@ -38,7 +38,7 @@ struct Geom {
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
   uint64_t nvec = 0, nsteps = 0;
   uint64_t wmul = 32, wspan = 32, dv = 32;   // decomposition (set_decomposition)
-  int mode = 0;                              // 0 = chunk, 1 = stride
+  int mode = 0;                              // 0 = chunk, 1 = stride, 2 = block chunk
   int khi = 0, klo = 0;
   uint64_t rowmul = 0, colmul = 0, vfull = 0, vany = 0, srows = 0, scols = 0;
   int slot_of_axis[TRIOT_MAXD] = {};
@@ -60,7 +60,8 @@ int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const i
                 int dtype, int op);
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype);
 
-// Work decomposition over `warps` warps: mode 0 = contiguous chunk per warp, 1 = grid stride.
+// Work decomposition over `warps` warps: mode 0 = contiguous chunk per warp, 1 = grid stride,
+// 2 = contiguous chunk per block (EV bulk-copy kernel; `warps` is then the number of blocks).
 // Sets wmul/wspan/dv and the mixed-radix digits of the per-step advance (dlt, khi, klo, step).
 void set_decomposition(Geom& g, int mode, uint64_t warps);
 

@@ -67,13 +67,18 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
         return W(off + r * T[x]["rho"] + c * T[x]["tau"])
 
     wmul, wspan, dv = desc["wmul"], desc["wspan"], desc["dv"]
-    nwarps = (nvec + wmul - 1) // wmul if desc["mode"] == 0 else dv // 32
-    for w in range(nwarps):
+    # mode 0: warp chunks; 1: grid stride; 2: block chunks, thread t starts at vector t
+    if desc["mode"] == 2:
+        units, lanes = (nvec + wmul - 1) // wmul, dv
+    else:
+        units = (nvec + wmul - 1) // wmul if desc["mode"] == 0 else dv // 32
+        lanes = 32
+    for w in range(units):
         base0 = w * wmul
         if base0 >= nvec:
             continue
         vend = min(base0 + wspan, nvec)
-        for lane in range(32):
+        for lane in range(lanes):
             v = base0 + lane
             u, off, oob = start(v)
             while v < vend:

@@ -62,6 +62,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--bpsm", default="0,1,2,3,4,6,8,12,16")
+    ap.add_argument("--modes", default="0,1")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -69,7 +70,7 @@ def main():
     for name in a.only.split(","):
         fn = op_fn(name, dev)
         nb = algorithmic_bytes(name)
-        for mode in (0, 1):
+        for mode in [int(x) for x in a.modes.split(",")]:
             for bpsm in [int(x) for x in a.bpsm.split(",")]:
                 T.triot_set_launch_policy(mode, bpsm)
                 single, b2b = timeit(fn, scrub)
