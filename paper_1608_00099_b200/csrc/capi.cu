@@ -177,7 +177,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
     d.out = out;
     d.ws = ws;
     void* args[1] = {&d};
-    cudaError_t e2 = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(TRIOT_BLOCK), args,
+    cudaError_t e2 = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(TRIOT_EV_TMA_BLOCK), args,
                                       TRIOT_EV_SMEM, (cudaStream_t)stream);
     if (e2 != cudaSuccess) return cuda_fail(e2, "cudaLaunchKernel");
     return TRIOT_OK;

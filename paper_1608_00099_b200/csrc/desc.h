@@ -71,8 +71,9 @@ struct Desc {
 #define TRIOT_EV_MAX_GRID 2048
 #define TRIOT_EV_WS_HEADER 256
 // EV bulk-copy pipeline: NSTAGE shared-memory stages of SVEC 32-byte vectors per block
-#define TRIOT_EV_NSTAGE 8
-#define TRIOT_EV_SVEC 512
+#define TRIOT_EV_NSTAGE 6
+#define TRIOT_EV_SVEC 1024
+#define TRIOT_EV_TMA_BLOCK 512
 #define TRIOT_EV_SMEM (TRIOT_EV_NSTAGE * TRIOT_EV_SVEC * 32 + 2 * TRIOT_EV_NSTAGE * 8)
 
 }  // namespace triot

@@ -344,16 +344,43 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
 // block, and the last block (ticket) sums the partials in a fixed order: deterministic run to
 // run ("each thread computes its own pre-result and these pre-results are amalgamated").
 
+// ---- expected-value accumulation with deferred weights
+// For one lane, sum_v u_k(v) s(v) (s = mass of vector v) telescopes to
+//     u_k(final) * S  -  sum over changes of digit k of (new - old) * S_at_change
+// where S is the running mass.  So per vector only S += s (plus the in-vector weights) is
+// computed, and digit k costs one FMA when it changes -- which the odometer makes amortised
+// O(1) per step, the same argument as Alg 3's.  Exact for integer-valued inputs; for
+// real inputs the extra rounding is a few ulps of sum |t_k p| (DESIGN.md §EV numerics).
+template <int D>
+struct EvAcc {
+  double S;        // running mass
+  double Wr, Wc;   // in-vector row / column weighted mass
+  double ev[D];    // -sum (delta u_k) * S_at_change
+};
+
 template <int D, typename IDX>
-__device__ __forceinline__ void digits_step(const Desc<IDX>& d, IDX (&u)[D]) {
+__device__ __forceinline__ void ev_acc_init(EvAcc<D>& a) {
+  a.S = a.Wr = a.Wc = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) a.ev[k] = 0.0;
+}
+
+// The odometer on digits only (no tensor offsets), recording weight events.
+template <int D, typename IDX>
+__device__ __forceinline__ void digits_step_ev(const Desc<IDX>& d, IDX (&u)[D], EvAcc<D>& a) {
   bool carry = false;
 #pragma unroll
   for (int k = D - 1; k >= 0; --k) {
     if (k > d.khi) continue;
-    IDX nu = u[k] + d.dlt[k] + (carry ? IDX(1) : IDX(0));
+    const IDX old = u[k];
+    IDX nu = old + d.dlt[k] + (carry ? IDX(1) : IDX(0));
     carry = nu >= d.ext[k];
     if (carry) nu -= d.ext[k];
     u[k] = nu;
+    if (nu != old) {
+      const double delta = (double)nu - (double)old;
+      a.ev[k] = fma(-delta, a.S, a.ev[k]);
+    }
     if (k <= d.klo && !carry) break;
   }
 }
@@ -381,11 +408,11 @@ __device__ __forceinline__ void ev_decode(const Desc<IDX>& d, IDX v, IDX (&u)[D]
   u[0] = v;
 }
 
-// One vector's contribution: s = sum_e p_e; acc_k += u_k * s for the outer digits; the vector
-// digit adds (first row or column) * s plus the in-vector row/column weights.
+// One vector: S += sum_e p_e; the in-vector row (e >> lgL) and column (e & (L-1)) weights
+// accumulate into Wr / Wc.  lgL is a runtime value but e is unrolled.
 template <int D, int ESZ, int V, typename IDX>
-__device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const IDX (&u)[D],
-                                              const uint32_t* w, double (&acc)[D + 1]) {
+__device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const uint32_t* w,
+                                              EvAcc<D>& a) {
   constexpr int EW = ESZ / 4;
   const uint32_t lgL = d.lgL;
   double x[V];
@@ -394,21 +421,35 @@ __device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const IDX (&u)
   double sum = x[0];
 #pragma unroll
   for (int e = 1; e < V; ++e) sum += x[e];
-  double wr = 0.0, wc = 0.0;
+  a.S += sum;
+  if (V > 1) {
+    double wr = 0.0, wc = 0.0;
 #pragma unroll
-  for (int e = 1; e < V; ++e) {
-    wr = fma((double)((uint32_t)e >> lgL), x[e], wr);
-    wc = fma((double)((uint32_t)e & ((1u << lgL) - 1u)), x[e], wc);
+    for (int e = 1; e < V; ++e) {
+      const uint32_t r = (uint32_t)e >> lgL, c = (uint32_t)e & ((1u << lgL) - 1u);
+      if (r) wr = fma((double)r, x[e], wr);
+      if (c) wc = fma((double)c, x[e], wc);
+    }
+    a.Wr += wr;
+    a.Wc += wc;
   }
+}
+
+// Weight slots of one lane at the end: slot k < D-1 -> u_k S + ev_k; slot D-1 (the vector digit)
+// -> vmul (u S + ev) + (Wr if collapsed else Wc); slot D (collapsed column) -> Wc.
+template <int D, typename IDX>
+__device__ __forceinline__ void ev_finish(const Desc<IDX>& d, const IDX (&u)[D],
+                                          const EvAcc<D>& a, double (&acc)[D + 1]) {
 #pragma unroll
-  for (int k = 0; k < D - 1; ++k) acc[k] = fma((double)u[k], sum, acc[k]);
+  for (int k = 0; k < D - 1; ++k) acc[k] = fma((double)u[k], a.S, a.ev[k]);
+  const double vmul = (double)(d.rowmul + d.colmul);
   const bool coll = d.collapsed != 0;
-  acc[D - 1] += fma((double)(u[D - 1] * (d.rowmul + d.colmul)), sum, coll ? wr : wc);
-  if (coll) acc[D] += wc;
+  acc[D - 1] = fma(vmul, fma((double)u[D - 1], a.S, a.ev[D - 1]), coll ? a.Wr : a.Wc);
+  acc[D] = coll ? a.Wc : 0.0;
 }
 
 // Fixed-order block reduction, one partial per block, ordered final sum by the last block.
-template <int NS, typename IDX>
+template <int NS, int BLOCK, typename IDX>
 __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS]) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -417,7 +458,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
   }
-  __shared__ double sm[kBlock / 32][NS];
+  __shared__ double sm[BLOCK / 32][NS];
   __shared__ int is_last;
   if (lane == 0) {
 #pragma unroll
@@ -429,7 +470,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
   if (threadIdx.x < NS) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < kBlock / 32; ++w) t += sm[w][threadIdx.x];
+    for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
     part[(size_t)blockIdx.x * NS + threadIdx.x] = t;
     __threadfence();
   }
@@ -441,7 +482,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
   double f[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) f[k] = 0.0;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += kBlock) {
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += BLOCK) {
 #pragma unroll
     for (int k = 0; k < NS; ++k) f[k] += __ldcg(part + (size_t)b * NS + k);
   }
@@ -460,7 +501,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
     const int sl = d.slot_of_axis[threadIdx.x];
     double t = 0.0;
     if (sl >= 0) {
-      for (int w = 0; w < kBlock / 32; ++w) t += sm[w][sl];
+      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][sl];
     }
     ((double*)d.out)[threadIdx.x] = t;
   }
@@ -485,6 +526,8 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
     IDX v = base0 + (IDX)lane;
     IDX u[D];
     ev_decode<D, IDX>(d, v, u);
+    EvAcc<D> a;
+    ev_acc_init<D, IDX>(a);
     for (IDX b = base0; b < vend; b += (IDX)K * dv) {
       uint32_t buf[K][NW];
 #pragma unroll
@@ -492,13 +535,14 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
         if (v + (IDX)j * dv < vend) ev_load<ESZ, V, IDX>(d.t[0], v + (IDX)j * dv, buf[j]);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        if (v < vend) ev_accumulate<D, ESZ, V, IDX>(d, u, buf[j], acc);
-        digits_step<D, IDX>(d, u);
+        if (v < vend) ev_accumulate<D, ESZ, V, IDX>(d, buf[j], a);
+        digits_step_ev<D, IDX>(d, u, a);
         v += dv;
       }
     }
+    ev_finish<D, IDX>(d, u, a, acc);
   }
-  ev_reduce<NS, IDX>(d, acc);
+  ev_reduce<NS, kBlock, IDX>(d, acc);
 }
 
 // ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
@@ -542,13 +586,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // the transferred bytes), all threads consume a stage from shared memory (thread t takes
 // vectors t, t+256, ...: the odometer steps +256 vectors) and each warp releases the stage on
 // its "empty" mbarrier before thread 0 refills it.  Requires V*ESZ == 32 and a 32-B aligned p.
+// Threads take vectors t, t+BLOCK, ...: the odometer steps +BLOCK vectors.
 template <int D, int ESZ, typename IDX>
-__global__ void __launch_bounds__(kBlock, 1) ev_tma_kernel(const __grid_constant__ Desc<IDX> d) {
+__global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
+    ev_tma_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int V = 32 / ESZ;
   constexpr int NS = D + 1;
   constexpr int NSTAGE = TRIOT_EV_NSTAGE;
   constexpr int SVEC = TRIOT_EV_SVEC;
-  constexpr int PER_THREAD = SVEC / kBlock;
+  constexpr int BLOCK = TRIOT_EV_TMA_BLOCK;
+  constexpr int PER_THREAD = SVEC / BLOCK;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)(smem + (size_t)NSTAGE * SVEC * 32);
   uint64_t* empty = full + NSTAGE;
@@ -561,7 +608,7 @@ __global__ void __launch_bounds__(kBlock, 1) ev_tma_kernel(const __grid_constant
 #pragma unroll
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBlock / 32);
+      mbar_init(&empty[s], BLOCK / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -576,11 +623,10 @@ __global__ void __launch_bounds__(kBlock, 1) ev_tma_kernel(const __grid_constant
                &full[i]);
     }
   }
-  double acc[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
   IDX u[D];
   ev_decode<D, IDX>(d, vb + (IDX)tid, u);
+  EvAcc<D> a;
+  ev_acc_init<D, IDX>(a);
   for (IDX i = 0; i < nst; ++i) {
     const int slot = (int)(i % NSTAGE);
     const uint32_t par = (uint32_t)((i / NSTAGE) & 1);
@@ -589,16 +635,16 @@ __global__ void __launch_bounds__(kBlock, 1) ev_tma_kernel(const __grid_constant
     const IDX v0 = vb + i * SVEC;
 #pragma unroll
     for (int j = 0; j < PER_THREAD; ++j) {
-      const int q = tid + j * kBlock;
+      const int q = tid + j * BLOCK;
       if (v0 + (IDX)q < ve) {
         uint32_t w[8];
         const uint4 lo = *(const uint4*)(st + q * 32);
         const uint4 hi = *(const uint4*)(st + q * 32 + 16);
         w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
         w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
-        ev_accumulate<D, ESZ, V, IDX>(d, u, w, acc);
+        ev_accumulate<D, ESZ, V, IDX>(d, w, a);
       }
-      digits_step<D, IDX>(d, u);
+      digits_step_ev<D, IDX>(d, u, a);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -611,7 +657,9 @@ __global__ void __launch_bounds__(kBlock, 1) ev_tma_kernel(const __grid_constant
                &full[slot]);
     }
   }
-  ev_reduce<NS, IDX>(d, acc);
+  double acc[NS];
+  ev_finish<D, IDX>(d, u, a, acc);
+  ev_reduce<NS, BLOCK, IDX>(d, acc);
 }
 
 }  // namespace triot

@@ -326,7 +326,7 @@ void set_decomposition(Geom& g, int mode, uint64_t warps) {
     uint64_t per = (g.nvec + warps - 1) / warps;
     per = (per + TRIOT_EV_SVEC - 1) / TRIOT_EV_SVEC * TRIOT_EV_SVEC;
     g.wmul = g.wspan = per;
-    g.dv = TRIOT_BLOCK;
+    g.dv = TRIOT_EV_TMA_BLOCK;
   } else if (mode == 1) {
     g.mode = 1;
     g.wmul = 32;

@@ -63,10 +63,34 @@ def main():
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--bpsm", default="0,1,2,3,4,6,8,12,16")
     ap.add_argument("--modes", default="0,1")
+    ap.add_argument("--membench", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    scrub = lambda: scratch.fill_(1)
+    clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
+
+    def scrub():
+        # evict everything and leave the L2 clean: write a buffer, then read another one (the
+        # read forces the write-back of every dirty line before the timed launch)
+        scratch.fill_(1)
+        clean.sum()
+    if a.membench:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import membench
+        L = membench.build()
+        src = torch.ones(134217728 // 4, dtype=torch.float32, device=dev)
+        sink = torch.zeros(4, dtype=torch.int32, device=dev)
+        s = torch.cuda.current_stream().cuda_stream
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        for bpsm in (2, 4, 8, 16):
+            for u in (4, 8):
+                single, b2b = timeit(lambda: L.mb_read(src.data_ptr(), 134217728, sms * bpsm, 256,
+                                                       u, sink.data_ptr(), s), scrub)
+                print(json.dumps({"config": "read134MB", "mode": -1, "bpsm": bpsm, "U": u,
+                                  "single_us": round(single * 1000, 2),
+                                  "b2b_us": round(b2b * 1000, 2),
+                                  "single_gbs": round(134217728 / single / 1e6, 1),
+                                  "b2b_gbs": round(134217728 / b2b / 1e6, 1)}), flush=True)
     for name in a.only.split(","):
         fn = op_fn(name, dev)
         nb = algorithmic_bytes(name)
