@@ -324,7 +324,6 @@ void set_decomposition(Geom& g, int mode, uint64_t warps) {
     // multiple of SVEC vectors and its threads step by one block (TRIOT_BLOCK vectors)
     g.mode = 2;
     uint64_t per = (g.nvec + warps - 1) / warps;
-    per = (per + TRIOT_EV_SVEC - 1) / TRIOT_EV_SVEC * TRIOT_EV_SVEC;
     g.wmul = g.wspan = per;
     g.dv = TRIOT_EV_TMA_BLOCK;
   } else if (mode == 1) {
