@@ -245,6 +245,29 @@ def run_ours(args, rank, world, local_rank):
     except Exception as exc:  # graph capture unavailable: report the host-bound number only
         c1_graph_us = f"unavailable: {exc}"
 
+    # ---- each op alone after a clean L2 scrub (write a 512 MB buffer, then read another so
+    # every dirty line is written back before the timed launch): median of 5 single launches
+    iso = {}
+    if not args.no_isolated:
+        scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
+        fns = {"C2": lambda: T.embed(g["dst2"], g["src2"]),
+               "C3": lambda: T.expected_value(g["p3"], out=g["m3"]),
+               "C4": lambda: T.apply_binary(g["a4"], g["b4"], "mul", out=g["c4"]),
+               "C5": lambda: T.embed(g["dst5"], g["src5"])}
+        for n, fn in fns.items():
+            ts = []
+            for _ in range(5):
+                scratch.fill_(1)
+                clean.sum()
+                ea.record(stream)
+                fn()
+                eb.record(stream)
+                torch.cuda.synchronize(dev)
+                ts.append(ea.elapsed_time(eb))
+            iso[n] = statistics.median(ts)
+        del scratch, clean
+
     # ---- e2e: same step through the public API with pinned HOST buffers; every step copies
     # its inputs H2D and reads its results back D2H inside the timed region
     e2e = run_e2e(args, host, dev, stream, T, world)
@@ -262,6 +285,13 @@ def run_ours(args, rank, world, local_rank):
                        "bytes": b, "us": round(per_op_ms[n] * 1000, 2), "gbs": round(gbs, 1),
                        "pct_of_8000": round(100 * gbs / NOMINAL_HBM_GBS, 1),
                        "pct_of_measured": round(100 * gbs / peak, 1)})
+    per_op_iso = []
+    for n, ms in iso.items():
+        b = algorithmic_bytes(n)
+        gbs = b / (ms * 1e-3) / 1e9
+        per_op_iso.append({"config": n, "us": round(ms * 1000, 2), "gbs": round(gbs, 1),
+                           "pct_of_8000": round(100 * gbs / NOMINAL_HBM_GBS, 1),
+                           "pct_of_measured": round(100 * gbs / peak, 1)})
     dom = max(per_op, key=lambda r: r["us"])
     traffic = None
     try:
@@ -286,6 +316,8 @@ def run_ours(args, rank, world, local_rank):
                          "by its predecessor",
                    "parallelism": f"replicas x{world} (weak; no data-path collective)"},
         "per_op": per_op,
+        "per_op_isolated": {"note": "each op alone after a clean L2 scrub, median of 5",
+                            "ops": per_op_iso},
         "c1_latency_us": {"per_call_host_bound": round(c1_us, 2),
                           "per_op_in_cuda_graph": (round(c1_graph_us, 3)
                                                    if isinstance(c1_graph_us, float)
@@ -468,6 +500,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-isolated", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -73,13 +73,13 @@ struct Policy {
 thread_local Policy g_override = {-1, 0, 0};
 
 // Tuned on B200 (tools/tune.py): short contiguous chunks per warp
-// (8 steps = 8 KB of a dense 32-B-vector tensor) and as many blocks as that takes, so the
-// hardware block scheduler hands out consecutive chunks as SMs free up -- the active window of
-// the tensors stays compact and every SM stays busy to the end.  1 wave at occupancy (the
-// earlier default) reached 5.0-5.8 TB/s; this reaches 6.1-6.7 TB/s on C2/C4/C5.
+// (>= 4 steps of 32 vectors) in a grid of up to 64 blocks per SM -- many waves, so the hardware
+// block scheduler hands out consecutive chunks as SMs free up: the active window of the tensors
+// stays compact and every SM stays busy to the end.  One wave at occupancy (the first version)
+// reached 5.0-5.9 TB/s on C2/C4/C5; this reaches 6.5-6.8 TB/s (single launch, clean L2).
 Policy auto_policy(const Geom& g) {
   if (g.op == OP_EV) return Policy{0, 0, 0};
-  return Policy{0, 0, 8};
+  return Policy{0, 64, 0};
 }
 
 int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
