@@ -160,6 +160,16 @@ TRIOT_API int triot_expected_value_workspace_size(const int64_t* shape, int d, i
 TRIOT_API int triot_expected_value(double* means, const void* p, const int64_t* shape, int d, int dtype,
                          void* workspace, size_t workspace_bytes, void* cuda_stream);
 
+/*
+ * triot_expected_value_mass -- as triot_expected_value, and additionally out[d] = sum_t p[t]
+ * (fp64): out must hold d + 1 doubles.  The mass is the term that amalgamates slab-sharded
+ * pre-results: a rank holding axis-0 rows [o, o + n) of a larger p adds o * out[d] to
+ * its out[0] before the cross-rank sum (paper_1608_00099_b200/parallel.py).
+ */
+TRIOT_API int triot_expected_value_mass(double* out, const void* p, const int64_t* shape, int d,
+                                        int dtype, void* workspace, size_t workspace_bytes,
+                                        void* cuda_stream);
+
 /* ---- diagnostics (host only; no device work, usable without a GPU) ---------------------- */
 
 /*

@@ -17,7 +17,8 @@ from __future__ import annotations
 from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED_FULL,
                    TRIOT_EMBED_REGION_ONLY, TRIOT_F32, TRIOT_F64, TRIOT_MUL, TRIOT_SUB,
                    TriotError, check, lib, triot_apply_binary, triot_embed,
-                   triot_expected_value, triot_expected_value_workspace_size,
+                   triot_expected_value, triot_expected_value_mass,
+                   triot_expected_value_workspace_size,
                    triot_fastdiv_magic, triot_last_error, triot_max_dimension,
                    triot_plan_describe, triot_set_launch_policy, triot_status_string,
                    LIB_PATH)
@@ -25,7 +26,7 @@ from .api import apply_binary, embed, expected_value, OPS
 
 __all__ = [
     "embed", "apply_binary", "expected_value", "OPS", "TriotError",
-    "triot_embed", "triot_apply_binary", "triot_expected_value",
+    "triot_embed", "triot_apply_binary", "triot_expected_value", "triot_expected_value_mass",
     "triot_expected_value_workspace_size", "triot_max_dimension", "triot_status_string",
     "triot_last_error", "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic",
     "LIB_PATH",

@@ -27,6 +27,7 @@ STATUS = {
 }
 EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "triot_embed",
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
+           "triot_expected_value_mass",
            "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
@@ -64,6 +65,8 @@ _lib.triot_expected_value_workspace_size.argtypes = [_i64p, ctypes.c_int, ctypes
 _lib.triot_expected_value.restype = ctypes.c_int
 _lib.triot_expected_value.argtypes = [_vp, _vp, _i64p, ctypes.c_int, ctypes.c_int, _vp,
                                       ctypes.c_size_t, _vp]
+_lib.triot_expected_value_mass.restype = ctypes.c_int
+_lib.triot_expected_value_mass.argtypes = _lib.triot_expected_value.argtypes
 _lib.triot_plan_describe.restype = ctypes.c_int
 _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
@@ -128,6 +131,12 @@ def triot_expected_value(means: int, p: int, shape, d: int, dtype: int, workspac
                          workspace_bytes: int, stream: int) -> int:
     return _lib.triot_expected_value(means, p, _shape(shape), d, dtype, workspace,
                                      workspace_bytes, stream)
+
+
+def triot_expected_value_mass(out: int, p: int, shape, d: int, dtype: int, workspace: int,
+                              workspace_bytes: int, stream: int) -> int:
+    return _lib.triot_expected_value_mass(out, p, _shape(shape), d, dtype, workspace,
+                                          workspace_bytes, stream)
 
 
 def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:

@@ -89,16 +89,21 @@ def workspace(p_shape, dtype_code: int, device):
     return ws
 
 
-def expected_value(p, out=None):
-    """means[k] = sum_t t_k * p[t] (fp64), k = 0..d-1.  Returns a (d,) float64 CUDA tensor."""
+def expected_value(p, out=None, with_mass: bool = False):
+    """means[k] = sum_t t_k * p[t] (fp64), k = 0..d-1.  Returns a (d,) float64 CUDA tensor, or
+    (d+1,) with out[d] = sum_t p[t] when with_mass (triot_expected_value_mass)."""
     torch = _torch()
     _check_tensor("p", p)
     code = _dtype_code(p)
     d = p.dim()
+    n = d + (1 if with_mass else 0)
     if out is None:
-        out = torch.empty(d, dtype=torch.float64, device=p.device)
+        out = torch.empty(n, dtype=torch.float64, device=p.device)
     _check_tensor("out", out, p.device)
+    if out.dtype != torch.float64 or out.numel() < n:
+        raise ValueError(f"out must be a float64 tensor of >= {n} elements")
     ws = workspace(tuple(p.shape), code, p.device)
-    _lib.check(_lib.triot_expected_value(out.data_ptr(), p.data_ptr(), tuple(p.shape), d, code,
-                                         ws.data_ptr(), ws.numel(), _stream(p.device)))
+    fn = _lib.triot_expected_value_mass if with_mass else _lib.triot_expected_value
+    _lib.check(fn(out.data_ptr(), p.data_ptr(), tuple(p.shape), d, code, ws.data_ptr(),
+                  ws.numel(), _stream(p.device)))
     return out

@@ -173,7 +173,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   if (blocks < 1) blocks = 1;
   set_decomposition(g, 2, blocks);
   uint64_t grid = (g.nvec + g.wmul - 1) / g.wmul;
-  size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 1) * sizeof(double);
+  size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 2) * sizeof(double);
   if (!ws || ws_bytes < need_ws)
     return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                      need_ws);
@@ -208,7 +208,7 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   int st = launch_geometry(fn, g, max_grid, &grid);
   if (st) return st;
   if (g.op == OP_EV) {
-    size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 1) * sizeof(double);
+    size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 2) * sizeof(double);
     if (!ws || ws_bytes < need)
       return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                        need);
@@ -219,7 +219,7 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
 }
 
 size_t ev_ws_bytes(int d) {
-  return TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * (size_t)(d + 1) * sizeof(double);
+  return TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * (size_t)(d + 2) * sizeof(double);
 }
 
 }  // namespace
@@ -280,22 +280,26 @@ int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, 
   return TRIOT_OK;
 }
 
-int triot_expected_value(double* means, const void* p, const int64_t* shape, int d, int dtype,
-                         void* workspace, size_t workspace_bytes, void* cuda_stream) {
+static int expected_value_impl(double* means, const void* p, const int64_t* shape, int d,
+                               int dtype, void* workspace, size_t workspace_bytes,
+                               void* cuda_stream, bool with_mass) {
   Geom g;
   int st = plan_ev(g, p, shape, d, dtype);
   if (st) return st;
+  g.with_mass = with_mass;
+  const int nout = d + (with_mass ? 1 : 0);
   if (!means) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: means is NULL");
   if (((uintptr_t)means) % 8)
     return set_error(TRIOT_ERR_MISALIGNED, "Misaligned: means is not 8-byte aligned");
   {
-    uintptr_t m0 = (uintptr_t)means, m1 = m0 + (uintptr_t)d * 8;
+    uintptr_t m0 = (uintptr_t)means, m1 = m0 + (uintptr_t)nout * 8;
     uintptr_t p0 = (uintptr_t)p, p1 = p0 + (uintptr_t)g.t[0].numel * (uintptr_t)g.esz;
     if (g.t[0].numel && m0 < p1 && p0 < m1)
       return set_error(TRIOT_ERR_ALIASING, "Aliasing: means overlaps p");
   }
   if (g.empty) {
-    cudaError_t e = cudaMemsetAsync(means, 0, (size_t)d * sizeof(double), (cudaStream_t)cuda_stream);
+    cudaError_t e =
+        cudaMemsetAsync(means, 0, (size_t)nout * sizeof(double), (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
     clear_error();
     return TRIOT_OK;
@@ -303,6 +307,18 @@ int triot_expected_value(double* means, const void* p, const int64_t* shape, int
   st = launch(g, cuda_stream, means, workspace, workspace_bytes);
   if (!st) clear_error();
   return st;
+}
+
+int triot_expected_value(double* means, const void* p, const int64_t* shape, int d, int dtype,
+                         void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  return expected_value_impl(means, p, shape, d, dtype, workspace, workspace_bytes, cuda_stream,
+                             false);
+}
+
+int triot_expected_value_mass(double* out, const void* p, const int64_t* shape, int d, int dtype,
+                              void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  return expected_value_impl(out, p, shape, d, dtype, workspace, workspace_bytes, cuda_stream,
+                             true);
 }
 
 int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape, int d,

@@ -58,8 +58,8 @@ struct Desc {
   IDX srows, scols;      // embed: per-element bounds of a partial vector
   // expected value: weight slots -> output
   int32_t collapsed;     // 1 iff R > 1
-  int32_t d_out;         // number of means written (the caller's d)
-  int32_t slot_of_axis[TRIOT_MAXD];  // means[j] = slot >= 0 ? total[slot] : 0
+  int32_t d_out;         // values written: the caller's d (+1 when the mass is requested)
+  int32_t slot_of_axis[TRIOT_MAXD + 1];  // out[j] = slot >= 0 ? total[slot] : 0 (slot D+1 = mass)
   int32_t op;            // binary op
   int32_t pad_;
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p
@@ -67,7 +67,7 @@ struct Desc {
   void* ws;              // EV: workspace (device)
 };
 
-// Workspace layout of the expected value: [ticket u32 | pad to 256 B] [grid x (D+1) doubles].
+// Workspace layout of the expected value: [ticket u32 | pad to 256 B] [grid x (D+2) doubles].
 #define TRIOT_EV_MAX_GRID 2048
 #define TRIOT_EV_WS_HEADER 256
 // EV bulk-copy pipeline: NSTAGE shared-memory stages of SVEC 32-byte vectors per block

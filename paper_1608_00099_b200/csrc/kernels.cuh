@@ -27,6 +27,25 @@ namespace triot {
 
 constexpr int kBlock = TRIOT_BLOCK;
 
+// Optional per-block timeline (tools/ev_probe.cu defines TRIOT_EV_TRACE; never in the library).
+#ifdef TRIOT_EV_TRACE
+__device__ unsigned long long* g_ev_trace;
+__device__ __forceinline__ void ev_trace(int slot) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_ev_trace[blockIdx.x * 8 + slot] = t;
+    g_ev_trace[blockIdx.x * 8 + 7] = smid;
+  }
+}
+#define TRIOT_TRACE(s) ev_trace(s)
+#else
+#define TRIOT_TRACE(s)
+#endif
+
+
 // ------------------------------------------------------------------ raw memory access (bits)
 
 template <int NB>
@@ -436,16 +455,18 @@ __device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const uint32_t
 }
 
 // Weight slots of one lane at the end: slot k < D-1 -> u_k S + ev_k; slot D-1 (the vector digit)
-// -> vmul (u S + ev) + (Wr if collapsed else Wc); slot D (collapsed column) -> Wc.
+// -> vmul (u S + ev) + (Wr if collapsed else Wc); slot D (collapsed column) -> Wc; slot D+1 ->
+// the mass S.
 template <int D, typename IDX>
 __device__ __forceinline__ void ev_finish(const Desc<IDX>& d, const IDX (&u)[D],
-                                          const EvAcc<D>& a, double (&acc)[D + 1]) {
+                                          const EvAcc<D>& a, double (&acc)[D + 2]) {
 #pragma unroll
   for (int k = 0; k < D - 1; ++k) acc[k] = fma((double)u[k], a.S, a.ev[k]);
   const double vmul = (double)(d.rowmul + d.colmul);
   const bool coll = d.collapsed != 0;
   acc[D - 1] = fma(vmul, fma((double)u[D - 1], a.S, a.ev[D - 1]), coll ? a.Wr : a.Wc);
   acc[D] = coll ? a.Wc : 0.0;
+  acc[D + 1] = a.S;  // the mass (slab-sharded EV amalgamation term)
 }
 
 // Fixed-order block reduction, one partial per block, ordered final sum by the last block.
@@ -477,6 +498,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
+  TRIOT_TRACE(3);
   if (!is_last) return;
   __threadfence();
   double f[NS];
@@ -512,7 +534,7 @@ template <int D, int ESZ, int V, typename IDX, int K>
 __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
   constexpr int NW = V * EW;
-  constexpr int NS = D + 1;  // weight slots (D digits + the column slot of a collapsed vector)
+  constexpr int NS = D + 2;  // D digit slots + collapsed column slot + mass
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
@@ -591,7 +613,7 @@ template <int D, int ESZ, typename IDX>
 __global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
     ev_tma_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int V = 32 / ESZ;
-  constexpr int NS = D + 1;
+  constexpr int NS = D + 2;
   constexpr int NSTAGE = TRIOT_EV_NSTAGE;
   constexpr int SVEC = TRIOT_EV_SVEC;
   constexpr int BLOCK = TRIOT_EV_TMA_BLOCK;
@@ -600,6 +622,7 @@ __global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
   uint64_t* full = (uint64_t*)(smem + (size_t)NSTAGE * SVEC * 32);
   uint64_t* empty = full + NSTAGE;
   const int tid = threadIdx.x, lane = tid & 31;
+  TRIOT_TRACE(0);
   const IDX vb = (IDX)blockIdx.x * d.wmul;
   IDX ve = vb + d.wmul;
   if (ve > d.nvec || ve < vb) ve = d.nvec;
@@ -631,6 +654,7 @@ __global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
     const int slot = (int)(i % NSTAGE);
     const uint32_t par = (uint32_t)((i / NSTAGE) & 1);
     mbar_wait(&full[slot], par);
+    if (i == 0) TRIOT_TRACE(1);
     const unsigned char* st = smem + (size_t)slot * SVEC * 32;
     const IDX v0 = vb + i * SVEC;
 #pragma unroll
@@ -657,9 +681,11 @@ __global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
                &full[slot]);
     }
   }
+  TRIOT_TRACE(2);
   double acc[NS];
   ev_finish<D, IDX>(d, u, a, acc);
   ev_reduce<NS, BLOCK, IDX>(d, acc);
+  TRIOT_TRACE(4);
 }
 
 }  // namespace triot

@@ -304,7 +304,7 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
     if (g.ext[k] + 32 > mx) mx = g.ext[k] + 32;
   g.idx64 = mx >= (1ull << 32) - 64;
   // 6. expected-value weight slots: digit k<D-1 -> axis; vector digit -> last (a) or row axis (b)
-  for (int j = 0; j < TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
   for (int k = 0; k < D - 1; ++k) g.slot_of_axis[ax[k].orig] = k;
   if (!c.collapsed) {
     g.slot_of_axis[ax[na - 1].orig] = D - 1;
@@ -315,6 +315,7 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
     g.nslots = D + 1;
   }
   if (g.N == 1 && n[ax[0].orig] == 1) g.slot_of_axis[ax[0].orig] = -1;  // weight 0 anyway
+  g.slot_of_axis[d] = D + 1;  // the total mass (read only when requested)
 }
 
 void set_decomposition(Geom& g, int mode, uint64_t warps) {
@@ -596,7 +597,7 @@ std::string describe(const Geom& g) {
   arr(s, "bnd", g.bnd, g.D);
   arr32(s, "fdm", g.fdm, g.D);
   arr32(s, "fds", g.fds, g.D);
-  arri(s, "slot_of_axis", g.slot_of_axis, g.d);
+  arri(s, "slot_of_axis", g.slot_of_axis, g.d + 1);
   s += "\"t\":[";
   for (int x = 0; x < g.ntensor; ++x) {
     s += x ? ",{" : "{";

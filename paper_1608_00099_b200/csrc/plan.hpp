@@ -41,8 +41,9 @@ struct Geom {
   int mode = 0;                              // 0 = chunk, 1 = stride, 2 = block chunk
   int khi = 0, klo = 0;
   uint64_t rowmul = 0, colmul = 0, vfull = 0, vany = 0, srows = 0, scols = 0;
-  int slot_of_axis[TRIOT_MAXD] = {};
+  int slot_of_axis[TRIOT_MAXD + 1] = {};
   int nslots = 0;
+  bool with_mass = false;   // EV: also write sum(p) after the d means
   struct T {
     uint64_t sig[TRIOT_MAXD] = {}, kap[TRIOT_MAXD] = {};
     uint64_t step = 0, rho = 0, tau = 1;
@@ -77,13 +78,13 @@ const char* last_error();
 
 template <typename IDX>
 void fill_desc(const Geom& g, Desc<IDX>& d) {
+  for (int k = 0; k <= TRIOT_MAXD; ++k) d.slot_of_axis[k] = g.slot_of_axis[k];
   for (int k = 0; k < TRIOT_MAXD; ++k) {
     d.ext[k] = (IDX)g.ext[k];
     d.dlt[k] = (IDX)g.dlt[k];
     d.bnd[k] = (IDX)g.bnd[k];
     d.fdm[k] = g.fdm[k];
     d.fds[k] = g.fds[k];
-    d.slot_of_axis[k] = g.slot_of_axis[k];
   }
   d.nvec = (IDX)g.nvec;
   d.wmul = (IDX)g.wmul;
@@ -100,7 +101,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.srows = (IDX)g.srows;
   d.scols = (IDX)g.scols;
   d.collapsed = g.collapsed ? 1 : 0;
-  d.d_out = g.d;
+  d.d_out = g.d + (g.with_mass ? 1 : 0);
   d.op = g.binop;
   d.pad_ = 0;
   for (int x = 0; x < TRIOT_MAXT; ++x) {

@@ -1,0 +1,81 @@
+"""Slab sharding of the TRIOT hot path over ranks (one process per GPU, torch.distributed).
+
+P:607: "Parallelism could be automatically exploited by specializing the classes in the template
+recursion that correspond to the outermost for loops ... This would allow multiple processors,
+cores, or GPUs to simultaneously process partitions of tensors", and, for inner products, "each
+thread computes its own pre-result and these pre-results are amalgamated together".
+
+Here the partition is a slab of axis 0 (the outermost loop):
+
+* embed and apply_binary need NO collective: rank r owns rows [lo, hi) of the output and reads
+  only the matching rows of the inputs (`slab_rows`, `embed_slab`, `apply_binary_slab`);
+* the expected value is the one exchange: each rank computes its slab's means and mass with
+  `triot_expected_value_mass`, shifts the axis-0 weight by its row offset (t_0 = lo + local t_0,
+  so m_0 += lo * mass), and the d-vectors are all-gathered and summed in rank order, so the result
+  is identical on every rank and deterministic run to run (an all-reduce would leave the
+  summation order to the collective's algorithm).
+
+The collective is over whatever process group the caller passes (NCCL for CUDA tensors across
+GPUs over NVLink; gloo for the CPU tests).  `local_ev` lets the host logic run with a stand-in
+for the GPU kernel (the CPU tests pass one); the default is the library's kernel.
+"""
+from __future__ import annotations
+
+
+def slab_rows(n0: int, world: int, rank: int) -> tuple[int, int]:
+    """Balanced contiguous slab [lo, hi) of n0 rows for `rank` of `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    return (rank * n0) // world, ((rank + 1) * n0) // world
+
+
+def embed_slab(dst_slab, src, lo: int, region_only: bool = False):
+    """Rows [lo, lo + dst_slab.shape[0]) of embed(dst, src): dst_slab is this rank's slab of the
+    global dst; src is the global src (or at least its rows from lo on) on this device."""
+    from . import api
+    hi = lo + dst_slab.shape[0]
+    s_hi = min(hi, src.shape[0])
+    src_part = src[lo:s_hi] if lo < s_hi else src[0:0]
+    return api.embed(dst_slab, src_part.contiguous(), region_only=region_only)
+
+
+def apply_binary_slab(a, b, lo: int, hi: int, op: str = "mul", out_slab=None, iter_shape=None):
+    """Rows [lo, hi) of apply_binary(a, b): a, b are the global operands on this device."""
+    from . import api
+    if iter_shape is None:
+        iter_shape = tuple(min(x, y) for x, y in zip(a.shape, b.shape))
+    hi = min(hi, iter_shape[0])
+    ish = (max(0, hi - lo),) + tuple(iter_shape[1:])
+    return api.apply_binary(a[lo:hi].contiguous() if lo < hi else a[0:0],
+                            b[lo:hi].contiguous() if lo < hi else b[0:0],
+                            op, out=out_slab, iter_shape=ish)
+
+
+def _default_local_ev(p_slab):
+    from . import api
+    return api.expected_value(p_slab, with_mass=True)
+
+
+def amalgamate(local_means_mass, lo: int):
+    """Shift a slab's (d means, mass) so axis 0 counts from the global origin: m_0 += lo*mass."""
+    v = local_means_mass.clone()
+    v[0] = v[0] + float(lo) * v[-1]
+    return v[:-1]
+
+
+def expected_value_sharded(p_slab, lo: int, group=None, local_ev=None):
+    """Global expected value of a p whose axis-0 rows [lo, lo + p_slab.shape[0]) this rank holds.
+
+    Returns the same (d,) float64 tensor on every rank of `group`."""
+    import torch
+    import torch.distributed as dist
+
+    local_ev = local_ev or _default_local_ev
+    part = amalgamate(local_ev(p_slab), lo)
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(part) for _ in range(world)]
+    dist.all_gather(parts, part, group=group)
+    total = parts[0].clone()
+    for r in range(1, world):        # rank order: deterministic
+        total += parts[r]
+    return total

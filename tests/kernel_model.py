@@ -121,6 +121,6 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
                 u, off, oob = step(u, off, oob)
                 v += dv
     if op == "ev":
-        d = len(desc["slot_of_axis"])
+        d = desc["d"]
         return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]
     return None

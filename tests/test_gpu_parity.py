@@ -263,3 +263,47 @@ def test_u64_index_path():
     assert not np.any(_bits(tail))
     del dst
     torch.cuda.empty_cache()
+
+
+def test_ev_mass_and_slab_amalgamation():
+    """triot_expected_value_mass + the slab shift of parallel.py, emulating 3 ranks on one GPU."""
+    from paper_1608_00099_b200 import parallel as P
+    p = make_inputs("C3")["p"]
+    ref = O.expected_value(p)
+    full = T.expected_value(_dev(p), with_mass=True).cpu().numpy()
+    assert abs(full[6] - math.fsum(p.ravel())) <= 1e-12
+    assert np.all(np.abs(full[:6] - ref) <= 1e-12 * np.abs(ref))
+    parts = []
+    for r in range(3):
+        lo, hi = P.slab_rows(16, 3, r)
+        parts.append(P.amalgamate(T.expected_value(_dev(p[lo:hi].copy()), with_mass=True), lo))
+    tot = parts[0] + parts[1] + parts[2]
+    assert np.all(np.abs(tot.cpu().numpy() - ref) <= 1e-12 * np.abs(ref))
+    # integer-valued: exact
+    q = np.random.default_rng(3).integers(0, 256, size=(9, 7, 5, 4)).astype(np.float64)
+    parts = []
+    for r in range(2):
+        lo, hi = P.slab_rows(9, 2, r)
+        parts.append(P.amalgamate(T.expected_value(_dev(q[lo:hi].copy()), with_mass=True), lo))
+    np.testing.assert_array_equal((parts[0] + parts[1]).cpu().numpy(), O.expected_value(q))
+
+
+def test_embed_and_binary_slabs_tile_the_result():
+    from paper_1608_00099_b200 import parallel as P
+    inp = make_inputs("C1")
+    ref = np.empty(inp["dst_shape"]); O.embed(ref, inp["src"])
+    src = _dev(inp["src"])
+    dst = _poisoned(inp["dst_shape"], np.float64)
+    for r in range(3):
+        lo, hi = P.slab_rows(8, 3, r)
+        P.embed_slab(dst[lo:hi], src, lo)
+    assert_bits_equal(dst, ref)
+    c4 = make_inputs("C4")
+    a, b = _dev(c4["a"][:4].copy()), _dev(c4["b"][:4].copy())
+    ish = (4,) + c4["iter_shape"][1:]
+    refc = O.apply_binary(c4["a"][:4].copy(), c4["b"][:4].copy(), "mul", iter_shape=ish)
+    out = torch.empty(ish, dtype=torch.float64, device=DEV)
+    for r in range(2):
+        lo, hi = P.slab_rows(4, 2, r)
+        P.apply_binary_slab(a, b, lo, hi, "mul", out_slab=out[lo:hi], iter_shape=ish)
+    assert_bits_equal(out, refc)

@@ -1,0 +1,100 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the slab-sharding host logic
+(paper_1608_00099_b200/parallel.py): slab bounds cover every row once, the per-rank embed and
+binary slabs tile the global result with no collective, and the sharded expected value -- with
+the oracle standing in for each rank's GPU kernel -- equals the oracle on the whole tensor."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_1608_00099_b200 import parallel as P
+from triot_inputs import make_inputs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_ev_with_mass(p_slab):
+    p = p_slab.numpy()
+    m = O.expected_value(p)
+    return torch.tensor(list(m) + [float(np.sum(p, dtype=np.float64))], dtype=torch.float64)
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        # expected value over a slab of C3's axis 0 (integer-valued copy: exact) and C3 itself
+        p_int = np.random.default_rng(5).integers(0, 256, size=(7, 5, 6, 3)).astype(np.float64)
+        p_c3 = make_inputs("C3")["p"][:, :4, :4].copy()
+        for name, p in (("int", p_int), ("c3", p_c3)):
+            lo, hi = P.slab_rows(p.shape[0], world, rank)
+            got = P.expected_value_sharded(torch.from_numpy(p[lo:hi].copy()), lo,
+                                           local_ev=_oracle_ev_with_mass)
+            res[name] = got.numpy()
+        # embed slab: each rank's slab of dst from the global src, oracle as the local kernel
+        src = make_inputs("C1")["src"]
+        dst_shape = (8, 16, 8, 8)
+        lo, hi = P.slab_rows(dst_shape[0], world, rank)
+        slab = np.empty((hi - lo,) + dst_shape[1:])
+        O.embed(slab, src[lo:min(hi, src.shape[0])].copy())
+        res["embed"] = (lo, hi, slab)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_ev_and_slabs_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    p_int = np.random.default_rng(5).integers(0, 256, size=(7, 5, 6, 3)).astype(np.float64)
+    ref_int = O.expected_value(p_int)
+    p_c3 = make_inputs("C3")["p"][:, :4, :4].copy()
+    ref_c3 = O.expected_value(p_c3)
+    for r in range(world):
+        np.testing.assert_array_equal(out[r]["int"], ref_int)          # exact
+        assert np.all(np.abs(out[r]["c3"] - ref_c3) <= 1e-12 * np.abs(ref_c3))
+    assert np.array_equal(out[0]["c3"], out[1]["c3"])                  # same on every rank
+    # embed slabs tile the global result
+    full = np.empty((8, 16, 8, 8))
+    O.embed(full, make_inputs("C1")["src"])
+    rows = []
+    for r in range(world):
+        lo, hi, slab = out[r]["embed"]
+        rows.append((lo, hi))
+        np.testing.assert_array_equal(slab, full[lo:hi])
+    assert sorted(rows)[0][0] == 0 and sorted(rows)[-1][1] == 8
+
+
+def test_slab_rows_cover_once():
+    for n0 in (0, 1, 5, 16, 384, 511):
+        for world in (1, 2, 3, 8):
+            spans = [P.slab_rows(n0, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n0
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def test_amalgamate_shift():
+    v = torch.tensor([2.0, 3.0, 10.0], dtype=torch.float64)    # m0, m1, mass
+    np.testing.assert_array_equal(P.amalgamate(v, 4).numpy(), [42.0, 3.0])

@@ -1,0 +1,69 @@
+"""Per-block timeline of the EV bulk-copy kernel on C3 (diagnostic; builds tools/libevprobe.so)."""
+import ctypes
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+SO = os.path.join(HERE, "libevprobe.so")
+
+
+def build():
+    srcs = [os.path.join(HERE, "ev_probe.cu"),
+            os.path.join(ROOT, "paper_1608_00099_b200", "csrc", "plan.cpp")]
+    if not os.path.exists(SO):
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                        "-shared", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+                        "-o", SO, *srcs], check=True)
+    L = ctypes.CDLL(SO)
+    L.probe_ev_c3.restype = ctypes.c_int
+    L.probe_ev_c3.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_void_p]
+    return L
+
+
+def main():
+    L = build()
+    from triot_inputs import make_inputs
+    dev = torch.device("cuda:0")
+    p = torch.from_numpy(make_inputs("C3")["p"]).to(dev)
+    means = torch.zeros(6, dtype=torch.float64, device=dev)
+    ws = torch.zeros(1 << 20, dtype=torch.uint8, device=dev)
+    trace = torch.zeros(4096 * 8, dtype=torch.int64, device=dev)
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    for rep in range(3):
+        scratch.fill_(1)
+        clean.sum()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        grid = L.probe_ev_c3(p.data_ptr(), means.data_ptr(), ws.data_ptr(), trace.data_ptr(),
+                             sms, s)
+        b.record()
+        torch.cuda.synchronize()
+        assert grid > 0, grid
+        tr = trace[: grid * 8].view(grid, 8).cpu().numpy().astype(np.int64)
+        t0 = tr[:, 0].min()
+        rel = (tr[:, :5] - t0) / 1000.0
+        pct = lambda col, qs: [round(float(np.percentile(rel[:, col], q)), 2) for q in qs]
+        print(json.dumps({
+            "grid": grid, "event_us": round(a.elapsed_time(b) * 1000, 2),
+            "start_us": pct(0, (0, 50, 100)),
+            "first_stage_us": pct(1, (0, 50, 100)),
+            "loop_end_us": pct(2, (0, 10, 50, 90, 100)),
+            "ticket_us": pct(3, (0, 50, 100)),
+            "exit_last_us": round(float(rel[:, 4].max()), 2),
+            "slowest_blocks_sm": [int(x) for x in tr[np.argsort(-tr[:, 2])[:8], 7]],
+            "fastest_blocks_sm": [int(x) for x in tr[np.argsort(tr[:, 2])[:8], 7]],
+            "means": means.cpu().tolist()}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
