@@ -128,6 +128,27 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   return TRIOT_OK;
 }
 
+// Every kernel is launched with programmatic stream serialization (PDL): it may be scheduled
+// while the previous kernel on the stream drains; it waits (griddepcontrol.wait) before its
+// first global memory access, so results are as with plain stream order.
+int launch_pdl(const void* fn, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+               void** args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC");
+  return TRIOT_OK;
+}
+
 template <typename IDX>
 int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void* out, void* ws) {
   Desc<IDX> d;
@@ -136,9 +157,7 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
   d.out = out;
   d.ws = ws;
   void* args[1] = {&d};
-  cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(TRIOT_BLOCK), args, 0, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
-  return TRIOT_OK;
+  return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args);
 }
 
 // EV bulk-copy fast path: full 32-byte vectors, 32-B aligned p, one persistent block per SM
@@ -186,10 +205,8 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
     d.out = out;
     d.ws = ws;
     void* args[1] = {&d};
-    cudaError_t e2 = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(TRIOT_EV_TMA_BLOCK), args,
-                                      TRIOT_EV_SMEM, (cudaStream_t)stream);
-    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaLaunchKernel");
-    return TRIOT_OK;
+    return launch_pdl(fn, (unsigned)grid, TRIOT_EV_TMA_BLOCK, TRIOT_EV_SMEM, (cudaStream_t)stream,
+                      args);
   };
   return g.idx64 ? go(uint64_t(0)) : go(uint32_t(0));
 }

@@ -99,6 +99,16 @@ struct Mem<4> {
   }
 };
 
+// Programmatic dependent launch (sm_90+): every kernel is launched with programmatic stream
+// serialization, so it may be scheduled while its predecessor on the stream drains.  It lets
+// its own successor be scheduled as soon as all its blocks have started (pdl_trigger), and it
+// touches no global memory before pdl_wait -- which returns once the predecessor grid has
+// completed and its writes are visible -- so stream order semantics are unchanged.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int ESZ, typename IDX>
 __device__ __forceinline__ const char* addr(const void* base, IDX off) {
   return (const char*)base + (uint64_t)off * ESZ;
@@ -219,6 +229,7 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   const int lane = threadIdx.x & 31;
   const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
   const IDX base0 = warp * d.wmul;
+  pdl_trigger();
   if (base0 >= d.nvec) return;
   const IDX vend = warp_end(d, base0);
   IDX u[D], off[2];
@@ -226,6 +237,7 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   IDX v = base0 + (IDX)lane;
   odo_start<D, 2, true, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
+  pdl_wait();
   for (IDX b = base0; b < vend; b += K * d.dv) {
     uint32_t buf[K][NW];
     IDX doff[K];
@@ -315,6 +327,7 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
   const int lane = threadIdx.x & 31;
   const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
   const IDX base0 = warp * d.wmul;
+  pdl_trigger();
   if (base0 >= d.nvec) return;
   const IDX vend = warp_end(d, base0);
   IDX u[D], off[3];
@@ -322,6 +335,7 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
   IDX v = base0 + (IDX)lane;
   odo_start<D, 3, false, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
+  pdl_wait();
   for (IDX b = base0; b < vend; b += K * d.dv) {
     uint32_t ba[K][NW], bb[K][NW];
     IDX coff[K];
@@ -542,6 +556,8 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
   double acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+  pdl_trigger();
+  pdl_wait();
   if (base0 < d.nvec) {
     const IDX vend = warp_end(d, base0);
     const IDX dv = d.dv;
@@ -635,6 +651,8 @@ __global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
+  pdl_wait();
   __syncthreads();
   const char* pbase = (const char*)d.t[0].ptr;
   if (tid == 0) {
