@@ -307,3 +307,46 @@ def test_embed_and_binary_slabs_tile_the_result():
         lo, hi = P.slab_rows(4, 2, r)
         P.apply_binary_slab(a, b, lo, hi, "mul", out_slab=out[lo:hi], iter_shape=ish)
     assert_bits_equal(out, refc)
+
+
+def _guarded(shape, dtype, fill, guard=4096, offset=0):
+    """A tensor placed between two guard zones of a sentinel bit pattern (writes outside the
+    tensor would change them; compute-sanitizer is unavailable on this pool)."""
+    n = math.prod(shape)
+    buf = torch.full((guard + offset + n + guard,), fill, dtype=dtype, device=DEV)
+    return buf, buf[guard + offset: guard + offset + n].view(shape)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_no_writes_outside_outputs(dtype):
+    rng = np.random.default_rng(21)
+    npdt = np.float32 if dtype == torch.float32 else np.float64
+    sentinel = -12345.0
+    for case in range(12):
+        d = int(rng.integers(1, 15))
+        src_shape = random_shape(rng, d, 30000, lo=1, hi=6 if d > 4 else 30)
+        dst_shape = tuple(max(1, s + int(rng.integers(-2, 4))) for s in src_shape)
+        if case % 3 == 0:
+            dst_shape = dst_shape[:-1] + (int(rng.choice([1, 2, 3, 4])),)
+        if math.prod(dst_shape) > 100000:
+            dst_shape = tuple(min(a, b) for a, b in zip(dst_shape, src_shape))
+        src = rng.standard_normal(src_shape).astype(npdt)
+        buf, dst = _guarded(dst_shape, dtype, sentinel, offset=case % 3)
+        T.embed(dst, _dev(src))
+        torch.cuda.synchronize()
+        g = 4096 + case % 3
+        assert torch.all(buf[:g] == sentinel) and torch.all(buf[g + dst.numel():] == sentinel)
+        # binary with c larger than iter: only the iter region of c may change
+        ish = tuple(max(1, s - 1) for s in src_shape)
+        cs = tuple(s + 1 for s in ish)
+        cbuf, c = _guarded(cs, dtype, sentinel, offset=case % 2)
+        T.apply_binary(_dev(src), _dev(src), "add", out=c, iter_shape=ish)
+        torch.cuda.synchronize()
+        g = 4096 + case % 2
+        assert torch.all(cbuf[:g] == sentinel) and torch.all(cbuf[g + c.numel():] == sentinel)
+        inside = c[tuple(slice(0, s) for s in ish)]
+        mask = torch.ones(cs, dtype=torch.bool, device=DEV)
+        mask[tuple(slice(0, s) for s in ish)] = False
+        assert torch.all(c[mask] == sentinel)
+        ref = O.apply_binary(src, src, "add", iter_shape=ish)
+        assert_bits_equal(inside.contiguous(), ref)
