@@ -71,6 +71,17 @@ def lib():
             L.oracle_expected_value_abs.restype = None
             L.oracle_expected_value_abs.argtypes = [_dblp, ctypes.c_void_p, _u64p,
                                                     ctypes.c_uint, ctypes.c_int]
+            L.oracle_view_bias.restype = ctypes.c_uint64
+            L.oracle_view_bias.argtypes = [_u64p, _u64p, ctypes.c_uint]
+            L.oracle_embed_view.restype = None
+            L.oracle_embed_view.argtypes = [ctypes.c_void_p, _u64p, _u64p, _u64p,
+                                            ctypes.c_void_p, _u64p, _u64p, _u64p,
+                                            ctypes.c_uint, ctypes.c_uint, ctypes.c_int]
+            L.oracle_apply_binary_view.restype = None
+            L.oracle_apply_binary_view.argtypes = [ctypes.c_void_p, _u64p, _u64p,
+                                                   ctypes.c_void_p, _u64p, _u64p,
+                                                   ctypes.c_void_p, _u64p, _u64p, _u64p,
+                                                   ctypes.c_uint, ctypes.c_int, ctypes.c_int]
             _lib = L
     return _lib
 
@@ -177,3 +188,33 @@ def expected_value_abs(p: np.ndarray) -> np.ndarray:
     out = (ctypes.c_double * d)()
     lib().oracle_expected_value_abs(out, _ptr(p), _shape(p.shape), d, _dtype_code(p))
     return np.array(out[:d], dtype=np.float64)
+
+
+# -- NEXT-1: views ------------------------------------------------------------
+
+def view_bias(start, base_shape) -> int:
+    """P:605: bias = tuple_to_index(start, base_shape)."""
+    return int(lib().oracle_view_bias(_shape(start), _shape(base_shape), len(base_shape)))
+
+
+def embed_view(dst_base: np.ndarray, dst_start, dst_window, src_base: np.ndarray, src_start,
+               src_window, region_only: bool = False) -> np.ndarray:
+    """In place on dst_base: the dst window receives the zero-padded src window."""
+    assert dst_base.dtype == src_base.dtype and dst_base.ndim == src_base.ndim
+    d = dst_base.ndim
+    lib().oracle_embed_view(_ptr(dst_base), _shape(dst_base.shape), _shape(dst_start),
+                            _shape(dst_window), _ptr(src_base), _shape(src_base.shape),
+                            _shape(src_start), _shape(src_window), d, dst_base.itemsize,
+                            1 if region_only else 0)
+    return dst_base
+
+
+def apply_binary_view(c_base: np.ndarray, c_start, a_base: np.ndarray, a_start,
+                      b_base: np.ndarray, b_start, iter_shape, op: str = "mul") -> np.ndarray:
+    """In place on c_base: c_view[t] = a_view[t] OP b_view[t] for t in iter_shape."""
+    d = a_base.ndim
+    lib().oracle_apply_binary_view(_ptr(c_base), _shape(c_base.shape), _shape(c_start),
+                                   _ptr(a_base), _shape(a_base.shape), _shape(a_start),
+                                   _ptr(b_base), _shape(b_base.shape), _shape(b_start),
+                                   _shape(iter_shape), d, _dtype_code(a_base), OPS[op])
+    return c_base

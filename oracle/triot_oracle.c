@@ -254,3 +254,73 @@ void oracle_expected_value_abs(double* out, const void* p, const u64* shape,
     oracle_advance_tuple(t, shape, dimension);
   }
 }
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT-1: tensor views ("a tensor slice starting at index tuple (i_1, ..., i_d) can
+ * be constructed by using a bias: bias <- tuple_to_index((i_1, ..., i_d), x.data_shape(), d).
+ * Any valid accesses to the tensor slice x_slice[flat_index] can be performed as
+ * x.flat[bias + flat_index]"), where flat_index of a window tuple t is taken with respect to the
+ * BASE shape (the window's elements are not contiguous in the base).  P:613: views window the
+ * intersecting support of PMFs.  A view is (base, base_shape, start, window).
+ * ---------------------------------------------------------------------------------------- */
+
+/* the bias of a slice starting at tuple `start`. */
+u64 oracle_view_bias(const u64* start, const u64* base_shape, unsigned int dimension) {
+  return oracle_tuple_to_index(start, base_shape, dimension);
+}
+
+/* embed between views: iterate t over the dst window (or min(dst, src windows) if region_only),
+ * dst_view[t] = (t < src window) ? src_view[t] : +0.0, with view[t] = base.flat[bias +
+ * tuple_to_index(t, base_shape)]. */
+void oracle_embed_view(void* dst, const u64* dst_base, const u64* dst_start, const u64* dst_win,
+                       const void* src, const u64* src_base, const u64* src_start,
+                       const u64* src_win, unsigned int dimension, unsigned int esz,
+                       int region_only) {
+  u64 counter_shape[64];
+  u64 t[64];
+  unsigned char* d = (unsigned char*)dst;
+  const unsigned char* s = (const unsigned char*)src;
+  u64 dst_bias = oracle_view_bias(dst_start, dst_base, dimension);
+  u64 src_bias = oracle_view_bias(src_start, src_base, dimension);
+  for (unsigned int k = 0; k < dimension; ++k)
+    counter_shape[k] = region_only ? (dst_win[k] < src_win[k] ? dst_win[k] : src_win[k])
+                                   : dst_win[k];
+  u64 n = flat_size(counter_shape, dimension);
+  memset(t, 0, sizeof(t));
+  for (u64 i = 0; i < n; ++i) {
+    u64 dst_index = dst_bias + oracle_tuple_to_index(t, dst_base, dimension);
+    int in_bounds = 1;
+    for (unsigned int k = 0; k < dimension; ++k)
+      if (!(t[k] < src_win[k])) in_bounds = 0;
+    if (in_bounds) {
+      u64 src_index = src_bias + oracle_tuple_to_index(t, src_base, dimension);
+      memcpy(d + dst_index * esz, s + src_index * esz, esz);
+    } else {
+      memset(d + dst_index * esz, 0, esz);
+    }
+    oracle_advance_tuple(t, counter_shape, dimension);
+  }
+}
+
+/* binary op between views: for t in iter, c_view[t] = a_view[t] OP b_view[t]. */
+void oracle_apply_binary_view(void* c, const u64* c_base, const u64* c_start, const void* a,
+                              const u64* a_base, const u64* a_start, const void* b,
+                              const u64* b_base, const u64* b_start, const u64* iter_shape,
+                              unsigned int dimension, int dtype, int op) {
+  u64 t[64];
+  u64 n = flat_size(iter_shape, dimension);
+  u64 cb = oracle_view_bias(c_start, c_base, dimension);
+  u64 ab = oracle_view_bias(a_start, a_base, dimension);
+  u64 bb = oracle_view_bias(b_start, b_base, dimension);
+  memset(t, 0, sizeof(t));
+  for (u64 i = 0; i < n; ++i) {
+    u64 ci = cb + oracle_tuple_to_index(t, c_base, dimension);
+    u64 ai = ab + oracle_tuple_to_index(t, a_base, dimension);
+    u64 bi = bb + oracle_tuple_to_index(t, b_base, dimension);
+    if (dtype == OR_F64)
+      ((double*)c)[ci] = op_f64(((const double*)a)[ai], ((const double*)b)[bi], op);
+    else
+      ((float*)c)[ci] = op_f32(((const float*)a)[ai], ((const float*)b)[bi], op);
+    oracle_advance_tuple(t, iter_shape, dimension);
+  }
+}

@@ -357,3 +357,64 @@ def test_configs_table_matches_baseline_json():
             if len(set(shp)) == 1 and len(shp) > 4:
                 continue
             assert str(shp).replace(" ", "").replace(",)", ")") in text.replace(" ", ""), (c.name, shp)
+
+
+# ---------------------------------------------------------------- NEXT-1: views
+
+def test_view_bias_and_visits_spec_example():
+    """P:605 bias; a (2,2) window at (1,2) of a (4,5) base has bias 7 and visits base
+    flat indices {7, 8, 12, 13}."""
+    assert O.view_bias([1, 2], [4, 5]) == 7
+    base = np.arange(20, dtype=np.float64).reshape(4, 5)
+    out = np.zeros((2, 2))
+    # embed from the view into a dense (2,2): the view's elements in order
+    O.embed_view(out, [0, 0], [2, 2], base, [1, 2], [2, 2])
+    assert out.ravel().tolist() == [7.0, 8.0, 12.0, 13.0]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_views_are_transparent(seed):
+    """any op on a view equals the op on a materialised copy of the window (numpy slice)."""
+    rng = np.random.default_rng(600 + seed)
+    d = int(rng.integers(1, 6))
+    base_a = rng.standard_normal(random_shape(rng, d, 4000, lo=2, hi=9))
+    win = tuple(int(rng.integers(1, s + 1)) for s in base_a.shape)
+    start_a = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base_a.shape, win))
+    base_b = rng.standard_normal(tuple(w + int(rng.integers(0, 4)) for w in win))
+    start_b = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base_b.shape, win))
+    base_c = np.full(tuple(w + int(rng.integers(0, 3)) for w in win), 7.0)
+    start_c = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base_c.shape, win))
+    sl = lambda st, w: tuple(slice(a, a + b) for a, b in zip(st, w))
+    mat_a, mat_b = base_a[sl(start_a, win)].copy(), base_b[sl(start_b, win)].copy()
+    # binary on views == binary on copies; c outside its window untouched
+    ref_c = base_c.copy()
+    ref_c[sl(start_c, win)] = mat_a * mat_b
+    O.apply_binary_view(base_c, start_c, base_a, start_a, base_b, start_b, win, "mul")
+    np.testing.assert_array_equal(base_c, ref_c)
+    # embed view -> view, pad and crop: == embed on the materialised windows
+    dwin = tuple(max(1, w + int(rng.integers(-1, 3))) for w in win)
+    dbase = np.full(tuple(w + 2 for w in dwin), -1.0)
+    dstart = (1,) * d
+    ref_d = dbase.copy()
+    tmp = np.empty(dwin)
+    O.embed(tmp, mat_a)
+    ref_d[sl(dstart, dwin)] = tmp
+    O.embed_view(dbase, dstart, dwin, base_a, start_a, win)
+    np.testing.assert_array_equal(dbase, ref_d)
+
+
+def test_pmf_product_over_intersecting_support():
+    """two PMFs over supports with different origins; views window the intersection.
+    A has support rows 2..6, cols 0..4; B has rows 4..8, cols 1..3.  The product over the
+    intersection (rows 4..5, cols 1..3) equals the numpy product of the aligned slices."""
+    rng = np.random.default_rng(77)
+    A = rng.random((5, 5)); A /= A.sum()       # support origin (2, 0)
+    B = rng.random((5, 3)); B /= B.sum()       # support origin (4, 1)
+    lo = (4, 1); hi = (min(2 + 5, 4 + 5), min(0 + 5, 1 + 3))
+    win = (hi[0] - lo[0], hi[1] - lo[1])
+    a_start = (lo[0] - 2, lo[1] - 0)
+    b_start = (lo[0] - 4, lo[1] - 1)
+    C = np.zeros(win)
+    O.apply_binary_view(C, (0, 0), A, a_start, B, b_start, win, "mul")
+    ref = A[2:2 + win[0], 1:1 + win[1]] * B[0:win[0], 0:win[1]]
+    np.testing.assert_array_equal(C, ref)
