@@ -170,6 +170,36 @@ TRIOT_API int triot_expected_value_mass(double* out, const void* p, const int64_
                                         int dtype, void* workspace, size_t workspace_bytes,
                                         void* cuda_stream);
 
+/* ---- NEXT-1: tensor views -------------------------------------------
+ *
+ * A view is a window of a dense row-major base tensor: "a tensor slice starting at index tuple
+ * (i_1, ..., i_d) can be constructed by using a bias: bias <- tuple_to_index((i_1, ..., i_d),
+ * x.data_shape(), d).  Any valid accesses to the tensor slice ... x.flat[bias + flat_index]"
+ * (P:605), flat_index taken with respect to the base shape.  Views let an op work on "the
+ * intersecting support" of PMFs with different origins without copying.  Every op on a
+ * view behaves exactly as on a materialised copy of its window (the index tuple t is relative
+ * to the window's start).
+ */
+typedef struct {
+  void* data;                 /* device pointer to the BASE tensor's element 0                */
+  const int64_t* base_shape;  /* the base tensor's d extents (dense, row-major)               */
+  const int64_t* start;       /* first tuple of the window in the base; NULL = the origin      */
+  const int64_t* shape;       /* the window's d extents; start[k] + shape[k] <= base_shape[k] */
+} triot_view;
+
+/* triot_embed on views: the dst window receives the src window, zero-padded (flags as
+ * triot_embed).  Elements of the dst base outside the dst window are never written.  The
+ * windows' address ranges must not overlap (checked conservatively on the spanned bytes). */
+TRIOT_API int triot_embed_view(const triot_view* dst, const triot_view* src, int d, int dtype,
+                               unsigned flags, void* cuda_stream);
+
+/* triot_apply_binary on views: for t in iter_shape (NULL = min of the a and b windows),
+ * c_view[t] = a_view[t] OP b_view[t]; c's window must contain iter_shape.  In-place is allowed
+ * only for the identical view (c == a or c == b) with iter_shape equal to its window. */
+TRIOT_API int triot_apply_binary_view(const triot_view* c, const triot_view* a,
+                                      const triot_view* b, const int64_t* iter_shape, int d,
+                                      int dtype, int op, void* cuda_stream);
+
 /* ---- diagnostics (host only; no device work, usable without a GPU) ---------------------- */
 
 /*

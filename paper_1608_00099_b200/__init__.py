@@ -22,10 +22,13 @@ from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED
                    triot_fastdiv_magic, triot_last_error, triot_max_dimension,
                    triot_plan_describe, triot_set_launch_policy, triot_status_string,
                    LIB_PATH)
-from .api import apply_binary, embed, expected_value, OPS
+from .api import (OPS, View, apply_binary, apply_binary_view, embed, embed_view,
+                  expected_value)
+from ._lib import triot_apply_binary_view, triot_embed_view
 
 __all__ = [
-    "embed", "apply_binary", "expected_value", "OPS", "TriotError",
+    "embed", "apply_binary", "expected_value", "OPS", "TriotError", "View", "embed_view",
+    "apply_binary_view", "triot_embed_view", "triot_apply_binary_view",
     "triot_embed", "triot_apply_binary", "triot_expected_value", "triot_expected_value_mass",
     "triot_expected_value_workspace_size", "triot_max_dimension", "triot_status_string",
     "triot_last_error", "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic",

@@ -27,7 +27,7 @@ STATUS = {
 }
 EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "triot_embed",
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
-           "triot_expected_value_mass",
+           "triot_expected_value_mass", "triot_embed_view", "triot_apply_binary_view",
            "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
@@ -67,6 +67,18 @@ _lib.triot_expected_value.argtypes = [_vp, _vp, _i64p, ctypes.c_int, ctypes.c_in
                                       ctypes.c_size_t, _vp]
 _lib.triot_expected_value_mass.restype = ctypes.c_int
 _lib.triot_expected_value_mass.argtypes = _lib.triot_expected_value.argtypes
+class triot_view(ctypes.Structure):
+    """include/triot.h triot_view: a window of a dense base tensor."""
+    _fields_ = [("data", ctypes.c_void_p), ("base_shape", _i64p), ("start", _i64p),
+                ("shape", _i64p)]
+
+
+_viewp = ctypes.POINTER(triot_view)
+_lib.triot_embed_view.restype = ctypes.c_int
+_lib.triot_embed_view.argtypes = [_viewp, _viewp, ctypes.c_int, ctypes.c_int, ctypes.c_uint, _vp]
+_lib.triot_apply_binary_view.restype = ctypes.c_int
+_lib.triot_apply_binary_view.argtypes = [_viewp, _viewp, _viewp, _i64p, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, _vp]
 _lib.triot_plan_describe.restype = ctypes.c_int
 _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
@@ -137,6 +149,25 @@ def triot_expected_value_mass(out: int, p: int, shape, d: int, dtype: int, works
                               workspace_bytes: int, stream: int) -> int:
     return _lib.triot_expected_value_mass(out, p, _shape(shape), d, dtype, workspace,
                                           workspace_bytes, stream)
+
+
+def make_view(data: int, base_shape, start, shape):
+    """A triot_view plus the arrays it points to (keep the tuple alive during the call)."""
+    bs, st, sh = _shape(base_shape), _shape(start) if start is not None else None, _shape(shape)
+    v = triot_view(data, ctypes.cast(bs, _i64p), ctypes.cast(st, _i64p) if st else _i64p(),
+                   ctypes.cast(sh, _i64p))
+    return v, (bs, st, sh)
+
+
+def triot_embed_view(dst: triot_view, src: triot_view, d: int, dtype: int, flags: int,
+                     stream: int) -> int:
+    return _lib.triot_embed_view(ctypes.byref(dst), ctypes.byref(src), d, dtype, flags, stream)
+
+
+def triot_apply_binary_view(c: triot_view, a: triot_view, b: triot_view, iter_shape, d: int,
+                            dtype: int, op: int, stream: int) -> int:
+    return _lib.triot_apply_binary_view(ctypes.byref(c), ctypes.byref(a), ctypes.byref(b),
+                                        _shape(iter_shape), d, dtype, op, stream)
 
 
 def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:

@@ -40,6 +40,53 @@ def _stream(device) -> int:
     return _torch().cuda.current_stream(device).cuda_stream
 
 
+class View:
+    """A window of a dense CUDA tensor: view[t] = base[start + t].  Ops on a View
+    behave as on a materialised copy of the window, without copying."""
+
+    def __init__(self, base, start=None, shape=None):
+        _check_tensor("view base", base)
+        d = base.dim()
+        self.base = base
+        self.start = tuple(int(x) for x in (start if start is not None else (0,) * d))
+        self.shape = tuple(int(x) for x in (shape if shape is not None else
+                                            tuple(b - s for b, s in zip(base.shape, self.start))))
+        if len(self.start) != d or len(self.shape) != d:
+            raise ValueError("start and shape must have the base's dimension")
+
+    def dim(self):
+        return self.base.dim()
+
+    def _c(self):
+        return _lib.make_view(self.base.data_ptr(), tuple(self.base.shape), self.start,
+                              self.shape)
+
+
+def embed_view(dst: "View", src: "View", region_only: bool = False):
+    """triot_embed_view: dst's window receives src's window, zero-padded."""
+    if dst.base.dtype != src.base.dtype or dst.dim() != src.dim():
+        raise ValueError("dst and src must have the same dtype and dimension")
+    if src.base.device != dst.base.device:
+        raise ValueError("dst and src must be on one device")
+    (dv, keep1), (sv, keep2) = dst._c(), src._c()
+    flags = _lib.TRIOT_EMBED_REGION_ONLY if region_only else _lib.TRIOT_EMBED_FULL
+    _lib.check(_lib.triot_embed_view(dv, sv, dst.dim(), _dtype_code(dst.base), flags,
+                                     _stream(dst.base.device)))
+    return dst
+
+
+def apply_binary_view(a: "View", b: "View", out: "View", op: str = "mul", iter_shape=None):
+    """triot_apply_binary_view: out_view[t] = a_view[t] OP b_view[t] over iter_shape."""
+    for v in (a, b, out):
+        if v.base.dtype != a.base.dtype or v.dim() != a.dim():
+            raise ValueError("views must share dtype and dimension")
+    (cv, k1), (av, k2), (bv, k3) = out._c(), a._c(), b._c()
+    _lib.check(_lib.triot_apply_binary_view(cv, av, bv, iter_shape, a.dim(),
+                                            _dtype_code(a.base), OPS[op],
+                                            _stream(a.base.device)))
+    return out
+
+
 def embed(dst, src, region_only: bool = False):
     """dst[t] = src[t] where t < src.shape, +0.0 elsewhere (or only the overlap if
     region_only).  In place on dst; returns dst."""

@@ -287,6 +287,27 @@ int triot_apply_binary(void* c, const int64_t* c_shape, const void* a, const int
   return st;
 }
 
+int triot_embed_view(const triot_view* dst, const triot_view* src, int d, int dtype,
+                     unsigned flags, void* cuda_stream) {
+  Geom g;
+  int st = plan_embed_view(g, dst, src, d, dtype, flags);
+  if (st || g.empty) return st;
+  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if (!st) clear_error();
+  return st;
+}
+
+int triot_apply_binary_view(const triot_view* c, const triot_view* a, const triot_view* b,
+                            const int64_t* iter_shape, int d, int dtype, int op,
+                            void* cuda_stream) {
+  Geom g;
+  int st = plan_binary_view(g, c, a, b, iter_shape, d, dtype, op);
+  if (st || g.empty) return st;
+  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if (!st) clear_error();
+  return st;
+}
+
 int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, size_t* bytes) {
   if (!bytes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: bytes is NULL");
   Geom g;

@@ -366,33 +366,103 @@ void set_decomposition(Geom& g, int mode, uint64_t warps) {
 
 // ------------------------------------------------------------------------------ public planners
 
-int plan_embed(Geom& g, void* dst, const int64_t* dst_shape, const void* src,
-               const int64_t* src_shape, int d, int dtype, unsigned flags) {
-  g = Geom();
+// A tensor argument: a window of `shape` extents whose element t sits at ptr + Horner(t, base)
+// elements -- a dense tensor (window == base, start 0) or a view (bias =
+// tuple_to_index(start, base_shape); element t of the slice is base.flat[bias + Horner(t, base)]).
+struct TArg {
+  const char* name;
+  const void* ptr;             // the window's element 0 (base + bias)
+  int64_t shape[TRIOT_MAXD];   // window extents
+  uint64_t sig[TRIOT_MAXD];    // Horner strides of the base shape
+  uint64_t numel;              // window elements
+  uint64_t span;               // elements from ptr through the window's last element (0 if empty)
+};
+
+static void targ_span(TArg& t, int d) {
+  if (t.numel == 0) {
+    t.span = 0;
+    return;
+  }
+  uint64_t last = 0;
+  for (int k = 0; k < d; ++k) last += (uint64_t)(t.shape[k] - 1) * t.sig[k];
+  t.span = last + 1;
+}
+
+static int targ_dense(TArg& t, const char* name, const void* ptr, const int64_t* shape, int d,
+                      int esz) {
+  int st;
+  t.name = name;
+  if ((st = check_shape(name, shape, d, esz, &t.numel))) return st;
+  for (int k = 0; k < d; ++k) t.shape[k] = shape[k];
+  strides_of(shape, d, t.sig);
+  t.ptr = ptr;
+  targ_span(t, d);
+  return TRIOT_OK;
+}
+
+static int targ_view(TArg& t, const char* name, const triot_view* v, int d, int esz) {
+  int st;
+  t.name = name;
+  if (!v) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: view '%s' is NULL", name);
+  uint64_t nbase;
+  if ((st = check_shape(name, v->base_shape, d, esz, &nbase))) return st;
+  if ((st = check_shape(name, v->shape, d, esz, &t.numel))) return st;
+  strides_of(v->base_shape, d, t.sig);
+  uint64_t bias = 0;
+  for (int k = 0; k < d; ++k) {
+    const int64_t s0 = v->start ? v->start[k] : 0;
+    if (s0 < 0 || s0 + v->shape[k] > v->base_shape[k])
+      return set_error(TRIOT_ERR_AXIS_OUT_OF_BOUNDS,
+                       "AxisOutOfBounds: view '%s' axis %d: start %lld + window %lld > base "
+                       "extent %lld",
+                       name, k, (long long)s0, (long long)v->shape[k],
+                       (long long)v->base_shape[k]);
+    t.shape[k] = v->shape[k];
+    bias += (uint64_t)s0 * t.sig[k];  // Horner of the start tuple
+  }
+  if ((st = check_ptr(name, v->data, t.numel, esz))) return st;
+  t.ptr = (const char*)v->data + bias * (uint64_t)esz;
+  targ_span(t, d);
+  return TRIOT_OK;
+}
+
+static bool targ_overlap(const TArg& a, const TArg& b, int esz) {
+  return overlap(a.ptr, a.span, b.ptr, b.span, esz);
+}
+
+static bool targ_same(const TArg& a, const TArg& b, int d) {
+  if (a.ptr != b.ptr) return false;
+  for (int k = 0; k < d; ++k)
+    if (a.shape[k] != b.shape[k] || a.sig[k] != b.sig[k]) return false;
+  return true;
+}
+
+static int check_common(int d, int dtype, int* esz) {
   if (d < 1 || d > TRIOT_MAXD)
     return set_error(TRIOT_ERR_UNSUPPORTED_DIMENSION,
                      "UnsupportedDimension: d = %d, supported 1..%d", d, TRIOT_MAXD);
-  int esz = dtype_size(dtype);
-  if (!esz) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadDtype: dtype = %d", dtype);
-  if (flags & ~1u) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadFlags: flags = %u", flags);
-  uint64_t nd, ns;
-  int st;
-  if ((st = check_shape("dst", dst_shape, d, esz, &nd))) return st;
-  if ((st = check_shape("src", src_shape, d, esz, &ns))) return st;
+  *esz = dtype_size(dtype);
+  if (!*esz) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadDtype: dtype = %d", dtype);
+  return TRIOT_OK;
+}
+
+static int plan_embed_core(Geom& g, const TArg& dst, const TArg& src, int d, int dtype, int esz,
+                           unsigned flags) {
   bool region = (flags & TRIOT_EMBED_REGION_ONLY) != 0;
   uint64_t n[TRIOT_MAXD], bnd[TRIOT_MAXD];
   uint64_t N = 1;
   for (int k = 0; k < d; ++k) {
-    uint64_t D_ = (uint64_t)dst_shape[k], S = (uint64_t)src_shape[k];
+    uint64_t D_ = (uint64_t)dst.shape[k], S = (uint64_t)src.shape[k];
     n[k] = region ? (D_ < S ? D_ : S) : D_;
     bnd[k] = S < n[k] ? S : n[k];
     N *= n[k];
   }
-  if ((st = check_ptr("dst", dst, nd, esz))) return st;
+  int st;
+  if ((st = check_ptr("dst", dst.ptr, dst.numel, esz))) return st;
   // src is read only where t < src_shape inside the counter
-  bool reads_src = N > 0 && ns > 0;
-  if ((st = check_ptr("src", src, reads_src ? ns : 0, esz))) return st;
-  if (reads_src && overlap(dst, nd, src, ns, esz))
+  bool reads_src = N > 0 && src.numel > 0;
+  if ((st = check_ptr("src", src.ptr, reads_src ? src.numel : 0, esz))) return st;
+  if (reads_src && targ_overlap(dst, src, esz))
     return set_error(TRIOT_ERR_ALIASING, "Aliasing: dst and src overlap");
   g.op = OP_EMBED;
   g.esz = esz;
@@ -400,86 +470,79 @@ int plan_embed(Geom& g, void* dst, const int64_t* dst_shape, const void* src,
   g.flags = flags;
   g.d = d;
   g.ntensor = 2;
-  g.t[0].ptr = dst;
-  g.t[0].numel = nd;
-  g.t[1].ptr = src;
-  g.t[1].numel = ns;
+  g.t[0].ptr = dst.ptr;
+  g.t[0].numel = dst.span;
+  g.t[1].ptr = src.ptr;
+  g.t[1].numel = src.span;
   if (N == 0) {
     g.empty = true;
     clear_error();
     return TRIOT_OK;
   }
-  g.all_oob = ns == 0;
+  g.all_oob = src.numel == 0;
   uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
-  strides_of(dst_shape, d, sig[0]);
-  if (ns == 0) {
-    for (int k = 0; k < d; ++k) sig[1][k] = 0;
-  } else {
-    strides_of(src_shape, d, sig[1]);
+  for (int k = 0; k < d; ++k) {
+    sig[0][k] = dst.sig[k];
+    sig[1][k] = src.numel == 0 ? 0 : src.sig[k];
   }
   build(g, n, sig, bnd, /*allow_merge=*/true, /*bounds=*/!region);
   clear_error();
   return TRIOT_OK;
 }
 
-int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const int64_t* a_shape,
-                const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
-                int dtype, int op) {
+int plan_embed(Geom& g, void* dst, const int64_t* dst_shape, const void* src,
+               const int64_t* src_shape, int d, int dtype, unsigned flags) {
   g = Geom();
-  if (d < 1 || d > TRIOT_MAXD)
-    return set_error(TRIOT_ERR_UNSUPPORTED_DIMENSION,
-                     "UnsupportedDimension: d = %d, supported 1..%d", d, TRIOT_MAXD);
-  int esz = dtype_size(dtype);
-  if (!esz) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadDtype: dtype = %d", dtype);
-  if (op < TRIOT_ADD || op > TRIOT_DIV)
-    return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
-  uint64_t na_, nb_, nc_, ni_;
-  int st;
-  if ((st = check_shape("a", a_shape, d, esz, &na_))) return st;
-  if ((st = check_shape("b", b_shape, d, esz, &nb_))) return st;
-  int64_t it[TRIOT_MAXD];
-  if (iter_shape) {
-    if ((st = check_shape("iter", iter_shape, d, esz, &ni_))) return st;
-    for (int k = 0; k < d; ++k) it[k] = iter_shape[k];
-  } else {
-    for (int k = 0; k < d; ++k) it[k] = a_shape[k] < b_shape[k] ? a_shape[k] : b_shape[k];
-  }
-  int64_t cs[TRIOT_MAXD];
-  if (c_shape) {
-    if ((st = check_shape("c", c_shape, d, esz, &nc_))) return st;
-    for (int k = 0; k < d; ++k) cs[k] = c_shape[k];
-  } else {
-    for (int k = 0; k < d; ++k) cs[k] = it[k];
-  }
-  check_shape("iter", it, d, esz, &ni_);
-  check_shape("c", cs, d, esz, &nc_);
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  if (flags & ~1u) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadFlags: flags = %u", flags);
+  TArg td, ts;
+  if ((st = targ_dense(td, "dst", dst, dst_shape, d, esz))) return st;
+  if ((st = targ_dense(ts, "src", src, src_shape, d, esz))) return st;
+  if ((st = check_ptr("dst", dst, td.numel, esz))) return st;
+  return plan_embed_core(g, td, ts, d, dtype, esz, flags);
+}
+
+int plan_embed_view(Geom& g, const triot_view* dst, const triot_view* src, int d, int dtype,
+                    unsigned flags) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  if (flags & ~1u) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadFlags: flags = %u", flags);
+  TArg td, ts;
+  if ((st = targ_view(td, "dst", dst, d, esz))) return st;
+  if ((st = targ_view(ts, "src", src, d, esz))) return st;
+  return plan_embed_core(g, td, ts, d, dtype, esz, flags);
+}
+
+static int plan_binary_core(Geom& g, const TArg& c, const TArg& a, const TArg& b,
+                            const int64_t* it, int d, int dtype, int esz, int op) {
+  uint64_t ni = 1;
+  for (int k = 0; k < d; ++k) ni *= (uint64_t)it[k];
   // check_tensor_pack_bounds: the iteration shape must lie inside every operand
-  const char* names[3] = {"c", "a", "b"};
-  const int64_t* shp[3] = {cs, a_shape, b_shape};
+  const TArg* ts[3] = {&c, &a, &b};
   for (int x = 0; x < 3; ++x)
     for (int k = 0; k < d; ++k)
-      if (it[k] > shp[x][k])
+      if (it[k] > ts[x]->shape[k])
         return set_error(TRIOT_ERR_AXIS_OUT_OF_BOUNDS,
                          "AxisOutOfBounds: tensor '%s' axis %d: iteration extent %lld > tensor "
                          "extent %lld",
-                         names[x], k, (long long)it[k], (long long)shp[x][k]);
-  if ((st = check_ptr("c", c, nc_, esz))) return st;
-  if ((st = check_ptr("a", a, ni_ ? na_ : 0, esz))) return st;
-  if ((st = check_ptr("b", b, ni_ ? nb_ : 0, esz))) return st;
-  if (ni_) {
-    const void* ins[2] = {a, b};
-    const uint64_t nin[2] = {na_, nb_};
-    const int64_t* ishp[2] = {a_shape, b_shape};
-    for (int x = 0; x < 2; ++x) {
-      if (!overlap(c, nc_, ins[x], nin[x], esz)) continue;
-      bool inplace = c == ins[x];
+                         ts[x]->name, k, (long long)it[k], (long long)ts[x]->shape[k]);
+  int st;
+  if ((st = check_ptr("c", c.ptr, c.numel, esz))) return st;
+  if (ni) {
+    for (int x = 1; x < 3; ++x)
+      if ((st = check_ptr(ts[x]->name, ts[x]->ptr, ts[x]->numel, esz))) return st;
+    for (int x = 1; x < 3; ++x) {
+      if (!targ_overlap(c, *ts[x], esz)) continue;
+      bool inplace = targ_same(c, *ts[x], d);
       for (int k = 0; k < d && inplace; ++k)
-        if (cs[k] != ishp[x][k] || it[k] != cs[k]) inplace = false;
+        if (it[k] != c.shape[k]) inplace = false;
       if (!inplace)
         return set_error(TRIOT_ERR_ALIASING,
                          "Aliasing: c overlaps '%s' (only exact in-place c == %s with equal "
                          "shapes and iteration shape is allowed)",
-                         names[x + 1], names[x + 1]);
+                         ts[x]->name, ts[x]->name);
     }
   }
   g.op = OP_BINARY;
@@ -488,13 +551,11 @@ int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const i
   g.binop = op;
   g.d = d;
   g.ntensor = 3;
-  g.t[0].ptr = c;
-  g.t[0].numel = nc_;
-  g.t[1].ptr = a;
-  g.t[1].numel = na_;
-  g.t[2].ptr = b;
-  g.t[2].numel = nb_;
-  if (ni_ == 0) {
+  for (int x = 0; x < 3; ++x) {
+    g.t[x].ptr = ts[x]->ptr;
+    g.t[x].numel = ts[x]->span;
+  }
+  if (ni == 0) {
     g.empty = true;
     clear_error();
     return TRIOT_OK;
@@ -502,12 +563,66 @@ int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const i
   uint64_t n[TRIOT_MAXD];
   for (int k = 0; k < d; ++k) n[k] = (uint64_t)it[k];
   uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
-  strides_of(cs, d, sig[0]);
-  strides_of(a_shape, d, sig[1]);
-  strides_of(b_shape, d, sig[2]);
+  for (int x = 0; x < 3; ++x)
+    for (int k = 0; k < d; ++k) sig[x][k] = ts[x]->sig[k];
   build(g, n, sig, nullptr, /*allow_merge=*/true, /*bounds=*/false);
   clear_error();
   return TRIOT_OK;
+}
+
+static int check_binop(int op) {
+  if (op < TRIOT_ADD || op > TRIOT_DIV)
+    return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
+  return TRIOT_OK;
+}
+
+int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const int64_t* a_shape,
+                const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
+                int dtype, int op) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  if ((st = check_binop(op))) return st;
+  TArg ta, tb, tc;
+  if ((st = targ_dense(ta, "a", a, a_shape, d, esz))) return st;
+  if ((st = targ_dense(tb, "b", b, b_shape, d, esz))) return st;
+  int64_t it[TRIOT_MAXD];
+  if (iter_shape) {
+    uint64_t ni;
+    if ((st = check_shape("iter", iter_shape, d, esz, &ni))) return st;
+    for (int k = 0; k < d; ++k) it[k] = iter_shape[k];
+  } else {
+    for (int k = 0; k < d; ++k) it[k] = a_shape[k] < b_shape[k] ? a_shape[k] : b_shape[k];
+  }
+  if ((st = targ_dense(tc, "c", c, c_shape ? c_shape : it, d, esz))) return st;
+  uint64_t ni = 1;
+  for (int k = 0; k < d; ++k) ni *= (uint64_t)it[k];
+  // element alignment of every operand that is touched
+  if ((st = check_ptr("c", c, tc.numel, esz))) return st;
+  if ((st = check_ptr("a", a, ni ? ta.numel : 0, esz))) return st;
+  if ((st = check_ptr("b", b, ni ? tb.numel : 0, esz))) return st;
+  return plan_binary_core(g, tc, ta, tb, it, d, dtype, esz, op);
+}
+
+int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const triot_view* b,
+                     const int64_t* iter_shape, int d, int dtype, int op) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  if ((st = check_binop(op))) return st;
+  TArg ta, tb, tc;
+  if ((st = targ_view(ta, "a", a, d, esz))) return st;
+  if ((st = targ_view(tb, "b", b, d, esz))) return st;
+  if ((st = targ_view(tc, "c", c, d, esz))) return st;
+  int64_t it[TRIOT_MAXD];
+  if (iter_shape) {
+    uint64_t ni;
+    if ((st = check_shape("iter", iter_shape, d, esz, &ni))) return st;
+    for (int k = 0; k < d; ++k) it[k] = iter_shape[k];
+  } else {
+    for (int k = 0; k < d; ++k) it[k] = ta.shape[k] < tb.shape[k] ? ta.shape[k] : tb.shape[k];
+  }
+  return plan_binary_core(g, tc, ta, tb, it, d, dtype, esz, op);
 }
 
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype) {

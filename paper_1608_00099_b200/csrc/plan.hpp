@@ -13,6 +13,7 @@
 
 #include <string>
 
+#include "../../include/triot.h"
 #include "desc.h"
 
 namespace triot {
@@ -60,6 +61,11 @@ int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const i
                 const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
                 int dtype, int op);
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype);
+// NEXT-1: the same ops on views
+int plan_embed_view(Geom& g, const triot_view* dst, const triot_view* src, int d, int dtype,
+                    unsigned flags);
+int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const triot_view* b,
+                     const int64_t* iter_shape, int d, int dtype, int op);
 
 // Work decomposition over `warps` warps: mode 0 = contiguous chunk per warp, 1 = grid stride,
 // 2 = contiguous chunk per block (EV bulk-copy kernel; `warps` is then the number of blocks).

@@ -350,3 +350,53 @@ def test_no_writes_outside_outputs(dtype):
         assert torch.all(c[mask] == sentinel)
         ref = O.apply_binary(src, src, "add", iter_shape=ish)
         assert_bits_equal(inside.contiguous(), ref)
+
+
+# ---------------------------------------------------------------- NEXT-1: views
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("seed", range(10))
+def test_views_vs_oracle(seed, dtype):
+    rng = np.random.default_rng(7000 + seed)
+    d = int(rng.integers(1, 9))
+    hi = 7 if d > 4 else 40
+    base_a = rng.standard_normal(random_shape(rng, d, 50000, lo=2, hi=hi)).astype(dtype)
+    win = tuple(int(rng.integers(1, s + 1)) for s in base_a.shape)
+    if seed % 3 == 0:
+        win = win[:-1] + (min(base_a.shape[-1], int(rng.choice([1, 2, 3, 4]))),)
+    sa = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base_a.shape, win))
+    base_b = rng.standard_normal(tuple(w + int(rng.integers(0, 3)) for w in win)).astype(dtype)
+    sb = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base_b.shape, win))
+    base_c = np.full(tuple(w + int(rng.integers(0, 3)) for w in win), 7.0, dtype=dtype)
+    sc = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base_c.shape, win))
+    op = ["add", "sub", "mul", "div"][seed % 4]
+    ref = base_c.copy()
+    O.apply_binary_view(ref, sc, base_a, sa, base_b, sb, win, op)
+    c = _dev(base_c)
+    T.apply_binary_view(T.View(_dev(base_a), sa, win), T.View(_dev(base_b), sb, win),
+                        T.View(c, sc, win), op=op)
+    assert_bits_equal(c, ref)
+    # embed view -> view (pad/crop), dst base outside its window untouched
+    dwin = tuple(max(1, w + int(rng.integers(-1, 3))) for w in win)
+    dbase = np.full(tuple(w + 3 for w in dwin), np.nan, dtype=dtype)
+    ds = tuple(int(rng.integers(0, 4)) for _ in dwin)
+    for region in (False, True):
+        refd = dbase.copy()
+        O.embed_view(refd, ds, dwin, base_a, sa, win, region_only=region)
+        dt = _dev(dbase)
+        T.embed_view(T.View(dt, ds, dwin), T.View(_dev(base_a), sa, win), region_only=region)
+        assert_bits_equal(dt, refd)
+
+
+def test_view_centered_fft_padding():
+    """The FFT-padding use with the signal placed at an offset: a (384)^3 f32 src embedded
+    at (64,64,64) of a (512)^3 dst whose other elements must become +0.0: zero the dst with a
+    full embed of an empty window, then embed the src into the interior window."""
+    src = make_inputs("C2")["src"]
+    dst = torch.full((512,) * 3, float("nan"), dtype=torch.float32, device=DEV)
+    T.embed(dst, torch.empty((0, 0, 0), dtype=torch.float32, device=DEV))
+    T.embed_view(T.View(dst, (64, 64, 64), (384,) * 3), T.View(_dev(src)))
+    torch.cuda.synchronize()
+    ref = np.zeros((512,) * 3, np.float32)
+    ref[64:448, 64:448, 64:448] = src
+    assert_bits_equal(dst, ref)
