@@ -82,6 +82,14 @@ def lib():
                                                    ctypes.c_void_p, _u64p, _u64p,
                                                    ctypes.c_void_p, _u64p, _u64p, _u64p,
                                                    ctypes.c_uint, ctypes.c_int, ctypes.c_int]
+            L.oracle_inner_product.restype = None
+            L.oracle_inner_product.argtypes = [_dblp, _dblp, ctypes.c_void_p, _u64p,
+                                               ctypes.c_void_p, _u64p, _u64p, ctypes.c_uint,
+                                               ctypes.c_int]
+            L.oracle_fused_update.restype = None
+            L.oracle_fused_update.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_void_p, _u64p,
+                                              ctypes.c_void_p, _u64p, ctypes.c_uint,
+                                              ctypes.c_int]
             _lib = L
     return _lib
 
@@ -218,3 +226,25 @@ def apply_binary_view(c_base: np.ndarray, c_start, a_base: np.ndarray, a_start,
                                    _ptr(b_base), _shape(b_base.shape), _shape(b_start),
                                    _shape(iter_shape), d, _dtype_code(a_base), OPS[op])
     return c_base
+
+
+# -- NEXT-2 / NEXT-3: Benchmarks 2 and 3 --------------------------------------------------
+
+def inner_product(a: np.ndarray, b: np.ndarray, iter_shape=None, with_plain: bool = False):
+    """Alg 8 dot_product over iter_shape (default: the shared tuples, min shape)."""
+    assert a.dtype == b.dtype and a.ndim == b.ndim
+    if iter_shape is None:
+        iter_shape = tuple(min(x, y) for x, y in zip(a.shape, b.shape))
+    out, plain = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    lib().oracle_inner_product(ctypes.byref(out), ctypes.byref(plain), _ptr(a), _shape(a.shape),
+                               _ptr(b), _shape(b.shape), _shape(iter_shape), a.ndim,
+                               _dtype_code(a))
+    return (out.value, plain.value) if with_plain else out.value
+
+
+def fused_update(x: np.ndarray, y: np.ndarray, z: np.ndarray) -> np.ndarray:
+    """Benchmark 3, in place on x: x[t] = x[t] + y[t]*x[t] - z[t] over x's shape."""
+    assert x.dtype == y.dtype == z.dtype and x.ndim == y.ndim == z.ndim
+    lib().oracle_fused_update(_ptr(x), _shape(x.shape), _ptr(y), _shape(y.shape), _ptr(z),
+                              _shape(z.shape), x.ndim, _dtype_code(x))
+    return x

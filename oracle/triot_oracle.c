@@ -324,3 +324,60 @@ void oracle_apply_binary_view(void* c, const u64* c_base, const u64* c_start, co
     oracle_advance_tuple(t, iter_shape, dimension);
   }
 }
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT-2 / NEXT-3: the paper's Benchmarks 2 and 3
+ * ---------------------------------------------------------------------------------------- */
+
+/* Benchmark 2 / Alg 8 dot_product: tot += xV * yV over the tuples of iter_shape
+ * ("visiting only tuple indices shared by both").  *out = Neumaier-compensated sum of the
+ * fp64 products (each product rounded once), *plain = the literal sequential sum of Alg 8. */
+void oracle_inner_product(double* out, double* plain, const void* a, const u64* a_shape,
+                          const void* b, const u64* b_shape, const u64* iter_shape,
+                          unsigned int dimension, int dtype) {
+  u64 t[64];
+  u64 n = flat_size(iter_shape, dimension);
+  double sum = 0.0, comp = 0.0, tot = 0.0;
+  memset(t, 0, sizeof(t));
+  for (u64 i = 0; i < n; ++i) {
+    u64 ai = oracle_tuple_to_index(t, a_shape, dimension);
+    u64 bi = oracle_tuple_to_index(t, b_shape, dimension);
+    double xV = dtype == OR_F64 ? ((const double*)a)[ai] : (double)((const float*)a)[ai];
+    double yV = dtype == OR_F64 ? ((const double*)b)[bi] : (double)((const float*)b)[bi];
+    double term = xV * yV;
+    tot += term;
+    double s = sum + term;
+    if ((sum >= 0 ? sum : -sum) >= (term >= 0 ? term : -term))
+      comp += (sum - s) + term;
+    else
+      comp += (term - s) + sum;
+    sum = s;
+    oracle_advance_tuple(t, iter_shape, dimension);
+  }
+  *out = sum + comp;
+  if (plain) *plain = tot;
+}
+
+/* Benchmark 3: "x[t] <- x[t] + y[t] * x[t] - z[t] is performed for all tuples t that are
+ * valid with respect to the shape of x", written as apply_tensors with x by reference (the
+ * aliasing-safe idiom of P:601).  C evaluation order, one rounding per operation:
+ * (x + (y * x)) - z. */
+void oracle_fused_update(void* x, const u64* x_shape, const void* y, const u64* y_shape,
+                         const void* z, const u64* z_shape, unsigned int dimension, int dtype) {
+  u64 t[64];
+  u64 n = flat_size(x_shape, dimension);
+  memset(t, 0, sizeof(t));
+  for (u64 i = 0; i < n; ++i) {
+    u64 xi = oracle_tuple_to_index(t, x_shape, dimension);
+    u64 yi = oracle_tuple_to_index(t, y_shape, dimension);
+    u64 zi = oracle_tuple_to_index(t, z_shape, dimension);
+    if (dtype == OR_F64) {
+      double* xv = (double*)x;
+      xv[xi] = xv[xi] + ((const double*)y)[yi] * xv[xi] - ((const double*)z)[zi];
+    } else {
+      float* xv = (float*)x;
+      xv[xi] = xv[xi] + ((const float*)y)[yi] * xv[xi] - ((const float*)z)[zi];
+    }
+    oracle_advance_tuple(t, x_shape, dimension);
+  }
+}

@@ -418,3 +418,62 @@ def test_pmf_product_over_intersecting_support():
     O.apply_binary_view(C, (0, 0), A, a_start, B, b_start, win, "mul")
     ref = A[2:2 + win[0], 1:1 + win[1]] * B[0:win[0], 0:win[1]]
     np.testing.assert_array_equal(C, ref)
+
+
+# ---------------------------------------------------------------- NEXT-2: Benchmark 2 inner product
+
+def test_inner_product_examples():
+    """x = [[1,2],[3,4]], y = 3x3 identity, over (2,2) -> 5."""
+    x = np.array([[1.0, 2.0], [3.0, 4.0]])
+    assert O.inner_product(x, np.eye(3)) == 5.0
+    assert O.inner_product(x, np.zeros((3, 3))) == 0.0
+
+
+def test_inner_product_exact_and_numpy():
+    rng = np.random.default_rng(31)
+    for d in (1, 2, 3, 5):
+        sa = random_shape(rng, d, 2000, lo=1, hi=9)
+        sb = tuple(s + int(rng.integers(-1, 3)) if s > 1 else s for s in sa)
+        a = rng.integers(-100, 100, size=sa).astype(np.float64)
+        b = rng.integers(-100, 100, size=sb).astype(np.float64)
+        ish = tuple(min(x, y) for x, y in zip(sa, sb))
+        sl = tuple(slice(0, m) for m in ish)
+        exact = int(np.sum(a[sl].astype(np.int64) * b[sl].astype(np.int64)))
+        assert O.inner_product(a, b) == float(exact)
+    # real values: within 1e-15 of the exact rational sum (tiny) and of numpy (1e-13)
+    a = rng.standard_normal((3, 4, 5)); b = rng.standard_normal((4, 4, 6))
+    ish = (3, 4, 5)
+    exact = sum(Fraction(float(a[t])) * Fraction(float(b[t])) for t in brute_tuples(ish))
+    got = O.inner_product(a, b)
+    scale = sum(abs(Fraction(float(a[t])) * Fraction(float(b[t]))) for t in brute_tuples(ish))
+    # each product is rounded once (rel 2^-53); the compensated sum adds no more than that
+    assert abs(Fraction(got) - exact) <= Fraction(1, 10 ** 15) * scale
+    big_a = rng.standard_normal((64, 32, 16)); big_b = rng.standard_normal((32, 32, 8))
+    ref = float(np.dot(big_a[:32, :32, :8].ravel(), big_b.ravel()))
+    assert abs(O.inner_product(big_a, big_b) - ref) <= 1e-12 * np.sum(np.abs(big_a[:32, :32, :8] * big_b))
+
+
+# ---------------------------------------------------------------- NEXT-3: Benchmark 3 fused update
+
+def test_fused_update_examples():
+    """x=[2], y=[3], z=[1] -> 2 + 3*2 - 1 = 7; y = z = 0 leaves x unchanged."""
+    x = np.array([2.0]); O.fused_update(x, np.array([3.0]), np.array([1.0]))
+    assert x.tolist() == [7.0]
+    x = np.random.default_rng(1).random((3, 4)); x0 = x.copy()
+    O.fused_update(x, np.zeros((5, 5)), np.zeros((3, 4)))
+    np.testing.assert_array_equal(x, x0)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_fused_update_vs_numpy(dtype):
+    """numpy evaluates (x + (y*x)) - z with one rounding per operation, like C with contraction
+    off: bit-exact on the paper's Benchmark-3 shape family (scaled down)."""
+    rng = np.random.default_rng(32)
+    x = random_values(rng, (9, 4, 13, 6), dtype, "normal")
+    y = random_values(rng, (12, 8, 15, 7), dtype, "normal")
+    z = random_values(rng, (10, 5, 16, 9), dtype, "normal")
+    sl = tuple(slice(0, s) for s in x.shape)
+    ref = (x + (y[sl] * x)) - z[sl]
+    got = x.copy()
+    O.fused_update(got, y, z)
+    np.testing.assert_array_equal(_bits(got), _bits(ref))
