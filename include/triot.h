@@ -200,6 +200,34 @@ TRIOT_API int triot_apply_binary_view(const triot_view* c, const triot_view* a,
                                       const triot_view* b, const int64_t* iter_shape, int d,
                                       int dtype, int op, void* cuda_stream);
 
+/* ---- NEXT-2 / NEXT-3: the paper's Benchmarks 2 and 3 ----------------------------- */
+
+/* Workspace bytes triot_inner_product needs (zero-filled once; the call leaves it ready). */
+TRIOT_API int triot_inner_product_workspace_size(size_t* bytes);
+
+/*
+ * triot_inner_product -- Benchmark 2: "an inner product between two tensors ... (visiting only
+ * tuple indices shared by both)", i.e. Alg 8's dot_product:
+ *   *out = sum over t in prod[0, iter_shape[k]) of a[t] * b[t]
+ * with a and b each indexed by its own shape; iter_shape NULL = element-wise min of the shapes.
+ * fp64 accumulation (f32 inputs are widened), deterministic run to run.
+ *   out: device pointer to one double.  workspace: see triot_inner_product_workspace_size.
+ */
+TRIOT_API int triot_inner_product(double* out, const void* a, const int64_t* a_shape,
+                                  const void* b, const int64_t* b_shape,
+                                  const int64_t* iter_shape, int d, int dtype, void* workspace,
+                                  size_t workspace_bytes, void* cuda_stream);
+
+/*
+ * triot_fused_update -- Benchmark 3: "x[t] <- x[t] + y[t] * x[t] - z[t] is performed for all
+ * tuples t that are valid with respect to the shape of x", in place on x (the
+ * aliasing-safe apply_tensors idiom of P:601).  Evaluated as (x + (y * x)) - z with one IEEE
+ * round-to-nearest rounding per operation.  y and z must contain x's shape and not overlap x.
+ */
+TRIOT_API int triot_fused_update(void* x, const int64_t* x_shape, const void* y,
+                                 const int64_t* y_shape, const void* z, const int64_t* z_shape,
+                                 int d, int dtype, void* cuda_stream);
+
 /* ---- diagnostics (host only; no device work, usable without a GPU) ---------------------- */
 
 /*
@@ -210,7 +238,9 @@ TRIOT_API int triot_apply_binary_view(const triot_view* c, const triot_view* a,
  *   op: 0 = embed (shapes[0]=dst, shapes[1]=src, flags as triot_embed),
  *       1 = binary (shapes[0]=c or NULL, shapes[1]=a, shapes[2]=b, iter or NULL; `flags`
  *           carries the triot_binop),
- *       2 = expected value (shapes[0]=p).
+ *       2 = expected value (shapes[0]=p),
+ *       3 = inner product (shapes[0]=a, shapes[1]=b, iter or NULL),
+ *       4 = fused update (shapes[0]=x, shapes[1]=y, shapes[2]=z).
  *   ptr_mod32: byte offsets modulo 32 of each tensor's data pointer (alignment model).
  *   mode, warps: the work decomposition to describe (0 = contiguous chunk per warp, 1 = grid
  *              stride, over `warps` warps; 2 = contiguous chunk per block of the expected-value

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libtriot.so")
 TRIOT_F32, TRIOT_F64 = 0, 1
 TRIOT_ADD, TRIOT_SUB, TRIOT_MUL, TRIOT_DIV = 0, 1, 2, 3
 TRIOT_EMBED_FULL, TRIOT_EMBED_REGION_ONLY = 0, 1
-OP_EMBED, OP_BINARY, OP_EV = 0, 1, 2
+OP_EMBED, OP_BINARY, OP_EV, OP_DOT, OP_UPDATE = 0, 1, 2, 3, 4
 
 STATUS = {
     0: "TRIOT_OK", 1: "TRIOT_ERR_NULL_POINTER", 2: "TRIOT_ERR_UNSUPPORTED_DIMENSION",
@@ -28,6 +28,7 @@ STATUS = {
 EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "triot_embed",
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
            "triot_expected_value_mass", "triot_embed_view", "triot_apply_binary_view",
+           "triot_inner_product_workspace_size", "triot_inner_product", "triot_fused_update",
            "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
@@ -79,6 +80,14 @@ _lib.triot_embed_view.argtypes = [_viewp, _viewp, ctypes.c_int, ctypes.c_int, ct
 _lib.triot_apply_binary_view.restype = ctypes.c_int
 _lib.triot_apply_binary_view.argtypes = [_viewp, _viewp, _viewp, _i64p, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, _vp]
+_lib.triot_inner_product_workspace_size.restype = ctypes.c_int
+_lib.triot_inner_product_workspace_size.argtypes = [ctypes.POINTER(ctypes.c_size_t)]
+_lib.triot_inner_product.restype = ctypes.c_int
+_lib.triot_inner_product.argtypes = [_vp, _vp, _i64p, _vp, _i64p, _i64p, ctypes.c_int,
+                                     ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+_lib.triot_fused_update.restype = ctypes.c_int
+_lib.triot_fused_update.argtypes = [_vp, _i64p, _vp, _i64p, _vp, _i64p, ctypes.c_int,
+                                    ctypes.c_int, _vp]
 _lib.triot_plan_describe.restype = ctypes.c_int
 _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
@@ -168,6 +177,25 @@ def triot_apply_binary_view(c: triot_view, a: triot_view, b: triot_view, iter_sh
                             dtype: int, op: int, stream: int) -> int:
     return _lib.triot_apply_binary_view(ctypes.byref(c), ctypes.byref(a), ctypes.byref(b),
                                         _shape(iter_shape), d, dtype, op, stream)
+
+
+def triot_inner_product_workspace_size() -> int:
+    out = ctypes.c_size_t(0)
+    check(_lib.triot_inner_product_workspace_size(ctypes.byref(out)))
+    return int(out.value)
+
+
+def triot_inner_product(out: int, a: int, a_shape, b: int, b_shape, iter_shape, d: int,
+                        dtype: int, workspace: int, workspace_bytes: int, stream: int) -> int:
+    return _lib.triot_inner_product(out, a, _shape(a_shape), b, _shape(b_shape),
+                                    _shape(iter_shape), d, dtype, workspace, workspace_bytes,
+                                    stream)
+
+
+def triot_fused_update(x: int, x_shape, y: int, y_shape, z: int, z_shape, d: int, dtype: int,
+                       stream: int) -> int:
+    return _lib.triot_fused_update(x, _shape(x_shape), y, _shape(y_shape), z, _shape(z_shape), d,
+                                   dtype, stream)
 
 
 def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:

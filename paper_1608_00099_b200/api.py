@@ -154,3 +154,40 @@ def expected_value(p, out=None, with_mass: bool = False):
     _lib.check(fn(out.data_ptr(), p.data_ptr(), tuple(p.shape), d, code, ws.data_ptr(),
                   ws.numel(), _stream(p.device)))
     return out
+
+
+def inner_product(a, b, iter_shape=None, out=None):
+    """Benchmark 2 / Alg 8 dot_product: sum_t a[t] * b[t] over iter_shape (default: the shared
+    tuples).  Returns a (1,) float64 CUDA tensor."""
+    torch = _torch()
+    _check_tensor("a", a)
+    _check_tensor("b", b, a.device)
+    if a.dtype != b.dtype or a.dim() != b.dim():
+        raise ValueError("a and b must have the same dtype and dimension")
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=a.device)
+    need = _lib.triot_inner_product_workspace_size()
+    key = ("dot", a.device, _stream(a.device))
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device=a.device)
+            _ws_cache[key] = ws
+    _lib.check(_lib.triot_inner_product(out.data_ptr(), a.data_ptr(), tuple(a.shape),
+                                        b.data_ptr(), tuple(b.shape), iter_shape, a.dim(),
+                                        _dtype_code(a), ws.data_ptr(), ws.numel(),
+                                        _stream(a.device)))
+    return out
+
+
+def fused_update(x, y, z):
+    """Benchmark 3: x[t] = x[t] + y[t]*x[t] - z[t] over x's shape, in place; returns x."""
+    _check_tensor("x", x)
+    _check_tensor("y", y, x.device)
+    _check_tensor("z", z, x.device)
+    if not (x.dtype == y.dtype == z.dtype) or not (x.dim() == y.dim() == z.dim()):
+        raise ValueError("x, y, z must share dtype and dimension")
+    _lib.check(_lib.triot_fused_update(x.data_ptr(), tuple(x.shape), y.data_ptr(), tuple(y.shape),
+                                       z.data_ptr(), tuple(z.shape), x.dim(), _dtype_code(x),
+                                       _stream(x.device)))
+    return x

@@ -28,6 +28,10 @@ const void* triot_table_2_4_0(int, int, int);
 const void* triot_table_2_8_0(int, int, int);
 const void* triot_table_2_4_1(int, int, int);
 const void* triot_table_2_8_1(int, int, int);
+const void* triot_table_3_4_0(int, int, int);
+const void* triot_table_3_8_0(int, int, int);
+const void* triot_table_4_4_0(int, int, int);
+const void* triot_table_4_8_0(int, int, int);
 }
 
 namespace triot {
@@ -39,6 +43,8 @@ TableFn table_for(const Geom& g) {
   const bool e8 = g.esz == 8;
   if (g.op == OP_EMBED) return e8 ? triot_table_0_8_0 : triot_table_0_4_0;
   if (g.op == OP_EV) return e8 ? triot_table_2_8_0 : triot_table_2_4_0;
+  if (g.op == OP_DOT) return e8 ? triot_table_3_8_0 : triot_table_3_4_0;
+  if (g.op == OP_UPDATE) return e8 ? triot_table_4_8_0 : triot_table_4_4_0;
   static const TableFn b4[4] = {triot_table_1_4_0, triot_table_1_4_1, triot_table_1_4_2,
                                 triot_table_1_4_3};
   static const TableFn b8[4] = {triot_table_1_8_0, triot_table_1_8_1, triot_table_1_8_2,
@@ -79,6 +85,7 @@ thread_local Policy g_override = {-1, 0, 0};
 // reached 5.0-5.9 TB/s on C2/C4/C5; this reaches 6.5-6.8 TB/s (single launch, clean L2).
 Policy auto_policy(const Geom& g) {
   if (g.op == OP_EV) return Policy{0, 0, 0};
+  if (g.op == OP_DOT) return Policy{0, 8, 0};  // <= 2048 partials for the reduction
   return Policy{0, 64, 0};
 }
 
@@ -220,12 +227,13 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   const void* fn = table_for(g)(g.D, vindex(g), g.idx64 ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no instance for D=%d V=%d", g.D, g.V);
   int max_grid = 1 << 30;
-  if (g.op == OP_EV) max_grid = TRIOT_EV_MAX_GRID;
+  if (g.op == OP_EV || g.op == OP_DOT) max_grid = TRIOT_EV_MAX_GRID;
   unsigned grid;
   int st = launch_geometry(fn, g, max_grid, &grid);
   if (st) return st;
-  if (g.op == OP_EV) {
-    size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 2) * sizeof(double);
+  if (g.op == OP_EV || g.op == OP_DOT) {
+    const size_t slots = g.op == OP_DOT ? 1 : (size_t)(g.D + 2);
+    size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * slots * sizeof(double);
     if (!ws || ws_bytes < need)
       return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                        need);
@@ -308,6 +316,43 @@ int triot_apply_binary_view(const triot_view* c, const triot_view* a, const trio
   return st;
 }
 
+int triot_inner_product_workspace_size(size_t* bytes) {
+  if (!bytes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: bytes is NULL");
+  *bytes = TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * sizeof(double);
+  return TRIOT_OK;
+}
+
+int triot_inner_product(double* out, const void* a, const int64_t* a_shape, const void* b,
+                        const int64_t* b_shape, const int64_t* iter_shape, int d, int dtype,
+                        void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  Geom g;
+  int st = plan_dot(g, a, a_shape, b, b_shape, iter_shape, d, dtype);
+  if (st) return st;
+  if (!out) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: out is NULL");
+  if (((uintptr_t)out) % 8)
+    return set_error(TRIOT_ERR_MISALIGNED, "Misaligned: out is not 8-byte aligned");
+  if (g.empty) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    clear_error();
+    return TRIOT_OK;
+  }
+  st = launch(g, cuda_stream, out, workspace, workspace_bytes);
+  if (!st) clear_error();
+  return st;
+}
+
+int triot_fused_update(void* x, const int64_t* x_shape, const void* y, const int64_t* y_shape,
+                       const void* z, const int64_t* z_shape, int d, int dtype,
+                       void* cuda_stream) {
+  Geom g;
+  int st = plan_update(g, x, x_shape, y, y_shape, z, z_shape, d, dtype);
+  if (st || g.empty) return st;
+  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if (!st) clear_error();
+  return st;
+}
+
 int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, size_t* bytes) {
   if (!bytes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: bytes is NULL");
   Geom g;
@@ -376,6 +421,12 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
                      (const void*)base[2], shapes[2], iter_shape, d, dtype, (int)flags);
   else if (op == OP_EV)
     st = plan_ev(g, (const void*)base[0], shapes[0], d, dtype);
+  else if (op == OP_DOT)
+    st = plan_dot(g, (const void*)base[0], shapes[0], (const void*)base[1], shapes[1], iter_shape,
+                  d, dtype);
+  else if (op == OP_UPDATE)
+    st = plan_update(g, (void*)base[0], shapes[0], (const void*)base[1], shapes[1],
+                     (const void*)base[2], shapes[2], d, dtype);
   else
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
   if (st) return st;

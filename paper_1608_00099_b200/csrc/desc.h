@@ -22,7 +22,7 @@
 
 namespace triot {
 
-enum Op { OP_EMBED = 0, OP_BINARY = 1, OP_EV = 2 };
+enum Op { OP_EMBED = 0, OP_BINARY = 1, OP_EV = 2, OP_DOT = 3, OP_UPDATE = 4 };
 
 template <typename IDX>
 struct TensorAcc {
@@ -62,7 +62,8 @@ struct Desc {
   int32_t slot_of_axis[TRIOT_MAXD + 1];  // out[j] = slot >= 0 ? total[slot] : 0 (slot D+1 = mass)
   int32_t op;            // binary op
   int32_t pad_;
-  TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p
+  TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
+                                  // update: x, y, z
   void* out;             // EV: means (device)
   void* ws;              // EV: workspace (device)
 };

@@ -5,7 +5,8 @@
 // paper's compile-time note (max dimension 16 compiles in 16 s).  The table replaces
 // LinearTemplateSearch (Alg 7): runtime (D, V, index width) -> kernel in O(1).
 //
-//   TRIOT_INST_OP   0 = embed, 1 = binary, 2 = expected value
+//   TRIOT_INST_OP   0 = embed, 1 = binary, 2 = expected value, 3 = inner product,
+//                   4 = fused update
 //   TRIOT_INST_ESZ  4 or 8
 //   TRIOT_INST_BOP  binary op 0..3 (binary); 1 = bulk-copy variant (expected value)
 #include "kernels.cuh"
@@ -42,6 +43,10 @@ const void* kptr() {
   return (const void*)&embed_kernel<D, ESZ, V, IDX, KEMBED>;
 #elif TRIOT_INST_OP == 1
   return (const void*)&binary_kernel<D, ESZ, V, IDX, KBIN, TRIOT_INST_BOP>;
+#elif TRIOT_INST_OP == 3
+  return (const void*)&dot_kernel<D, ESZ, V, IDX, KBIN>;
+#elif TRIOT_INST_OP == 4
+  return (const void*)&update_kernel<D, ESZ, V, IDX, KBIN>;
 #elif TRIOT_INST_BOP == 1
   // EV bulk-copy fast path: only the 32-byte vector width exists
   return V == 32 / ESZ ? (const void*)&ev_tma_kernel<D, ESZ, IDX> : nullptr;

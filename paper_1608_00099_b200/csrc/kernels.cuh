@@ -583,6 +583,107 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
   ev_reduce<NS, kBlock, IDX>(d, acc);
 }
 
+// ------------------------------------------------------------------ NEXT-2: inner product
+// Benchmark 2 / Alg 8 dot_product: sum_t a[t] * b[t] over the iteration
+// shape, each operand indexed by its own shape.  fp64 accumulation (one fused multiply-add per
+// element), the EV's deterministic block/last-block reduction with one slot.
+template <int D, int ESZ, int V, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) dot_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  double acc[1] = {0.0};
+  pdl_trigger();
+  if (base0 < d.nvec) {
+    const IDX vend = warp_end(d, base0);
+    IDX u[D], off[2];
+    uint32_t oob;
+    IDX v = base0 + (IDX)lane;
+    odo_start<D, 2, false, IDX>(d, v, u, off, oob);
+    const uint32_t lgL = d.lgL;
+    pdl_wait();
+    for (IDX b = base0; b < vend; b += K * d.dv) {
+      uint32_t ba[K][NW], bb[K][NW];
+      bool valid[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        valid[j] = v < vend;
+        v += d.dv;
+        if (valid[j]) {
+          load_vec<ESZ, V, IDX>(d.t[0], off[0], lgL, ba[j]);
+          load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, bb[j]);
+        }
+        odo_step<D, 2, false, IDX>(d, u, off, oob);
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (!valid[j]) continue;
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          acc[0] = fma((double)Elem<ESZ>::get(ba[j] + e * EW),
+                       (double)Elem<ESZ>::get(bb[j] + e * EW), acc[0]);
+      }
+    }
+  } else {
+    pdl_wait();
+  }
+  ev_reduce<1, kBlock, IDX>(d, acc);
+}
+
+// ------------------------------------------------------------------ NEXT-3: fused update
+// Benchmark 3: x[t] <- x[t] + y[t] * x[t] - z[t] for every t of x's shape, in place on x
+// (the aliasing-safe apply_tensors idiom).  C evaluation order with one rounding per
+// operation: (x + (y * x)) - z.  Tensor 0 = x, 1 = y, 2 = z.
+template <int D, int ESZ, int V, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  using T = typename Elem<ESZ>::T;
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[3];
+  uint32_t oob;
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 3, false, IDX>(d, v, u, off, oob);
+  const uint32_t lgL = d.lgL;
+  pdl_wait();
+  for (IDX b = base0; b < vend; b += K * d.dv) {
+    uint32_t bx[K][NW], by[K][NW], bz[K][NW];
+    IDX xoff[K];
+    bool valid[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      valid[j] = v < vend;
+      v += d.dv;
+      xoff[j] = off[0];
+      if (valid[j]) {
+        load_vec<ESZ, V, IDX>(d.t[0], off[0], lgL, bx[j]);
+        load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, by[j]);
+        load_vec<ESZ, V, IDX>(d.t[2], off[2], lgL, bz[j]);
+      }
+      odo_step<D, 3, false, IDX>(d, u, off, oob);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (!valid[j]) continue;
+      uint32_t r[NW];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const T x = Elem<ESZ>::get(bx[j] + e * EW);
+        const T yx = bop<2>(Elem<ESZ>::get(by[j] + e * EW), x);
+        Elem<ESZ>::put(r + e * EW, bop<1>(bop<0>(x, yx), Elem<ESZ>::get(bz[j] + e * EW)));
+      }
+      store_vec<ESZ, V, IDX>(d.t[0], xoff[j], lgL, r);
+    }
+  }
+}
+
 // ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

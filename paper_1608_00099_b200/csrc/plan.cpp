@@ -625,6 +625,113 @@ int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const tr
   return plan_binary_core(g, tc, ta, tb, it, d, dtype, esz, op);
 }
 
+// NEXT-2: Benchmark 2 / Alg 8 dot_product over iter (NULL = the shared tuples).
+int plan_dot(Geom& g, const void* a, const int64_t* a_shape, const void* b,
+             const int64_t* b_shape, const int64_t* iter_shape, int d, int dtype) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  TArg ta, tb;
+  if ((st = targ_dense(ta, "a", a, a_shape, d, esz))) return st;
+  if ((st = targ_dense(tb, "b", b, b_shape, d, esz))) return st;
+  int64_t it[TRIOT_MAXD];
+  if (iter_shape) {
+    uint64_t ni;
+    if ((st = check_shape("iter", iter_shape, d, esz, &ni))) return st;
+    for (int k = 0; k < d; ++k) it[k] = iter_shape[k];
+  } else {
+    for (int k = 0; k < d; ++k) it[k] = a_shape[k] < b_shape[k] ? a_shape[k] : b_shape[k];
+  }
+  const TArg* ts[2] = {&ta, &tb};
+  uint64_t ni = 1;
+  for (int k = 0; k < d; ++k) ni *= (uint64_t)it[k];
+  for (int x = 0; x < 2; ++x) {
+    for (int k = 0; k < d; ++k)
+      if (it[k] > ts[x]->shape[k])
+        return set_error(TRIOT_ERR_AXIS_OUT_OF_BOUNDS,
+                         "AxisOutOfBounds: tensor '%s' axis %d: iteration extent %lld > tensor "
+                         "extent %lld",
+                         ts[x]->name, k, (long long)it[k], (long long)ts[x]->shape[k]);
+    if ((st = check_ptr(ts[x]->name, ts[x]->ptr, ni ? ts[x]->numel : 0, esz))) return st;
+  }
+  g.op = OP_DOT;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.d = d;
+  g.nout = 1;
+  g.ntensor = 2;
+  for (int x = 0; x < 2; ++x) {
+    g.t[x].ptr = ts[x]->ptr;
+    g.t[x].numel = ts[x]->span;
+  }
+  if (ni == 0) {
+    g.empty = true;
+    clear_error();
+    return TRIOT_OK;
+  }
+  uint64_t n[TRIOT_MAXD];
+  uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) {
+    n[k] = (uint64_t)it[k];
+    sig[0][k] = ta.sig[k];
+    sig[1][k] = tb.sig[k];
+  }
+  build(g, n, sig, nullptr, /*allow_merge=*/true, /*bounds=*/false);
+  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  g.slot_of_axis[0] = 0;
+  clear_error();
+  return TRIOT_OK;
+}
+
+// NEXT-3: Benchmark 3: x[t] <- x[t] + y[t]*x[t] - z[t] for t in x's shape, in place.
+int plan_update(Geom& g, void* x, const int64_t* x_shape, const void* y, const int64_t* y_shape,
+                const void* z, const int64_t* z_shape, int d, int dtype) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  TArg tx, ty, tz;
+  if ((st = targ_dense(tx, "x", x, x_shape, d, esz))) return st;
+  if ((st = targ_dense(ty, "y", y, y_shape, d, esz))) return st;
+  if ((st = targ_dense(tz, "z", z, z_shape, d, esz))) return st;
+  const TArg* ts[3] = {&tx, &ty, &tz};
+  for (int q = 1; q < 3; ++q)
+    for (int k = 0; k < d; ++k)
+      if (x_shape[k] > ts[q]->shape[k])
+        return set_error(TRIOT_ERR_AXIS_OUT_OF_BOUNDS,
+                         "AxisOutOfBounds: tensor '%s' axis %d: iteration extent %lld > tensor "
+                         "extent %lld",
+                         ts[q]->name, k, (long long)x_shape[k], (long long)ts[q]->shape[k]);
+  for (int q = 0; q < 3; ++q)
+    if ((st = check_ptr(ts[q]->name, ts[q]->ptr, tx.numel ? ts[q]->numel : 0, esz))) return st;
+  if (tx.numel)
+    for (int q = 1; q < 3; ++q)
+      if (targ_overlap(tx, *ts[q], esz))
+        return set_error(TRIOT_ERR_ALIASING, "Aliasing: x overlaps '%s'", ts[q]->name);
+  g.op = OP_UPDATE;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.d = d;
+  g.ntensor = 3;
+  for (int q = 0; q < 3; ++q) {
+    g.t[q].ptr = ts[q]->ptr;
+    g.t[q].numel = ts[q]->span;
+  }
+  if (tx.numel == 0) {
+    g.empty = true;
+    clear_error();
+    return TRIOT_OK;
+  }
+  uint64_t n[TRIOT_MAXD];
+  uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) {
+    n[k] = (uint64_t)x_shape[k];
+    for (int q = 0; q < 3; ++q) sig[q][k] = ts[q]->sig[k];
+  }
+  build(g, n, sig, nullptr, /*allow_merge=*/true, /*bounds=*/false);
+  clear_error();
+  return TRIOT_OK;
+}
+
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype) {
   g = Geom();
   if (d < 1 || d > TRIOT_MAXD)

@@ -45,6 +45,7 @@ struct Geom {
   int slot_of_axis[TRIOT_MAXD + 1] = {};
   int nslots = 0;
   bool with_mass = false;   // EV: also write sum(p) after the d means
+  int nout = -1;            // reduction outputs if not d (+mass): the inner product writes 1
   struct T {
     uint64_t sig[TRIOT_MAXD] = {}, kap[TRIOT_MAXD] = {};
     uint64_t step = 0, rho = 0, tau = 1;
@@ -61,6 +62,11 @@ int plan_binary(Geom& g, void* c, const int64_t* c_shape, const void* a, const i
                 const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
                 int dtype, int op);
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype);
+// NEXT-2 / NEXT-3: Benchmark 2 inner product and Benchmark 3 fused update
+int plan_dot(Geom& g, const void* a, const int64_t* a_shape, const void* b,
+             const int64_t* b_shape, const int64_t* iter_shape, int d, int dtype);
+int plan_update(Geom& g, void* x, const int64_t* x_shape, const void* y, const int64_t* y_shape,
+                const void* z, const int64_t* z_shape, int d, int dtype);
 // NEXT-1: the same ops on views
 int plan_embed_view(Geom& g, const triot_view* dst, const triot_view* src, int d, int dtype,
                     unsigned flags);
@@ -107,7 +113,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.srows = (IDX)g.srows;
   d.scols = (IDX)g.scols;
   d.collapsed = g.collapsed ? 1 : 0;
-  d.d_out = g.d + (g.with_mass ? 1 : 0);
+  d.d_out = g.nout >= 0 ? g.nout : g.d + (g.with_mass ? 1 : 0);
   d.op = g.binop;
   d.pad_ = 0;
   for (int x = 0; x < TRIOT_MAXT; ++x) {

@@ -98,6 +98,15 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
                                     vals[e] = bufs[1][eoff(1, off[1], e)]
                         for e in range(V):
                             bufs[0][eoff(0, off[0], e)] = vals[e]
+                    elif op == "dot":
+                        for e in range(V):
+                            slots[0] += float(bufs[0][eoff(0, off[0], e)]) * \
+                                float(bufs[1][eoff(1, off[1], e)])
+                    elif op == "update":
+                        for e in range(V):
+                            xi = eoff(0, off[0], e)
+                            x, y, z = bufs[0][xi], bufs[1][eoff(1, off[1], e)], bufs[2][eoff(2, off[2], e)]
+                            bufs[0][xi] = (x + (y * x)) - z
                     elif op == "binary":
                         fn = {"add": np.add, "sub": np.subtract, "mul": np.multiply,
                               "div": np.divide}[binop]
@@ -120,6 +129,8 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
                             slots[D - 1] += base * s_ + wc
                 u, off, oob = step(u, off, oob)
                 v += dv
+    if op == "dot":
+        return slots[0]
     if op == "ev":
         d = desc["d"]
         return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]

@@ -33,7 +33,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     decl = declared_symbols()
-    assert len(decl) == 13, decl
+    assert len(decl) == 16, decl
     out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))
@@ -306,3 +306,38 @@ def test_model_views_vs_oracle(seed):
                                       base_a.reshape(-1)[bias(sa, base_a.shape):],
                                       base_b.reshape(-1)[bias(sb, base_b.shape):]], binop="add")
     np.testing.assert_array_equal(out, ref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_model_dot_and_update_vs_oracle(seed):
+    rng = np.random.default_rng(5000 + seed)
+    d = int(rng.integers(1, 7))
+    ish = random_shape(rng, d, 2000, lo=1, hi=7 if d > 3 else 12)
+    a = rng.integers(-50, 50, size=tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(np.float64)
+    b = rng.integers(-50, 50, size=tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(np.float64)
+    desc = T.triot_plan_describe(3, [a.shape, b.shape], ish, d, F64, 0, mode=seed % 2,
+                                 warps=int(rng.integers(1, 6)))
+    got = kernel_model.run(desc, "dot", [a.reshape(-1), b.reshape(-1)])
+    assert got == O.inner_product(a, b, iter_shape=ish)          # integers: exact
+    x = rng.standard_normal(ish)
+    y = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in ish))
+    z = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in ish))
+    ref = x.copy()
+    O.fused_update(ref, y, z)
+    desc = T.triot_plan_describe(4, [x.shape, y.shape, z.shape], None, d, F64, 0,
+                                 mode=seed % 2, warps=int(rng.integers(1, 6)))
+    got = x.copy()
+    kernel_model.run(desc, "update", [got.reshape(-1), y.reshape(-1), z.reshape(-1)])
+    np.testing.assert_array_equal(_bits(got), _bits(ref))
+
+
+def test_validation_dot_and_update():
+    ws = T.triot_inner_product_workspace_size()
+    st = T.triot_inner_product(FAKE, FAKE * 2, (3, 3), FAKE * 3, (3, 3), (4, 3), 2, F64, FAKE * 4,
+                               ws, 0)
+    assert st == 4
+    # y smaller than x on an axis
+    st = T.triot_fused_update(FAKE, (4, 4), FAKE * 2, (3, 4), FAKE * 3, (4, 4), 2, F64, 0)
+    assert st == 4 and "'y'" in T.triot_last_error()
+    st = T.triot_fused_update(FAKE, (4, 4), FAKE + 64, (4, 4), FAKE * 3, (4, 4), 2, F64, 0)
+    assert st == 7

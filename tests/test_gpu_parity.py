@@ -400,3 +400,58 @@ def test_view_centered_fft_padding():
     ref = np.zeros((512,) * 3, np.float32)
     ref[64:448, 64:448, 64:448] = src
     assert_bits_equal(dst, ref)
+
+
+# ---------------------------------------------------------------- NEXT-2/3: paper Benchmarks 1-3
+
+def test_paper_benchmark1_crop_full():
+    from triot_inputs import make_paper_inputs
+    inp = make_paper_inputs("B1")
+    ref = np.empty(inp["dst_shape"]); O.embed(ref, inp["src"])
+    dst = _poisoned(inp["dst_shape"], np.float64)
+    T.embed(dst, _dev(inp["src"]))
+    assert_bits_equal(dst, ref)
+
+
+def test_paper_benchmark2_inner_product_full():
+    from triot_inputs import make_paper_inputs
+    inp = make_paper_inputs("B2")
+    ref = O.inner_product(inp["a"], inp["b"])
+    a, b = _dev(inp["a"]), _dev(inp["b"])
+    g1 = T.inner_product(a, b).item()
+    g2 = T.inner_product(a, b).item()
+    assert abs(g1 - ref) <= 1e-12 * abs(ref) and g1 == g2
+
+
+def test_paper_benchmark3_fused_update_full():
+    from triot_inputs import make_paper_inputs
+    inp = make_paper_inputs("B3")
+    ref = inp["x"].copy(); O.fused_update(ref, inp["y"], inp["z"])
+    x = _dev(inp["x"])
+    T.fused_update(x, _dev(inp["y"]), _dev(inp["z"]))
+    assert_bits_equal(x, ref)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 6, 9, 13, 16])
+def test_inner_product_and_update_random(d, dtype):
+    rng = np.random.default_rng(800 + d + (dtype == np.float64))
+    hi = 5 if d > 8 else (9 if d > 4 else 40)
+    for rep in range(3):
+        ish = random_shape(rng, d, 60000, lo=1, hi=hi)
+        if rep == 1:
+            ish = ish[:-1] + (int(rng.choice([1, 2, 3, 5])),)
+        a = rng.integers(-64, 64, size=tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(dtype)
+        b = rng.integers(-64, 64, size=tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(dtype)
+        got = T.inner_product(_dev(a, rep % 2), _dev(b), iter_shape=ish).item()
+        assert got == O.inner_product(a, b, iter_shape=ish)        # integer-valued: exact
+        x = rng.standard_normal(ish).astype(dtype)
+        y = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(dtype)
+        z = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in ish)).astype(dtype)
+        ref = x.copy(); O.fused_update(ref, y, z)
+        xt = _dev(x, rep)
+        T.fused_update(xt, _dev(y), _dev(z))
+        assert_bits_equal(xt, ref)
+    # empty iteration -> 0.0
+    e = T.inner_product(_dev(np.zeros((0,) * d, dtype)), _dev(np.zeros((2,) * d, dtype)))
+    assert e.item() == 0.0

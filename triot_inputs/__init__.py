@@ -42,6 +42,34 @@ CONFIGS = {
 }
 
 
+# The paper's own Benchmarks 1-3, §8(f) NEXT-2/3.  The paper states shapes only; the
+# element type (double, as in its listings) and the values (uniform[0,1),
+# seeds 11-15) are this build's choice.
+PAPER_BENCHMARKS = {
+    "B1": Config("B1", "embed", "f64", {"src": (1024, 512, 256), "dst": (512, 512, 32)},
+                 "Benchmark 1: copy (crop) a (2^10,2^9,2^8) tensor into (2^9,2^9,2^5)"),
+    "B2": Config("B2", "dot", "f64", {"a": (1024, 512, 256), "b": (512, 512, 32)},
+                 "Benchmark 2: inner product over the shared tuples"),
+    "B3": Config("B3", "update", "f64",
+                 {"x": (129, 32, 13, 16), "y": (253, 64, 64, 23), "z": (256, 39, 64, 33)},
+                 "Benchmark 3: x[t] <- x[t] + y[t]*x[t] - z[t] over x's shape"),
+}
+
+
+def make_paper_inputs(name: str) -> dict:
+    if name == "B1":
+        return {"src": np.random.default_rng(11).random((1024, 512, 256)),
+                "dst_shape": (512, 512, 32)}
+    if name == "B2":
+        return {"a": np.random.default_rng(12).random((1024, 512, 256)),
+                "b": np.random.default_rng(13).random((512, 512, 32))}
+    if name == "B3":
+        return {"x": np.random.default_rng(14).random((129, 32, 13, 16)),
+                "y": np.random.default_rng(15).random((253, 64, 64, 23)),
+                "z": np.random.default_rng(16).random((256, 39, 64, 33))}
+    raise KeyError(name)
+
+
 def _np_dtype(s: str):
     return np.float32 if s == "f32" else np.float64
 
