@@ -268,6 +268,43 @@ def run_ours(args, rank, world, local_rank):
             iso[n] = statistics.median(ts)
         del scratch, clean
 
+    # ---- the paper's own Benchmarks 1-3 (§8(f) NEXT-2/3), same isolated protocol
+    paper = {}
+    if not args.no_isolated:
+        from triot_inputs import make_paper_inputs
+        scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
+        b1 = make_paper_inputs("B1")
+        y1 = torch.from_numpy(b1["src"]).to(dev)
+        x1 = torch.empty(b1["dst_shape"], dtype=torch.float64, device=dev)
+        b2 = make_paper_inputs("B2")
+        a2, bb2 = torch.from_numpy(b2["a"]).to(dev), torch.from_numpy(b2["b"]).to(dev)
+        o2 = torch.empty(1, dtype=torch.float64, device=dev)
+        b3 = make_paper_inputs("B3")
+        x3 = torch.from_numpy(b3["x"]).to(dev)
+        y3, z3 = torch.from_numpy(b3["y"]).to(dev), torch.from_numpy(b3["z"]).to(dev)
+        n1 = math.prod(b1["dst_shape"]) * 8
+        n3 = math.prod(b3["x"].shape) * 8
+        cases = {"B1 crop copy": (lambda: T.embed(x1, y1), 2 * n1),
+                 "B2 inner product": (lambda: T.inner_product(a2, bb2, out=o2), 2 * n1 + 8),
+                 "B3 fused update": (lambda: T.fused_update(x3, y3, z3), 4 * n3)}
+        for name, (fn, nbytes) in cases.items():
+            fn()
+            ts = []
+            for _ in range(5):
+                scratch.fill_(1)
+                clean.sum()
+                ea.record(stream)
+                fn()
+                eb.record(stream)
+                torch.cuda.synchronize(dev)
+                ts.append(ea.elapsed_time(eb))
+            ms = statistics.median(ts)
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            paper[name] = {"bytes": nbytes, "us": round(ms * 1000, 2), "gbs": round(gbs, 1),
+                           "pct_of_8000": round(100 * gbs / NOMINAL_HBM_GBS, 1)}
+        del scratch, clean, y1, x1, a2, bb2, x3, y3, z3
+
     # ---- e2e: same step through the public API with pinned HOST buffers; every step copies
     # its inputs H2D and reads its results back D2H inside the timed region
     e2e = run_e2e(args, host, dev, stream, T, world)
@@ -318,6 +355,9 @@ def run_ours(args, rank, world, local_rank):
         "per_op": per_op,
         "per_op_isolated": {"note": "each op alone after a clean L2 scrub, median of 5",
                             "ops": per_op_iso},
+        "paper_benchmarks": {"note": "P:333 Benchmarks 1-3 at the paper's shapes, f64, "
+                                     "isolated as per_op_isolated (B3 is 27 MB: launch-bound)",
+                             "ops": paper},
         "c1_latency_us": {"per_call_host_bound": round(c1_us, 2),
                           "per_op_in_cuda_graph": (round(c1_graph_us, 3)
                                                    if isinstance(c1_graph_us, float)

@@ -90,6 +90,10 @@ def lib():
             L.oracle_fused_update.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_void_p, _u64p,
                                               ctypes.c_void_p, _u64p, ctypes.c_uint,
                                               ctypes.c_int]
+            L.oracle_naive_convolve.restype = None
+            L.oracle_naive_convolve.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _u64p,
+                                                ctypes.c_void_p, _u64p, ctypes.c_uint,
+                                                ctypes.c_int]
             _lib = L
     return _lib
 
@@ -248,3 +252,14 @@ def fused_update(x: np.ndarray, y: np.ndarray, z: np.ndarray) -> np.ndarray:
     lib().oracle_fused_update(_ptr(x), _shape(x.shape), _ptr(y), _shape(y.shape), _ptr(z),
                               _shape(z.shape), x.ndim, _dtype_code(x))
     return x
+
+
+# -- NEXT-4: naive convolution, Alg 15 ---------------------------------------------
+
+def naive_convolve(lhs: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """Alg 15: result (shape lhs + rhs - 1) with result[t_l + t_r] += lhs[t_l] * rhs[t_r]."""
+    assert lhs.dtype == rhs.dtype and lhs.ndim == rhs.ndim
+    out = np.empty(tuple(a + b - 1 for a, b in zip(lhs.shape, rhs.shape)), dtype=lhs.dtype)
+    lib().oracle_naive_convolve(_ptr(out), _ptr(lhs), _shape(lhs.shape), _ptr(rhs),
+                                _shape(rhs.shape), lhs.ndim, _dtype_code(lhs))
+    return out

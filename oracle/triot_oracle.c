@@ -381,3 +381,40 @@ void oracle_fused_update(void* x, const u64* x_shape, const void* y, const u64* 
     oracle_advance_tuple(t, x_shape, dimension);
   }
 }
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT-4: naive multidimensional convolution, Alg 15 (Benchmark 4)
+ * ---------------------------------------------------------------------------------------- */
+
+/* Alg 15: result has shape lhs + rhs - 1, is filled with 0.0, then for every
+ * lhs tuple (outer enumerate_for_each_tensors) and every rhs tuple (inner one):
+ * counter_result = counter_lhs + counter_rhs;
+ * result.flat()[tuple_to_index(counter_result, result.data_shape())] += lhs_val * rhs_val
+ * -- one rounding for the product, one for the sum.  All extents must be >= 1. */
+void oracle_naive_convolve(void* result, const void* lhs, const u64* lhs_shape, const void* rhs,
+                           const u64* rhs_shape, unsigned int dimension, int dtype) {
+  u64 res_shape[64], tl[64], tr[64], tres[64];
+  for (unsigned int k = 0; k < dimension; ++k) res_shape[k] = lhs_shape[k] + rhs_shape[k] - 1;
+  u64 nres = flat_size(res_shape, dimension);
+  u64 nl = flat_size(lhs_shape, dimension), nr = flat_size(rhs_shape, dimension);
+  if (dtype == OR_F64)
+    for (u64 i = 0; i < nres; ++i) ((double*)result)[i] = 0.0;
+  else
+    for (u64 i = 0; i < nres; ++i) ((float*)result)[i] = 0.0f;
+  memset(tl, 0, sizeof(tl));
+  for (u64 i = 0; i < nl; ++i) {
+    u64 li = oracle_tuple_to_index(tl, lhs_shape, dimension);
+    memset(tr, 0, sizeof(tr));
+    for (u64 j = 0; j < nr; ++j) {
+      u64 ri = oracle_tuple_to_index(tr, rhs_shape, dimension);
+      for (unsigned int k = 0; k < dimension; ++k) tres[k] = tl[k] + tr[k];
+      u64 oi = oracle_tuple_to_index(tres, res_shape, dimension);
+      if (dtype == OR_F64)
+        ((double*)result)[oi] += ((const double*)lhs)[li] * ((const double*)rhs)[ri];
+      else
+        ((float*)result)[oi] += ((const float*)lhs)[li] * ((const float*)rhs)[ri];
+      oracle_advance_tuple(tr, rhs_shape, dimension);
+    }
+    oracle_advance_tuple(tl, lhs_shape, dimension);
+  }
+}

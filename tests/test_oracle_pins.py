@@ -477,3 +477,52 @@ def test_fused_update_vs_numpy(dtype):
     got = x.copy()
     O.fused_update(got, y, z)
     np.testing.assert_array_equal(_bits(got), _bits(ref))
+
+
+# ---------------------------------------------------------------- NEXT-4: naive convolution (Alg 15)
+
+def test_convolve_examples():
+    """[1,2] * [3,4] = [3,10,8]; a unit impulse is the identity; [[1,1],[1,1]] * [[1]]."""
+    assert O.naive_convolve(np.array([1.0, 2.0]), np.array([3.0, 4.0])).tolist() == [3.0, 10.0, 8.0]
+    x = np.random.default_rng(2).random((3, 4, 2))
+    np.testing.assert_array_equal(O.naive_convolve(x, np.ones((1, 1, 1))), x)
+    np.testing.assert_array_equal(O.naive_convolve(np.ones((2, 2)), np.ones((1, 1))), np.ones((2, 2)))
+
+
+def test_convolve_vs_scipy_and_conservation():
+    import scipy.signal
+    rng = np.random.default_rng(41)
+    for d in (1, 2, 3):
+        ls = random_shape(rng, d, 300, lo=1, hi=9)
+        rs = random_shape(rng, d, 300, lo=1, hi=9)
+        li = rng.integers(-20, 20, size=ls).astype(np.float64)
+        ri = rng.integers(-20, 20, size=rs).astype(np.float64)
+        ref = scipy.signal.convolve(li, ri, method="direct")
+        np.testing.assert_array_equal(O.naive_convolve(li, ri), ref)          # integers: exact
+        lf, rf = rng.random(ls), rng.random(rs)
+        got = O.naive_convolve(lf, rf)
+        np.testing.assert_allclose(got, scipy.signal.convolve(lf, rf, method="direct"),
+                                   rtol=1e-13, atol=0)
+        assert abs(math.fsum(got.ravel()) - math.fsum(lf.ravel()) * math.fsum(rf.ravel())) <= \
+            1e-12 * math.fsum(got.ravel())                                       # S:302
+    # f32: same recurrence in float
+    lf = rng.random((5, 3)).astype(np.float32); rf = rng.random((4, 2)).astype(np.float32)
+    got = O.naive_convolve(lf, rf)
+    assert got.dtype == np.float32 and got.shape == (8, 4)
+    np.testing.assert_allclose(got, scipy.signal.convolve(lf.astype(np.float64),
+                                                          rf.astype(np.float64)), rtol=1e-5)
+
+
+def test_convolve_order_is_lhs_lexicographic():
+    """Alg 15 adds the contributions to one output in lexicographic order of the lhs tuple
+    (the outer enumerate): reproduce that order with an explicit Python sum and compare bits."""
+    rng = np.random.default_rng(42)
+    lhs, rhs = rng.standard_normal((4, 3)), rng.standard_normal((3, 2))
+    got = O.naive_convolve(lhs, rhs)
+    for u in brute_tuples(got.shape):
+        acc = 0.0
+        for tl in brute_tuples(lhs.shape):
+            tr = tuple(a - b for a, b in zip(u, tl))
+            if all(0 <= tr[k] < rhs.shape[k] for k in range(2)):
+                acc = acc + lhs[tl] * rhs[tr]
+        assert got[u] == acc
