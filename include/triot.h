@@ -228,6 +228,21 @@ TRIOT_API int triot_fused_update(void* x, const int64_t* x_shape, const void* y,
                                  const int64_t* y_shape, const void* z, const int64_t* z_shape,
                                  int d, int dtype, void* cuda_stream);
 
+/* ---- NEXT-4: naive multidimensional convolution (Alg 15; Benchmark 4) -------- */
+
+/*
+ * triot_naive_convolve -- result (dense, shape lhs_shape + rhs_shape - 1, written entirely) =
+ * the convolution of Alg 15: for every lhs tuple t_l and rhs tuple t_r,
+ *   result[t_l + t_r] += lhs[t_l] * rhs[t_r]        (result starts at 0.0)
+ * "small problems are often much faster to solve using the naive approach".  Each
+ * output is the sum of its rounded products in the order Alg 15 visits them (lexicographic in
+ * t_l), so the result is bit-identical to the sequential algorithm.  All extents must be >= 1
+ * and every tensor must have < 2^31 elements.  result must not overlap lhs or rhs.
+ */
+TRIOT_API int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape,
+                                   const void* rhs, const int64_t* rhs_shape, int d, int dtype,
+                                   void* cuda_stream);
+
 /* ---- diagnostics (host only; no device work, usable without a GPU) ---------------------- */
 
 /*
@@ -240,7 +255,8 @@ TRIOT_API int triot_fused_update(void* x, const int64_t* x_shape, const void* y,
  *           carries the triot_binop),
  *       2 = expected value (shapes[0]=p),
  *       3 = inner product (shapes[0]=a, shapes[1]=b, iter or NULL),
- *       4 = fused update (shapes[0]=x, shapes[1]=y, shapes[2]=z).
+ *       4 = fused update (shapes[0]=x, shapes[1]=y, shapes[2]=z),
+ *       5 = naive convolution (shapes[0]=lhs, shapes[1]=rhs).
  *   ptr_mod32: byte offsets modulo 32 of each tensor's data pointer (alignment model).
  *   mode, warps: the work decomposition to describe (0 = contiguous chunk per warp, 1 = grid
  *              stride, over `warps` warps; 2 = contiguous chunk per block of the expected-value

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libtriot.so")
 TRIOT_F32, TRIOT_F64 = 0, 1
 TRIOT_ADD, TRIOT_SUB, TRIOT_MUL, TRIOT_DIV = 0, 1, 2, 3
 TRIOT_EMBED_FULL, TRIOT_EMBED_REGION_ONLY = 0, 1
-OP_EMBED, OP_BINARY, OP_EV, OP_DOT, OP_UPDATE = 0, 1, 2, 3, 4
+OP_EMBED, OP_BINARY, OP_EV, OP_DOT, OP_UPDATE, OP_CONV = 0, 1, 2, 3, 4, 5
 
 STATUS = {
     0: "TRIOT_OK", 1: "TRIOT_ERR_NULL_POINTER", 2: "TRIOT_ERR_UNSUPPORTED_DIMENSION",
@@ -29,6 +29,7 @@ EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "tr
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
            "triot_expected_value_mass", "triot_embed_view", "triot_apply_binary_view",
            "triot_inner_product_workspace_size", "triot_inner_product", "triot_fused_update",
+           "triot_naive_convolve",
            "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
@@ -88,6 +89,9 @@ _lib.triot_inner_product.argtypes = [_vp, _vp, _i64p, _vp, _i64p, _i64p, ctypes.
 _lib.triot_fused_update.restype = ctypes.c_int
 _lib.triot_fused_update.argtypes = [_vp, _i64p, _vp, _i64p, _vp, _i64p, ctypes.c_int,
                                     ctypes.c_int, _vp]
+_lib.triot_naive_convolve.restype = ctypes.c_int
+_lib.triot_naive_convolve.argtypes = [_vp, _vp, _i64p, _vp, _i64p, ctypes.c_int, ctypes.c_int,
+                                      _vp]
 _lib.triot_plan_describe.restype = ctypes.c_int
 _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
@@ -196,6 +200,12 @@ def triot_fused_update(x: int, x_shape, y: int, y_shape, z: int, z_shape, d: int
                        stream: int) -> int:
     return _lib.triot_fused_update(x, _shape(x_shape), y, _shape(y_shape), z, _shape(z_shape), d,
                                    dtype, stream)
+
+
+def triot_naive_convolve(result: int, lhs: int, lhs_shape, rhs: int, rhs_shape, d: int,
+                         dtype: int, stream: int) -> int:
+    return _lib.triot_naive_convolve(result, lhs, _shape(lhs_shape), rhs, _shape(rhs_shape), d,
+                                     dtype, stream)
 
 
 def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:

@@ -191,3 +191,22 @@ def fused_update(x, y, z):
                                        z.data_ptr(), tuple(z.shape), x.dim(), _dtype_code(x),
                                        _stream(x.device)))
     return x
+
+
+def naive_convolve(lhs, rhs, out=None):
+    """Alg 15 (Benchmark 4): result[t_l + t_r] += lhs[t_l] * rhs[t_r], shape lhs + rhs - 1."""
+    torch = _torch()
+    _check_tensor("lhs", lhs)
+    _check_tensor("rhs", rhs, lhs.device)
+    if lhs.dtype != rhs.dtype or lhs.dim() != rhs.dim():
+        raise ValueError("lhs and rhs must have the same dtype and dimension")
+    shape = tuple(a + b - 1 for a, b in zip(lhs.shape, rhs.shape))
+    if out is None:
+        out = torch.empty(shape, dtype=lhs.dtype, device=lhs.device)
+    _check_tensor("out", out, lhs.device)
+    if tuple(out.shape) != shape or out.dtype != lhs.dtype:
+        raise ValueError(f"out must be {lhs.dtype} of shape {shape}")
+    _lib.check(_lib.triot_naive_convolve(out.data_ptr(), lhs.data_ptr(), tuple(lhs.shape),
+                                         rhs.data_ptr(), tuple(rhs.shape), lhs.dim(),
+                                         _dtype_code(lhs), _stream(lhs.device)))
+    return out

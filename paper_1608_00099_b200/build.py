@@ -37,6 +37,7 @@ for _esz in (4, 8):
                                                   "-DTRIOT_INST_BOP=1"]))
     UNITS.append((f"inst_3_{_esz}_0", "inst.cu", ["-DTRIOT_INST_OP=3", f"-DTRIOT_INST_ESZ={_esz}"]))
     UNITS.append((f"inst_4_{_esz}_0", "inst.cu", ["-DTRIOT_INST_OP=4", f"-DTRIOT_INST_ESZ={_esz}"]))
+    UNITS.append((f"inst_5_{_esz}_0", "inst.cu", ["-DTRIOT_INST_OP=5", f"-DTRIOT_INST_ESZ={_esz}"]))
     for _op in range(4):
         UNITS.append((f"inst_1_{_esz}_{_op}", "inst.cu",
                       [f"-DTRIOT_INST_OP=1", f"-DTRIOT_INST_ESZ={_esz}", f"-DTRIOT_INST_BOP={_op}"]))

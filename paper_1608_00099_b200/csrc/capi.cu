@@ -32,6 +32,8 @@ const void* triot_table_3_4_0(int, int, int);
 const void* triot_table_3_8_0(int, int, int);
 const void* triot_table_4_4_0(int, int, int);
 const void* triot_table_4_8_0(int, int, int);
+const void* triot_table_5_4_0(int, int, int);
+const void* triot_table_5_8_0(int, int, int);
 }
 
 namespace triot {
@@ -353,6 +355,25 @@ int triot_fused_update(void* x, const int64_t* x_shape, const void* y, const int
   return st;
 }
 
+int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape,
+                         const void* rhs, const int64_t* rhs_shape, int d, int dtype,
+                         void* cuda_stream) {
+  Geom g;
+  int st = plan_conv(g, result, lhs, lhs_shape, rhs, rhs_shape, d, dtype);
+  if (st) return st;
+  const void* fn = (g.esz == 8 ? triot_table_5_8_0 : triot_table_5_4_0)(g.D, 2, 0);
+  if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no convolution instance for d=%d", d);
+  Desc<uint32_t> desc;
+  memset(&desc, 0, sizeof(desc));
+  fill_desc<uint32_t>(g, desc);
+  desc.out = result;
+  void* args[1] = {&desc};
+  unsigned grid = (unsigned)((g.nvec + TRIOT_BLOCK - 1) / TRIOT_BLOCK);
+  st = launch_pdl(fn, grid, TRIOT_BLOCK, 0, (cudaStream_t)cuda_stream, args);
+  if (!st) clear_error();
+  return st;
+}
+
 int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, size_t* bytes) {
   if (!bytes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: bytes is NULL");
   Geom g;
@@ -424,6 +445,9 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
   else if (op == OP_DOT)
     st = plan_dot(g, (const void*)base[0], shapes[0], (const void*)base[1], shapes[1], iter_shape,
                   d, dtype);
+  else if (op == OP_CONV)
+    st = plan_conv(g, (void*)base[2], (const void*)base[0], shapes[0], (const void*)base[1],
+                   shapes[1], d, dtype);
   else if (op == OP_UPDATE)
     st = plan_update(g, (void*)base[0], shapes[0], (const void*)base[1], shapes[1],
                      (const void*)base[2], shapes[2], d, dtype);

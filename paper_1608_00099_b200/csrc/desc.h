@@ -22,7 +22,7 @@
 
 namespace triot {
 
-enum Op { OP_EMBED = 0, OP_BINARY = 1, OP_EV = 2, OP_DOT = 3, OP_UPDATE = 4 };
+enum Op { OP_EMBED = 0, OP_BINARY = 1, OP_EV = 2, OP_DOT = 3, OP_UPDATE = 4, OP_CONV = 5 };
 
 template <typename IDX>
 struct TensorAcc {

@@ -6,7 +6,7 @@
 // LinearTemplateSearch (Alg 7): runtime (D, V, index width) -> kernel in O(1).
 //
 //   TRIOT_INST_OP   0 = embed, 1 = binary, 2 = expected value, 3 = inner product,
-//                   4 = fused update
+//                   4 = fused update, 5 = naive convolution
 //   TRIOT_INST_ESZ  4 or 8
 //   TRIOT_INST_BOP  binary op 0..3 (binary); 1 = bulk-copy variant (expected value)
 #include "kernels.cuh"
@@ -47,6 +47,9 @@ const void* kptr() {
   return (const void*)&dot_kernel<D, ESZ, V, IDX, KBIN>;
 #elif TRIOT_INST_OP == 4
   return (const void*)&update_kernel<D, ESZ, V, IDX, KBIN>;
+#elif TRIOT_INST_OP == 5
+  // naive convolution: one instance per D (32-bit indices, no vector width)
+  return (V == 1 && sizeof(IDX) == 4) ? (const void*)&conv_kernel<D, ESZ> : nullptr;
 #elif TRIOT_INST_BOP == 1
   // EV bulk-copy fast path: only the 32-byte vector width exists
   return V == 32 / ESZ ? (const void*)&ev_tma_kernel<D, ESZ, IDX> : nullptr;

@@ -684,6 +684,72 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
   }
 }
 
+// ------------------------------------------------------------------ NEXT-4: naive convolution
+// Alg 15: result[t_l + t_r] += lhs[t_l] * rhs[t_r].  Output-stationary: one thread
+// per output tuple u gathers every (t_l, u - t_l) pair -- the valid t_l form a box
+// [max(0, u_k - R_k + 1), min(L_k - 1, u_k)] per axis -- and walks the box in lexicographic
+// order with the Alg 3 odometer, adding each rounded product in exactly the order Alg 15's outer
+// enumerate visits t_l, so the result is bit-identical to the sequential algorithm (and needs
+// no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
+// t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
+template <int D, int ESZ>
+__global__ void __launch_bounds__(kBlock) conv_kernel(const __grid_constant__ Desc<uint32_t> d) {
+  using T = typename Elem<ESZ>::T;
+  const uint32_t u_flat = blockIdx.x * kBlock + threadIdx.x;
+  pdl_trigger();
+  if (u_flat >= d.nvec) return;
+  uint32_t u[D];
+  {
+    uint32_t r = u_flat;
+#pragma unroll
+    for (int k = D - 1; k >= 1; --k) {
+      const uint32_t q = divq<uint32_t>(r, d.ext[k], d.fdm[k], d.fds[k]);
+      u[k] = r - q * d.ext[k];
+      r = q;
+    }
+    u[0] = r;
+  }
+  uint32_t lo[D], hi[D], t[D];
+  uint32_t offL = 0, offR = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const uint32_t L = d.bnd[k], R = d.dlt[k];
+    lo[k] = u[k] + 1 > R ? u[k] + 1 - R : 0;
+    hi[k] = u[k] < L - 1 ? u[k] : L - 1;
+    t[k] = lo[k];
+    offL += lo[k] * d.t[0].sig[k];
+    offR += (u[k] - lo[k]) * d.t[1].sig[k];
+  }
+  pdl_wait();
+  const T* lhs = (const T*)d.t[0].ptr;
+  const T* rhs = (const T*)d.t[1].ptr;
+  T acc = T(0);
+  for (;;) {
+    acc = bop<0>(acc, bop<2>(lhs[offL], rhs[offR]));
+    // Alg 3 over the box: innermost digit fastest, carry resets a digit to its low end
+    int k = D - 1;
+#pragma unroll
+    for (int kk = D - 1; kk >= 0; --kk) {
+      if (kk != k) continue;
+      if (t[kk] < hi[kk]) {
+        ++t[kk];
+        offL += d.t[0].sig[kk];
+        offR -= d.t[1].sig[kk];
+        k = -2;  // done advancing
+      } else {
+        const uint32_t span = hi[kk] - lo[kk];
+        offL -= span * d.t[0].sig[kk];
+        offR += span * d.t[1].sig[kk];
+        t[kk] = lo[kk];
+        k = kk - 1;
+      }
+    }
+    if (k == -1) break;  // carried out of digit 0: the box is exhausted
+  }
+  T* res = (T*)d.out;
+  res[u_flat] = acc;
+}
+
 // ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

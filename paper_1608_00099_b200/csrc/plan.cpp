@@ -732,6 +732,61 @@ int plan_update(Geom& g, void* x, const int64_t* x_shape, const void* y, const i
   return TRIOT_OK;
 }
 
+// NEXT-4: Alg 15 naive convolution.  The launch uses its own descriptor layout
+// (conv_kernel): ext/fdm/fds = result shape, bnd = lhs extents, dlt = rhs extents.
+int plan_conv(Geom& g, void* result, const void* lhs, const int64_t* lhs_shape, const void* rhs,
+              const int64_t* rhs_shape, int d, int dtype) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  TArg tl, tr;
+  if ((st = targ_dense(tl, "lhs", lhs, lhs_shape, d, esz))) return st;
+  if ((st = targ_dense(tr, "rhs", rhs, rhs_shape, d, esz))) return st;
+  int64_t rs[TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) {
+    if (lhs_shape[k] < 1 || rhs_shape[k] < 1)
+      return set_error(TRIOT_ERR_BAD_SHAPE,
+                       "BadShape: convolution operands need extents >= 1 (axis %d)", k);
+    rs[k] = lhs_shape[k] + rhs_shape[k] - 1;
+  }
+  TArg to;
+  if ((st = targ_dense(to, "result", result, rs, d, esz))) return st;
+  const uint64_t lim = 1ull << 31;
+  if (to.numel >= lim || tl.numel >= lim || tr.numel >= lim)
+    return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: convolution tensors must have < 2^31 elements");
+  if ((st = check_ptr("result", result, to.numel, esz))) return st;
+  if ((st = check_ptr("lhs", lhs, tl.numel, esz))) return st;
+  if ((st = check_ptr("rhs", rhs, tr.numel, esz))) return st;
+  if (targ_overlap(to, tl, esz) || targ_overlap(to, tr, esz))
+    return set_error(TRIOT_ERR_ALIASING, "Aliasing: result overlaps an operand");
+  g.op = OP_CONV;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.d = d;
+  g.D = d;
+  g.V = 1;
+  g.ntensor = 3;
+  g.nvec = to.numel;
+  g.N = to.numel;
+  for (int k = 0; k < d; ++k) {
+    g.ext[k] = (uint64_t)rs[k];
+    g.bnd[k] = (uint64_t)lhs_shape[k];
+    g.dlt[k] = (uint64_t)rhs_shape[k];
+    fastdiv_magic((uint32_t)rs[k], &g.fdm[k], &g.fds[k]);
+    g.t[0].sig[k] = tl.sig[k];
+    g.t[1].sig[k] = tr.sig[k];
+    g.t[2].sig[k] = to.sig[k];
+  }
+  g.t[0].ptr = lhs;
+  g.t[1].ptr = rhs;
+  g.t[2].ptr = result;
+  g.t[0].numel = tl.numel;
+  g.t[1].numel = tr.numel;
+  g.t[2].numel = to.numel;
+  clear_error();
+  return TRIOT_OK;
+}
+
 int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype) {
   g = Geom();
   if (d < 1 || d > TRIOT_MAXD)

@@ -67,6 +67,9 @@ int plan_dot(Geom& g, const void* a, const int64_t* a_shape, const void* b,
              const int64_t* b_shape, const int64_t* iter_shape, int d, int dtype);
 int plan_update(Geom& g, void* x, const int64_t* x_shape, const void* y, const int64_t* y_shape,
                 const void* z, const int64_t* z_shape, int d, int dtype);
+// NEXT-4: Alg 15 naive convolution
+int plan_conv(Geom& g, void* result, const void* lhs, const int64_t* lhs_shape, const void* rhs,
+              const int64_t* rhs_shape, int d, int dtype);
 // NEXT-1: the same ops on views
 int plan_embed_view(Geom& g, const triot_view* dst, const triot_view* src, int d, int dtype,
                     unsigned flags);

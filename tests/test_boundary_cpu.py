@@ -33,7 +33,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     decl = declared_symbols()
-    assert len(decl) == 16, decl
+    assert len(decl) == 17, decl
     out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))
@@ -341,3 +341,12 @@ def test_validation_dot_and_update():
     assert st == 4 and "'y'" in T.triot_last_error()
     st = T.triot_fused_update(FAKE, (4, 4), FAKE + 64, (4, 4), FAKE * 3, (4, 4), 2, F64, 0)
     assert st == 7
+
+
+def test_validation_conv():
+    st = T.triot_naive_convolve(FAKE, FAKE * 2, (3, 0), FAKE * 3, (2, 2), 2, F64, 0)
+    assert st == 3
+    st = T.triot_naive_convolve(FAKE * 2 + 8, FAKE * 2, (4, 4), FAKE * 3, (2, 2), 2, F64, 0)
+    assert st == 7                                             # result overlaps lhs
+    p = T.triot_plan_describe(5, [(256, 8), (256, 8)], None, 2, F64, 0)
+    assert p["N"] == 511 * 15 and p["ext"] == [511, 15]

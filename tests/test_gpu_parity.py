@@ -455,3 +455,29 @@ def test_inner_product_and_update_random(d, dtype):
     # empty iteration -> 0.0
     e = T.inner_product(_dev(np.zeros((0,) * d, dtype)), _dev(np.zeros((2,) * d, dtype)))
     assert e.item() == 0.0
+
+
+# ---------------------------------------------------------------- NEXT-4: naive convolution
+
+def test_paper_benchmark4_convolution():
+    """Benchmark 4: two (2^8, 2^3) matrices; bit-identical to Alg 15."""
+    rng = np.random.default_rng(17)
+    lhs, rhs = rng.random((256, 8)), rng.random((256, 8))
+    ref = O.naive_convolve(lhs, rhs)
+    got = T.naive_convolve(_dev(lhs), _dev(rhs))
+    assert tuple(got.shape) == (511, 15)
+    assert_bits_equal(got, ref)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 7, 10])
+def test_convolution_random(d, dtype):
+    rng = np.random.default_rng(900 + d + (dtype == np.float32))
+    for rep in range(2):
+        ls = random_shape(rng, d, 3000 if d < 5 else 600, lo=1, hi=6 if d > 3 else 14)
+        rs = random_shape(rng, d, 600 if d < 5 else 200, lo=1, hi=5 if d > 3 else 10)
+        lhs = rng.standard_normal(ls).astype(dtype)
+        rhs = rng.standard_normal(rs).astype(dtype)
+        ref = O.naive_convolve(lhs, rhs)
+        got = T.naive_convolve(_dev(lhs, rep), _dev(rhs))
+        assert_bits_equal(got, ref)
