@@ -303,6 +303,32 @@ def run_ours(args, rank, world, local_rank):
             gbs = nbytes / (ms * 1e-3) / 1e9
             paper[name] = {"bytes": nbytes, "us": round(ms * 1000, 2), "gbs": round(gbs, 1),
                            "pct_of_8000": round(100 * gbs / NOMINAL_HBM_GBS, 1)}
+        # Benchmark 4: naive 2-D convolution of two (2^8, 2^3) matrices --
+        # latency-bound (7,665 sequential sums of up to 2,048 rounded products), so reported
+        # as time and multiply-adds per second next to the oracle's time, not as HBM bandwidth
+        rng4 = np.random.default_rng(17)
+        l4 = torch.from_numpy(rng4.random((256, 8))).to(dev)
+        r4 = torch.from_numpy(rng4.random((256, 8))).to(dev)
+        o4 = torch.empty((511, 15), dtype=torch.float64, device=dev)
+        T.naive_convolve(l4, r4, out=o4)
+        ea.record(stream)
+        for _ in range(20):
+            T.naive_convolve(l4, r4, out=o4)
+        eb.record(stream)
+        torch.cuda.synchronize(dev)
+        us4 = ea.elapsed_time(eb) * 1000 / 20
+        macs = 256 * 8 * 256 * 8
+        t_or = None
+        if rank == 0:
+            from oracle import oracle as O
+            ln, rn = l4.cpu().numpy(), r4.cpu().numpy()
+            t0 = time.perf_counter()
+            O.naive_convolve(ln, rn)
+            t_or = time.perf_counter() - t0
+        paper["B4 naive convolution"] = {
+            "macs": macs, "us": round(us4, 2), "gmacs_per_s": round(macs / us4 / 1e3, 1),
+            "oracle_us_1core": round(t_or * 1e6, 1) if t_or else None,
+            "bound": "latency (sequential per-output sums, bit-exact order)"}
         del scratch, clean, y1, x1, a2, bb2, x3, y3, z3
 
     # ---- e2e: same step through the public API with pinned HOST buffers; every step copies

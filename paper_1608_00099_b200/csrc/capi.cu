@@ -368,8 +368,8 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   fill_desc<uint32_t>(g, desc);
   desc.out = result;
   void* args[1] = {&desc};
-  unsigned grid = (unsigned)((g.nvec + TRIOT_BLOCK - 1) / TRIOT_BLOCK);
-  st = launch_pdl(fn, grid, TRIOT_BLOCK, 0, (cudaStream_t)cuda_stream, args);
+  unsigned grid = (unsigned)((g.nvec + TRIOT_CONV_BLOCK - 1) / TRIOT_CONV_BLOCK);
+  st = launch_pdl(fn, grid, TRIOT_CONV_BLOCK, 0, (cudaStream_t)cuda_stream, args);
   if (!st) clear_error();
   return st;
 }

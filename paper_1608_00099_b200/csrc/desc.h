@@ -18,7 +18,8 @@
 
 #define TRIOT_MAXD 16
 #define TRIOT_MAXT 3
-#define TRIOT_BLOCK 256   // threads per block of every kernel
+#define TRIOT_BLOCK 256   // threads per block of the streaming kernels
+#define TRIOT_CONV_BLOCK 64  // the convolution has few, long threads: spread them over all SMs
 
 namespace triot {
 

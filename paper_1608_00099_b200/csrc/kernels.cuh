@@ -693,9 +693,10 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
 // t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
 template <int D, int ESZ>
-__global__ void __launch_bounds__(kBlock) conv_kernel(const __grid_constant__ Desc<uint32_t> d) {
+__global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
+    const __grid_constant__ Desc<uint32_t> d) {
   using T = typename Elem<ESZ>::T;
-  const uint32_t u_flat = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t u_flat = blockIdx.x * TRIOT_CONV_BLOCK + threadIdx.x;
   pdl_trigger();
   if (u_flat >= d.nvec) return;
   uint32_t u[D];
@@ -723,19 +724,31 @@ __global__ void __launch_bounds__(kBlock) conv_kernel(const __grid_constant__ De
   pdl_wait();
   const T* lhs = (const T*)d.t[0].ptr;
   const T* rhs = (const T*)d.t[1].ptr;
+  // the innermost axis is a contiguous run: lhs forward, rhs backward (both dense, stride 1)
+  const int n = (int)(hi[D - 1] - lo[D - 1]) + 1;
   T acc = T(0);
   for (;;) {
-    acc = bop<0>(acc, bop<2>(lhs[offL], rhs[offR]));
-    // Alg 3 over the box: innermost digit fastest, carry resets a digit to its low end
-    int k = D - 1;
+    const T* pl = lhs + offL;
+    const T* pr = rhs + offR;
+    int i = 0;
+    for (; i + 4 <= n; i += 4) {  // independent loads and products, then the adds in order
+      const T p0 = bop<2>(__ldg(pl + i), __ldg(pr - i));
+      const T p1 = bop<2>(__ldg(pl + i + 1), __ldg(pr - i - 1));
+      const T p2 = bop<2>(__ldg(pl + i + 2), __ldg(pr - i - 2));
+      const T p3 = bop<2>(__ldg(pl + i + 3), __ldg(pr - i - 3));
+      acc = bop<0>(bop<0>(bop<0>(bop<0>(acc, p0), p1), p2), p3);
+    }
+    for (; i < n; ++i) acc = bop<0>(acc, bop<2>(__ldg(pl + i), __ldg(pr - i)));
+    // Alg 3 over the outer digits of the box: the innermost digit already ran its whole range
+    int k = D - 2;
 #pragma unroll
-    for (int kk = D - 1; kk >= 0; --kk) {
+    for (int kk = D - 2; kk >= 0; --kk) {
       if (kk != k) continue;
       if (t[kk] < hi[kk]) {
         ++t[kk];
         offL += d.t[0].sig[kk];
         offR -= d.t[1].sig[kk];
-        k = -2;  // done advancing
+        k = -2;
       } else {
         const uint32_t span = hi[kk] - lo[kk];
         offL -= span * d.t[0].sig[kk];
@@ -744,7 +757,7 @@ __global__ void __launch_bounds__(kBlock) conv_kernel(const __grid_constant__ De
         k = kk - 1;
       }
     }
-    if (k == -1) break;  // carried out of digit 0: the box is exhausted
+    if (k != -2) break;  // carried out of digit 0 (or D == 1): the box is exhausted
   }
   T* res = (T*)d.out;
   res[u_flat] = acc;
