@@ -361,15 +361,32 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   Geom g;
   int st = plan_conv(g, result, lhs, lhs_shape, rhs, rhs_shape, d, dtype);
   if (st) return st;
-  const void* fn = (g.esz == 8 ? triot_table_5_8_0 : triot_table_5_4_0)(g.D, 2, 0);
+  // stage both operands in shared memory when they fit (<= 96 KB together)
+  const uint64_t nl_pad = (g.t[0].numel + 3) & ~3ull;
+  const size_t smem = (size_t)(nl_pad + g.t[1].numel) * (size_t)g.esz;
+  const bool use_smem = smem <= 96 * 1024;
+  const void* fn = (g.esz == 8 ? triot_table_5_8_0 : triot_table_5_4_0)(g.D, 2, use_smem ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no convolution instance for d=%d", d);
+  if (use_smem) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_occ.find(fn) == g_occ.end()) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           96 * 1024);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+      g_occ.emplace(fn, 1);
+    }
+  }
   Desc<uint32_t> desc;
   memset(&desc, 0, sizeof(desc));
   fill_desc<uint32_t>(g, desc);
   desc.out = result;
+  desc.t[0].rho = (uint32_t)g.t[0].numel;  // operand element counts for the staging loop
+  desc.t[1].rho = (uint32_t)g.t[1].numel;
+  desc.t[0].numel_pad = (uint32_t)nl_pad;
   void* args[1] = {&desc};
   unsigned grid = (unsigned)((g.nvec + TRIOT_CONV_BLOCK - 1) / TRIOT_CONV_BLOCK);
-  st = launch_pdl(fn, grid, TRIOT_CONV_BLOCK, 0, (cudaStream_t)cuda_stream, args);
+  st = launch_pdl(fn, grid, TRIOT_CONV_BLOCK, use_smem ? smem : 0, (cudaStream_t)cuda_stream,
+                  args);
   if (!st) clear_error();
   return st;
 }

@@ -33,7 +33,7 @@ struct TensorAcc {
   IDX rho;               // stride of the row inside a collapsed vector (R > 1)
   IDX tau;               // stride of the innermost counter axis (1 for contiguous rows)
   uint32_t vec;          // 1: V elements are contiguous and V*esz-aligned -> one wide access
-  uint32_t pad_;
+  uint32_t numel_pad;    // convolution: operand elements rounded up (shared-memory layout)
   const void* ptr;       // device base pointer
 };
 

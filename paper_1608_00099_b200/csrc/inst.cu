@@ -48,8 +48,10 @@ const void* kptr() {
 #elif TRIOT_INST_OP == 4
   return (const void*)&update_kernel<D, ESZ, V, IDX, KBIN>;
 #elif TRIOT_INST_OP == 5
-  // naive convolution: one instance per D (32-bit indices, no vector width)
-  return (V == 1 && sizeof(IDX) == 4) ? (const void*)&conv_kernel<D, ESZ> : nullptr;
+  // naive convolution: one instance per D; idx64 slot = the shared-memory staged variant
+  return V != 1 ? nullptr
+                : (sizeof(IDX) == 4 ? (const void*)&conv_kernel<D, ESZ, false>
+                                    : (const void*)&conv_kernel<D, ESZ, true>);
 #elif TRIOT_INST_BOP == 1
   // EV bulk-copy fast path: only the 32-byte vector width exists
   return V == 32 / ESZ ? (const void*)&ev_tma_kernel<D, ESZ, IDX> : nullptr;

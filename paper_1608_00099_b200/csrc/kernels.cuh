@@ -692,12 +692,29 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // enumerate visits t_l, so the result is bit-identical to the sequential algorithm (and needs
 // no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
 // t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
-template <int D, int ESZ>
+// SMEM: lhs and rhs are first copied into shared memory (they are re-read by every output of
+// the block; the paper's (2^8, 2^3) operands are 16 KB each).
+template <int D, int ESZ, bool SMEM>
 __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     const __grid_constant__ Desc<uint32_t> d) {
   using T = typename Elem<ESZ>::T;
   const uint32_t u_flat = blockIdx.x * TRIOT_CONV_BLOCK + threadIdx.x;
   pdl_trigger();
+  const T* lhs = (const T*)d.t[0].ptr;
+  const T* rhs = (const T*)d.t[1].ptr;
+  if (SMEM) {
+    extern __shared__ __align__(16) unsigned char conv_smem[];
+    T* sl = (T*)conv_smem;
+    T* sr = sl + d.t[0].numel_pad;
+    pdl_wait();
+    for (uint32_t i = threadIdx.x; i < (uint32_t)d.t[0].numel_pad; i += TRIOT_CONV_BLOCK)
+      sl[i] = i < (uint32_t)d.t[0].rho ? __ldg(lhs + i) : T(0);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)d.t[1].rho; i += TRIOT_CONV_BLOCK)
+      sr[i] = __ldg(rhs + i);
+    __syncthreads();
+    lhs = sl;
+    rhs = sr;
+  }
   if (u_flat >= d.nvec) return;
   uint32_t u[D];
   {
@@ -721,9 +738,7 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     offL += lo[k] * d.t[0].sig[k];
     offR += (u[k] - lo[k]) * d.t[1].sig[k];
   }
-  pdl_wait();
-  const T* lhs = (const T*)d.t[0].ptr;
-  const T* rhs = (const T*)d.t[1].ptr;
+  if (!SMEM) pdl_wait();
   // the innermost axis is a contiguous run: lhs forward, rhs backward (both dense, stride 1)
   const int n = (int)(hi[D - 1] - lo[D - 1]) + 1;
   T acc = T(0);
@@ -732,13 +747,13 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     const T* pr = rhs + offR;
     int i = 0;
     for (; i + 4 <= n; i += 4) {  // independent loads and products, then the adds in order
-      const T p0 = bop<2>(__ldg(pl + i), __ldg(pr - i));
-      const T p1 = bop<2>(__ldg(pl + i + 1), __ldg(pr - i - 1));
-      const T p2 = bop<2>(__ldg(pl + i + 2), __ldg(pr - i - 2));
-      const T p3 = bop<2>(__ldg(pl + i + 3), __ldg(pr - i - 3));
+      const T p0 = bop<2>(pl[i], pr[-i]);
+      const T p1 = bop<2>(pl[i + 1], pr[-i - 1]);
+      const T p2 = bop<2>(pl[i + 2], pr[-i - 2]);
+      const T p3 = bop<2>(pl[i + 3], pr[-i - 3]);
       acc = bop<0>(bop<0>(bop<0>(bop<0>(acc, p0), p1), p2), p3);
     }
-    for (; i < n; ++i) acc = bop<0>(acc, bop<2>(__ldg(pl + i), __ldg(pr - i)));
+    for (; i < n; ++i) acc = bop<0>(acc, bop<2>(pl[i], pr[-i]));
     // Alg 3 over the outer digits of the box: the innermost digit already ran its whole range
     int k = D - 2;
 #pragma unroll

@@ -128,7 +128,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
     d.t[x].rho = (IDX)g.t[x].rho;
     d.t[x].tau = (IDX)g.t[x].tau;
     d.t[x].vec = g.t[x].vec ? 1u : 0u;
-    d.t[x].pad_ = 0;
+    d.t[x].numel_pad = 0;
     d.t[x].ptr = g.t[x].ptr;
   }
   d.out = nullptr;
