@@ -583,6 +583,42 @@ __global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc
   ev_reduce<NS, kBlock, IDX>(d, acc);
 }
 
+// ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ------------------------------------------------------------------ NEXT-2: inner product
 // Benchmark 2 / Alg 8 dot_product: sum_t a[t] * b[t] over the iteration
 // shape, each operand indexed by its own shape.  fp64 accumulation (one fused multiply-add per
@@ -703,14 +739,28 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
   const T* lhs = (const T*)d.t[0].ptr;
   const T* rhs = (const T*)d.t[1].ptr;
   if (SMEM) {
-    extern __shared__ __align__(16) unsigned char conv_smem[];
+    // one bulk copy per operand (16-B multiple; the few tail elements with plain loads)
+    extern __shared__ __align__(128) unsigned char conv_smem[];
+    __shared__ __align__(8) uint64_t bar;
     T* sl = (T*)conv_smem;
     T* sr = sl + d.t[0].numel_pad;
+    const uint32_t nl = (uint32_t)d.t[0].rho, nr = (uint32_t)d.t[1].rho;
+    const bool al = ((uintptr_t)lhs & 15u) == 0, ar = ((uintptr_t)rhs & 15u) == 0;
+    const uint32_t bl = al ? (nl * ESZ) & ~15u : 0u, br = ar ? (nr * ESZ) & ~15u : 0u;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     pdl_wait();
-    for (uint32_t i = threadIdx.x; i < (uint32_t)d.t[0].numel_pad; i += TRIOT_CONV_BLOCK)
-      sl[i] = i < (uint32_t)d.t[0].rho ? __ldg(lhs + i) : T(0);
-    for (uint32_t i = threadIdx.x; i < (uint32_t)d.t[1].rho; i += TRIOT_CONV_BLOCK)
-      sr[i] = __ldg(rhs + i);
+    if (threadIdx.x == 0 && bl + br) {
+      mbar_expect_tx(&bar, bl + br);
+      if (bl) bulk_g2s(sl, lhs, bl, &bar);
+      if (br) bulk_g2s(sr, rhs, br, &bar);
+    }
+    for (uint32_t i = bl / ESZ + threadIdx.x; i < nl; i += TRIOT_CONV_BLOCK) sl[i] = __ldg(lhs + i);
+    for (uint32_t i = br / ESZ + threadIdx.x; i < nr; i += TRIOT_CONV_BLOCK) sr[i] = __ldg(rhs + i);
+    if (bl + br) mbar_wait(&bar, 0);
     __syncthreads();
     lhs = sl;
     rhs = sr;
@@ -776,42 +826,6 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
   }
   T* res = (T*)d.out;
   res[u_flat] = acc;
-}
-
-// ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // EV fast path.  Block b owns vectors [b*wmul, min((b+1)*wmul, W)) of the dense p; thread 0
