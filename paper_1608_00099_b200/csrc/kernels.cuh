@@ -728,83 +728,21 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // enumerate visits t_l, so the result is bit-identical to the sequential algorithm (and needs
 // no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
 // t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
-// SMEM: lhs and rhs are first copied into shared memory (they are re-read by every output of
-// the block; the paper's (2^8, 2^3) operands are 16 KB each).
-template <int D, int ESZ, bool SMEM>
-__global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
-    const __grid_constant__ Desc<uint32_t> d) {
-  using T = typename Elem<ESZ>::T;
-  const uint32_t u_flat = blockIdx.x * TRIOT_CONV_BLOCK + threadIdx.x;
-  pdl_trigger();
-  const T* lhs = (const T*)d.t[0].ptr;
-  const T* rhs = (const T*)d.t[1].ptr;
-  if (SMEM) {
-    // one bulk copy per operand (16-B multiple; the few tail elements with plain loads)
-    extern __shared__ __align__(128) unsigned char conv_smem[];
-    __shared__ __align__(8) uint64_t bar;
-    T* sl = (T*)conv_smem;
-    T* sr = sl + d.t[0].numel_pad;
-    const uint32_t nl = (uint32_t)d.t[0].rho, nr = (uint32_t)d.t[1].rho;
-    const bool al = ((uintptr_t)lhs & 15u) == 0, ar = ((uintptr_t)rhs & 15u) == 0;
-    const uint32_t bl = al ? (nl * ESZ) & ~15u : 0u, br = ar ? (nr * ESZ) & ~15u : 0u;
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    pdl_wait();
-    if (threadIdx.x == 0 && bl + br) {
-      mbar_expect_tx(&bar, bl + br);
-      if (bl) bulk_g2s(sl, lhs, bl, &bar);
-      if (br) bulk_g2s(sr, rhs, br, &bar);
-    }
-    for (uint32_t i = bl / ESZ + threadIdx.x; i < nl; i += TRIOT_CONV_BLOCK) sl[i] = __ldg(lhs + i);
-    for (uint32_t i = br / ESZ + threadIdx.x; i < nr; i += TRIOT_CONV_BLOCK) sr[i] = __ldg(rhs + i);
-    if (bl + br) mbar_wait(&bar, 0);
-    __syncthreads();
-    lhs = sl;
-    rhs = sr;
-  }
-  if (u_flat >= d.nvec) return;
-  uint32_t u[D];
-  {
-    uint32_t r = u_flat;
+// The walk over one output's box: the innermost axis is a contiguous run (lhs forward, rhs
+// backward, both dense), the outer digits advance with the Alg 3 odometer.  L and R are either
+// shared-memory or global arrays (separate instantiations, so shared accesses compile to LDS).
+template <int D, typename T>
+__device__ __forceinline__ T conv_box(const Desc<uint32_t>& d, const T* __restrict__ L,
+                                      const T* __restrict__ R, const uint32_t (&lo)[D],
+                                      const uint32_t (&hi)[D], uint32_t offL, uint32_t offR) {
+  uint32_t t[D];
 #pragma unroll
-    for (int k = D - 1; k >= 1; --k) {
-      const uint32_t q = divq<uint32_t>(r, d.ext[k], d.fdm[k], d.fds[k]);
-      u[k] = r - q * d.ext[k];
-      r = q;
-    }
-    u[0] = r;
-  }
-  uint32_t lo[D], hi[D], t[D];
-  uint32_t offL = 0, offR = 0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const uint32_t L = d.bnd[k], R = d.dlt[k];
-    lo[k] = u[k] + 1 > R ? u[k] + 1 - R : 0;
-    hi[k] = u[k] < L - 1 ? u[k] : L - 1;
-    t[k] = lo[k];
-    offL += lo[k] * d.t[0].sig[k];
-    offR += (u[k] - lo[k]) * d.t[1].sig[k];
-  }
-  if (!SMEM) pdl_wait();
-  // the innermost axis is a contiguous run: lhs forward, rhs backward (both dense, stride 1)
+  for (int k = 0; k < D; ++k) t[k] = lo[k];
   const int n = (int)(hi[D - 1] - lo[D - 1]) + 1;
   T acc = T(0);
   for (;;) {
-    const T* pl = lhs + offL;
-    const T* pr = rhs + offR;
-    int i = 0;
-    for (; i + 4 <= n; i += 4) {  // independent loads and products, then the adds in order
-      const T p0 = bop<2>(pl[i], pr[-i]);
-      const T p1 = bop<2>(pl[i + 1], pr[-i - 1]);
-      const T p2 = bop<2>(pl[i + 2], pr[-i - 2]);
-      const T p3 = bop<2>(pl[i + 3], pr[-i - 3]);
-      acc = bop<0>(bop<0>(bop<0>(bop<0>(acc, p0), p1), p2), p3);
-    }
-    for (; i < n; ++i) acc = bop<0>(acc, bop<2>(pl[i], pr[-i]));
-    // Alg 3 over the outer digits of the box: the innermost digit already ran its whole range
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) acc = bop<0>(acc, bop<2>(L[offL + i], R[offR - i]));
     int k = D - 2;
 #pragma unroll
     for (int kk = D - 2; kk >= 0; --kk) {
@@ -823,6 +761,72 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
       }
     }
     if (k != -2) break;  // carried out of digit 0 (or D == 1): the box is exhausted
+  }
+  return acc;
+}
+
+// SMEM: lhs and rhs are first copied into shared memory by two bulk copies (they are re-read
+// by every output of the block; the paper's (2^8, 2^3) operands are 16 KB each).
+template <int D, int ESZ, bool SMEM>
+__global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
+    const __grid_constant__ Desc<uint32_t> d) {
+  using T = typename Elem<ESZ>::T;
+  const uint32_t u_flat = blockIdx.x * TRIOT_CONV_BLOCK + threadIdx.x;
+  pdl_trigger();
+  const T* lhs = (const T*)d.t[0].ptr;
+  const T* rhs = (const T*)d.t[1].ptr;
+  extern __shared__ __align__(128) unsigned char conv_smem[];
+  T* sl = (T*)conv_smem;
+  T* sr = sl + d.t[0].numel_pad;
+  if (SMEM) {
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t nl = (uint32_t)d.t[0].rho, nr = (uint32_t)d.t[1].rho;
+    const bool al = ((uintptr_t)lhs & 15u) == 0, ar = ((uintptr_t)rhs & 15u) == 0;
+    const uint32_t bl = al ? (nl * ESZ) & ~15u : 0u, br = ar ? (nr * ESZ) & ~15u : 0u;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    if (threadIdx.x == 0 && bl + br) {
+      mbar_expect_tx(&bar, bl + br);
+      if (bl) bulk_g2s(sl, lhs, bl, &bar);
+      if (br) bulk_g2s(sr, rhs, br, &bar);
+    }
+    for (uint32_t i = bl / ESZ + threadIdx.x; i < nl; i += TRIOT_CONV_BLOCK) sl[i] = __ldg(lhs + i);
+    for (uint32_t i = br / ESZ + threadIdx.x; i < nr; i += TRIOT_CONV_BLOCK) sr[i] = __ldg(rhs + i);
+    if (bl + br) mbar_wait(&bar, 0);
+    __syncthreads();
+  }
+  if (u_flat >= d.nvec) return;
+  uint32_t u[D];
+  {
+    uint32_t r = u_flat;
+#pragma unroll
+    for (int k = D - 1; k >= 1; --k) {
+      const uint32_t q = divq<uint32_t>(r, d.ext[k], d.fdm[k], d.fds[k]);
+      u[k] = r - q * d.ext[k];
+      r = q;
+    }
+    u[0] = r;
+  }
+  uint32_t lo[D], hi[D];
+  uint32_t offL = 0, offR = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const uint32_t Lk = d.bnd[k], Rk = d.dlt[k];
+    lo[k] = u[k] + 1 > Rk ? u[k] + 1 - Rk : 0;
+    hi[k] = u[k] < Lk - 1 ? u[k] : Lk - 1;
+    offL += lo[k] * d.t[0].sig[k];
+    offR += (u[k] - lo[k]) * d.t[1].sig[k];
+  }
+  T acc;
+  if (SMEM) {
+    acc = conv_box<D, T>(d, sl, sr, lo, hi, offL, offR);
+  } else {
+    pdl_wait();
+    acc = conv_box<D, T>(d, lhs, rhs, lo, hi, offL, offR);
   }
   T* res = (T*)d.out;
   res[u_flat] = acc;
