@@ -19,7 +19,7 @@
 #define TRIOT_MAXD 16
 #define TRIOT_MAXT 3
 #define TRIOT_BLOCK 256   // threads per block of the streaming kernels
-#define TRIOT_CONV_BLOCK 64  // the convolution has few, long threads: spread them over all SMs
+#define TRIOT_CONV_BLOCK 256  // convolution: one warp per output, 8 outputs per block
 
 namespace triot {
 

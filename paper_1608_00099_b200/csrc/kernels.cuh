@@ -721,46 +721,67 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ NEXT-4: naive convolution
-// Alg 15: result[t_l + t_r] += lhs[t_l] * rhs[t_r].  Output-stationary: one thread
-// per output tuple u gathers every (t_l, u - t_l) pair -- the valid t_l form a box
-// [max(0, u_k - R_k + 1), min(L_k - 1, u_k)] per axis -- and walks the box in lexicographic
-// order with the Alg 3 odometer, adding each rounded product in exactly the order Alg 15's outer
-// enumerate visits t_l, so the result is bit-identical to the sequential algorithm (and needs
-// no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
+// Alg 15: result[t_l + t_r] += lhs[t_l] * rhs[t_r].  Output-stationary: each output
+// tuple u gathers every (t_l, u - t_l) pair -- the valid t_l form a box
+// [max(0, u_k - R_k + 1), min(L_k - 1, u_k)] per axis -- in lexicographic order of t_l, adding
+// each rounded product in exactly the order Alg 15's outer enumerate visits t_l, so the result
+// is bit-identical to the sequential algorithm (and needs no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
 // t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
-// The walk over one output's box: the innermost axis is a contiguous run (lhs forward, rhs
-// backward, both dense), the outer digits advance with the Alg 3 odometer.  L and R are either
-// shared-memory or global arrays (separate instantiations, so shared accesses compile to LDS).
+// One warp per output tuple u.  Its terms are the box of valid t_l in lexicographic order; lane i
+// takes terms i, i+32, ... (its box tuple advances by +32 in the box's mixed radix, the Alg 3
+// odometer with per-output extents), computes the rounded product, and the warp folds the 32
+// products of each chunk in term order with shuffles into one dependent add chain -- exactly
+// Alg 15's sequence of additions, so the result is bit-identical.  Invalid lanes contribute
+// +0.0, which never changes the sum (it starts at +0.0 and so can never be -0.0).
 template <int D, typename T>
-__device__ __forceinline__ T conv_box(const Desc<uint32_t>& d, const T* __restrict__ L,
-                                      const T* __restrict__ R, const uint32_t (&lo)[D],
-                                      const uint32_t (&hi)[D], uint32_t offL, uint32_t offR) {
-  uint32_t t[D];
+__device__ __forceinline__ T conv_warp(const Desc<uint32_t>& d, const T* __restrict__ L,
+                                       const T* __restrict__ R, const uint32_t (&u)[D],
+                                       int lane) {
+  uint32_t lo[D], ext[D], dig[D], dl[D];
+  uint64_t M = 1;
 #pragma unroll
-  for (int k = 0; k < D; ++k) t[k] = lo[k];
-  const int n = (int)(hi[D - 1] - lo[D - 1]) + 1;
+  for (int k = 0; k < D; ++k) {
+    const uint32_t Lk = d.bnd[k], Rk = d.dlt[k];
+    lo[k] = u[k] + 1 > Rk ? u[k] + 1 - Rk : 0;
+    const uint32_t hik = u[k] < Lk - 1 ? u[k] : Lk - 1;
+    ext[k] = hik - lo[k] + 1;
+    M *= ext[k];
+  }
+  // decode the lane's first term (lane) and the +32 step into the box radix (once per output)
+  uint32_t j = (uint32_t)lane, st = 32u;
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) {
+    dig[k] = j % ext[k];
+    j /= ext[k];
+    dl[k] = st % ext[k];
+    st /= ext[k];
+  }
+  const uint32_t top = j;  // nonzero only when lane >= M: the lane starts past the box
+  (void)top;
+  uint32_t offL = 0, offR = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    offL += (lo[k] + dig[k]) * d.t[0].sig[k];
+    offR += (u[k] - lo[k] - dig[k]) * d.t[1].sig[k];
+  }
   T acc = T(0);
-  for (;;) {
-#pragma unroll 4
-    for (int i = 0; i < n; ++i) acc = bop<0>(acc, bop<2>(L[offL + i], R[offR - i]));
-    int k = D - 2;
+  for (uint64_t base = 0; base < M; base += 32) {
+    const bool valid = base + (uint64_t)lane < M;
+    const T p = valid ? bop<2>(L[offL], R[offR]) : T(0);
 #pragma unroll
-    for (int kk = D - 2; kk >= 0; --kk) {
-      if (kk != k) continue;
-      if (t[kk] < hi[kk]) {
-        ++t[kk];
-        offL += d.t[0].sig[kk];
-        offR -= d.t[1].sig[kk];
-        k = -2;
-      } else {
-        const uint32_t span = hi[kk] - lo[kk];
-        offL -= span * d.t[0].sig[kk];
-        offR += span * d.t[1].sig[kk];
-        t[kk] = lo[kk];
-        k = kk - 1;
-      }
+    for (int i = 0; i < 32; ++i) acc = bop<0>(acc, __shfl_sync(0xffffffffu, p, i));
+    // advance the lane's term by 32 (mixed-radix add; past the end it is never used)
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      uint32_t nd = dig[k] + dl[k] + c;
+      c = nd >= ext[k] ? 1u : 0u;
+      if (c) nd -= ext[k];
+      const int32_t delta = (int32_t)nd - (int32_t)dig[k];
+      offL += (uint32_t)(delta * (int32_t)d.t[0].sig[k]);
+      offR -= (uint32_t)(delta * (int32_t)d.t[1].sig[k]);
+      dig[k] = nd;
     }
-    if (k != -2) break;  // carried out of digit 0 (or D == 1): the box is exhausted
   }
   return acc;
 }
@@ -771,7 +792,8 @@ template <int D, int ESZ, bool SMEM>
 __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     const __grid_constant__ Desc<uint32_t> d) {
   using T = typename Elem<ESZ>::T;
-  const uint32_t u_flat = blockIdx.x * TRIOT_CONV_BLOCK + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t u_flat = blockIdx.x * (TRIOT_CONV_BLOCK / 32) + (threadIdx.x >> 5);
   pdl_trigger();
   const T* lhs = (const T*)d.t[0].ptr;
   const T* rhs = (const T*)d.t[1].ptr;
@@ -811,25 +833,14 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     }
     u[0] = r;
   }
-  uint32_t lo[D], hi[D];
-  uint32_t offL = 0, offR = 0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const uint32_t Lk = d.bnd[k], Rk = d.dlt[k];
-    lo[k] = u[k] + 1 > Rk ? u[k] + 1 - Rk : 0;
-    hi[k] = u[k] < Lk - 1 ? u[k] : Lk - 1;
-    offL += lo[k] * d.t[0].sig[k];
-    offR += (u[k] - lo[k]) * d.t[1].sig[k];
-  }
   T acc;
   if (SMEM) {
-    acc = conv_box<D, T>(d, sl, sr, lo, hi, offL, offR);
+    acc = conv_warp<D, T>(d, sl, sr, u, lane);
   } else {
     pdl_wait();
-    acc = conv_box<D, T>(d, lhs, rhs, lo, hi, offL, offR);
+    acc = conv_warp<D, T>(d, lhs, rhs, u, lane);
   }
-  T* res = (T*)d.out;
-  res[u_flat] = acc;
+  if (lane == 0) ((T*)d.out)[u_flat] = acc;
 }
 
 // EV fast path.  Block b owns vectors [b*wmul, min((b+1)*wmul, W)) of the dense p; thread 0
