@@ -170,6 +170,27 @@ TRIOT_API int triot_expected_value_mass(double* out, const void* p, const int64_
                                         int dtype, void* workspace, size_t workspace_bytes,
                                         void* cuda_stream);
 
+/* ---- host-buffer entry points: chunked streaming through device staging memory --------
+ *
+ * "a GPU speed-up is most likely when operating on a large, contiguous block of memory,
+ * which is allocated on the GPU or copied to the GPU in chunks, which are subsequently processed
+ * on the GPU".  These take HOST pointers (pinned memory for full overlap), split the output's
+ * axis 0 into slabs that fit half of the caller's device `staging` buffer, and pipeline
+ * host->device copy / the device op / device->host copy of consecutive slabs on three streams.
+ * Results are bit-identical to the device entry points.  The call is asynchronous with respect
+ * to the host: `cuda_stream` completes when the whole output is in host memory.  One staging
+ * buffer per concurrently used stream; calls on one device are serialised by the library.
+ */
+TRIOT_API int triot_embed_host(void* dst, const int64_t* dst_shape, const void* src,
+                               const int64_t* src_shape, int d, int dtype, unsigned flags,
+                               void* staging, size_t staging_bytes, void* cuda_stream);
+
+/* c (host, dense in iter_shape, NULL = element-wise min) = a OP b, all host buffers. */
+TRIOT_API int triot_apply_binary_host(void* c, const void* a, const int64_t* a_shape,
+                                      const void* b, const int64_t* b_shape,
+                                      const int64_t* iter_shape, int d, int dtype, int op,
+                                      void* staging, size_t staging_bytes, void* cuda_stream);
+
 /* ---- NEXT-1: tensor views -------------------------------------------
  *
  * A view is a window of a dense row-major base tensor: "a tensor slice starting at index tuple

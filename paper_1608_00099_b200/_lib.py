@@ -29,7 +29,7 @@ EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "tr
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
            "triot_expected_value_mass", "triot_embed_view", "triot_apply_binary_view",
            "triot_inner_product_workspace_size", "triot_inner_product", "triot_fused_update",
-           "triot_naive_convolve",
+           "triot_naive_convolve", "triot_embed_host", "triot_apply_binary_host",
            "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
@@ -92,6 +92,12 @@ _lib.triot_fused_update.argtypes = [_vp, _i64p, _vp, _i64p, _vp, _i64p, ctypes.c
 _lib.triot_naive_convolve.restype = ctypes.c_int
 _lib.triot_naive_convolve.argtypes = [_vp, _vp, _i64p, _vp, _i64p, ctypes.c_int, ctypes.c_int,
                                       _vp]
+_lib.triot_embed_host.restype = ctypes.c_int
+_lib.triot_embed_host.argtypes = [_vp, _i64p, _vp, _i64p, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_uint, _vp, ctypes.c_size_t, _vp]
+_lib.triot_apply_binary_host.restype = ctypes.c_int
+_lib.triot_apply_binary_host.argtypes = [_vp, _vp, _i64p, _vp, _i64p, _i64p, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
 _lib.triot_plan_describe.restype = ctypes.c_int
 _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_uint, ctypes.POINTER(ctypes.c_uint),
@@ -206,6 +212,20 @@ def triot_naive_convolve(result: int, lhs: int, lhs_shape, rhs: int, rhs_shape, 
                          dtype: int, stream: int) -> int:
     return _lib.triot_naive_convolve(result, lhs, _shape(lhs_shape), rhs, _shape(rhs_shape), d,
                                      dtype, stream)
+
+
+def triot_embed_host(dst: int, dst_shape, src: int, src_shape, d: int, dtype: int, flags: int,
+                     staging: int, staging_bytes: int, stream: int) -> int:
+    return _lib.triot_embed_host(dst, _shape(dst_shape), src, _shape(src_shape), d, dtype, flags,
+                                 staging, staging_bytes, stream)
+
+
+def triot_apply_binary_host(c: int, a: int, a_shape, b: int, b_shape, iter_shape, d: int,
+                            dtype: int, op: int, staging: int, staging_bytes: int,
+                            stream: int) -> int:
+    return _lib.triot_apply_binary_host(c, a, _shape(a_shape), b, _shape(b_shape),
+                                        _shape(iter_shape), d, dtype, op, staging,
+                                        staging_bytes, stream)
 
 
 def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:

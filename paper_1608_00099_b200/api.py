@@ -210,3 +210,68 @@ def naive_convolve(lhs, rhs, out=None):
                                          rhs.data_ptr(), tuple(rhs.shape), lhs.dim(),
                                          _dtype_code(lhs), _stream(lhs.device)))
     return out
+
+
+# ---- host buffers: chunked streaming through a device staging buffer ----------------
+
+STAGING_BYTES = 256 << 20
+
+
+def staging(device, nbytes: int | None = None):
+    """The cached device staging buffer for (device, current stream)."""
+    torch = _torch()
+    nbytes = STAGING_BYTES if nbytes is None else nbytes
+    key = ("staging", device, _stream(device))
+    with _ws_lock:
+        buf = _ws_cache.get(key)
+        if buf is None or buf.numel() != nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            _ws_cache[key] = buf
+    return buf
+
+
+def _check_host(name, t):
+    if t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous host (CPU) tensor; pin it for overlap")
+
+
+def embed_host(dst, src, device=None):
+    """embed on HOST tensors (pinned for full overlap): slabs of dst's axis 0 are streamed
+    through device staging memory (H2D / kernel / D2H overlapped).  Asynchronous: synchronize
+    the current stream before reading dst."""
+    torch = _torch()
+    _check_host("dst", dst)
+    _check_host("src", src)
+    if src.dtype != dst.dtype or src.dim() != dst.dim():
+        raise ValueError("dst and src must have the same dtype and dimension")
+    device = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    buf = staging(device)
+    with torch.cuda.device(device):
+        _lib.check(_lib.triot_embed_host(dst.data_ptr(), tuple(dst.shape), src.data_ptr(),
+                                         tuple(src.shape), dst.dim(), _dtype_code(dst),
+                                         _lib.TRIOT_EMBED_FULL, buf.data_ptr(), buf.numel(),
+                                         _stream(device)))
+    return dst
+
+
+def apply_binary_host(a, b, op: str = "mul", out=None, iter_shape=None, device=None):
+    """apply_binary on HOST tensors; out (host, dense in iter_shape) is created pinned if None."""
+    torch = _torch()
+    _check_host("a", a)
+    _check_host("b", b)
+    if iter_shape is None:
+        iter_shape = tuple(min(x, y) for x, y in zip(a.shape, b.shape))
+    iter_shape = tuple(int(x) for x in iter_shape)
+    if out is None:
+        out = torch.empty(iter_shape, dtype=a.dtype).pin_memory()
+    _check_host("out", out)
+    device = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    buf = staging(device)
+    with torch.cuda.device(device):
+        _lib.check(_lib.triot_apply_binary_host(out.data_ptr(), a.data_ptr(), tuple(a.shape),
+                                                b.data_ptr(), tuple(b.shape), iter_shape,
+                                                a.dim(), _dtype_code(a), OPS[op], buf.data_ptr(),
+                                                buf.numel(), _stream(device)))
+    return out

@@ -29,7 +29,7 @@ NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fvisib
            "-I", CSRC, "-I", INCLUDE, "-diag-suppress", "177"]
 
 # (object name, source, extra defines)
-UNITS = [("plan", "plan.cpp", []), ("capi", "capi.cu", [])]
+UNITS = [("plan", "plan.cpp", []), ("capi", "capi.cu", []), ("capi_host", "capi_host.cu", [])]
 for _esz in (4, 8):
     UNITS.append((f"inst_0_{_esz}_0", "inst.cu", [f"-DTRIOT_INST_OP=0", f"-DTRIOT_INST_ESZ={_esz}"]))
     UNITS.append((f"inst_2_{_esz}_0", "inst.cu", [f"-DTRIOT_INST_OP=2", f"-DTRIOT_INST_ESZ={_esz}"]))

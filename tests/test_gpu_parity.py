@@ -481,3 +481,32 @@ def test_convolution_random(d, dtype):
         ref = O.naive_convolve(lhs, rhs)
         got = T.naive_convolve(_dev(lhs, rep), _dev(rhs))
         assert_bits_equal(got, ref)
+
+
+# ---------------------------------------------------------------- host-buffer streaming
+
+def test_host_streaming_embed_and_binary():
+    from paper_1608_00099_b200 import api
+    for name in ("C1", "C2"):
+        inp = make_inputs(name)
+        ref = np.empty(inp["dst_shape"], inp["src"].dtype); O.embed(ref, inp["src"])
+        src = torch.from_numpy(inp["src"]).pin_memory()
+        dst = torch.full(inp["dst_shape"], float("nan"), dtype=src.dtype).pin_memory()
+        T.embed_host(dst, src)
+        torch.cuda.synchronize()
+        assert_bits_equal(dst, ref)
+    # small staging forces many slabs and slot reuse
+    inp = make_inputs("C4")
+    a, b = torch.from_numpy(inp["a"][:9].copy()).pin_memory(), torch.from_numpy(inp["b"][:9].copy()).pin_memory()
+    ish = (9,) + inp["iter_shape"][1:]
+    ref = O.apply_binary(inp["a"][:9].copy(), inp["b"][:9].copy(), "mul", iter_shape=ish)
+    old = api.STAGING_BYTES
+    try:
+        api._ws_cache.clear()
+        api.STAGING_BYTES = 64 << 20        # two slots of 32 MB: ~1 row of a + b + c per slab
+        out = T.apply_binary_host(a, b, "mul", iter_shape=ish)
+        torch.cuda.synchronize()
+    finally:
+        api.STAGING_BYTES = old
+        api._ws_cache.clear()
+    assert_bits_equal(out, ref)
