@@ -63,27 +63,21 @@ int pipe_init(Pipe& p) {
   return TRIOT_OK;
 }
 
-uint64_t row_elems(const int64_t* shape, int d) {
+int esz_of(int dtype) { return dtype == TRIOT_F32 ? 4 : dtype == TRIOT_F64 ? 8 : 0; }
+
+// Elements of one index of axis k: prod_{j > k} shape[j].
+uint64_t sub_elems(const int64_t* shape, int d, int k) {
   uint64_t n = 1;
-  for (int k = 1; k < d; ++k) n *= (uint64_t)shape[k];
+  for (int j = k + 1; j < d; ++j) n *= (uint64_t)shape[j];
   return n;
 }
 
-// A slab of `rows` rows starting at row `lo` of a tensor of `shape`, clipped to its extent.
-struct Slab {
-  uint64_t lo, rows;
-};
-Slab clip(uint64_t lo, uint64_t rows, int64_t extent0) {
-  uint64_t e = (uint64_t)extent0;
-  if (lo >= e) return Slab{lo, 0};
-  return Slab{lo, rows < e - lo ? rows : e - lo};
-}
-
-int esz_of(int dtype) { return dtype == TRIOT_F32 ? 4 : dtype == TRIOT_F64 ? 8 : 0; }
-
-// The generic pipeline.  `nin` inputs are copied in (their slabs of the output's rows), the op
-// runs on the device slabs, the output slab is copied out.  `op(slot, rows_out, in_rows[],
-// dev_in[], dev_out)` enqueues the device op on `compute`.
+// The generic pipeline.  A chunk is a prefix tuple (t_0 .. t_{k-1}) of the output plus a range
+// [a, a + rows) of axis k: a contiguous block of the row-major output and of every input that
+// contains the prefix (inputs that do not -- an embed's src outside the prefix -- contribute an
+// empty slab).  k is the first axis whose sub-rows let two slots of one chunk fit the staging.
+// `op(out_sub_shape, in_sub_shapes, dev_in[], dev_out, dsub)` enqueues the device op on the
+// caller's stream for the chunk (shapes of dsub = d - k dimensions).
 template <typename OpFn>
 int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* const* in_h,
                  const int64_t* const* in_shape, int d, int esz, void* staging,
@@ -94,28 +88,32 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
   Pipe& P = *pp;
   std::lock_guard<std::mutex> lk(P.mu);
   if ((st = pipe_init(P))) return st;
-  const uint64_t n0 = (uint64_t)out_shape[0];
-  const uint64_t out_row = row_elems(out_shape, d) * (uint64_t)esz;
-  uint64_t in_row[TRIOT_MAXT];
-  uint64_t per_row = out_row;
-  for (int i = 0; i < nin; ++i) {
-    in_row[i] = row_elems(in_shape[i], d) * (uint64_t)esz;
-    per_row += in_row[i];
-  }
-  // two slots, each holding a slab of every operand, 256-B aligned pieces
   const uint64_t slot_bytes = staging_bytes / 2;
-  uint64_t rows = per_row ? (slot_bytes - 256 * (uint64_t)(nin + 1)) / per_row : n0;
-  if (rows < 1 || slot_bytes < 256 * (uint64_t)(nin + 1) + per_row)
+  const uint64_t pad = 256 * (uint64_t)(nin + 1);
+  // choose the chunk axis k and the rows per chunk
+  int k = 0;
+  uint64_t per_row = 0;
+  for (; k < d; ++k) {
+    per_row = sub_elems(out_shape, d, k) * (uint64_t)esz;
+    for (int i = 0; i < nin; ++i) per_row += sub_elems(in_shape[i], d, k) * (uint64_t)esz;
+    if (slot_bytes > pad && per_row <= slot_bytes - pad) break;
+  }
+  if (k == d)
     return set_error(TRIOT_ERR_WORKSPACE,
-                     "Workspace: %zu staging bytes cannot hold two slabs of one row (%llu B)",
-                     staging_bytes, (unsigned long long)(2 * (per_row + 256 * (nin + 1))));
-  if (rows > n0) rows = n0 ? n0 : 1;
+                     "Workspace: %zu staging bytes cannot hold two chunks of one element",
+                     staging_bytes);
+  const uint64_t nk = (uint64_t)out_shape[k];
+  uint64_t rows = (slot_bytes - pad) / per_row;
+  if (rows > nk) rows = nk ? nk : 1;
+  const int dsub = d - k;
+  const uint64_t out_row = sub_elems(out_shape, d, k) * (uint64_t)esz;
+  uint64_t in_row[TRIOT_MAXT];
+  for (int i = 0; i < nin; ++i) in_row[i] = sub_elems(in_shape[i], d, k) * (uint64_t)esz;
   auto align = [](uint64_t x) { return (x + 255) & ~255ull; };
-  char* slot_base[2] = {(char*)staging, (char*)staging + slot_bytes};
   char* dev_out[2];
   char* dev_in[2][TRIOT_MAXT];
   for (int s = 0; s < 2; ++s) {
-    char* q = slot_base[s];
+    char* q = (char*)staging + (size_t)s * slot_bytes;
     dev_out[s] = q;
     q += align(rows * out_row);
     for (int i = 0; i < nin; ++i) {
@@ -130,43 +128,71 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
     return cuda_err(e, "wait");
   if ((e = cudaStreamWaitEvent(P.d2h, P.computed[0], 0)) != cudaSuccess)
     return cuda_err(e, "wait");
+  uint64_t prefix[TRIOT_MAXD] = {0};
+  uint64_t npre = 1;
+  for (int j = 0; j < k; ++j) npre *= (uint64_t)out_shape[j];
   uint64_t chunk = 0;
-  for (uint64_t lo = 0; lo < n0; lo += rows, ++chunk) {
-    const int s = (int)(chunk & 1);
-    const uint64_t r = lo + rows <= n0 ? rows : n0 - lo;
-    // slot reuse: the inputs of chunk-2 were consumed by its compute, its output drained
-    if (chunk >= 2) {
-      if ((e = cudaStreamWaitEvent(P.h2d, P.computed[s], 0)) != cudaSuccess)
-        return cuda_err(e, "wait");
-      if ((e = cudaStreamWaitEvent(compute, P.drained[s], 0)) != cudaSuccess)
-        return cuda_err(e, "wait");
-    }
-    uint64_t in_rows[TRIOT_MAXT];
+  for (uint64_t pi = 0; pi < npre; ++pi) {
+    // Horner offsets of the prefix (in units of axis-k rows) in the output and each input
+    uint64_t out_base = 0, in_base[TRIOT_MAXT];
+    bool in_ok[TRIOT_MAXT];
+    for (int j = 0; j < k; ++j) out_base = out_base * (uint64_t)out_shape[j] + prefix[j];
+    out_base *= nk;
     for (int i = 0; i < nin; ++i) {
-      Slab sl = clip(lo, r, in_shape[i][0]);
-      in_rows[i] = sl.rows;
-      if (sl.rows) {
-        e = cudaMemcpyAsync(dev_in[s][i], (const char*)in_h[i] + sl.lo * in_row[i],
-                            sl.rows * in_row[i], cudaMemcpyHostToDevice, P.h2d);
-        if (e != cudaSuccess) return cuda_err(e, "cudaMemcpyAsync H2D");
+      uint64_t b = 0;
+      in_ok[i] = true;
+      for (int j = 0; j < k; ++j) {
+        if (prefix[j] >= (uint64_t)in_shape[i][j]) in_ok[i] = false;
+        b = b * (uint64_t)in_shape[i][j] + prefix[j];
       }
+      in_base[i] = b * (uint64_t)in_shape[i][k];
     }
-    if ((e = cudaEventRecord(P.loaded[s], P.h2d)) != cudaSuccess) return cuda_err(e, "record");
-    if ((e = cudaStreamWaitEvent(compute, P.loaded[s], 0)) != cudaSuccess)
-      return cuda_err(e, "wait");
-    if ((st = op(lo, r, in_rows, dev_in[s], dev_out[s]))) return st;
-    if ((e = cudaEventRecord(P.computed[s], compute)) != cudaSuccess)
-      return cuda_err(e, "record");
-    if ((e = cudaStreamWaitEvent(P.d2h, P.computed[s], 0)) != cudaSuccess)
-      return cuda_err(e, "wait");
-    if (out_h) {
-      e = cudaMemcpyAsync((char*)out_h + lo * out_row, dev_out[s], r * out_row,
+    for (uint64_t a = 0; a < nk; a += rows, ++chunk) {
+      const int s = (int)(chunk & 1);
+      const uint64_t r = a + rows <= nk ? rows : nk - a;
+      if (chunk >= 2) {  // slot reuse: chunk-2's inputs consumed, its output drained
+        if ((e = cudaStreamWaitEvent(P.h2d, P.computed[s], 0)) != cudaSuccess)
+          return cuda_err(e, "wait");
+        if ((e = cudaStreamWaitEvent(compute, P.drained[s], 0)) != cudaSuccess)
+          return cuda_err(e, "wait");
+      }
+      int64_t in_sub[TRIOT_MAXT][TRIOT_MAXD];
+      for (int i = 0; i < nin; ++i) {
+        const uint64_t ext = (uint64_t)in_shape[i][k];
+        uint64_t ir = (!in_ok[i] || a >= ext) ? 0 : (r < ext - a ? r : ext - a);
+        in_sub[i][0] = (int64_t)ir;
+        for (int j = 1; j < dsub; ++j) in_sub[i][j] = in_shape[i][k + j];
+        if (ir) {
+          e = cudaMemcpyAsync(dev_in[s][i], (const char*)in_h[i] + (in_base[i] + a) * in_row[i],
+                              ir * in_row[i], cudaMemcpyHostToDevice, P.h2d);
+          if (e != cudaSuccess) return cuda_err(e, "cudaMemcpyAsync H2D");
+        }
+      }
+      if ((e = cudaEventRecord(P.loaded[s], P.h2d)) != cudaSuccess) return cuda_err(e, "record");
+      if ((e = cudaStreamWaitEvent(compute, P.loaded[s], 0)) != cudaSuccess)
+        return cuda_err(e, "wait");
+      int64_t out_sub[TRIOT_MAXD];
+      out_sub[0] = (int64_t)r;
+      for (int j = 1; j < dsub; ++j) out_sub[j] = out_shape[k + j];
+      const int64_t* in_sub_p[TRIOT_MAXT];
+      for (int i = 0; i < nin; ++i) in_sub_p[i] = in_sub[i];
+      if ((st = op(out_sub, in_sub_p, dev_in[s], dev_out[s], dsub))) return st;
+      if ((e = cudaEventRecord(P.computed[s], compute)) != cudaSuccess)
+        return cuda_err(e, "record");
+      if ((e = cudaStreamWaitEvent(P.d2h, P.computed[s], 0)) != cudaSuccess)
+        return cuda_err(e, "wait");
+      e = cudaMemcpyAsync((char*)out_h + (out_base + a) * out_row, dev_out[s], r * out_row,
                           cudaMemcpyDeviceToHost, P.d2h);
       if (e != cudaSuccess) return cuda_err(e, "cudaMemcpyAsync D2H");
+      if ((e = cudaEventRecord(P.drained[s], P.d2h)) != cudaSuccess)
+        return cuda_err(e, "record");
     }
-    if ((e = cudaEventRecord(P.drained[s], P.d2h)) != cudaSuccess) return cuda_err(e, "record");
+    for (int j = k - 1; j >= 0; --j) {  // Alg 3 on the prefix
+      if (++prefix[j] < (uint64_t)out_shape[j]) break;
+      prefix[j] = 0;
+    }
   }
-  // the caller's stream completes only when the last slab has landed in host memory
+  // the caller's stream completes only when the last chunk has landed in host memory
   for (int s = 0; s < 2; ++s)
     if (chunk > (uint64_t)s)
       if ((e = cudaStreamWaitEvent(compute, P.drained[s], 0)) != cudaSuccess)
@@ -201,17 +227,10 @@ int triot_embed_host(void* dst, const int64_t* dst_shape, const void* src,
                      "BadFlags: triot_embed_host supports TRIOT_EMBED_FULL only");
   }
   return run_pipeline(dst, dst_shape, 1, ins, ishp, d, esz, staging, staging_bytes, cs,
-                      [&](uint64_t lo, uint64_t rows, const uint64_t* in_rows, char* const* din,
-                          char* dout) -> int {
-                        int64_t ds[TRIOT_MAXD], ss[TRIOT_MAXD];
-                        for (int k = 0; k < d; ++k) {
-                          ds[k] = dst_shape[k];
-                          ss[k] = src_shape[k];
-                        }
-                        ds[0] = (int64_t)rows;
-                        ss[0] = (int64_t)in_rows[0];
-                        (void)lo;
-                        return triot_embed(dout, ds, din[0], ss, d, dtype, flags, cs);
+                      [&](const int64_t* out_sub, const int64_t* const* in_sub, char* const* din,
+                          char* dout, int dsub) -> int {
+                        return triot_embed(dout, out_sub, din[0], in_sub[0], dsub, dtype, flags,
+                                           cs);
                       });
 }
 
@@ -232,20 +251,10 @@ int triot_apply_binary_host(void* c, const void* a, const int64_t* a_shape, cons
   const int64_t* ishp[2] = {a_shape, b_shape};
   cudaStream_t cs = (cudaStream_t)cuda_stream;
   return run_pipeline(c, it, 2, ins, ishp, d, esz, staging, staging_bytes, cs,
-                      [&](uint64_t lo, uint64_t rows, const uint64_t* in_rows, char* const* din,
-                          char* dout) -> int {
-                        int64_t as[TRIOT_MAXD], bs[TRIOT_MAXD], is[TRIOT_MAXD];
-                        for (int k = 0; k < d; ++k) {
-                          as[k] = a_shape[k];
-                          bs[k] = b_shape[k];
-                          is[k] = it[k];
-                        }
-                        as[0] = (int64_t)in_rows[0];
-                        bs[0] = (int64_t)in_rows[1];
-                        is[0] = (int64_t)rows;
-                        (void)lo;
-                        return triot_apply_binary(dout, is, din[0], as, din[1], bs, is, d, dtype,
-                                                  op, cs);
+                      [&](const int64_t* out_sub, const int64_t* const* in_sub, char* const* din,
+                          char* dout, int dsub) -> int {
+                        return triot_apply_binary(dout, out_sub, din[0], in_sub[0], din[1],
+                                                  in_sub[1], out_sub, dsub, dtype, op, cs);
                       });
 }
 
