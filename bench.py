@@ -428,12 +428,25 @@ def run_e2e(args, host, dev, stream, T, world):
 
     # host-buffer entry points (triot_embed_host / triot_apply_binary_host): axis-0 slabs
     # streamed through a device staging buffer with H2D, kernel and D2H overlapped
+    # Each op is issued on its own stream (the user-level concurrency the API allows), so one
+    # op's device-to-host drain overlaps the next op's host-to-device feed; the step ends when
+    # every stream has finished (the timed region joins them).
+    side = [torch.cuda.Stream(dev) for _ in range(4)]
+
     def e2e_step():
-        T.embed_host(outs["dst2"], pin["src2"], device=dev)
-        m3 = T.expected_value(pin["p3"].to(dev, non_blocking=True))
-        outs["m3"].copy_(m3, non_blocking=True)
-        T.apply_binary_host(pin["a4"], pin["b4"], "mul", out=outs["c4"], device=dev)
-        T.embed_host(outs["dst5"], pin["src5"], device=dev)
+        for sd in side:
+            sd.wait_stream(stream)
+        with torch.cuda.stream(side[0]):
+            T.embed_host(outs["dst2"], pin["src2"], device=dev)
+        with torch.cuda.stream(side[1]):
+            m3 = T.expected_value(pin["p3"].to(dev, non_blocking=True))
+            outs["m3"].copy_(m3, non_blocking=True)
+        with torch.cuda.stream(side[2]):
+            T.apply_binary_host(pin["a4"], pin["b4"], "mul", out=outs["c4"], device=dev)
+        with torch.cuda.stream(side[3]):
+            T.embed_host(outs["dst5"], pin["src5"], device=dev)
+        for sd in side:
+            stream.wait_stream(sd)
 
     e2e_step()
     torch.cuda.synchronize(dev)
@@ -451,7 +464,8 @@ def run_e2e(args, host, dev, stream, T, world):
             "ms_per_step": round(ms, 3),
             "note": "public API from pinned host buffers: embed_host / apply_binary_host "
                     "(slab-streamed, H2D / kernel / D2H overlapped) and expected_value on a "
-                    "copied p; every input's H2D and every result's D2H inside the timed region"}
+                    "copied p, one stream per op; every input's H2D and every result's D2H "
+                    "inside the timed region"}
 
 
 # ----------------------------------------------------------------------------- oracle arms
