@@ -19,7 +19,7 @@
 #define TRIOT_MAXD 16
 #define TRIOT_MAXT 3
 #define TRIOT_BLOCK 256   // threads per block of the streaming kernels
-#define TRIOT_CONV_BLOCK 256  // convolution: one warp per output, 8 outputs per block
+#define TRIOT_CONV_BLOCK 64   // convolution: one thread per output; few, long threads: spread
 
 namespace triot {
 
