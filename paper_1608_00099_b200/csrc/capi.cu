@@ -384,7 +384,7 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   desc.t[1].rho = (uint32_t)g.t[1].numel;
   desc.t[0].numel_pad = (uint32_t)nl_pad;
   void* args[1] = {&desc};
-  const uint64_t per_block = TRIOT_CONV_BLOCK;  // one thread per output
+  const uint64_t per_block = TRIOT_CONV_BLOCK / TRIOT_CONV_GROUP;  // outputs per block
   unsigned grid = (unsigned)((g.nvec + per_block - 1) / per_block);
   st = launch_pdl(fn, grid, TRIOT_CONV_BLOCK, use_smem ? smem : 0, (cudaStream_t)cuda_stream,
                   args);

@@ -19,7 +19,8 @@
 #define TRIOT_MAXD 16
 #define TRIOT_MAXT 3
 #define TRIOT_BLOCK 256   // threads per block of the streaming kernels
-#define TRIOT_CONV_BLOCK 64   // convolution: one thread per output; few, long threads: spread
+#define TRIOT_CONV_BLOCK 128  // convolution: threads per block
+#define TRIOT_CONV_GROUP 4    // convolution: lanes per output (TRIOT_CONV_BLOCK/4 outputs/block)
 
 namespace triot {
 

@@ -727,103 +727,63 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // each rounded product in exactly the order Alg 15's outer enumerate visits t_l, so the result
 // is bit-identical to the sequential algorithm (and needs no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
 // t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
-// One thread per output tuple u walks its box in lexicographic order (the innermost axis is a
-// contiguous run: lhs forward, rhs backward; outer digits advance with the Alg 3 odometer) and
-// keeps only the dependent fp64 add chain on the critical path: the loads of batch b+1 are
-// issued, then the adds of batch b run, then batch b+1's products are formed.
-template <int D, typename T>
-struct ConvIter {
-  uint32_t lo[D], hi[D], t[D];
-  uint32_t offL, offR;
-  uint32_t run, n;       // terms left in the current innermost run, run length
-  uint64_t left;         // terms left in the box
-};
-
-template <int D, typename T>
-__device__ __forceinline__ void conv_iter_init(const Desc<uint32_t>& d, const uint32_t (&u)[D],
-                                               ConvIter<D, T>& it) {
-  it.offL = it.offR = 0;
-  it.left = 1;
+// A group of G consecutive lanes per output tuple u.  The output's terms are its box of valid
+// t_l in lexicographic order; lane j of the group takes terms j, j+G, ... (its box tuple
+// advances by +G in the box's mixed radix: the Alg 3 odometer with per-output extents) and forms
+// the rounded product; each round the group folds its G products in term order (width-G
+// shuffles) into the one dependent add chain -- exactly Alg 15's sequence of additions.
+// Invalid lanes contribute +0.0, which never changes the sum (it starts at +0.0, so it can
+// never be -0.0).  G = 4 keeps the shuffle/add issue per term low while 8 outputs share a warp.
+template <int D, int G, typename T>
+__device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const T* __restrict__ L,
+                                        const T* __restrict__ R, const uint32_t (&u)[D], int j,
+                                        bool active) {
+  uint32_t lo[D], ext[D], dig[D], dl[D];
+  uint64_t M = 1;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const uint32_t Lk = d.bnd[k], Rk = d.dlt[k];
-    it.lo[k] = u[k] + 1 > Rk ? u[k] + 1 - Rk : 0;
-    it.hi[k] = u[k] < Lk - 1 ? u[k] : Lk - 1;
-    it.t[k] = it.lo[k];
-    it.offL += it.lo[k] * d.t[0].sig[k];
-    it.offR += (u[k] - it.lo[k]) * d.t[1].sig[k];
-    it.left *= (uint64_t)(it.hi[k] - it.lo[k] + 1);
+    lo[k] = u[k] + 1 > Rk ? u[k] + 1 - Rk : 0;
+    const uint32_t hik = u[k] < Lk - 1 ? u[k] : Lk - 1;
+    ext[k] = hik - lo[k] + 1;
+    M *= ext[k];
   }
-  it.n = it.hi[D - 1] - it.lo[D - 1] + 1;
-  it.run = it.n;
-}
-
-// step to the next term: along the run, or to the start of the next run (Alg 3 on digits < D-1)
-template <int D, typename T>
-__device__ __forceinline__ void conv_iter_next(const Desc<uint32_t>& d, ConvIter<D, T>& it) {
-  --it.left;
-  if (--it.run) {
-    ++it.offL;
-    --it.offR;
-    return;
-  }
-  it.run = it.n;
-  const uint32_t back = it.n - 1;  // rewind the innermost digit to its low end
-  it.offL -= back;
-  it.offR += back;
-  bool carry = true;
+  if (!active) M = 0;
+  uint32_t jj = (uint32_t)j, st = (uint32_t)G;
 #pragma unroll
-  for (int k = D - 2; k >= 0; --k) {
-    if (!carry) break;
-    if (it.t[k] < it.hi[k]) {
-      ++it.t[k];
-      it.offL += d.t[0].sig[k];
-      it.offR -= d.t[1].sig[k];
-      carry = false;
-    } else {
-      const uint32_t span = it.hi[k] - it.lo[k];
-      it.offL -= span * d.t[0].sig[k];
-      it.offR += span * d.t[1].sig[k];
-      it.t[k] = it.lo[k];
-    }
+  for (int k = D - 1; k >= 0; --k) {
+    dig[k] = jj % ext[k];
+    jj /= ext[k];
+    dl[k] = st % ext[k];
+    st /= ext[k];
   }
-}
-
-template <int D, typename T>
-__device__ __forceinline__ T conv_thread(const Desc<uint32_t>& d, const T* __restrict__ L,
-                                         const T* __restrict__ R, const uint32_t (&u)[D]) {
-  constexpr int B = 8;
-  ConvIter<D, T> it;
-  conv_iter_init<D, T>(d, u, it);
-  T x[B], y[B], p[B];
-  int cnt = 0;
+  uint32_t offL = 0, offR = 0;
 #pragma unroll
-  for (int i = 0; i < B; ++i) {  // prologue: batch 0
-    const bool v = it.left > 0;
-    x[i] = v ? L[it.offL] : T(0);
-    y[i] = v ? R[it.offR] : T(0);
-    cnt += v ? 1 : 0;
-    if (v) conv_iter_next<D, T>(d, it);
+  for (int k = 0; k < D; ++k) {
+    offL += (lo[k] + dig[k]) * d.t[0].sig[k];
+    offR += (u[k] - lo[k] - dig[k]) * d.t[1].sig[k];
   }
-#pragma unroll
-  for (int i = 0; i < B; ++i) p[i] = bop<2>(x[i], y[i]);
   T acc = T(0);
-  while (cnt > 0) {
-    int cnt2 = 0;
+  for (uint64_t base = 0; __any_sync(0xffffffffu, base < M); base += G) {
+    const bool valid = base + (uint64_t)j < M;
+    const T p = valid ? bop<2>(L[offL], R[offR]) : T(0);
+    T q[G];
 #pragma unroll
-    for (int i = 0; i < B; ++i) {  // loads of the next batch
-      const bool v = it.left > 0;
-      x[i] = v ? L[it.offL] : T(0);
-      y[i] = v ? R[it.offR] : T(0);
-      cnt2 += v ? 1 : 0;
-      if (v) conv_iter_next<D, T>(d, it);
+    for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p, i, G);
+#pragma unroll
+    for (int i = 0; i < G; ++i) acc = bop<0>(acc, q[i]);
+    // advance the lane's term by G (mixed-radix add; past the end it is never used)
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      uint32_t nd = dig[k] + dl[k] + c;
+      c = nd >= ext[k] ? 1u : 0u;
+      if (c) nd -= ext[k];
+      const int32_t delta = (int32_t)nd - (int32_t)dig[k];
+      offL += (uint32_t)(delta * (int32_t)d.t[0].sig[k]);
+      offR -= (uint32_t)(delta * (int32_t)d.t[1].sig[k]);
+      dig[k] = nd;
     }
-#pragma unroll
-    for (int i = 0; i < B; ++i)  // the add chain of this batch, in Alg 15's order
-      if (i < cnt) acc = bop<0>(acc, p[i]);
-#pragma unroll
-    for (int i = 0; i < B; ++i) p[i] = bop<2>(x[i], y[i]);
-    cnt = cnt2;
   }
   return acc;
 }
@@ -834,7 +794,9 @@ template <int D, int ESZ, bool SMEM>
 __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     const __grid_constant__ Desc<uint32_t> d) {
   using T = typename Elem<ESZ>::T;
-  const uint32_t u_flat = blockIdx.x * TRIOT_CONV_BLOCK + threadIdx.x;
+  constexpr int G = TRIOT_CONV_GROUP;
+  const int j = threadIdx.x % G;
+  const uint32_t u_flat = blockIdx.x * (TRIOT_CONV_BLOCK / G) + threadIdx.x / G;
   pdl_trigger();
   const T* lhs = (const T*)d.t[0].ptr;
   const T* rhs = (const T*)d.t[1].ptr;
@@ -862,10 +824,12 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     if (bl + br) mbar_wait(&bar, 0);
     __syncthreads();
   }
-  if (u_flat >= d.nvec) return;
+  // every lane stays to the end (the group shuffles need the full warp); past-the-end groups
+  // compute nothing
+  const bool active = u_flat < d.nvec;
   uint32_t u[D];
   {
-    uint32_t r = u_flat;
+    uint32_t r = active ? u_flat : 0u;
 #pragma unroll
     for (int k = D - 1; k >= 1; --k) {
       const uint32_t q = divq<uint32_t>(r, d.ext[k], d.fdm[k], d.fds[k]);
@@ -876,12 +840,12 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
   }
   T acc;
   if (SMEM) {
-    acc = conv_thread<D, T>(d, sl, sr, u);
+    acc = conv_group<D, G, T>(d, sl, sr, u, j, active);
   } else {
     pdl_wait();
-    acc = conv_thread<D, T>(d, lhs, rhs, u);
+    acc = conv_group<D, G, T>(d, lhs, rhs, u, j, active);
   }
-  ((T*)d.out)[u_flat] = acc;
+  if (active && j == 0) ((T*)d.out)[u_flat] = acc;
 }
 
 // EV fast path.  Block b owns vectors [b*wmul, min((b+1)*wmul, W)) of the dense p; thread 0
