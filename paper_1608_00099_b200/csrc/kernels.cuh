@@ -733,7 +733,8 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // the rounded product; each round the group folds its G products in term order (width-G
 // shuffles) into the one dependent add chain -- exactly Alg 15's sequence of additions.
 // Invalid lanes contribute +0.0, which never changes the sum (it starts at +0.0, so it can
-// never be -0.0).  G = 4 keeps the shuffle/add issue per term low while 8 outputs share a warp.
+// never be -0.0).  G = 8: the shuffle/add issue per term stays low (4 outputs share a warp) and
+// each round's 8-add chain hides the pipelined loads, products and shuffles of later rounds.
 template <int D, int G, typename T>
 __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const T* __restrict__ L,
                                         const T* __restrict__ R, const uint32_t (&u)[D], int j,
@@ -763,16 +764,7 @@ __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const T* __rest
     offL += (lo[k] + dig[k]) * d.t[0].sig[k];
     offR += (u[k] - lo[k] - dig[k]) * d.t[1].sig[k];
   }
-  T acc = T(0);
-  for (uint64_t base = 0; __any_sync(0xffffffffu, base < M); base += G) {
-    const bool valid = base + (uint64_t)j < M;
-    const T p = valid ? bop<2>(L[offL], R[offR]) : T(0);
-    T q[G];
-#pragma unroll
-    for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p, i, G);
-#pragma unroll
-    for (int i = 0; i < G; ++i) acc = bop<0>(acc, q[i]);
-    // advance the lane's term by G (mixed-radix add; past the end it is never used)
+  auto advance = [&]() {  // the lane's term += G (mixed-radix add; past the end never used)
     uint32_t c = 0;
 #pragma unroll
     for (int k = D - 1; k >= 0; --k) {
@@ -784,6 +776,41 @@ __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const T* __rest
       offR -= (uint32_t)(delta * (int32_t)d.t[1].sig[k]);
       dig[k] = nd;
     }
+  };
+  // Software pipeline over rounds r (G terms each): loads run two rounds ahead, the product and
+  // its shuffles one round ahead, so in program order the dependent add chain of round r is
+  // followed by work that does not wait on it.
+  uint64_t term = (uint64_t)j;  // this lane's term index for the loads being issued
+  T la = T(0), ra = T(0);
+  if (term < M) { la = L[offL]; ra = R[offR]; }   // round 0
+  advance();
+  term += G;
+  T q[G];
+  {
+    const T p0 = bop<2>(la, ra);
+#pragma unroll
+    for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p0, i, G);
+  }
+  la = ra = T(0);
+  if (term < M) { la = L[offL]; ra = R[offR]; }   // round 1
+  advance();
+  term += G;
+  T acc = T(0);
+  for (uint64_t base = 0; __any_sync(0xffffffffu, base < M); base += G) {
+    // a. loads of round r+2
+    T lb = T(0), rb = T(0);
+    if (term < M) { lb = L[offL]; rb = R[offR]; }
+    // b. the ordered add chain of round r (+0.0 for terms past the box)
+#pragma unroll
+    for (int i = 0; i < G; ++i) acc = bop<0>(acc, q[i]);
+    // c, d. product of round r+1 and its shuffles
+    const T p1 = bop<2>(la, ra);
+#pragma unroll
+    for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p1, i, G);
+    la = lb;
+    ra = rb;
+    advance();
+    term += G;
   }
   return acc;
 }
