@@ -727,6 +727,26 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // each rounded product in exactly the order Alg 15's outer enumerate visits t_l, so the result
 // is bit-identical to the sequential algorithm (and needs no atomics).  Descriptor use: ext / fdm / fds = result shape; t[0].sig = lhs strides,
 // t[1].sig = rhs strides, t[2].sig = result strides; bnd[k] = lhs extents, dlt[k] = rhs extents.
+// Operand access for the convolution: shared memory through 32-bit shared-window addresses
+// (ld.shared; generic pointers into shared memory made the compiler rebuild the window address
+// every iteration) or global memory through the read-only path.
+template <typename T, bool SMEM>
+struct ConvSrc {
+  const T* g;
+  uint32_t s;  // shared-window byte address
+  __device__ __forceinline__ T at(uint32_t i) const {
+    if (SMEM) {
+      T v;
+      if (sizeof(T) == 8)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(*(double*)&v) : "r"(s + i * 8u));
+      else
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(*(float*)&v) : "r"(s + i * 4u));
+      return v;
+    }
+    return __ldg(g + i);
+  }
+};
+
 // A group of G consecutive lanes per output tuple u.  The output's terms are its box of valid
 // t_l in lexicographic order; lane j of the group takes terms j, j+G, ... (its box tuple
 // advances by +G in the box's mixed radix: the Alg 3 odometer with per-output extents) and forms
@@ -735,10 +755,9 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // Invalid lanes contribute +0.0, which never changes the sum (it starts at +0.0, so it can
 // never be -0.0).  G = 8: the shuffle/add issue per term stays low (4 outputs share a warp) and
 // each round's 8-add chain hides the pipelined loads, products and shuffles of later rounds.
-template <int D, int G, typename T>
-__device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const T* __restrict__ L,
-                                        const T* __restrict__ R, const uint32_t (&u)[D], int j,
-                                        bool active) {
+template <int D, int G, typename T, typename Src>
+__device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const Src& L, const Src& R,
+                                        const uint32_t (&u)[D], int j, bool active) {
   uint32_t lo[D], ext[D], dig[D], dl[D];
   uint64_t M = 1;
 #pragma unroll
@@ -780,35 +799,38 @@ __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const T* __rest
   // Software pipeline over rounds r (G terms each): loads run two rounds ahead, the product and
   // its shuffles one round ahead, so in program order the dependent add chain of round r is
   // followed by work that does not wait on it.
+  // branch-free loads: a lane past its box loads element 0 and its product is replaced by +0.0
   uint64_t term = (uint64_t)j;  // this lane's term index for the loads being issued
-  T la = T(0), ra = T(0);
-  if (term < M) { la = L[offL]; ra = R[offR]; }   // round 0
+  bool va = term < M;
+  T la = L.at(va ? offL : 0u), ra = R.at(va ? offR : 0u);   // round 0
   advance();
   term += G;
   T q[G];
   {
-    const T p0 = bop<2>(la, ra);
+    const T p0 = va ? bop<2>(la, ra) : T(0);
 #pragma unroll
     for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p0, i, G);
   }
-  la = ra = T(0);
-  if (term < M) { la = L[offL]; ra = R[offR]; }   // round 1
+  va = term < M;
+  la = L.at(va ? offL : 0u);
+  ra = R.at(va ? offR : 0u);   // round 1
   advance();
   term += G;
   T acc = T(0);
   for (uint64_t base = 0; __any_sync(0xffffffffu, base < M); base += G) {
     // a. loads of round r+2
-    T lb = T(0), rb = T(0);
-    if (term < M) { lb = L[offL]; rb = R[offR]; }
+    const bool vb = term < M;
+    const T lb = L.at(vb ? offL : 0u), rb = R.at(vb ? offR : 0u);
     // b. the ordered add chain of round r (+0.0 for terms past the box)
 #pragma unroll
     for (int i = 0; i < G; ++i) acc = bop<0>(acc, q[i]);
     // c, d. product of round r+1 and its shuffles
-    const T p1 = bop<2>(la, ra);
+    const T p1 = va ? bop<2>(la, ra) : T(0);
 #pragma unroll
     for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p1, i, G);
     la = lb;
     ra = rb;
+    va = vb;
     advance();
     term += G;
   }
@@ -867,10 +889,12 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
   }
   T acc;
   if (SMEM) {
-    acc = conv_group<D, G, T>(d, sl, sr, u, j, active);
+    const ConvSrc<T, true> Ls{nullptr, smem_u32(sl)}, Rs{nullptr, smem_u32(sr)};
+    acc = conv_group<D, G, T>(d, Ls, Rs, u, j, active);
   } else {
     pdl_wait();
-    acc = conv_group<D, G, T>(d, lhs, rhs, u, j, active);
+    const ConvSrc<T, false> Lg{lhs, 0u}, Rg{rhs, 0u};
+    acc = conv_group<D, G, T>(d, Lg, Rg, u, j, active);
   }
   if (active && j == 0) ((T*)d.out)[u_flat] = acc;
 }
