@@ -115,9 +115,12 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
     occ = it->second;
   }
   Policy pol = auto_policy(g);
-  if (g_override.mode >= 0) pol.mode = g_override.mode;
+  // mode 2 (block chunks) exists only for the EV bulk-copy kernel: other kernels read the
+  // descriptor per warp, so for them an override of 2 means "automatic"
+  if (g_override.mode == 0 || g_override.mode == 1) pol.mode = g_override.mode;
   if (g_override.bpsm > 0) pol.bpsm = g_override.bpsm;
-  if (g_override.mode >= 0 && g_override.bpsm == 0 && pol.mode != 0) pol.q = 0;
+  if ((g_override.mode == 0 || g_override.mode == 1) && g_override.bpsm == 0 && pol.mode != 0)
+    pol.q = 0;
   const uint64_t wpb = TRIOT_BLOCK / 32;
   const uint64_t kMinSteps = 4;  // >= 4 steps per warp amortise the start decode
   uint64_t grid = (uint64_t)sms * (uint64_t)(pol.bpsm > 0 ? pol.bpsm : occ);

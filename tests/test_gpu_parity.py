@@ -510,3 +510,28 @@ def test_host_streaming_embed_and_binary():
         api.STAGING_BYTES = old
         api._ws_cache.clear()
     assert_bits_equal(out, ref)
+
+
+def test_results_independent_of_launch_policy():
+    """Every work decomposition gives bit-identical embed / binary / dot / update results, and the
+    expected value stays deterministic per policy and within 1e-12 across policies."""
+    rng = np.random.default_rng(55)
+    src = rng.standard_normal((37, 29, 11)).astype(np.float32)
+    a = rng.standard_normal((33, 17, 9, 6)); b = rng.standard_normal((35, 17, 12, 8))
+    p = rng.random((13, 7, 9, 5))
+    ref_e = np.empty((41, 32, 12), np.float32); O.embed(ref_e, src)
+    ref_b = O.apply_binary(a, b, "div")
+    ref_m = O.expected_value(p)
+    try:
+        for mode, bpsm in [(0, 1), (0, 7), (0, 64), (1, 1), (1, 3), (2, 1), (-1, 0)]:
+            T.triot_set_launch_policy(mode, bpsm)
+            dst = _poisoned((41, 32, 12), np.float32)
+            T.embed(dst, _dev(src))
+            assert_bits_equal(dst, ref_e)
+            assert_bits_equal(T.apply_binary(_dev(a), _dev(b), "div"), ref_b)
+            m1 = T.expected_value(_dev(p)).cpu().numpy()
+            m2 = T.expected_value(_dev(p)).cpu().numpy()
+            assert _bits(m1).tolist() == _bits(m2).tolist()
+            assert np.all(np.abs(m1 - ref_m) <= 1e-12 * np.abs(ref_m))
+    finally:
+        T.triot_set_launch_policy(-1, 0)
