@@ -34,6 +34,23 @@ def main():
             torch.cuda.synchronize()
             print(name, "ok", flush=True)
             continue
+        if name in ("B2", "B3"):
+            from triot_inputs import make_paper_inputs
+            pin = make_paper_inputs(name)
+            if name == "B2":
+                x = torch.from_numpy(pin["a"]).to(dev)
+                y = torch.from_numpy(pin["b"]).to(dev)
+                fn = lambda: T.inner_product(x, y)
+            else:
+                x = torch.from_numpy(pin["x"]).to(dev)
+                y = torch.from_numpy(pin["y"]).to(dev)
+                z = torch.from_numpy(pin["z"]).to(dev)
+                fn = lambda: T.fused_update(x, y, z)
+            for _ in range(a.reps):
+                fn()
+            torch.cuda.synchronize()
+            print(name, "ok", flush=True)
+            continue
         inp = make_inputs(name)
         if name in ("C1", "C2", "C5"):
             src = torch.from_numpy(inp["src"]).to(dev)
