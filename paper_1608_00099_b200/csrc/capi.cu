@@ -55,6 +55,7 @@ TableFn table_for(const Geom& g) {
 }
 
 int vindex(const Geom& g) {
+  if (g.flat) return 3;
   if (g.V == 32 / g.esz) return 0;
   if (g.V == 16 / g.esz) return 1;
   return 2;
@@ -175,7 +176,7 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
 // EV bulk-copy fast path: full 32-byte vectors, 32-B aligned p, one persistent block per SM
 int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, bool* used) {
   *used = false;
-  if (g.op != OP_EV || g.V * g.esz != 32 || !g.t[0].vec) return TRIOT_OK;
+  if (g.op != OP_EV || g.flat || g.V * g.esz != 32 || !g.t[0].vec) return TRIOT_OK;
   if (g_override.mode >= 0 && g_override.mode != 2) return TRIOT_OK;
   const void* fn = (g.esz == 8 ? triot_table_2_8_1 : triot_table_2_4_1)(g.D, 0, g.idx64 ? 1 : 0);
   if (!fn) return TRIOT_OK;

@@ -6,6 +6,9 @@
 //   counter    the iteration shape (dst for embed, iter for binary, p for EV), after
 //              canonicalisation (unit axes dropped, contiguous axes merged).
 //   vector     V consecutive counter elements (32 bytes when geometry and alignment allow).
+//   flat       (odd innermost extents) vectors of V consecutive elements of the flattened
+//              counter that may cross rows: digits are then element digits (D = all axes) and
+//              the kernel walks the V elements with the +1 odometer.
 //   digits     u[0..D-1]: the mixed-radix coordinates of a vector.  Digits 0..D-2 are counter
 //              axes; digit D-1 (the "vector digit") is either the vector index inside a counter
 //              row (R == 1) or a group of R whole rows when rows are shorter than a vector
@@ -46,6 +49,7 @@ struct Desc {
   uint32_t fdm[TRIOT_MAXD];  // fast-division magic multiplier per digit extent (IDX = u32)
   uint32_t fds[TRIOT_MAXD];  // fast-division shifts: s1 | s2 << 8
   IDX nvec;              // number of vectors W
+  IDX nelem;             // counter elements N (flat vectors: the last vector may be partial)
   // work decomposition: warp w starts at vector w*wmul + lane, owns
   // the window [w*wmul, min(w*wmul + wspan, W)) and advances by dv vectors per step.
   //   chunk mode:  wmul = wspan = Q*32, dv = 32      (each warp streams a contiguous run)

@@ -60,16 +60,33 @@ const void* kptr() {
 #endif
 }
 
-// table index: ((D-1) * 3 + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element
+// flat-vector instances (odd innermost extents): embed, binary, expected value
+template <int D, typename IDX>
+const void* kptr_flat() {
+#if TRIOT_INST_OP == 0
+  return (const void*)&embed_flat_kernel<D, ESZ, IDX, 2>;
+#elif TRIOT_INST_OP == 1
+  return (const void*)&binary_flat_kernel<D, ESZ, IDX, 2, TRIOT_INST_BOP>;
+#elif TRIOT_INST_OP == 2 && TRIOT_INST_BOP == 0
+  return (const void*)&ev_flat_kernel<D, ESZ, IDX, 2>;
+#else
+  return nullptr;
+#endif
+}
+
+// table index: ((D-1) * 4 + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
+// 3 = flat 32-B vectors
 template <int D>
 struct Fill {
   static void run(const void** t) {
-    t[((D - 1) * 3 + 0) * 2 + 0] = kptr<D, 32 / ESZ, uint32_t>();
-    t[((D - 1) * 3 + 0) * 2 + 1] = kptr<D, 32 / ESZ, uint64_t>();
-    t[((D - 1) * 3 + 1) * 2 + 0] = kptr<D, 16 / ESZ, uint32_t>();
-    t[((D - 1) * 3 + 1) * 2 + 1] = kptr<D, 16 / ESZ, uint64_t>();
-    t[((D - 1) * 3 + 2) * 2 + 0] = kptr<D, 1, uint32_t>();
-    t[((D - 1) * 3 + 2) * 2 + 1] = kptr<D, 1, uint64_t>();
+    t[((D - 1) * 4 + 0) * 2 + 0] = kptr<D, 32 / ESZ, uint32_t>();
+    t[((D - 1) * 4 + 0) * 2 + 1] = kptr<D, 32 / ESZ, uint64_t>();
+    t[((D - 1) * 4 + 1) * 2 + 0] = kptr<D, 16 / ESZ, uint32_t>();
+    t[((D - 1) * 4 + 1) * 2 + 1] = kptr<D, 16 / ESZ, uint64_t>();
+    t[((D - 1) * 4 + 2) * 2 + 0] = kptr<D, 1, uint32_t>();
+    t[((D - 1) * 4 + 2) * 2 + 1] = kptr<D, 1, uint64_t>();
+    t[((D - 1) * 4 + 3) * 2 + 0] = kptr_flat<D, uint32_t>();
+    t[((D - 1) * 4 + 3) * 2 + 1] = kptr_flat<D, uint64_t>();
     Fill<D - 1>::run(t);
   }
 };
@@ -79,7 +96,7 @@ struct Fill<0> {
 };
 
 struct Table {
-  const void* t[TRIOT_MAXD * 3 * 2];
+  const void* t[TRIOT_MAXD * 4 * 2];
   Table() { Fill<TRIOT_MAXD>::run(t); }
 };
 
@@ -88,6 +105,6 @@ struct Table {
 
 extern "C" const void* TRIOT_NAME(int D, int vi, int idx64) {
   static const triot::Table tab;  // thread-safe one-time init
-  if (D < 1 || D > TRIOT_MAXD || vi < 0 || vi > 2) return nullptr;
-  return tab.t[((D - 1) * 3 + vi) * 2 + (idx64 ? 1 : 0)];
+  if (D < 1 || D > TRIOT_MAXD || vi < 0 || vi > 3) return nullptr;
+  return tab.t[((D - 1) * 4 + vi) * 2 + (idx64 ? 1 : 0)];
 }

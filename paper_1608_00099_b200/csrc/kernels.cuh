@@ -131,7 +131,7 @@ __device__ __forceinline__ uint64_t divq<uint64_t>(uint64_t n, uint64_t e, uint3
 }
 
 // Decode vector index v into digits, then Horner offsets per tensor (Alg 2).
-template <int D, int NT, bool BOUNDS, typename IDX>
+template <int D, int NT, bool BOUNDS, typename IDX, bool ALLB = false>
 __device__ __forceinline__ void odo_start(const Desc<IDX>& d, IDX v, IDX (&u)[D],
                                           IDX (&off)[NT], uint32_t& oob) {
 #pragma unroll
@@ -151,12 +151,12 @@ __device__ __forceinline__ void odo_start(const Desc<IDX>& d, IDX v, IDX (&u)[D]
   oob = 0;
   if (BOUNDS) {
 #pragma unroll
-    for (int k = 0; k < D - 1; ++k) oob |= (uint32_t)(u[k] >= d.bnd[k]) << k;
+    for (int k = 0; k < (ALLB ? D : D - 1); ++k) oob |= (uint32_t)(u[k] >= d.bnd[k]) << k;
   }
 }
 
 // +32 vectors: Alg 3's carry loop, unrolled over the D digits (Alg 6) with early exit.
-template <int D, int NT, bool BOUNDS, typename IDX>
+template <int D, int NT, bool BOUNDS, typename IDX, bool ALLB = false>
 __device__ __forceinline__ void odo_step(const Desc<IDX>& d, IDX (&u)[D], IDX (&off)[NT],
                                          uint32_t& oob) {
 #pragma unroll
@@ -173,8 +173,31 @@ __device__ __forceinline__ void odo_step(const Desc<IDX>& d, IDX (&u)[D], IDX (&
       for (int x = 0; x < NT; ++x) off[x] += d.t[x].kap[k];
     }
     u[k] = nu;
-    if (BOUNDS && k < D - 1) oob = (oob & ~(1u << k)) | ((uint32_t)(nu >= d.bnd[k]) << k);
+    if (BOUNDS && (ALLB || k < D - 1))
+      oob = (oob & ~(1u << k)) | ((uint32_t)(nu >= d.bnd[k]) << k);
     if (k <= d.klo && !carry) break;  // "No more carry operations" (Alg 3)
+  }
+}
+
+// +1 element: Alg 3 itself -- increment the last digit, carry while it overflows --
+// with every tensor offset kept equal to Horner of the new tuple (flat vectors).
+template <int D, int NT, bool BOUNDS, typename IDX>
+__device__ __forceinline__ void odo_inc1(const Desc<IDX>& d, IDX (&u)[D], IDX (&off)[NT],
+                                         uint32_t& oob) {
+#pragma unroll
+  for (int x = 0; x < NT; ++x) off[x] += d.t[x].sig[D - 1];
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) {
+    IDX nu = u[k] + 1;
+    const bool carry = k > 0 && nu >= d.ext[k];
+    if (carry) {
+      nu = 0;
+#pragma unroll
+      for (int x = 0; x < NT; ++x) off[x] += d.t[x].kap[k];
+    }
+    u[k] = nu;
+    if (BOUNDS) oob = (oob & ~(1u << k)) | ((uint32_t)(nu >= d.bnd[k]) << k);
+    if (!carry) break;
   }
 }
 
@@ -360,6 +383,129 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
         Elem<ESZ>::put(r + e * EW,
                        bop<OP>(Elem<ESZ>::get(ba[j] + e * EW), Elem<ESZ>::get(bb[j] + e * EW)));
       store_vec<ESZ, V, IDX>(d.t[0], coff[j], lgL, r);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ flat vectors (odd extents)
+// When no vector width divides the counter's innermost extent (3, 5, 7, 999, ...), a vector is
+// V consecutive elements of the flattened counter, crossing rows.  The lane decodes the tuple of
+// its vector's first element once, walks the V elements with the +1 odometer (Alg 3), and then
+// skips to its next vector with the mixed-radix step.  Tensors dense with the counter (dst of a
+// full embed, a dense c, p) are accessed 32 B at a time at flat offset v*V; the others are
+// gathered element by element at their own Horner offsets.
+
+template <int D, int ESZ, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) embed_flat_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int V = 32 / ESZ;
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[2];
+  uint32_t oob;
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 2, true, IDX, true>(d, v * (IDX)V, u, off, oob);
+  pdl_wait();
+  const bool dvec = d.t[0].vec != 0;
+  for (IDX b = base0; b < vend; b += K * d.dv) {
+    uint32_t buf[K][NW];
+    IDX doff[K][V];
+    IDX vj[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      vj[j] = v;
+      v += d.dv;
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const bool in = vj[j] < vend && vj[j] * (IDX)V + (IDX)e < d.nelem && oob == 0;
+        if (in) {
+          Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1]), buf[j] + e * EW);
+        } else {
+#pragma unroll
+          for (int q = 0; q < EW; ++q) buf[j][e * EW + q] = 0u;
+        }
+        doff[j][e] = off[0];
+        odo_inc1<D, 2, true, IDX>(d, u, off, oob);
+      }
+      odo_step<D, 2, true, IDX, true>(d, u, off, oob);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (vj[j] >= vend) continue;
+      const IDX f0 = vj[j] * (IDX)V;
+      if (dvec && f0 + (IDX)V <= d.nelem) {
+        Mem<32>::st((void*)addr<ESZ>(d.t[0].ptr, f0), buf[j]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (f0 + (IDX)e < d.nelem)
+            Mem<ESZ>::st((void*)addr<ESZ>(d.t[0].ptr, doff[j][e]), buf[j] + e * EW);
+      }
+    }
+  }
+}
+
+template <int D, int ESZ, typename IDX, int K, int OP>
+__global__ void __launch_bounds__(kBlock) binary_flat_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int V = 32 / ESZ;
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[3];
+  uint32_t oob;
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 3, false, IDX>(d, v * (IDX)V, u, off, oob);
+  pdl_wait();
+  const bool cvec = d.t[0].vec != 0, avec = d.t[1].vec != 0, bvec = d.t[2].vec != 0;
+  for (IDX b = base0; b < vend; b += K * d.dv) {
+    uint32_t ba[K][NW], bb[K][NW];
+    IDX coff[K][V];
+    IDX vj[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      vj[j] = v;
+      v += d.dv;
+      const IDX f0 = vj[j] * (IDX)V;
+      const bool full = vj[j] < vend && f0 + (IDX)V <= d.nelem;
+      if (full && avec) Mem<32>::ld(addr<ESZ>(d.t[1].ptr, f0), ba[j]);
+      if (full && bvec) Mem<32>::ld(addr<ESZ>(d.t[2].ptr, f0), bb[j]);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const bool in = vj[j] < vend && f0 + (IDX)e < d.nelem;
+        if (in && !(full && avec)) Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1]), ba[j] + e * EW);
+        if (in && !(full && bvec)) Mem<ESZ>::ld(addr<ESZ>(d.t[2].ptr, off[2]), bb[j] + e * EW);
+        coff[j][e] = off[0];
+        odo_inc1<D, 3, false, IDX>(d, u, off, oob);
+      }
+      odo_step<D, 3, false, IDX>(d, u, off, oob);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (vj[j] >= vend) continue;
+      const IDX f0 = vj[j] * (IDX)V;
+      uint32_t r[NW];
+#pragma unroll
+      for (int e = 0; e < V; ++e)
+        Elem<ESZ>::put(r + e * EW,
+                       bop<OP>(Elem<ESZ>::get(ba[j] + e * EW), Elem<ESZ>::get(bb[j] + e * EW)));
+      if (cvec && f0 + (IDX)V <= d.nelem) {
+        Mem<32>::st((void*)addr<ESZ>(d.t[0].ptr, f0), r);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (f0 + (IDX)e < d.nelem)
+            Mem<ESZ>::st((void*)addr<ESZ>(d.t[0].ptr, coff[j][e]), r + e * EW);
+      }
     }
   }
 }
@@ -718,6 +864,82 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
       store_vec<ESZ, V, IDX>(d.t[0], xoff[j], lgL, r);
     }
   }
+}
+
+// EV on flat vectors (odd innermost extents): p is the counter itself, so vector v is elements
+// [v*V, v*V + V) of p; the element digits are the weights, walked with the +1 odometer and its
+// deferred-weight events.
+template <int D, int ESZ, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int V = 32 / ESZ;
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  constexpr int NS = D + 2;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
+  const IDX base0 = warp * d.wmul;
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+  pdl_trigger();
+  pdl_wait();
+  if (base0 < d.nvec) {
+    const IDX vend = warp_end(d, base0);
+    const IDX dv = d.dv;
+    IDX v = base0 + (IDX)lane;
+    IDX u[D];
+    ev_decode<D, IDX>(d, v * (IDX)V, u);
+    EvAcc<D> a;
+    ev_acc_init<D, IDX>(a);
+    const bool pvec = d.t[0].vec != 0;
+    for (IDX b = base0; b < vend; b += (IDX)K * dv) {
+      uint32_t buf[K][NW];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const IDX vj = v + (IDX)j * dv;
+        const IDX f0 = vj * (IDX)V;
+        if (vj < vend && pvec && f0 + (IDX)V <= d.nelem) {
+          Mem<32>::ld(addr<ESZ>(d.t[0].ptr, f0), buf[j]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            if (vj < vend && f0 + (IDX)e < d.nelem) {
+              Mem<ESZ>::ld(addr<ESZ>(d.t[0].ptr, f0 + (IDX)e), buf[j] + e * EW);
+            } else {
+#pragma unroll
+              for (int q = 0; q < EW; ++q) buf[j][e * EW + q] = 0u;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          a.S += (double)Elem<ESZ>::get(buf[j] + e * EW);  // +0.0 past the end
+          // +1 element with weight events (Alg 3 on the digits)
+#pragma unroll
+          for (int k = D - 1; k >= 0; --k) {
+            const IDX old = u[k];
+            IDX nu = old + 1;
+            const bool carry = k > 0 && nu >= d.ext[k];
+            if (carry) nu = 0;
+            u[k] = nu;
+            a.ev[k] = fma(-((double)nu - (double)old), a.S, a.ev[k]);
+            if (!carry) break;
+          }
+        }
+        digits_step_ev<D, IDX>(d, u, a);
+        v += dv;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = fma((double)u[k], a.S, a.ev[k]);
+    acc[D] = 0.0;
+    acc[D + 1] = a.S;
+  }
+  ev_reduce<NS, kBlock, IDX>(d, acc);
 }
 
 // ------------------------------------------------------------------ NEXT-4: naive convolution

@@ -114,6 +114,54 @@ static int ilog2(uint64_t v) {
   return l;
 }
 
+static void finish_geometry(Geom& g, int nt);
+
+// Flat-vector geometry: digits are the canonical axes at element granularity; vector v covers
+// counter elements [v*V, v*V + V) (the last one may be partial).  A tensor gets full-width
+// access iff it is dense with the counter (its strides are the counter's Horner strides) and
+// 32-B aligned.
+static void plan_flat(Geom& g, const Axis* ax, int na, int nt, bool bounds, const uint64_t* n0) {
+  const int V = 32 / g.esz;
+  g.flat = true;
+  g.V = V;
+  g.R = 1;
+  g.collapsed = false;
+  g.D = na;
+  g.lgL = ilog2((uint64_t)V);
+  uint64_t hs = 1;  // counter Horner stride, innermost first
+  uint64_t cstr[TRIOT_MAXD];
+  for (int k = na - 1; k >= 0; --k) {
+    cstr[k] = hs;
+    hs *= ax[k].n;
+  }
+  for (int k = 0; k < na; ++k) {
+    g.ext[k] = ax[k].n;
+    g.bnd[k] = bounds ? ax[k].bnd : ax[k].n;
+    for (int x = 0; x < nt; ++x) g.t[x].sig[k] = ax[k].sig[x];
+  }
+  for (int x = 0; x < nt; ++x) {
+    bool dense = ((uintptr_t)g.t[x].ptr % 32) == 0;
+    for (int k = 0; k < na; ++k)
+      if (ax[k].sig[x] != cstr[k]) dense = false;
+    g.t[x].vec = dense;
+    g.t[x].rho = 0;
+    g.t[x].tau = ax[na - 1].sig[x];
+  }
+  g.rowmul = g.colmul = 0;
+  g.srows = g.scols = 0;
+  g.vfull = g.vany = 0;
+  g.N = 1;
+  for (int k = 0; k < na; ++k) g.N *= ax[k].n;
+  g.nvec = (g.N + V - 1) / V;
+  g.nsteps = (g.nvec + 31) / 32;
+  finish_geometry(g, nt);
+  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  for (int k = 0; k < na; ++k) g.slot_of_axis[ax[k].orig] = k;
+  g.nslots = na;
+  if (g.N == 1 && n0[ax[0].orig] == 1) g.slot_of_axis[ax[0].orig] = -1;
+  g.slot_of_axis[g.d] = na + 1;  // the mass
+}
+
 static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
                   const uint64_t* bnd, bool allow_merge, bool bounds) {
   const int d = g.d, nt = g.ntensor;
@@ -224,6 +272,13 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
       best = ci;
     }
   }
+  // flat vectors: when no vector width fits the innermost extent (odd extents: 3, 5, 7, 999),
+  // take V consecutive elements of the flattened counter instead of one element per lane, for
+  // the ops that have flat kernels.  The counter-dense tensors then still get full-width access.
+  if (cc[best].V == 1 && vmax > 1 && g.flat_ok) {
+    plan_flat(g, ax, na, nt, bounds, n);
+    return;
+  }
   const Cand& c = cc[best];
   g.V = c.V;
   g.R = c.R;
@@ -286,6 +341,26 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   for (int k = 0; k < na; ++k) g.N *= ax[k].n;
   g.nvec = g.N / V;
   g.nsteps = (g.nvec + 31) / 32;
+  finish_geometry(g, nt);
+  // 6. expected-value weight slots: digit k<D-1 -> axis; vector digit -> last (a) or row axis (b)
+  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  for (int k = 0; k < D - 1; ++k) g.slot_of_axis[ax[k].orig] = k;
+  if (!c.collapsed) {
+    g.slot_of_axis[ax[na - 1].orig] = D - 1;
+    g.nslots = D;
+  } else {
+    g.slot_of_axis[ax[na - 2].orig] = D - 1;
+    g.slot_of_axis[ax[na - 1].orig] = D;
+    g.nslots = D + 1;
+  }
+  if (g.N == 1 && n[ax[0].orig] == 1) g.slot_of_axis[ax[0].orig] = -1;  // weight 0 anyway
+  g.slot_of_axis[d] = D + 1;  // the total mass (read only when requested)
+}
+
+// carry deltas, the default decomposition, fast-division magics, index width
+static void finish_geometry(Geom& g, int nt) {
+  const int D = g.D;
+  const uint64_t V = (uint64_t)g.V;
   for (int x = 0; x < nt; ++x) {
     g.t[x].kap[0] = 0;
     for (int k = 1; k < D; ++k) g.t[x].kap[k] = g.t[x].sig[k - 1] - g.ext[k] * g.t[x].sig[k];
@@ -303,19 +378,6 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   for (int k = 0; k < D; ++k)
     if (g.ext[k] + 32 > mx) mx = g.ext[k] + 32;
   g.idx64 = mx >= (1ull << 32) - 64;
-  // 6. expected-value weight slots: digit k<D-1 -> axis; vector digit -> last (a) or row axis (b)
-  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
-  for (int k = 0; k < D - 1; ++k) g.slot_of_axis[ax[k].orig] = k;
-  if (!c.collapsed) {
-    g.slot_of_axis[ax[na - 1].orig] = D - 1;
-    g.nslots = D;
-  } else {
-    g.slot_of_axis[ax[na - 2].orig] = D - 1;
-    g.slot_of_axis[ax[na - 1].orig] = D;
-    g.nslots = D + 1;
-  }
-  if (g.N == 1 && n[ax[0].orig] == 1) g.slot_of_axis[ax[0].orig] = -1;  // weight 0 anyway
-  g.slot_of_axis[d] = D + 1;  // the total mass (read only when requested)
 }
 
 void set_decomposition(Geom& g, int mode, uint64_t warps) {
@@ -339,9 +401,10 @@ void set_decomposition(Geom& g, int mode, uint64_t warps) {
     g.wmul = g.wspan = 32 * q;
     g.dv = 32;
   }
-  // the step in mixed radix (digit 0 absorbs the rest; it only matters past the end)
+  // the step in mixed radix (digit 0 absorbs the rest; it only matters past the end).  Flat
+  // vectors: the kernel walks the vector's V elements with +1 steps, then skips (dv-1)*V.
   const int D = g.D;
-  uint64_t rem = g.dv;
+  uint64_t rem = g.flat ? (g.dv - 1) * (uint64_t)g.V : g.dv;
   for (int k = D - 1; k >= 1; --k) {
     g.dlt[k] = rem % g.ext[k];
     rem /= g.ext[k];
@@ -354,8 +417,9 @@ void set_decomposition(Geom& g, int mode, uint64_t warps) {
       if (k > g.khi) g.khi = k;
       if (k < g.klo) g.klo = k;
     }
-  if (g.khi < 0) {  // cannot happen for dv >= 1; keep the kernel loop well-formed
-    g.khi = g.klo = 0;
+  if (g.khi < 0) {  // a zero step (flat vectors with dv == 1): no digit changes
+    g.khi = -1;
+    g.klo = D;
   }
   for (int x = 0; x < g.ntensor; ++x) {
     uint64_t st = 0;
@@ -465,6 +529,7 @@ static int plan_embed_core(Geom& g, const TArg& dst, const TArg& src, int d, int
   if (reads_src && targ_overlap(dst, src, esz))
     return set_error(TRIOT_ERR_ALIASING, "Aliasing: dst and src overlap");
   g.op = OP_EMBED;
+  g.flat_ok = true;
   g.esz = esz;
   g.dtype = dtype;
   g.flags = flags;
@@ -546,6 +611,7 @@ static int plan_binary_core(Geom& g, const TArg& c, const TArg& a, const TArg& b
     }
   }
   g.op = OP_BINARY;
+  g.flat_ok = true;
   g.esz = esz;
   g.dtype = dtype;
   g.binop = op;
@@ -799,6 +865,7 @@ int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype) {
   if ((st = check_shape("p", shape, d, esz, &np_))) return st;
   if ((st = check_ptr("p", p, np_, esz))) return st;
   g.op = OP_EV;
+  g.flat_ok = true;
   g.esz = esz;
   g.dtype = dtype;
   g.d = d;
@@ -855,12 +922,12 @@ std::string describe(const Geom& g) {
   char b[1024];
   snprintf(b, sizeof(b),
            "\"op\":%d,\"esz\":%d,\"d\":%d,\"empty\":%s,\"idx64\":%s,\"all_oob\":%s,\"Dc\":%d,"
-           "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"N\":%llu,\"nvec\":%llu,"
+           "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"flat\":%s,\"N\":%llu,\"nvec\":%llu,"
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
-           g.collapsed ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
+           g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
            (unsigned long long)g.nsteps, g.mode, (unsigned long long)g.wmul,
            (unsigned long long)g.wspan, (unsigned long long)g.dv, g.khi, g.klo, (unsigned long long)g.rowmul,
            (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,

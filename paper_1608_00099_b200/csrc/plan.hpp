@@ -34,6 +34,8 @@ struct Geom {
   // digits
   int D = 0, V = 1, R = 1, lgL = 0;
   bool collapsed = false;
+  bool flat = false;   // flat vectors: V consecutive counter elements across rows (odd extents)
+  bool flat_ok = false;  // the op has flat-vector kernels (embed, binary, expected value)
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
@@ -102,6 +104,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
     d.fds[k] = g.fds[k];
   }
   d.nvec = (IDX)g.nvec;
+  d.nelem = (IDX)g.N;
   d.wmul = (IDX)g.wmul;
   d.wspan = (IDX)g.wspan;
   d.dv = (IDX)g.dv;

@@ -66,6 +66,8 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
         r, c = e >> lgL, e & (L - 1)
         return W(off + r * T[x]["rho"] + c * T[x]["tau"])
 
+    if desc.get("flat"):
+        return run_flat(desc, op, bufs, binop)
     wmul, wspan, dv = desc["wmul"], desc["wspan"], desc["dv"]
     # mode 0: warp chunks; 1: grid stride; 2: block chunks, thread t starts at vector t
     if desc["mode"] == 2:
@@ -131,6 +133,90 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
                 v += dv
     if op == "dot":
         return slots[0]
+    if op == "ev":
+        d = desc["d"]
+        return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]
+    return None
+
+
+def run_flat(desc: dict, op: str, bufs: list, binop: str = "mul"):
+    """Flat vectors: vector v is counter elements [v*V, v*V+V); the lane walks them with the
+    +1 odometer (Alg 3), then skips (dv-1)*V elements with the mixed-radix step."""
+    D, V, idx64 = desc["D"], desc["V"], desc["idx64"]
+    ext, dlt, bnd = desc["ext"], desc["dlt"], desc["bnd"]
+    khi, klo = desc["khi"], desc["klo"]
+    T = desc["t"]
+    nt = len(T)
+    N, nvec = desc["N"], desc["nvec"]
+    W = lambda x: _wrap(x, idx64)
+    slots = [0.0] * (D + 2)
+
+    def start(f):
+        u = [0] * D
+        for k in range(D - 1, 0, -1):
+            u[k] = f % ext[k]
+            f //= ext[k]
+        u[0] = f
+        off = [W(sum(u[k] * T[x]["sig"][k] for k in range(D))) for x in range(nt)]
+        return u, off
+
+    def inc1(u, off):
+        off = [W(off[x] + T[x]["sig"][D - 1]) for x in range(nt)]
+        for k in range(D - 1, -1, -1):
+            nu = u[k] + 1
+            carry = k > 0 and nu >= ext[k]
+            if carry:
+                nu = 0
+                off = [W(off[x] + T[x]["kap"][k]) for x in range(nt)]
+            u[k] = nu
+            if not carry:
+                break
+        return u, off
+
+    def skip(u, off):
+        off = [W(off[x] + T[x]["step"]) for x in range(nt)]
+        carry = 0
+        for k in range(D - 1, -1, -1):
+            if k > khi:
+                continue
+            nu = u[k] + dlt[k] + carry
+            carry = int(nu >= ext[k])
+            if carry:
+                nu -= ext[k]
+                off = [W(off[x] + T[x]["kap"][k]) for x in range(nt)]
+            u[k] = nu
+            if k <= klo and not carry:
+                break
+        return u, off
+
+    wmul, wspan, dv = desc["wmul"], desc["wspan"], desc["dv"]
+    units = (nvec + wmul - 1) // wmul if desc["mode"] == 0 else dv // 32
+    fn = {"add": np.add, "sub": np.subtract, "mul": np.multiply, "div": np.divide}.get(binop)
+    for w in range(units):
+        base0 = w * wmul
+        if base0 >= nvec:
+            continue
+        vend = min(base0 + wspan, nvec)
+        for lane in range(32):
+            v = base0 + lane
+            u, off = start(v * V)
+            while v < vend:
+                for e in range(V):
+                    f = v * V + e
+                    if f < N:
+                        if op == "embed":
+                            inb = all(u[k] < bnd[k] for k in range(D))
+                            bufs[0][off[0]] = bufs[1][off[1]] if inb else 0
+                        elif op == "binary":
+                            with np.errstate(all="ignore"):
+                                bufs[0][off[0]] = fn(bufs[1][off[1]], bufs[2][off[2]])
+                        elif op == "ev":
+                            x = float(bufs[0][off[0]])
+                            for k in range(D):
+                                slots[k] += u[k] * x
+                    u, off = inc1(u, off)
+                u, off = skip(u, off)
+                v += dv
     if op == "ev":
         d = desc["d"]
         return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]

@@ -350,3 +350,48 @@ def test_validation_conv():
     assert st == 7                                             # result overlaps lhs
     p = T.triot_plan_describe(5, [(256, 8), (256, 8)], None, 2, F64, 0)
     assert p["N"] == 511 * 15 and p["ext"] == [511, 15]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_model_flat_vectors_vs_oracle(seed):
+    """Odd innermost extents take flat vectors (V consecutive counter elements across rows)."""
+    rng = np.random.default_rng(6000 + seed)
+    d = int(rng.integers(1, 6))
+    odd = int(rng.choice([3, 5, 7, 9, 11]))
+    dst_shape = random_shape(rng, d - 1, 800, lo=1, hi=9) + (odd,) if d > 1 else (odd * 37,)
+    src_shape = tuple(max(1, s + int(rng.integers(-2, 2))) for s in dst_shape)
+    dtype = "f32" if seed % 2 else "f64"
+    dt = F32 if dtype == "f32" else F64
+    src = random_values(rng, src_shape, dtype, "normal")
+    ref = np.full(dst_shape, -7.0, dtype=src.dtype)
+    O.embed(ref, src)
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, dt, 0, mode=seed % 2,
+                                 warps=int(rng.integers(1, 6)))
+    out = np.full(dst_shape, -7.0, dtype=src.dtype)
+    kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
+    np.testing.assert_array_equal(_bits(out), _bits(ref))
+    # binary over the odd shape, c dense
+    a = random_values(rng, tuple(s + int(rng.integers(0, 2)) for s in dst_shape), dtype, "normal")
+    b = random_values(rng, dst_shape, dtype, "normal")
+    refc = O.apply_binary(a, b, "mul", iter_shape=dst_shape)
+    desc = T.triot_plan_describe(1, [None, a.shape, b.shape], dst_shape, d, dt, 2, mode=seed % 2,
+                                 warps=int(rng.integers(1, 6)))
+    c = np.full(dst_shape, 5.0, dtype=a.dtype)
+    kernel_model.run(desc, "binary", [c.reshape(-1), a.reshape(-1), b.reshape(-1)], binop="mul")
+    np.testing.assert_array_equal(_bits(c), _bits(refc))
+    # expected value over the odd shape (integers: exact)
+    p = rng.integers(0, 256, size=dst_shape).astype(np.float64)
+    desc = T.triot_plan_describe(2, [dst_shape], None, d, F64, 0, mode=seed % 2,
+                                 warps=int(rng.integers(1, 6)))
+    got = kernel_model.run(desc, "ev", [p.reshape(-1)])
+    np.testing.assert_array_equal(np.array(got), O.expected_value(p))
+
+
+def test_flat_geometry_chosen_for_odd_innermost():
+    p = T.triot_plan_describe(0, [(5, 7), (4, 6)], None, 2, F32, 0)
+    assert p["flat"] and p["V"] == 8 and p["D"] == 2 and p["nvec"] == 5
+    assert [t["vec"] for t in p["t"]] == [True, False]
+    p = T.triot_plan_describe(2, [(7,) * 5], None, 5, F64, 0)
+    assert p["flat"] and p["V"] == 4 and p["nvec"] == (7 ** 5 + 3) // 4
+    p = T.triot_plan_describe(0, [(4, 8), (3, 8)], None, 2, F32, 0)
+    assert not p["flat"]                       # a vector width fits: regular geometry

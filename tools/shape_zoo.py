@@ -1,0 +1,94 @@
+"""Throughput of the general path on awkward shapes (diagnostic): odd / prime innermost extents
+(narrow or scalar vector widths), high d, crops, misaligned bases.  One line per case:
+effective GB/s (algorithmic bytes / single-launch time after a clean L2 scrub)."""
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1608_00099_b200 as T  # noqa: E402
+
+dev = torch.device("cuda:0")
+scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
+
+
+def timed(fn, reps=5):
+    fn()
+    ts = []
+    for _ in range(reps):
+        scratch.fill_(1)
+        clean.sum()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sorted(ts)[len(ts) // 2]
+
+
+def embed_case(name, dst_shape, src_shape, dtype=torch.float32, off=0):
+    src = torch.rand(src_shape, dtype=dtype, device=dev)
+    n = math.prod(dst_shape)
+    buf = torch.empty(n + off, dtype=dtype, device=dev)
+    dst = buf[off:].view(dst_shape)
+    ms = timed(lambda: T.embed(dst, src))
+    esz = src.element_size()
+    nbytes = (math.prod(min(a, b) for a, b in zip(src_shape, dst_shape)) + n) * esz
+    d = len(dst_shape)
+    plan = T.triot_plan_describe(0, [dst_shape, src_shape], None, d,
+                                 0 if dtype == torch.float32 else 1, 0, (off * esz % 32, 0, 0))
+    print(json.dumps({"case": name, "op": "embed", "us": round(ms * 1e3, 1),
+                      "gbs": round(nbytes / ms / 1e6, 1), "V": plan["V"], "D": plan["D"],
+                      "vec": [t["vec"] for t in plan["t"]]}), flush=True)
+
+
+def binary_case(name, a_shape, b_shape, dtype=torch.float64):
+    a = torch.rand(a_shape, dtype=dtype, device=dev)
+    b = torch.rand(b_shape, dtype=dtype, device=dev)
+    ish = tuple(min(x, y) for x, y in zip(a_shape, b_shape))
+    c = torch.empty(ish, dtype=dtype, device=dev)
+    ms = timed(lambda: T.apply_binary(a, b, "mul", out=c))
+    nbytes = 3 * math.prod(ish) * a.element_size()
+    d = len(ish)
+    plan = T.triot_plan_describe(1, [None, a_shape, b_shape], None, d,
+                                 0 if dtype == torch.float32 else 1, 2)
+    print(json.dumps({"case": name, "op": "binary", "us": round(ms * 1e3, 1),
+                      "gbs": round(nbytes / ms / 1e6, 1), "V": plan["V"], "D": plan["D"],
+                      "vec": [t["vec"] for t in plan["t"]]}), flush=True)
+
+
+def ev_case(name, shape, dtype=torch.float64, off=0):
+    n = math.prod(shape)
+    buf = torch.rand(n + off, dtype=dtype, device=dev)
+    p = buf[off:].view(shape)
+    out = torch.empty(len(shape), dtype=torch.float64, device=dev)
+    ms = timed(lambda: T.expected_value(p, out=out))
+    nbytes = n * p.element_size()
+    print(json.dumps({"case": name, "op": "ev", "us": round(ms * 1e3, 1),
+                      "gbs": round(nbytes / ms / 1e6, 1)}), flush=True)
+
+
+embed_case("pad 2-D, innermost 999 (odd: 1-element vectors)", (1000, 1001), (900, 999))
+embed_case("pad 2-D, innermost 1000 (16-B vectors)", (1000, 1000), (900, 998))
+embed_case("pad 2-D, innermost 1024", (1000, 1024), (900, 1000))
+embed_case("crop 3-D to innermost 3", (4096, 512, 3), (4100, 600, 7))
+embed_case("pad d=16 (2)^16 from (1,2,...)", (2,) * 16 + (), (1,) + (2,) * 15)
+embed_case("pad d=8 (7)^8 from (5)^8 (prime)", (7,) * 8, (5,) * 8)
+embed_case("pad d=10 (5)^10 from (4)^10", (5,) * 10, (4,) * 10)
+embed_case("C2 with dst misaligned by 1 element", (512,) * 3, (384,) * 3, off=1)
+embed_case("f64 pad (128)^4 from (100)^4", (128,) * 4, (100,) * 4, dtype=torch.float64)
+binary_case("binary f64 innermost 5 (scalar)", (200, 300, 401, 5), (201, 300, 400, 5))
+binary_case("binary f64 (64)^4 vs (80)^4", (64, 64, 64, 64), (80, 80, 80, 80))
+binary_case("binary f32 d=12 (4)^12 vs (5)^12", (4,) * 12, (5,) * 12, dtype=torch.float32)
+ev_case("EV f64 (4096, 4096)", (4096, 4096))
+ev_case("EV f64 (7,)*9 (odd innermost: LDG path)", (7,) * 9)
+ev_case("EV f32 (512,)*3", (512,) * 3, dtype=torch.float32)
+ev_case("EV f64 C3 misaligned by 1 (LDG path)", (16,) * 6, off=1)
