@@ -177,8 +177,14 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
 int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, bool* used) {
   *used = false;
   if (g.op != OP_EV || g.flat || g.V * g.esz != 32 || !g.t[0].vec) return TRIOT_OK;
-  if (g_override.mode >= 0 && g_override.mode != 2) return TRIOT_OK;
-  const void* fn = (g.esz == 8 ? triot_table_2_8_1 : triot_table_2_4_1)(g.D, 0, g.idx64 ? 1 : 0);
+  if (g_override.mode >= 0 && g_override.mode != 2 && g_override.mode != 3) return TRIOT_OK;
+  // mode 2: one persistent 512-thread block per SM, 6 x 32 KB stages; mode 3: small stages
+  // (4 x 16 KB, 256 threads, several blocks per SM, many blocks)
+  const bool small = g_override.mode == 3;
+  const int block = small ? TRIOT_EVS_BLOCK : TRIOT_EV_TMA_BLOCK;
+  const int smem = small ? TRIOT_EVS_SMEM : TRIOT_EV_SMEM;
+  const void* fn =
+      (g.esz == 8 ? triot_table_2_8_1 : triot_table_2_4_1)(g.D, small ? 1 : 0, g.idx64 ? 1 : 0);
   if (!fn) return TRIOT_OK;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -193,17 +199,20 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
     }
     sms = g_sms[dev];
     if (g_occ.find(fn) == g_occ.end()) {
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIOT_EV_SMEM);
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
       g_occ.emplace(fn, 1);
     }
   }
   uint64_t blocks = (uint64_t)sms * (uint64_t)(g_override.bpsm > 0 ? g_override.bpsm : 1);
-  uint64_t need = (g.nvec + TRIOT_EV_SVEC - 1) / TRIOT_EV_SVEC;
+  const uint64_t svec = small ? TRIOT_EVS_SVEC : TRIOT_EV_SVEC;
+  uint64_t need = (g.nvec + svec - 1) / svec;
   if (need < blocks) blocks = need;
   if (blocks > TRIOT_EV_MAX_GRID) blocks = TRIOT_EV_MAX_GRID;
   if (blocks < 1) blocks = 1;
   set_decomposition(g, 2, blocks);
+  g.dv = (uint64_t)block;  // threads step by one block
+  set_step(g);
   uint64_t grid = (g.nvec + g.wmul - 1) / g.wmul;
   size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 2) * sizeof(double);
   if (!ws || ws_bytes < need_ws)
@@ -218,8 +227,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
     d.out = out;
     d.ws = ws;
     void* args[1] = {&d};
-    return launch_pdl(fn, (unsigned)grid, TRIOT_EV_TMA_BLOCK, TRIOT_EV_SMEM, (cudaStream_t)stream,
-                      args);
+    return launch_pdl(fn, (unsigned)grid, block, smem, (cudaStream_t)stream, args);
   };
   return g.idx64 ? go(uint64_t(0)) : go(uint32_t(0));
 }
@@ -476,7 +484,7 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
   else
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadOp: op = %d", op);
   if (st) return st;
-  if (mode < 0 || mode > 2) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadMode: %d", mode);
+  if (mode < 0 || mode > 2) return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadMode: %d", mode);  // 3 = 2 with small stages
   if (!g.empty) set_decomposition(g, mode, warps ? warps : 1);
   std::string s = describe(g);
   if (buf && buf_len) {
@@ -488,7 +496,7 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
 }
 
 int triot_set_launch_policy(int mode, int blocks_per_sm) {
-  if (mode < -1 || mode > 2 || blocks_per_sm < 0 || blocks_per_sm > 1024)
+  if (mode < -1 || mode > 3 || blocks_per_sm < 0 || blocks_per_sm > 1024)
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadPolicy: mode %d, blocks_per_sm %d", mode,
                      blocks_per_sm);
   g_override.mode = mode;

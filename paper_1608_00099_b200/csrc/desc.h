@@ -75,12 +75,18 @@ struct Desc {
 };
 
 // Workspace layout of the expected value: [ticket u32 | pad to 256 B] [grid x (D+2) doubles].
-#define TRIOT_EV_MAX_GRID 2048
+#define TRIOT_EV_MAX_GRID 8192
 #define TRIOT_EV_WS_HEADER 256
 // EV bulk-copy pipeline: NSTAGE shared-memory stages of SVEC 32-byte vectors per block
 #define TRIOT_EV_NSTAGE 6
 #define TRIOT_EV_SVEC 1024
 #define TRIOT_EV_TMA_BLOCK 512
 #define TRIOT_EV_SMEM (TRIOT_EV_NSTAGE * TRIOT_EV_SVEC * 32 + 2 * TRIOT_EV_NSTAGE * 8)
+// the small-stage variant: several resident blocks per SM, many blocks per launch (the hardware
+// block scheduler balances the SMs; each block's partial keeps the sum deterministic)
+#define TRIOT_EVS_NSTAGE 4
+#define TRIOT_EVS_SVEC 512
+#define TRIOT_EVS_BLOCK 256
+#define TRIOT_EVS_SMEM (TRIOT_EVS_NSTAGE * TRIOT_EVS_SVEC * 32 + 2 * TRIOT_EVS_NSTAGE * 8)
 
 }  // namespace triot

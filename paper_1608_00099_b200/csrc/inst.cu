@@ -53,8 +53,13 @@ const void* kptr() {
                 : (sizeof(IDX) == 4 ? (const void*)&conv_kernel<D, ESZ, false>
                                     : (const void*)&conv_kernel<D, ESZ, true>);
 #elif TRIOT_INST_BOP == 1
-  // EV bulk-copy fast path: only the 32-byte vector width exists
-  return V == 32 / ESZ ? (const void*)&ev_tma_kernel<D, ESZ, IDX> : nullptr;
+  // EV bulk-copy fast path: only the 32-byte vector width exists; vi slot 1 (16 B) carries the
+  // small-stage variant
+  if (V == 32 / ESZ) return (const void*)&ev_tma_kernel<D, ESZ, IDX>;
+  if (V == 16 / ESZ)
+    return (const void*)&ev_tma_kernel<D, ESZ, IDX, TRIOT_EVS_NSTAGE, TRIOT_EVS_SVEC,
+                                       TRIOT_EVS_BLOCK>;
+  return nullptr;
 #else
   return (const void*)&ev_kernel<D, ESZ, V, IDX, KEV>;
 #endif

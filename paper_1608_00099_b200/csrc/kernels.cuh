@@ -1127,14 +1127,11 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
 // vectors t, t+256, ...: the odometer steps +256 vectors) and each warp releases the stage on
 // its "empty" mbarrier before thread 0 refills it.  Requires V*ESZ == 32 and a 32-B aligned p.
 // Threads take vectors t, t+BLOCK, ...: the odometer steps +BLOCK vectors.
-template <int D, int ESZ, typename IDX>
-__global__ void __launch_bounds__(TRIOT_EV_TMA_BLOCK, 1)
-    ev_tma_kernel(const __grid_constant__ Desc<IDX> d) {
+template <int D, int ESZ, typename IDX, int NSTAGE = TRIOT_EV_NSTAGE, int SVEC = TRIOT_EV_SVEC,
+          int BLOCK = TRIOT_EV_TMA_BLOCK>
+__global__ void __launch_bounds__(BLOCK) ev_tma_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int V = 32 / ESZ;
   constexpr int NS = D + 2;
-  constexpr int NSTAGE = TRIOT_EV_NSTAGE;
-  constexpr int SVEC = TRIOT_EV_SVEC;
-  constexpr int BLOCK = TRIOT_EV_TMA_BLOCK;
   constexpr int PER_THREAD = SVEC / BLOCK;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)(smem + (size_t)NSTAGE * SVEC * 32);

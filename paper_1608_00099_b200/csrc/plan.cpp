@@ -401,8 +401,13 @@ void set_decomposition(Geom& g, int mode, uint64_t warps) {
     g.wmul = g.wspan = 32 * q;
     g.dv = 32;
   }
-  // the step in mixed radix (digit 0 absorbs the rest; it only matters past the end).  Flat
-  // vectors: the kernel walks the vector's V elements with +1 steps, then skips (dv-1)*V.
+  set_step(g);
+}
+
+// the step of dv vectors in mixed radix (digit 0 absorbs the rest; it only matters past the
+// end).  Flat vectors: the kernel walks the vector's V elements with +1 steps, then skips
+// (dv-1)*V.
+void set_step(Geom& g) {
   const int D = g.D;
   uint64_t rem = g.flat ? (g.dv - 1) * (uint64_t)g.V : g.dv;
   for (int k = D - 1; k >= 1; --k) {

@@ -82,6 +82,8 @@ int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const tr
 // 2 = contiguous chunk per block (EV bulk-copy kernel; `warps` is then the number of blocks).
 // Sets wmul/wspan/dv and the mixed-radix digits of the per-step advance (dlt, khi, klo, step).
 void set_decomposition(Geom& g, int mode, uint64_t warps);
+// (Re)compute the mixed-radix digits of the per-step advance for the current g.dv.
+void set_step(Geom& g);
 
 // Granlund-Montgomery round-up magic for an invariant 32-bit divisor (>= 1).
 void fastdiv_magic(uint32_t div, uint32_t* mul, uint32_t* shift);
