@@ -257,7 +257,7 @@ def run_ours(args, rank, world, local_rank):
                "C5": lambda: T.embed(g["dst5"], g["src5"])}
         for n, fn in fns.items():
             ts = []
-            for _ in range(5):
+            for _ in range(15):   # event timestamps are quantised (~2 us here): average
                 scratch.fill_(1)
                 clean.sum()
                 ea.record(stream)
@@ -265,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
                 eb.record(stream)
                 torch.cuda.synchronize(dev)
                 ts.append(ea.elapsed_time(eb))
-            iso[n] = statistics.median(ts)
+            iso[n] = statistics.fmean(ts)
         del scratch, clean
 
     # ---- the paper's own Benchmarks 1-3 (§8(f) NEXT-2/3), same isolated protocol
@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
         for name, (fn, nbytes) in cases.items():
             fn()
             ts = []
-            for _ in range(5):
+            for _ in range(15):
                 scratch.fill_(1)
                 clean.sum()
                 ea.record(stream)
@@ -299,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
                 eb.record(stream)
                 torch.cuda.synchronize(dev)
                 ts.append(ea.elapsed_time(eb))
-            ms = statistics.median(ts)
+            ms = statistics.fmean(ts)
             gbs = nbytes / (ms * 1e-3) / 1e9
             paper[name] = {"bytes": nbytes, "us": round(ms * 1000, 2), "gbs": round(gbs, 1),
                            "pct_of_8000": round(100 * gbs / NOMINAL_HBM_GBS, 1)}
@@ -379,7 +379,8 @@ def run_ours(args, rank, world, local_rank):
                          "by its predecessor",
                    "parallelism": f"replicas x{world} (weak; no data-path collective)"},
         "per_op": per_op,
-        "per_op_isolated": {"note": "each op alone after a clean L2 scrub, median of 5",
+        "per_op_isolated": {"note": "each op alone after a clean L2 scrub, mean of 15 launches "
+                                    "(event timestamps are quantised to ~2 us)",
                             "ops": per_op_iso},
         "paper_benchmarks": {"note": "P:333 Benchmarks 1-3 at the paper's shapes, f64, "
                                      "isolated as per_op_isolated (B3 is 27 MB: launch-bound)",

@@ -35,7 +35,7 @@ constexpr int ESZ = TRIOT_INST_ESZ;
 // loads in flight per lane per batch (bytes in flight, SURVEY §8(d) Little's law)
 constexpr int KEMBED = 4;
 constexpr int KBIN = 2;
-constexpr int KEV = 4;
+constexpr int KEV = 2;
 
 template <int D, int V, typename IDX>
 const void* kptr() {

@@ -691,7 +691,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
 }
 
 template <int D, int ESZ, int V, typename IDX, int K>
-__global__ void __launch_bounds__(kBlock) ev_kernel(const __grid_constant__ Desc<IDX> d) {
+__global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
   constexpr int NW = V * EW;
   constexpr int NS = D + 2;  // D digit slots + collapsed column slot + mass

@@ -21,8 +21,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--policy", default=None, help="mode,blocks_per_sm (triot_set_launch_policy)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
+    if a.policy:
+        mode, bpsm = (int(x) for x in a.policy.split(","))
+        T.triot_set_launch_policy(mode, bpsm)
     for name in a.only.split(","):
         if name == "B4":
             import numpy as np
