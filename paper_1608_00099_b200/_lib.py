@@ -229,7 +229,8 @@ def triot_apply_binary_host(c: int, a: int, a_shape, b: int, b_shape, iter_shape
 
 
 def triot_set_launch_policy(mode: int, blocks_per_sm: int = 0) -> None:
-    """Tuning hook: -1 = automatic, 0 = chunk per warp, 1 = grid stride (thread-local)."""
+    """Tuning hook (thread-local): -1 = automatic, 0 = chunk per warp, 1 = grid stride,
+    2 / 3 = EV bulk-copy pipeline, 4 = chunk per warp with a split EV reduction."""
     check(_lib.triot_set_launch_policy(mode, blocks_per_sm))
 
 

@@ -11,6 +11,7 @@
 #include "../../include/triot.h"
 #include "desc.h"
 #include "plan.hpp"
+#include "kernels.cuh"
 
 // dispatch tables, one per compiled family (inst.cu)
 extern "C" {
@@ -86,8 +87,10 @@ thread_local Policy g_override = {-1, 0, 0};
 // block scheduler hands out consecutive chunks as SMs free up: the active window of the tensors
 // stays compact and every SM stays busy to the end.  One wave at occupancy (the first version)
 // reached 5.0-5.9 TB/s on C2/C4/C5; this reaches 6.5-6.8 TB/s (single launch, clean L2).
+constexpr bool kEvSplitDefault = false;
+constexpr int kEvSplitBpsm = 16;
 Policy auto_policy(const Geom& g) {
-  if (g.op == OP_EV) return Policy{0, 0, 0};
+  if (g.op == OP_EV) return kEvSplitDefault ? Policy{0, kEvSplitBpsm, 0} : Policy{0, 0, 0};
   if (g.op == OP_DOT) return Policy{0, 8, 0};  // <= 2048 partials for the reduction
   return Policy{0, 64, 0};
 }
@@ -119,8 +122,10 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   // mode 2 (block chunks) exists only for the EV bulk-copy kernel: other kernels read the
   // descriptor per warp, so for them an override of 2 means "automatic"
   if (g_override.mode == 0 || g_override.mode == 1) pol.mode = g_override.mode;
+  if (g_override.mode == 4) pol.mode = 0;
   if (g_override.bpsm > 0) pol.bpsm = g_override.bpsm;
-  if ((g_override.mode == 0 || g_override.mode == 1) && g_override.bpsm == 0 && pol.mode != 0)
+  if ((g_override.mode == 0 || g_override.mode == 1 || g_override.mode == 4) &&
+      g_override.bpsm == 0 && pol.mode != 0)
     pol.q = 0;
   const uint64_t wpb = TRIOT_BLOCK / 32;
   const uint64_t kMinSteps = 4;  // >= 4 steps per warp amortise the start decode
@@ -247,6 +252,10 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   unsigned grid;
   int st = launch_geometry(fn, g, max_grid, &grid);
   if (st) return st;
+  if (g.zmask) {  // embed with zero runs (set_step): its own instance, same geometry
+    fn = table_for(g)(g.D, 4, g.idx64 ? 1 : 0);
+    if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no zero-run instance for D=%d", g.D);
+  }
   if (g.op == OP_EV || g.op == OP_DOT) {
     const size_t slots = g.op == OP_DOT ? 1 : (size_t)(g.D + 2);
     size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * slots * sizeof(double);
@@ -254,9 +263,23 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
       return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                        need);
   }
+  // EV: partials per block, summed by ev_final_kernel (PDL) -- no fence or atomic ticket per
+  // block, so many short blocks cost no serialised tail (mode 4, see auto_policy)
+  g.split = g.op == OP_EV && (g_override.mode == 4 || (g_override.mode < 0 && kEvSplitDefault));
   cudaStream_t s = (cudaStream_t)stream;
-  return g.idx64 ? launch_t<uint64_t>(g, fn, grid, s, out, ws)
-                 : launch_t<uint32_t>(g, fn, grid, s, out, ws);
+  int st2 = g.idx64 ? launch_t<uint64_t>(g, fn, grid, s, out, ws)
+                    : launch_t<uint32_t>(g, fn, grid, s, out, ws);
+  if (st2 || !g.split) return st2;
+  EvFin f;
+  memset(&f, 0, sizeof(f));
+  f.part = (const double*)((const char*)ws + TRIOT_EV_WS_HEADER);
+  f.out = (double*)out;
+  f.nblk = grid;
+  f.ns = g.D + 2;
+  f.d_out = g.nout >= 0 ? g.nout : g.d + (g.with_mass ? 1 : 0);
+  for (int k = 0; k <= TRIOT_MAXD; ++k) f.slot_of_axis[k] = g.slot_of_axis[k];
+  void* args[1] = {&f};
+  return launch_pdl((const void*)&ev_final_kernel<kFinBlock>, 1, kFinBlock, 0, s, args);
 }
 
 size_t ev_ws_bytes(int d) {
@@ -498,7 +521,7 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
 }
 
 int triot_set_launch_policy(int mode, int blocks_per_sm) {
-  if (mode < -1 || mode > 3 || blocks_per_sm < 0 || blocks_per_sm > 1024)
+  if (mode < -1 || mode > 4 || blocks_per_sm < 0 || blocks_per_sm > 1024)
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadPolicy: mode %d, blocks_per_sm %d", mode,
                      blocks_per_sm);
   g_override.mode = mode;

@@ -67,7 +67,11 @@ struct Desc {
   int32_t d_out;         // values written: the caller's d (+1 when the mass is requested)
   int32_t slot_of_axis[TRIOT_MAXD + 1];  // out[j] = slot >= 0 ? total[slot] : 0 (slot D+1 = mass)
   int32_t op;            // binary op
-  int32_t pad_;
+  int32_t split;         // reductions: 1 = write the block partial only; ev_final_kernel sums
+  // embed zero runs: 32 vectors == one unit of digit khi (lanes share digits 0..khi) and dst is
+  // dense in the counter, so while a digit <= khi is out of bounds the warp stores zeros at
+  // dst + r * step without touching the odometer (zmask = oob bits of digits 0..khi, 0 = off)
+  uint32_t zmask;
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
                                   // update: x, y, z
   void* out;             // EV: means (device)

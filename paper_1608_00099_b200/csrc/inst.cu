@@ -40,7 +40,7 @@ constexpr int KEV = 2;
 template <int D, int V, typename IDX>
 const void* kptr() {
 #if TRIOT_INST_OP == 0
-  return (const void*)&embed_kernel<D, ESZ, V, IDX, KEMBED>;
+  return (const void*)&embed_kernel<D, ESZ, V, IDX, KEMBED, false>;
 #elif TRIOT_INST_OP == 1
   return (const void*)&binary_kernel<D, ESZ, V, IDX, KBIN, TRIOT_INST_BOP>;
 #elif TRIOT_INST_OP == 3
@@ -79,19 +79,32 @@ const void* kptr_flat() {
 #endif
 }
 
-// table index: ((D-1) * 4 + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
-// 3 = flat 32-B vectors
+// embed with zero runs (32-B vectors, dst dense in the counter; Desc::zmask)
+template <int D, typename IDX>
+const void* kptr_zero_runs() {
+#if TRIOT_INST_OP == 0
+  return (const void*)&embed_kernel<D, ESZ, 32 / ESZ, IDX, KEMBED, true>;
+#else
+  return nullptr;
+#endif
+}
+
+// table index: ((D-1) * NVI + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
+// 3 = flat 32-B vectors, 4 = 32 B with embed zero runs
+constexpr int NVI = 5;
 template <int D>
 struct Fill {
   static void run(const void** t) {
-    t[((D - 1) * 4 + 0) * 2 + 0] = kptr<D, 32 / ESZ, uint32_t>();
-    t[((D - 1) * 4 + 0) * 2 + 1] = kptr<D, 32 / ESZ, uint64_t>();
-    t[((D - 1) * 4 + 1) * 2 + 0] = kptr<D, 16 / ESZ, uint32_t>();
-    t[((D - 1) * 4 + 1) * 2 + 1] = kptr<D, 16 / ESZ, uint64_t>();
-    t[((D - 1) * 4 + 2) * 2 + 0] = kptr<D, 1, uint32_t>();
-    t[((D - 1) * 4 + 2) * 2 + 1] = kptr<D, 1, uint64_t>();
-    t[((D - 1) * 4 + 3) * 2 + 0] = kptr_flat<D, uint32_t>();
-    t[((D - 1) * 4 + 3) * 2 + 1] = kptr_flat<D, uint64_t>();
+    t[((D - 1) * NVI + 4) * 2 + 0] = kptr_zero_runs<D, uint32_t>();
+    t[((D - 1) * NVI + 4) * 2 + 1] = kptr_zero_runs<D, uint64_t>();
+    t[((D - 1) * NVI + 0) * 2 + 0] = kptr<D, 32 / ESZ, uint32_t>();
+    t[((D - 1) * NVI + 0) * 2 + 1] = kptr<D, 32 / ESZ, uint64_t>();
+    t[((D - 1) * NVI + 1) * 2 + 0] = kptr<D, 16 / ESZ, uint32_t>();
+    t[((D - 1) * NVI + 1) * 2 + 1] = kptr<D, 16 / ESZ, uint64_t>();
+    t[((D - 1) * NVI + 2) * 2 + 0] = kptr<D, 1, uint32_t>();
+    t[((D - 1) * NVI + 2) * 2 + 1] = kptr<D, 1, uint64_t>();
+    t[((D - 1) * NVI + 3) * 2 + 0] = kptr_flat<D, uint32_t>();
+    t[((D - 1) * NVI + 3) * 2 + 1] = kptr_flat<D, uint64_t>();
     Fill<D - 1>::run(t);
   }
 };
@@ -101,7 +114,7 @@ struct Fill<0> {
 };
 
 struct Table {
-  const void* t[TRIOT_MAXD * 4 * 2];
+  const void* t[TRIOT_MAXD * NVI * 2];
   Table() { Fill<TRIOT_MAXD>::run(t); }
 };
 
@@ -110,6 +123,6 @@ struct Table {
 
 extern "C" const void* TRIOT_NAME(int D, int vi, int idx64) {
   static const triot::Table tab;  // thread-safe one-time init
-  if (D < 1 || D > TRIOT_MAXD || vi < 0 || vi > 3) return nullptr;
-  return tab.t[((D - 1) * 4 + vi) * 2 + (idx64 ? 1 : 0)];
+  if (D < 1 || D > TRIOT_MAXD || vi < 0 || vi >= triot::NVI) return nullptr;
+  return tab.t[((D - 1) * triot::NVI + vi) * 2 + (idx64 ? 1 : 0)];
 }

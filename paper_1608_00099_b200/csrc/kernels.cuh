@@ -245,7 +245,7 @@ __device__ __forceinline__ void store_vec(const TensorAcc<IDX>& t, IDX off, uint
 // dst[t] = (t < src_shape) ? src[t] : +0.0 over the counter.
 // Tensor 0 = dst, tensor 1 = src.  Raw 32-bit words are moved; no floating point.
 
-template <int D, int ESZ, int V, typename IDX, int K>
+template <int D, int ESZ, int V, typename IDX, int K, bool ZR>
 __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
   constexpr int NW = V * EW;
@@ -261,46 +261,78 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   odo_start<D, 2, true, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
   pdl_wait();
-  for (IDX b = base0; b < vend; b += K * d.dv) {
-    uint32_t buf[K][NW];
-    IDX doff[K];
-    bool valid[K];
+  IDX b = base0;
+  for (;;) {
+    while (b < vend && !(ZR && (oob & d.zmask))) {
+      b += K * d.dv;
+      uint32_t buf[K][NW];
+      IDX doff[K];
+      bool valid[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      valid[j] = v < vend;
-      v += d.dv;
-      doff[j] = off[0];
-      if (valid[j]) {
-        const IDX uv = u[D - 1];
-        const bool any = oob == 0 && uv < d.vany;
-        if (any && uv < d.vfull) {
-          load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, buf[j]);
-        } else if (!any) {
+      for (int j = 0; j < K; ++j) {
+        valid[j] = v < vend;
+        v += d.dv;
+        doff[j] = off[0];
+        if (valid[j]) {
+          const IDX uv = u[D - 1];
+          const bool any = oob == 0 && uv < d.vany;
+          if (any && uv < d.vfull) {
+            load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, buf[j]);
+          } else if (!any) {
 #pragma unroll
-          for (int q = 0; q < NW; ++q) buf[j][q] = 0u;
-        } else {
-          // partial vector: per-element bounds (rows of a collapsed vector, columns at the
-          // src edge)
-          const IDX row0 = uv * d.rowmul, col0 = uv * d.colmul;
+            for (int q = 0; q < NW; ++q) buf[j][q] = 0u;
+          } else {
+            // partial vector: per-element bounds (rows of a collapsed vector, columns at the
+            // src edge)
+            const IDX row0 = uv * d.rowmul, col0 = uv * d.colmul;
 #pragma unroll
-          for (int e = 0; e < V; ++e) {
-            const IDX r = (IDX)((uint32_t)e >> lgL);
-            const IDX c = (IDX)((uint32_t)e & ((1u << lgL) - 1u));
-            if (row0 + r < d.srows && col0 + c < d.scols) {
-              Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1] + r * d.t[1].rho + c * d.t[1].tau),
-                           buf[j] + e * EW);
-            } else {
+            for (int e = 0; e < V; ++e) {
+              const IDX r = (IDX)((uint32_t)e >> lgL);
+              const IDX c = (IDX)((uint32_t)e & ((1u << lgL) - 1u));
+              if (row0 + r < d.srows && col0 + c < d.scols) {
+                Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1] + r * d.t[1].rho + c * d.t[1].tau),
+                             buf[j] + e * EW);
+              } else {
 #pragma unroll
-              for (int q = 0; q < EW; ++q) buf[j][e * EW + q] = 0u;
+                for (int q = 0; q < EW; ++q) buf[j][e * EW + q] = 0u;
+              }
             }
           }
         }
+        odo_step<D, 2, true, IDX>(d, u, off, oob);
       }
-      odo_step<D, 2, true, IDX>(d, u, off, oob);
-    }
 #pragma unroll
-    for (int j = 0; j < K; ++j)
-      if (valid[j]) store_vec<ESZ, V, IDX>(d.t[0], doff[j], lgL, buf[j]);
+      for (int j = 0; j < K; ++j)
+        if (valid[j]) store_vec<ESZ, V, IDX>(d.t[0], doff[j], lgL, buf[j]);
+    }
+    if (!ZR || b >= vend) break;
+    // zero run (warp-uniform: digits 0..khi are the same in every lane).  m = the most
+    // significant out-of-bounds digit; it stays out of bounds until digits m..khi wrap, i.e.
+    // for N - S more steps (N, S = size and mixed-radix value of the sub-counter m..khi).
+    const int m = __ffs(oob & d.zmask) - 1;
+    IDX S = 0, N = 1;
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k)
+      if (k >= m && k <= d.khi) {
+        S = S * d.ext[k] + u[k];
+        N = N * d.ext[k];
+      }
+    IDX run = N - S;
+    const IDX left = (vend - b + 31) / 32;
+    if (run > left) run = left;
+    const IDX full = (b + run * 32 <= vend) ? run : run - 1;
+    const IDX st0 = d.t[0].step;
+    IDX o = off[0];
+    uint32_t z[NW];
+#pragma unroll
+    for (int q = 0; q < NW; ++q) z[q] = 0u;
+#pragma unroll 1
+    for (IDX r = 0; r < full; ++r, o += st0) store_vec<ESZ, V, IDX>(d.t[0], o, lgL, z);
+    if (full < run && v + full * 32 < vend) store_vec<ESZ, V, IDX>(d.t[0], o, lgL, z);
+    b += run * 32;
+    v += run * 32;
+    if (b >= vend) break;
+    odo_start<D, 2, true, IDX>(d, v, u, off, oob);
   }
 }
 
@@ -653,7 +685,11 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
 #pragma unroll
     for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
     part[(size_t)blockIdx.x * NS + threadIdx.x] = t;
-    __threadfence();
+    if (!d.split) __threadfence();
+  }
+  if (d.split) {  // ev_final_kernel sums the partials once this grid has completed
+    pdl_trigger();
+    return;
   }
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -690,6 +726,52 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
   if (threadIdx.x == 0) *ticket = 0u;  // leave the workspace ready for the next call
 }
 
+// Second half of a split reduction: launched after the reduction kernel with programmatic
+// stream serialization; griddepcontrol.wait returns once every partial is written and visible.
+// Fixed order for a fixed partial count: per thread a strided sequential sum, warp butterfly,
+// warps in index order -- deterministic like the single-kernel ticket path.
+constexpr int kFinBlock = 512;
+struct EvFin {
+  const double* part;
+  double* out;
+  uint32_t nblk;
+  int32_t ns, d_out;
+  int32_t slot_of_axis[TRIOT_MAXD + 1];
+};
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) ev_final_kernel(const __grid_constant__ EvFin f) {
+  constexpr int NSMAX = TRIOT_MAXD + 2;
+  pdl_trigger();
+  pdl_wait();
+  double a[NSMAX];
+#pragma unroll
+  for (int k = 0; k < NSMAX; ++k) a[k] = 0.0;
+  for (uint32_t b = threadIdx.x; b < f.nblk; b += BLOCK) {
+    const double* p = f.part + (size_t)b * (size_t)f.ns;
+#pragma unroll
+    for (int k = 0; k < NSMAX; ++k)
+      if (k < f.ns) a[k] += __ldcg(p + k);
+  }
+  __shared__ double sm[BLOCK / 32][NSMAX];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NSMAX; ++k) {
+    if (k < f.ns) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+      if (lane == 0) sm[wib][k] = a[k];
+    }
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < f.d_out) {
+    const int sl = f.slot_of_axis[threadIdx.x];
+    double t = 0.0;
+    if (sl >= 0)
+      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][sl];
+    f.out[threadIdx.x] = t;
+  }
+}
+
 template <int D, int ESZ, int V, typename IDX, int K>
 __global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
@@ -702,7 +784,7 @@ __global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ D
   double acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-  pdl_trigger();
+  if (!d.split) pdl_trigger();
   pdl_wait();
   if (base0 < d.nvec) {
     const IDX vend = warp_end(d, base0);
@@ -882,7 +964,7 @@ __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__
   double acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-  pdl_trigger();
+  if (!d.split) pdl_trigger();
   pdl_wait();
   if (base0 < d.nvec) {
     const IDX vend = warp_end(d, base0);

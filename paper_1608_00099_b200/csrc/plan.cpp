@@ -431,6 +431,15 @@ void set_step(Geom& g) {
     for (int k = 0; k < D; ++k) st += g.dlt[k] * g.t[x].sig[k];
     g.t[x].step = st;
   }
+  // embed zero runs: a step of exactly one unit of digit khi < D-1 and dst offsets linear in it
+  g.zmask = 0;
+  if (g.op == OP_EMBED && !g.flat && g.mode == 0 && g.dv == 32 && g.khi >= 0 && g.khi < D - 1 &&
+      g.dlt[g.khi] == 1 && g.t[0].vec && g.V * g.esz == 32) {
+    bool ok = true;
+    for (int k = 0; k < D; ++k) ok = ok && (k == g.khi ? true : g.dlt[k] == 0);
+    for (int k = 1; k <= g.khi; ++k) ok = ok && g.t[0].kap[k] == 0;
+    if (ok) g.zmask = (uint32_t)((2ull << g.khi) - 1ull);
+  }
 }
 
 // ------------------------------------------------------------------------------ public planners
@@ -929,14 +938,14 @@ std::string describe(const Geom& g) {
            "\"op\":%d,\"esz\":%d,\"d\":%d,\"empty\":%s,\"idx64\":%s,\"all_oob\":%s,\"Dc\":%d,"
            "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"flat\":%s,\"N\":%llu,\"nvec\":%llu,"
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
-           "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,",
+           "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
            (unsigned long long)g.nsteps, g.mode, (unsigned long long)g.wmul,
            (unsigned long long)g.wspan, (unsigned long long)g.dv, g.khi, g.klo, (unsigned long long)g.rowmul,
            (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,
-           (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots);
+           (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots, g.zmask);
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

@@ -48,6 +48,8 @@ struct Geom {
   int nslots = 0;
   bool with_mass = false;   // EV: also write sum(p) after the d means
   int nout = -1;            // reduction outputs if not d (+mass): the inner product writes 1
+  bool split = false;       // reductions: partials summed by a second (PDL) kernel
+  uint32_t zmask = 0;       // embed zero runs (desc.h)
   struct T {
     uint64_t sig[TRIOT_MAXD] = {}, kap[TRIOT_MAXD] = {};
     uint64_t step = 0, rho = 0, tau = 1;
@@ -123,7 +125,8 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.collapsed = g.collapsed ? 1 : 0;
   d.d_out = g.nout >= 0 ? g.nout : g.d + (g.with_mass ? 1 : 0);
   d.op = g.binop;
-  d.pad_ = 0;
+  d.split = g.split ? 1 : 0;
+  d.zmask = g.zmask;
   for (int x = 0; x < TRIOT_MAXT; ++x) {
     for (int k = 0; k < TRIOT_MAXD; ++k) {
       d.t[x].sig[k] = (IDX)g.t[x].sig[k];

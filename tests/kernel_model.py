@@ -83,7 +83,25 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
         for lane in range(lanes):
             v = base0 + lane
             u, off, oob = start(v)
+            zmask = desc.get("zmask", 0)
             while v < vend:
+                if op == "embed" and oob & zmask:
+                    # zero run: digit m stays out of bounds until digits m..khi wrap
+                    m = ((oob & zmask) & -(oob & zmask)).bit_length() - 1
+                    S, N = 0, 1
+                    for k in range(m, khi + 1):
+                        S, N = S * ext[k] + u[k], N * ext[k]
+                    run_ = min(N - S, (vend - (v - lane) + 31) // 32)
+                    o = off[0]
+                    for r in range(run_):
+                        if v + 32 * r < vend:
+                            for e in range(V):
+                                bufs[0][eoff(0, o, e)] = 0
+                        o = W(o + T[0]["step"])
+                    v += 32 * run_
+                    if v < vend:
+                        u, off, oob = start(v)
+                    continue
                 if True:
                     uv = u[D - 1]
                     if op == "embed":

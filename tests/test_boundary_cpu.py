@@ -55,6 +55,19 @@ def test_constants_and_status_strings():
         assert T.triot_status_string(code) == name
 
 
+def test_launch_policy_range():
+    """Modes -1..4 and 0..1024 blocks per SM are accepted (host state only); others rejected."""
+    lib = L.lib()
+    try:
+        for mode in range(-1, 5):
+            assert lib.triot_set_launch_policy(mode, 16) == 0
+        for mode, bpsm in [(-2, 0), (5, 0), (0, -1), (0, 1025)]:
+            assert lib.triot_set_launch_policy(mode, bpsm) == 5
+            assert "BadPolicy" in T.triot_last_error()
+    finally:
+        lib.triot_set_launch_policy(-1, 0)
+
+
 def _embed(dst_shape, src_shape, d=None, dtype=F64, flags=0, dst=FAKE, src=FAKE * 2):
     d = len(dst_shape) if d is None else d
     return T.triot_embed(dst, dst_shape, src, src_shape, d, dtype, flags, 0)
@@ -226,6 +239,31 @@ def test_model_embed_vs_oracle(dtype, seed):
     out = np.full(dst_shape, -7.0, dtype=src.dtype)
     kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
     np.testing.assert_array_equal(_bits(out), _bits(ref))
+
+
+@pytest.mark.parametrize("dst_shape,src_shape,dtype,warps", [
+    ((4,) * 7, (3,) * 7, "f32", 5),               # C5's structure at 4^7: 32 vectors = 4^2 x 2
+    ((4,) * 7, (3,) * 7, "f32", 1),
+    ((5, 4, 4, 2, 8), (2, 3, 4, 2, 5), "f32", 3),  # 32 vectors = 4 x 4 x 2 rows of 8
+    ((3, 6, 2, 4, 4, 4), (3, 4, 1, 3, 2, 4), "f64", 7),  # f64: 4 per vector, 2 x 4 x 4 = 32
+    ((4, 4, 4, 4, 4), (4, 4, 4, 4, 4), "f32", 2),  # no zeros at all
+])
+def test_model_embed_zero_runs_vs_oracle(dst_shape, src_shape, dtype, warps):
+    """Embed zero runs (the warp stores zeros while an outer digit is out of bounds, then
+    re-decodes): the plan enables them for these shapes and the model's output is the oracle's."""
+    rng = np.random.default_rng(77)
+    src = random_values(rng, src_shape, dtype, "normal")
+    dt = F32 if dtype == "f32" else F64
+    for region in (False, True):
+        ref = np.full(dst_shape, -7.0, dtype=src.dtype)
+        O.embed(ref, src, region_only=region)
+        desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, len(dst_shape), dt,
+                                     1 if region else 0, mode=0, warps=warps)
+        if not region and dst_shape != src_shape:
+            assert desc["zmask"] != 0, desc
+        out = np.full(dst_shape, -7.0, dtype=src.dtype)
+        kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
+        np.testing.assert_array_equal(_bits(out), _bits(ref))
 
 
 @pytest.mark.parametrize("seed", range(10))

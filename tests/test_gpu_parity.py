@@ -512,26 +512,51 @@ def test_host_streaming_embed_and_binary():
     assert_bits_equal(out, ref)
 
 
+@pytest.mark.parametrize("dst_shape,src_shape,dtype", [
+    ((4,) * 9, (3,) * 9, np.float32),
+    ((5, 4, 4, 2, 8), (2, 3, 4, 2, 5), np.float32),
+    ((3, 6, 2, 4, 4, 4), (3, 4, 1, 3, 2, 4), np.float64),
+    ((7, 3, 4, 4, 4, 4), (7, 3, 4, 4, 3, 3), np.float32),  # zero runs of one step only
+])
+def test_embed_zero_runs(dst_shape, src_shape, dtype):
+    """Shapes whose plan stores zero runs without the odometer, under several chunkings (runs
+    cut by chunk ends, ragged last step), bit-exact against the oracle."""
+    rng = np.random.default_rng(91)
+    src = rng.standard_normal(src_shape).astype(dtype)
+    ref = np.empty(dst_shape, dtype); O.embed(ref, src)
+    try:
+        for mode, bpsm in [(-1, 0), (0, 1), (0, 3), (0, 200)]:
+            T.triot_set_launch_policy(mode, bpsm)
+            dst = _poisoned(dst_shape, dtype)
+            T.embed(dst, _dev(src))
+            assert_bits_equal(dst, ref)
+    finally:
+        T.triot_set_launch_policy(-1, 0)
+
+
 def test_results_independent_of_launch_policy():
     """Every work decomposition gives bit-identical embed / binary / dot / update results, and the
     expected value stays deterministic per policy and within 1e-12 across policies."""
     rng = np.random.default_rng(55)
     src = rng.standard_normal((37, 29, 11)).astype(np.float32)
     a = rng.standard_normal((33, 17, 9, 6)); b = rng.standard_normal((35, 17, 12, 8))
-    p = rng.random((13, 7, 9, 5))
+    ps = [rng.random((13, 7, 9, 5)), rng.random((9, 16, 8, 12))]  # flat / 32-B vectors
     ref_e = np.empty((41, 32, 12), np.float32); O.embed(ref_e, src)
     ref_b = O.apply_binary(a, b, "div")
-    ref_m = O.expected_value(p)
+    ref_ms = [O.expected_value(p) for p in ps]
     try:
-        for mode, bpsm in [(0, 1), (0, 7), (0, 64), (1, 1), (1, 3), (2, 1), (-1, 0)]:
+        for mode, bpsm in [(0, 1), (0, 7), (0, 64), (1, 1), (1, 3), (2, 1), (3, 2), (4, 1),
+                           (4, 16), (4, 64), (-1, 0)]:
             T.triot_set_launch_policy(mode, bpsm)
             dst = _poisoned((41, 32, 12), np.float32)
             T.embed(dst, _dev(src))
             assert_bits_equal(dst, ref_e)
             assert_bits_equal(T.apply_binary(_dev(a), _dev(b), "div"), ref_b)
-            m1 = T.expected_value(_dev(p)).cpu().numpy()
-            m2 = T.expected_value(_dev(p)).cpu().numpy()
-            assert _bits(m1).tolist() == _bits(m2).tolist()
-            assert np.all(np.abs(m1 - ref_m) <= 1e-12 * np.abs(ref_m))
+            for p, ref_m in zip(ps, ref_ms):
+                m1 = T.expected_value(_dev(p), with_mass=True).cpu().numpy()
+                m2 = T.expected_value(_dev(p), with_mass=True).cpu().numpy()
+                assert _bits(m1).tolist() == _bits(m2).tolist()
+                assert np.all(np.abs(m1[:-1] - ref_m) <= 1e-12 * np.abs(ref_m))
+                assert abs(m1[-1] - p.sum()) <= 1e-12 * p.sum()
     finally:
         T.triot_set_launch_policy(-1, 0)

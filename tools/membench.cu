@@ -215,3 +215,57 @@ extern "C" int mb_mix_bc(const void* src, void* dst, uint64_t bytes, int blocks,
   else mix_bc<2><<<blocks,threads,0,s>>>((const char*)src,(char*)dst,n32,per,rd);
   return (int)cudaGetLastError();
 }
+
+// one-shot grid (the shape of torch's elementwise kernels): block b writes blockDim*U vectors of
+// VB bytes starting at b*blockDim*U*VB, interleaved by thread; every thread exits after U stores
+template <int VB, int U>
+__global__ void write_os(char* dst, uint64_t nv) {
+  uint64_t base = (uint64_t)blockIdx.x * blockDim.x * U + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    uint64_t v = base + (uint64_t)j * blockDim.x;
+    if (v < nv) {
+      if (VB == 32) st256<1>(dst + v * 32, 0u, 0u);
+      else asm volatile("st.global.v4.b32 [%0], {%1,%1,%1,%1};" ::"l"(dst + v * 16), "r"(0u) : "memory");
+    }
+  }
+}
+extern "C" int mb_write_os(void* dst, uint64_t bytes, int vb, int threads, int u, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t nv = bytes / vb;
+  uint64_t per = (uint64_t)threads * u;
+  unsigned blocks = (unsigned)((nv + per - 1) / per);
+#define OS(VB_, U_) write_os<VB_, U_><<<blocks, threads, 0, s>>>((char*)dst, nv)
+  if (vb == 32) { if (u == 1) OS(32, 1); else if (u == 2) OS(32, 2); else if (u == 4) OS(32, 4); else OS(32, 8); }
+  else { if (u == 1) OS(16, 1); else if (u == 2) OS(16, 2); else if (u == 4) OS(16, 4); else OS(16, 8); }
+  return (int)cudaGetLastError();
+}
+
+// one-shot read: block b reads blockDim*U 32-B vectors starting at b*blockDim*U, interleaved by
+// thread, folds them and writes one word per block (the shape of a one-partial-per-block
+// reduction)
+template <int U>
+__global__ void read_os(const char* src, uint64_t nv, uint32_t* part) {
+  uint64_t base = (uint64_t)blockIdx.x * blockDim.x * U + threadIdx.x;
+  W8 r[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    uint64_t v = base + (uint64_t)j * blockDim.x;
+    if (v < nv) r[j] = ld256(src + v * 32); else r[j] = W8{};
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= r[j].w[k];
+  acc = __reduce_xor_sync(0xffffffffu, acc);
+  if ((threadIdx.x & 31) == 0) atomicXor(part + blockIdx.x, acc);
+}
+extern "C" int mb_read_os(const void* src, uint64_t bytes, int threads, int u, void* part, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t nv = bytes / 32, per = (uint64_t)threads * u;
+  unsigned blocks = (unsigned)((nv + per - 1) / per);
+#define ROS(U_) read_os<U_><<<blocks, threads, 0, s>>>((const char*)src, nv, (uint32_t*)part)
+  if (u == 1) ROS(1); else if (u == 2) ROS(2); else if (u == 4) ROS(4); else if (u == 8) ROS(8); else ROS(16);
+  return (int)cudaGetLastError();
+}

@@ -24,7 +24,8 @@ def build():
         subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
                         "-Xcompiler", "-fPIC", "-o", SO, src], check=True)
     L = ctypes.CDLL(SO)
-    for f in ("mb_write", "mb_read", "mb_mix", "mb_write_gs", "mb_mix_gs", "mb_mix_bc"):
+    for f in ("mb_write", "mb_read", "mb_mix", "mb_write_gs", "mb_mix_gs", "mb_mix_bc",
+              "mb_write_os"):
         getattr(L, f).restype = ctypes.c_int
     L.mb_write.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
@@ -35,6 +36,8 @@ def build():
     L.mb_write_gs.argtypes = L.mb_write.argtypes
     L.mb_mix_gs.argtypes = L.mb_mix.argtypes
     L.mb_mix_bc.argtypes = L.mb_mix.argtypes
+    L.mb_write_os.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_void_p]
     return L
 
 
@@ -76,6 +79,17 @@ def main():
         print(json.dumps(out[-1]), flush=True)
 
     rec("torch.fill_", "", nbytes, timeit(lambda: dst.fill_(0.0), scrub))
+    if "--os" in sys.argv:
+        for vb in (16, 32):
+            for th in (128, 256, 512):
+                for u in (1, 2, 4, 8):
+                    rec("write_os", f"vb={vb} threads={th} U={u}", nbytes,
+                        timeit(lambda: L.mb_write_os(dst.data_ptr(), nbytes, vb, th, u, s), scrub))
+        for bpsm in (8, 16, 32, 64):
+            rec("write", f"bpsm={bpsm} pol=1 U=4", nbytes,
+                timeit(lambda: L.mb_write(dst.data_ptr(), nbytes, sms * bpsm, 256, 1, 4, s), scrub))
+        rec("torch.fill_", "again", nbytes, timeit(lambda: dst.fill_(0.0), scrub))
+        return
     if "--gs" in sys.argv:
         for bpsm in (2, 4, 8, 16):
             for pol in (0, 2):
