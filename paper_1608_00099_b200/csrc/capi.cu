@@ -92,6 +92,13 @@ constexpr int kEvSplitBpsm = 16;
 Policy auto_policy(const Geom& g) {
   if (g.op == OP_EV) return kEvSplitDefault ? Policy{0, kEvSplitBpsm, 0} : Policy{0, 0, 0};
   if (g.op == OP_DOT) return Policy{0, 8, 0};  // <= 2048 partials for the reduction
+  if (g.op == OP_EMBED) {
+    // zero-run embeds (C5: 94 % of the steps are zero runs) keep improving up to the 4-step
+    // minimum chunk (ncu, C5: 64 / 128 / 192 blocks per SM -> 160.4 / 156.6 / 156.3 us)
+    Geom probe = g;
+    set_decomposition(probe, 0, 1);
+    if (probe.zmask) return Policy{0, 256, 0};
+  }
   return Policy{0, 64, 0};
 }
 

@@ -269,3 +269,13 @@ extern "C" int mb_read_os(const void* src, uint64_t bytes, int threads, int u, v
   if (u == 1) ROS(1); else if (u == 2) ROS(2); else if (u == 4) ROS(4); else if (u == 8) ROS(8); else ROS(16);
   return (int)cudaGetLastError();
 }
+
+// write_k<pol 1, U 4> with occupancy limited by dynamic shared memory (blocks per SM)
+extern "C" int mb_write_occ(void* dst, uint64_t bytes, int blocks, int threads, int smem, void* stream) {
+  uint64_t n32 = bytes / 32, q;
+  geom(n32, blocks, threads, &q);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(write_k<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  write_k<1, 4><<<blocks, threads, smem, s>>>((char*)dst, n32, q);
+  return (int)cudaGetLastError();
+}

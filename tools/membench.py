@@ -25,7 +25,7 @@ def build():
                         "-Xcompiler", "-fPIC", "-o", SO, src], check=True)
     L = ctypes.CDLL(SO)
     for f in ("mb_write", "mb_read", "mb_mix", "mb_write_gs", "mb_mix_gs", "mb_mix_bc",
-              "mb_write_os"):
+              "mb_write_os", "mb_write_occ"):
         getattr(L, f).restype = ctypes.c_int
     L.mb_write.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
@@ -36,6 +36,8 @@ def build():
     L.mb_write_gs.argtypes = L.mb_write.argtypes
     L.mb_mix_gs.argtypes = L.mb_mix.argtypes
     L.mb_mix_bc.argtypes = L.mb_mix.argtypes
+    L.mb_write_occ.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_void_p]
     L.mb_write_os.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                               ctypes.c_int, ctypes.c_void_p]
     return L
@@ -79,6 +81,12 @@ def main():
         print(json.dumps(out[-1]), flush=True)
 
     rec("torch.fill_", "", nbytes, timeit(lambda: dst.fill_(0.0), scrub))
+    if "--occ" in sys.argv:
+        for smem, nb in ((0, 8), (36 << 10, 6), (44 << 10, 5), (54 << 10, 4), (72 << 10, 3), (110 << 10, 2)):
+            for bpsm in (64, 128):
+                rec("write_occ", f"blocks/SM={nb} bpsm={bpsm}", nbytes,
+                    timeit(lambda: L.mb_write_occ(dst.data_ptr(), nbytes, sms * bpsm, 256, smem, s), scrub))
+        return
     if "--os" in sys.argv:
         for vb in (16, 32):
             for th in (128, 256, 512):
