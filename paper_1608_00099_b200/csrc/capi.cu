@@ -228,7 +228,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   g.dv = (uint64_t)block;  // threads step by one block
   set_step(g);
   uint64_t grid = (g.nvec + g.wmul - 1) / g.wmul;
-  size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)(g.D + 2) * sizeof(double);
+  size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)ev_slot_pad(g.D + 2) * sizeof(double);
   if (!ws || ws_bytes < need_ws)
     return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                      need_ws);
@@ -264,7 +264,7 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
     if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no zero-run instance for D=%d", g.D);
   }
   if (g.op == OP_EV || g.op == OP_DOT) {
-    const size_t slots = g.op == OP_DOT ? 1 : (size_t)(g.D + 2);
+    const size_t slots = (size_t)ev_slot_pad(g.op == OP_DOT ? 1 : g.D + 2);
     size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * slots * sizeof(double);
     if (!ws || ws_bytes < need)
       return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
@@ -290,7 +290,7 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
 }
 
 size_t ev_ws_bytes(int d) {
-  return TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * (size_t)(d + 2) * sizeof(double);
+  return TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * (size_t)ev_slot_pad(d + 2) * sizeof(double);
 }
 
 }  // namespace

@@ -661,60 +661,108 @@ __device__ __forceinline__ void ev_finish(const Desc<IDX>& d, const IDX (&u)[D],
   acc[D + 1] = a.S;  // the mass (slab-sharded EV amalgamation term)
 }
 
+// partial slots per block, padded to a power of two so the final sum reads them coalesced
+__host__ __device__ constexpr int ev_slot_pad(int ns) {
+  return ns <= 1 ? 1 : ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 8 ? 8 : ns <= 16 ? 16 : 32;
+}
+
+// Warp reduce-scatter of NS partial sums (fixed order): at each butterfly level a lane keeps
+// half of its slots and adds the partner's copy of them, so after log2(P) levels (P = NS rounded
+// up to a power of two) every lane holds one slot's sum over its group and plain butterfly levels
+// finish it -- NS + log2 levels of shuffles instead of 5 * NS.  Returns the value; `slot` gets
+// its slot index (lanes with the same slot hold identical values).
+template <int NS>
+__device__ __forceinline__ double warp_reduce_scatter(const double (&acc)[NS], int lane,
+                                                      int& slot) {
+  constexpr int P = NS <= 1 ? 1 : NS <= 2 ? 2 : NS <= 4 ? 4 : NS <= 8 ? 8 : NS <= 16 ? 16 : 32;
+  double a[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) a[k] = k < NS ? acc[k] : 0.0;
+  int base = 0;
+#pragma unroll
+  for (int L = 0; L < 5; ++L) {
+    const int o = 16 >> L;
+    const int h = P >> L;
+    if (h > 1) {
+      const int half = h / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const double send = up ? a[j] : a[j + half];
+        const double keep = up ? a[j + half] : a[j];
+        a[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      if (up) base += half;
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], o);
+    }
+  }
+  slot = base;
+  return a[0];
+}
+
 // Fixed-order block reduction, one partial per block, ordered final sum by the last block.
 template <int NS, int BLOCK, typename IDX>
 __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS]) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NS; ++k) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-  }
+  constexpr int GRP = NS <= 1 ? 32 : NS <= 2 ? 16 : NS <= 4 ? 8 : NS <= 8 ? 4 : NS <= 16 ? 2 : 1;
   __shared__ double sm[BLOCK / 32][NS];
   __shared__ int is_last;
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k) sm[wib][k] = acc[k];
+  {
+    int slot;
+    const double v = warp_reduce_scatter<NS>(acc, lane, slot);
+    if ((lane & (GRP - 1)) == 0 && slot < NS) sm[wib][slot] = v;
   }
   __syncthreads();
   unsigned* ticket = (unsigned*)d.ws;
   double* part = (double*)((char*)d.ws + TRIOT_EV_WS_HEADER);
-  if (threadIdx.x < NS) {
+  constexpr int P = ev_slot_pad(NS);
+  static_assert(BLOCK % P == 0, "slots must tile the block");
+  if (threadIdx.x < P) {  // padding slots carry +0.0
     double t = 0.0;
+    if (threadIdx.x < NS) {
 #pragma unroll
-    for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
-    part[(size_t)blockIdx.x * NS + threadIdx.x] = t;
-    if (!d.split) __threadfence();
+      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
+    }
+    part[(size_t)blockIdx.x * P + threadIdx.x] = t;
   }
-  if (d.split) {  // ev_final_kernel sums the partials once this grid has completed
-    pdl_trigger();
-    return;
-  }
+  if (d.split) return;  // ev_final_kernel sums the partials once this grid has completed
+  // Ticket: the barrier orders this block's partial stores before thread 0's acq_rel atomic
+  // (release is cumulative over them); the last block's acquire + barrier orders its partial
+  // loads (L2, __ldcg) after every other block's release.  Cheaper than __threadfence's
+  // MEMBAR.SC + L1 invalidate per block.
   __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ticket) : "memory");
+    is_last = old == gridDim.x - 1;
+  }
   __syncthreads();
   TRIOT_TRACE(3);
   if (!is_last) return;
-  __threadfence();
-  double f[NS];
+  // The last block reads the grid x P partials coalesced: thread t always meets slot t % P
+  // (P divides the block) and sums blocks t / P, t / P + BLOCK / P, ... in order, 4 loads in
+  // flight; lanes with the same slot are then combined by a butterfly and warps in index order.
+  const unsigned total = gridDim.x * (unsigned)P;
+  double f = 0.0;
+  for (unsigned i0 = threadIdx.x; i0 < total; i0 += 4 * BLOCK) {
+    double x[4];
 #pragma unroll
-  for (int k = 0; k < NS; ++k) f[k] = 0.0;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+    for (int i = 0; i < 4; ++i) {
+      const unsigned idx = i0 + (unsigned)i * BLOCK;
+      x[i] = idx < total ? __ldcg(part + idx) : 0.0;
+    }
 #pragma unroll
-    for (int k = 0; k < NS; ++k) f[k] += __ldcg(part + (size_t)b * NS + k);
+    for (int i = 0; i < 4; ++i) f += x[i];
   }
+  TRIOT_TRACE(5);
 #pragma unroll
-  for (int k = 0; k < NS; ++k) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) f[k] += __shfl_xor_sync(0xffffffffu, f[k], o);
-  }
+  for (int o = 16; o >= P; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
   __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k) sm[wib][k] = f[k];
-  }
+  if (lane < NS) sm[wib][lane] = f;
   __syncthreads();
+  TRIOT_TRACE(6);
   if (threadIdx.x < (unsigned)d.d_out) {
     const int sl = d.slot_of_axis[threadIdx.x];
     double t = 0.0;
@@ -743,25 +791,24 @@ __global__ void __launch_bounds__(BLOCK) ev_final_kernel(const __grid_constant__
   constexpr int NSMAX = TRIOT_MAXD + 2;
   pdl_trigger();
   pdl_wait();
-  double a[NSMAX];
+  // same order as ev_reduce's last block: slot t % P, blocks in order, butterfly, warps
+  const unsigned P = (unsigned)ev_slot_pad(f.ns);
+  const unsigned total = f.nblk * P;
+  double a = 0.0;
+  for (unsigned i0 = threadIdx.x; i0 < total; i0 += 4 * BLOCK) {
+    double x[4];
 #pragma unroll
-  for (int k = 0; k < NSMAX; ++k) a[k] = 0.0;
-  for (uint32_t b = threadIdx.x; b < f.nblk; b += BLOCK) {
-    const double* p = f.part + (size_t)b * (size_t)f.ns;
+    for (int i = 0; i < 4; ++i) {
+      const unsigned idx = i0 + (unsigned)i * BLOCK;
+      x[i] = idx < total ? __ldcg(f.part + idx) : 0.0;
+    }
 #pragma unroll
-    for (int k = 0; k < NSMAX; ++k)
-      if (k < f.ns) a[k] += __ldcg(p + k);
+    for (int i = 0; i < 4; ++i) a += x[i];
   }
   __shared__ double sm[BLOCK / 32][NSMAX];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NSMAX; ++k) {
-    if (k < f.ns) {
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-      if (lane == 0) sm[wib][k] = a[k];
-    }
-  }
+  for (unsigned o = 16; o >= P; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane < f.ns) sm[wib][lane] = a;
   __syncthreads();
   if ((int)threadIdx.x < f.d_out) {
     const int sl = f.slot_of_axis[threadIdx.x];
@@ -772,8 +819,8 @@ __global__ void __launch_bounds__(BLOCK) ev_final_kernel(const __grid_constant__
   }
 }
 
-template <int D, int ESZ, int V, typename IDX, int K>
-__global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ Desc<IDX> d) {
+template <int D, int ESZ, int V, typename IDX, int K, int MINB = 4>
+__global__ void __launch_bounds__(kBlock, MINB) ev_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
   constexpr int NW = V * EW;
   constexpr int NS = D + 2;  // D digit slots + collapsed column slot + mass
@@ -784,8 +831,9 @@ __global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ D
   double acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-  if (!d.split) pdl_trigger();
+  pdl_trigger();
   pdl_wait();
+  TRIOT_TRACE(0);
   if (base0 < d.nvec) {
     const IDX vend = warp_end(d, base0);
     const IDX dv = d.dv;
@@ -795,6 +843,7 @@ __global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ D
     EvAcc<D> a;
     ev_acc_init<D, IDX>(a);
     for (IDX b = base0; b < vend; b += (IDX)K * dv) {
+      if (b == base0) TRIOT_TRACE(1);
       uint32_t buf[K][NW];
 #pragma unroll
       for (int j = 0; j < K; ++j)
@@ -808,7 +857,9 @@ __global__ void __launch_bounds__(kBlock, 4) ev_kernel(const __grid_constant__ D
     }
     ev_finish<D, IDX>(d, u, a, acc);
   }
+  TRIOT_TRACE(2);
   ev_reduce<NS, kBlock, IDX>(d, acc);
+  TRIOT_TRACE(4);
 }
 
 // ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
@@ -860,6 +911,7 @@ __global__ void __launch_bounds__(kBlock) dot_kernel(const __grid_constant__ Des
   const IDX base0 = warp * d.wmul;
   double acc[1] = {0.0};
   pdl_trigger();
+  TRIOT_TRACE(0);
   if (base0 < d.nvec) {
     const IDX vend = warp_end(d, base0);
     IDX u[D], off[2];
@@ -893,7 +945,9 @@ __global__ void __launch_bounds__(kBlock) dot_kernel(const __grid_constant__ Des
   } else {
     pdl_wait();
   }
+  TRIOT_TRACE(2);
   ev_reduce<1, kBlock, IDX>(d, acc);
+  TRIOT_TRACE(4);
 }
 
 // ------------------------------------------------------------------ NEXT-3: fused update
@@ -964,7 +1018,7 @@ __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__
   double acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-  if (!d.split) pdl_trigger();
+  pdl_trigger();
   pdl_wait();
   if (base0 < d.nvec) {
     const IDX vend = warp_end(d, base0);

@@ -1,4 +1,5 @@
-"""Per-block timeline of the EV bulk-copy kernel on C3 (diagnostic; builds tools/libevprobe.so)."""
+"""Per-block timeline of the EV kernel on C3: bulk-copy kernel, or the default LDG kernel with
+--ldg (diagnostic; builds tools/libevprobe.so)."""
 import ctypes
 import json
 import os
@@ -17,13 +18,16 @@ SO = os.path.join(HERE, "libevprobe.so")
 def build():
     srcs = [os.path.join(HERE, "ev_probe.cu"),
             os.path.join(ROOT, "paper_1608_00099_b200", "csrc", "plan.cpp")]
-    if not os.path.exists(SO):
+    if not os.path.exists(SO) or any(os.path.getmtime(x) > os.path.getmtime(SO) for x in srcs):
         subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
                         "-shared", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                         "-o", SO, *srcs], check=True)
     L = ctypes.CDLL(SO)
-    L.probe_ev_c3.restype = ctypes.c_int
-    L.probe_ev_c3.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_void_p]
+    for f in (L.probe_ev_c3, L.probe_ev_ldg_c3):
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int, ctypes.c_void_p]
+    L.probe_dot_b2.restype = ctypes.c_int
+    L.probe_dot_b2.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int, ctypes.c_void_p]
     return L
 
 
@@ -39,13 +43,22 @@ def main():
     clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ldg = "--ldg" in sys.argv or "--dot" in sys.argv
+    probe = L.probe_ev_ldg_c3 if ldg else L.probe_ev_c3
+    nblk = sms * (4 if ldg else 1)
+    if "--dot" in sys.argv:
+        from triot_inputs import make_paper_inputs
+        inp = make_paper_inputs("B2")
+        A = torch.from_numpy(inp["a"]).to(dev)
+        B = torch.from_numpy(inp["b"]).to(dev)
+        probe = lambda p_, m_, w_, t_, n_, s_: L.probe_dot_b2(A.data_ptr(), B.data_ptr(), m_, w_,
+                                                               t_, n_, s_)
     for rep in range(3):
         scratch.fill_(1)
         clean.sum()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        grid = L.probe_ev_c3(p.data_ptr(), means.data_ptr(), ws.data_ptr(), trace.data_ptr(),
-                             sms, s)
+        grid = probe(p.data_ptr(), means.data_ptr(), ws.data_ptr(), trace.data_ptr(), nblk, s)
         b.record()
         torch.cuda.synchronize()
         assert grid > 0, grid
@@ -60,6 +73,8 @@ def main():
             "loop_end_us": pct(2, (0, 10, 50, 90, 100)),
             "ticket_us": pct(3, (0, 50, 100)),
             "exit_last_us": round(float(rel[:, 4].max()), 2),
+            "last_block_loads_done_us": round(float(((tr[:, 5].max()) - t0) / 1000.0), 2),
+            "last_block_reduced_us": round(float(((tr[:, 6].max()) - t0) / 1000.0), 2),
             "slowest_blocks_sm": [int(x) for x in tr[np.argsort(-tr[:, 2])[:8], 7]],
             "fastest_blocks_sm": [int(x) for x in tr[np.argsort(tr[:, 2])[:8], 7]],
             "means": means.cpu().tolist()}), flush=True)
