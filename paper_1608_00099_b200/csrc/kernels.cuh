@@ -588,8 +588,8 @@ __device__ __forceinline__ void digits_step_ev(const Desc<IDX>& d, IDX (&u)[D], 
     carry = nu >= d.ext[k];
     if (carry) nu -= d.ext[k];
     u[k] = nu;
-    if (nu != old) {
-      const double delta = (double)nu - (double)old;
+    if (nu != old) {  // one exact conversion of the signed change (|delta| < 2^53)
+      const double delta = (double)((int64_t)nu - (int64_t)old);
       a.ev[k] = fma(-delta, a.S, a.ev[k]);
     }
     if (k <= d.klo && !carry) break;
@@ -633,7 +633,14 @@ __device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const uint32_t
 #pragma unroll
   for (int e = 1; e < V; ++e) sum += x[e];
   a.S += sum;
-  if (V > 1) {
+  if (V > 1 && d.collapsed == 0) {
+    // one row per vector (lgL = log2 V): column weight e, row weight 0 -- immediate constants,
+    // the same FMA sequence as the general path below
+    double wc = 0.0;
+#pragma unroll
+    for (int e = 1; e < V; ++e) wc = fma((double)e, x[e], wc);
+    a.Wc += wc;
+  } else if (V > 1) {
     double wr = 0.0, wc = 0.0;
 #pragma unroll
     for (int e = 1; e < V; ++e) {
