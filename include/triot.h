@@ -179,7 +179,9 @@ TRIOT_API int triot_expected_value_mass(double* out, const void* p, const int64_
  * host->device copy / the device op / device->host copy of consecutive slabs on three streams.
  * Results are bit-identical to the device entry points.  The call is asynchronous with respect
  * to the host: `cuda_stream` completes when the whole output is in host memory.  One staging
- * buffer per concurrently used stream; calls on one device are serialised by the library.
+ * buffer per concurrently used stream.  Each (device, cuda_stream) pair gets its own pair of
+ * copy streams, so calls issued on different streams overlap one op's device-to-host drain with
+ * another's host-to-device feed; calls on the same stream run in issue order.
  */
 TRIOT_API int triot_embed_host(void* dst, const int64_t* dst_shape, const void* src,
                                const int64_t* src_shape, int d, int dtype, unsigned flags,

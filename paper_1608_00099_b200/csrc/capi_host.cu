@@ -12,7 +12,10 @@
 #include <cuda_runtime.h>
 #include <string.h>
 
+#include <map>
+#include <memory>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "../../include/triot.h"
@@ -26,23 +29,28 @@ int cuda_err(cudaError_t e, const char* what) {
   return set_error(TRIOT_ERR_CUDA, "CUDA: %s: %s", what, cudaGetErrorString(e));
 }
 
-// Per-device pool of the two copy streams and the pipeline events (created once, reused;
-// guarded by a mutex: one host-buffer call at a time per device).
+// The two copy streams and the pipeline events of one (device, caller stream) pair -- created
+// on first use, reused, never destroyed (one per stream the caller pipelines on).  Calls on
+// different caller streams get different copy streams, so one op's device-to-host drain runs
+// while another op's host-to-device feed is in flight (PCIe is full duplex); a mutex keeps
+// concurrent calls on the same caller stream in order.
 struct Pipe {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t loaded[2], computed[2], drained[2];
   std::mutex mu;
   bool ready = false;
 };
-Pipe g_pipes[64];
+std::mutex g_pipes_mu;
+std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Pipe>> g_pipes;
 
-int pipe_for(Pipe** out) {
+int pipe_for(cudaStream_t caller, Pipe** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice");
-  if (dev < 0 || dev >= 64) return set_error(TRIOT_ERR_CUDA, "CUDA: device id %d", dev);
-  Pipe& p = g_pipes[dev];
-  *out = &p;
+  std::lock_guard<std::mutex> lk(g_pipes_mu);
+  std::unique_ptr<Pipe>& p = g_pipes[std::make_pair(dev, caller)];
+  if (!p) p.reset(new Pipe());
+  *out = p.get();
   return TRIOT_OK;
 }
 
@@ -83,7 +91,7 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
                  const int64_t* const* in_shape, int d, int esz, void* staging,
                  size_t staging_bytes, cudaStream_t compute, OpFn op) {
   Pipe* pp;
-  int st = pipe_for(&pp);
+  int st = pipe_for(compute, &pp);
   if (st) return st;
   Pipe& P = *pp;
   std::lock_guard<std::mutex> lk(P.mu);
