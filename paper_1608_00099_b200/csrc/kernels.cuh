@@ -155,6 +155,25 @@ __device__ __forceinline__ void odo_start(const Desc<IDX>& d, IDX v, IDX (&u)[D]
   }
 }
 
+// Offsets (Alg 2, Horner per tensor) and bounds of a known tuple -- odo_start without the
+// division step, for a tuple obtained by a carry.
+template <int D, int NT, bool BOUNDS, typename IDX>
+__device__ __forceinline__ void odo_horner(const Desc<IDX>& d, const IDX (&u)[D], IDX (&off)[NT],
+                                           uint32_t& oob) {
+#pragma unroll
+  for (int x = 0; x < NT; ++x) {
+    IDX o = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) o += u[k] * d.t[x].sig[k];
+    off[x] = o;
+  }
+  oob = 0;
+  if (BOUNDS) {
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k) oob |= (uint32_t)(u[k] >= d.bnd[k]) << k;
+  }
+}
+
 // +32 vectors: Alg 3's carry loop, unrolled over the D digits (Alg 6) with early exit.
 template <int D, int NT, bool BOUNDS, typename IDX, bool ALLB = false>
 __device__ __forceinline__ void odo_step(const Desc<IDX>& d, IDX (&u)[D], IDX (&off)[NT],
@@ -332,7 +351,21 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
     b += run * 32;
     v += run * 32;
     if (b >= vend) break;
-    odo_start<D, 2, true, IDX>(d, v, u, off, oob);
+    // the run ended because digits m..khi wrapped: they restart at 0 and digit m-1 takes the
+    // carry (Alg 3) -- no re-decode; m >= 1 here (digit 0 wrapping is the end)
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k)
+      if (k >= m && k <= d.khi) u[k] = 0;
+    bool cy = true;
+#pragma unroll
+    for (int k = D - 2; k >= 0; --k) {
+      if (k < m && cy) {
+        const IDX nu = u[k] + 1;
+        cy = k > 0 && nu >= d.ext[k];
+        u[k] = cy ? IDX(0) : nu;
+      }
+    }
+    odo_horner<D, 2, true, IDX>(d, u, off, oob);
   }
 }
 

@@ -100,7 +100,19 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
                         o = W(o + T[0]["step"])
                     v += 32 * run_
                     if v < vend:
+                        # the kernel's carry instead of a re-decode: digits m..khi restart at 0,
+                        # digit m-1 takes the carry; must equal the decoded tuple of v
+                        nu_ = list(u)
+                        for k in range(m, khi + 1):
+                            nu_[k] = 0
+                        for k in range(m - 1, -1, -1):
+                            nu_[k] += 1
+                            if k > 0 and nu_[k] >= ext[k]:
+                                nu_[k] = 0
+                                continue
+                            break
                         u, off, oob = start(v)
+                        assert nu_ == u, (nu_, u)
                     continue
                 if True:
                     uv = u[D - 1]
