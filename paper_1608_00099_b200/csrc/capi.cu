@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <utility>
 #include <unordered_map>
 
 #include "../../include/triot.h"
@@ -405,11 +406,35 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   Geom g;
   int st = plan_conv(g, result, lhs, lhs_shape, rhs, rhs_shape, d, dtype);
   if (st) return st;
+  // Few outputs (the paper's Benchmark 4: 7,665) cannot fill the SMs one lane per output, so G
+  // lanes share an output (group kernel: latency-bound on the add chain, 28 us); with >= 8 warps
+  // of outputs per SM the lane-per-output kernel issues ~6x fewer instructions per term.  It
+  // iterates the smaller operand's index space (reversed order when that is rhs: tensors 0/1
+  // and their extents swap).  Policy mode 1 forces the group kernel, mode 0 the lane kernel.
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (dev >= 0 && dev < 64) {
+        if (!g_sms[dev]) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms[dev]) sms = g_sms[dev];
+      }
+    }
+  }
+  const bool group = g_override.mode == 1 ||
+                     (g_override.mode != 0 && g.nvec < (uint64_t)sms * 8 * 32);
+  const bool rev = !group && g.t[1].numel < g.t[0].numel;
+  if (rev) {
+    std::swap(g.t[0], g.t[1]);
+    for (int k = 0; k < g.D; ++k) std::swap(g.bnd[k], g.dlt[k]);
+  }
   // stage both operands in shared memory when they fit (<= 96 KB together)
   const uint64_t nl_pad = (g.t[0].numel + 3) & ~3ull;
   const size_t smem = (size_t)(nl_pad + g.t[1].numel) * (size_t)g.esz;
   const bool use_smem = smem <= 96 * 1024;
-  const void* fn = (g.esz == 8 ? triot_table_5_8_0 : triot_table_5_4_0)(g.D, 2, use_smem ? 1 : 0);
+  const void* fn = (g.esz == 8 ? triot_table_5_8_0 : triot_table_5_4_0)(
+      g.D, group ? 2 : (rev ? 1 : 0), use_smem ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no convolution instance for d=%d", d);
   if (use_smem) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -428,10 +453,10 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   desc.t[1].rho = (uint32_t)g.t[1].numel;
   desc.t[0].numel_pad = (uint32_t)nl_pad;
   void* args[1] = {&desc};
-  const uint64_t per_block = TRIOT_CONV_BLOCK / TRIOT_CONV_GROUP;  // outputs per block
+  const unsigned block = group ? TRIOT_CONV_BLOCK : kConvLaneBlock;
+  const uint64_t per_block = group ? TRIOT_CONV_BLOCK / TRIOT_CONV_GROUP : kConvLaneBlock;
   unsigned grid = (unsigned)((g.nvec + per_block - 1) / per_block);
-  st = launch_pdl(fn, grid, TRIOT_CONV_BLOCK, use_smem ? smem : 0, (cudaStream_t)cuda_stream,
-                  args);
+  st = launch_pdl(fn, grid, block, use_smem ? smem : 0, (cudaStream_t)cuda_stream, args);
   if (!st) clear_error();
   return st;
 }

@@ -23,7 +23,7 @@
 #define TRIOT_MAXT 3
 #define TRIOT_BLOCK 256   // threads per block of the streaming kernels
 #define TRIOT_CONV_BLOCK 128  // convolution: threads per block
-#define TRIOT_CONV_GROUP 8    // convolution: lanes per output (TRIOT_CONV_BLOCK/8 outputs/block)
+#define TRIOT_CONV_GROUP 8    // convolution, group kernel: lanes per output
 
 namespace triot {
 

@@ -48,10 +48,12 @@ const void* kptr() {
 #elif TRIOT_INST_OP == 4
   return (const void*)&update_kernel<D, ESZ, V, IDX, KBIN>;
 #elif TRIOT_INST_OP == 5
-  // naive convolution: one instance per D; idx64 slot = the shared-memory staged variant
-  return V != 1 ? nullptr
-                : (sizeof(IDX) == 4 ? (const void*)&conv_kernel<D, ESZ, false>
-                                    : (const void*)&conv_kernel<D, ESZ, true>);
+  // naive convolution, idx64 slot = the shared-memory staged variant: vi 2 (V = 1) = the group
+  // kernel, vi 0 / 1 (the V = 32 / 16 byte slots) = the lane-per-output kernel forward / reversed
+  constexpr bool S = sizeof(IDX) == 8;
+  if (V == 1) return (const void*)&conv_kernel<D, ESZ, S>;
+  if (V == 32 / ESZ) return (const void*)&conv_lane_kernel<D, ESZ, S, false>;
+  return (const void*)&conv_lane_kernel<D, ESZ, S, true>;
 #elif TRIOT_INST_BOP == 1
   // EV bulk-copy fast path: only the 32-byte vector width exists; vi slot 1 (16 B) carries the
   // small-stage variant

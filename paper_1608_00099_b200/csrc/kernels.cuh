@@ -1198,23 +1198,51 @@ __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const Src& L, c
   // its shuffles one round ahead, so in program order the dependent add chain of round r is
   // followed by work that does not wait on it.
   // branch-free loads: a lane past its box loads element 0 and its product is replaced by +0.0
+  // The group's G products of a round reach every lane of the group through a per-warp
+  // double-buffered shared-memory slot (one store per lane, G/2 16-byte loads) instead of G
+  // shuffles; the __syncwarp after each round's stores orders them before the next round's loads
+  // and after the previous round's loads of the same buffer.
+  __shared__ __align__(16) T xbuf[TRIOT_CONV_BLOCK / 32][2][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g0 = lane - j;
   uint64_t term = (uint64_t)j;  // this lane's term index for the loads being issued
   bool va = term < M;
   T la = L.at(va ? offL : 0u), ra = R.at(va ? offR : 0u);   // round 0
   advance();
   term += G;
-  T q[G];
-  {
-    const T p0 = va ? bop<2>(la, ra) : T(0);
-#pragma unroll
-    for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p0, i, G);
-  }
+  xbuf[w][0][lane] = va ? bop<2>(la, ra) : T(0);
+  __syncwarp();
   va = term < M;
   la = L.at(va ? offL : 0u);
   ra = R.at(va ? offR : 0u);   // round 1
   advance();
   term += G;
+  // products of round 0 -> registers (the loop loads round r+1's right after its __syncwarp, so
+  // the shared-memory latency overlaps the next round's operand loads)
+  T q[G];
+  auto fetch = [&](int buf) {
+    if constexpr (sizeof(T) == 8) {
+      const double2* x2 = reinterpret_cast<const double2*>(&xbuf[w][buf][g0]);
+#pragma unroll
+      for (int i = 0; i < G / 2; ++i) {
+        const double2 v = x2[i];
+        q[2 * i] = v.x;
+        q[2 * i + 1] = v.y;
+      }
+    } else {
+      const float4* x4 = reinterpret_cast<const float4*>(&xbuf[w][buf][g0]);
+#pragma unroll
+      for (int i = 0; i < G / 4; ++i) {
+        const float4 v = x4[i];
+        q[4 * i] = v.x;
+        q[4 * i + 1] = v.y;
+        q[4 * i + 2] = v.z;
+        q[4 * i + 3] = v.w;
+      }
+    }
+  };
+  fetch(0);
   T acc = T(0);
+  int cur = 0;
   for (uint64_t base = 0; __any_sync(0xffffffffu, base < M); base += G) {
     // a. loads of round r+2
     const bool vb = term < M;
@@ -1222,10 +1250,11 @@ __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const Src& L, c
     // b. the ordered add chain of round r (+0.0 for terms past the box)
 #pragma unroll
     for (int i = 0; i < G; ++i) acc = bop<0>(acc, q[i]);
-    // c, d. product of round r+1 and its shuffles
-    const T p1 = va ? bop<2>(la, ra) : T(0);
-#pragma unroll
-    for (int i = 0; i < G; ++i) q[i] = __shfl_sync(0xffffffffu, p1, i, G);
+    // c. product of round r+1 into the other buffer, then its G products into registers
+    xbuf[w][cur ^ 1][lane] = va ? bop<2>(la, ra) : T(0);
+    __syncwarp();
+    cur ^= 1;
+    fetch(cur);
     la = lb;
     ra = rb;
     va = vb;
@@ -1235,8 +1264,182 @@ __device__ __forceinline__ T conv_group(const Desc<uint32_t>& d, const Src& L, c
   return acc;
 }
 
-// SMEM: lhs and rhs are first copied into shared memory by two bulk copies (they are re-read
-// by every output of the block; the paper's (2^8, 2^3) operands are 16 KB each).
+// Both operands into shared memory: two bulk copies of their 16-B-aligned prefixes (mbarrier
+// complete_tx) plus element copies of the tails.  Calls griddepcontrol.wait before reading.
+template <typename T, int BLOCK>
+__device__ __forceinline__ void conv_stage(const Desc<uint32_t>& d, const T* lhs, const T* rhs,
+                                           T* sl, T* sr) {
+  constexpr int ESZ = (int)sizeof(T);
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t nl = (uint32_t)d.t[0].rho, nr = (uint32_t)d.t[1].rho;
+  const bool al = ((uintptr_t)lhs & 15u) == 0, ar = ((uintptr_t)rhs & 15u) == 0;
+  const uint32_t bl = al ? (nl * ESZ) & ~15u : 0u, br = ar ? (nr * ESZ) & ~15u : 0u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  if (threadIdx.x == 0 && bl + br) {
+    mbar_expect_tx(&bar, bl + br);
+    if (bl) bulk_g2s(sl, lhs, bl, &bar);
+    if (br) bulk_g2s(sr, rhs, br, &bar);
+  }
+  for (uint32_t i = bl / ESZ + threadIdx.x; i < nl; i += BLOCK) sl[i] = __ldg(lhs + i);
+  for (uint32_t i = br / ESZ + threadIdx.x; i < nr; i += BLOCK) sr[i] = __ldg(rhs + i);
+  if (bl + br) mbar_wait(&bar, 0);
+  __syncthreads();
+}
+
+// Lane per output (the default).  Tensor 0 is the operand whose index space is iterated (A),
+// tensor 1 the other (B); bnd / dlt = their extents.  The 32 outputs of a warp iterate the union
+// of their boxes of valid A-tuples (warp-uniform odometer: A's offsets are uniform, so its loads
+// are shared-memory broadcasts) with a per-lane validity mask; an invalid term adds +0.0, which
+// leaves the sum unchanged (it starts at +0.0 and so is never -0.0).  Forward lexicographic order
+// when A = lhs; when A = rhs (the host picks the smaller operand as A) the order is reversed,
+// which is lexicographic in t_l = u - t_r.  Either way each output adds its rounded products in
+// exactly Alg 15's order: bit-identical to the sequential algorithm, one add chain per lane.
+constexpr int kConvLaneBlock = 64;
+template <int D, int ESZ, bool SMEM, bool REV>
+__global__ void __launch_bounds__(kConvLaneBlock) conv_lane_kernel(
+    const __grid_constant__ Desc<uint32_t> d) {
+  using T = typename Elem<ESZ>::T;
+  pdl_trigger();
+  const T* ga = (const T*)d.t[0].ptr;
+  const T* gb = (const T*)d.t[1].ptr;
+  extern __shared__ __align__(128) unsigned char conv_smem[];
+  T* sa = (T*)conv_smem;
+  T* sb = sa + d.t[0].numel_pad;
+  if (SMEM) conv_stage<T, kConvLaneBlock>(d, ga, gb, sa, sb);
+  else pdl_wait();
+  const ConvSrc<T, SMEM> A{ga, SMEM ? smem_u32(sa) : 0u}, B{gb, SMEM ? smem_u32(sb) : 0u};
+  const uint32_t uf = blockIdx.x * kConvLaneBlock + threadIdx.x;
+  const bool active = uf < d.nvec;
+  uint32_t u[D], lo[D], hi[D];
+  {
+    uint32_t r = active ? uf : 0u;
+#pragma unroll
+    for (int k = D - 1; k >= 1; --k) {
+      const uint32_t q = divq<uint32_t>(r, d.ext[k], d.fdm[k], d.fds[k]);
+      u[k] = r - q * d.ext[k];
+      r = q;
+    }
+    u[0] = r;
+  }
+  uint32_t baseB = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const uint32_t Ak = d.bnd[k], Bk = d.dlt[k];
+    lo[k] = active ? (u[k] + 1 > Bk ? u[k] + 1 - Bk : 0u) : 0xffffffffu;
+    hi[k] = active ? (u[k] < Ak - 1 ? u[k] : Ak - 1) : 0u;
+    baseB += u[k] * d.t[1].sig[k];
+  }
+  uint32_t ulo[D], uhi[D], t[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    ulo[k] = __reduce_min_sync(0xffffffffu, lo[k]);
+    uhi[k] = __reduce_max_sync(0xffffffffu, hi[k]);
+    t[k] = REV ? uhi[k] : ulo[k];
+  }
+  if (ulo[0] > uhi[0]) return;  // no active output in this warp
+  const uint32_t sA = d.t[0].sig[D - 1], sB = d.t[1].sig[D - 1];
+  const uint32_t n = uhi[D - 1] - ulo[D - 1] + 1;  // terms per row of the union box
+  const uint32_t ilo = lo[D - 1], ihi = hi[D - 1];
+  // The union box is walked in chunks of RB terms along its rows (a chunk never crosses a row;
+  // a row's last chunk is padded with +0.0 terms).  Software pipeline: the next chunk's loads are
+  // issued before the current chunk's products join the add chain, so the chain -- one dependent
+  // add per term, Alg 15's order -- is the critical path.
+  constexpr int RB = 8;
+  struct Chunk {
+    uint32_t offA, idxB, ti, rem;  // A offset / B index of the first term, its inner digit,
+    bool vo, live;                 // terms left in the row; outer digits in this lane's box
+  };
+  auto row_start = [&](Chunk& c) {
+    uint32_t hB = 0;
+    c.offA = 0;
+    c.vo = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      c.offA += t[k] * d.t[0].sig[k];
+      hB += t[k] * d.t[1].sig[k];
+      if (k < D - 1) c.vo = c.vo && t[k] >= lo[k] && t[k] <= hi[k];
+    }
+    c.idxB = baseB - hB;
+    c.ti = t[D - 1];
+    c.rem = n;
+    c.live = true;
+  };
+  auto advance = [&](Chunk& c) {
+    if (c.rem > (uint32_t)RB) {
+      c.rem -= RB;
+      if (REV) {
+        c.ti -= RB;
+        c.offA -= RB * sA;
+        c.idxB += RB * sB;
+      } else {
+        c.ti += RB;
+        c.offA += RB * sA;
+        c.idxB -= RB * sB;
+      }
+      return;
+    }
+    // next row of the union box: Alg 3's carry on digits 0..D-2 (a borrow when reversed)
+    bool carry = true;
+#pragma unroll
+    for (int k = D - 2; k >= 0; --k) {
+      if (carry) {
+        if (REV ? t[k] > ulo[k] : t[k] < uhi[k]) {
+          t[k] = REV ? t[k] - 1 : t[k] + 1;
+          carry = false;
+        } else {
+          t[k] = REV ? uhi[k] : ulo[k];
+        }
+      }
+    }
+    if (carry) {
+      c.live = false;
+      return;
+    }
+    row_start(c);
+  };
+  auto issue = [&](const Chunk& c, T (&xa)[RB], T (&xb)[RB], bool (&xv)[RB]) {
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const bool inrow = c.live && (uint32_t)q < c.rem;
+      const uint32_t tq = REV ? c.ti - q : c.ti + q;
+      xv[q] = inrow && c.vo && tq >= ilo && tq <= ihi;
+      xa[q] = A.at(inrow ? (REV ? c.offA - q * sA : c.offA + q * sA) : 0u);
+      xb[q] = B.at(xv[q] ? (REV ? c.idxB + q * sB : c.idxB - q * sB) : 0u);
+    }
+  };
+  Chunk c;
+  row_start(c);
+  T xa[RB], xb[RB];
+  bool xv[RB];
+  issue(c, xa, xb, xv);
+  T acc = T(0);
+  while (c.live) {
+    Chunk nc = c;
+    advance(nc);
+    T ya[RB], yb[RB];
+    bool yv[RB];
+    issue(nc, ya, yb, yv);
+#pragma unroll
+    for (int q = 0; q < RB; ++q) acc = bop<0>(acc, xv[q] ? bop<2>(xa[q], xb[q]) : T(0));
+    c = nc;
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      xa[q] = ya[q];
+      xb[q] = yb[q];
+      xv[q] = yv[q];
+    }
+  }
+  if (active) ((T*)d.out)[uf] = acc;
+}
+
+// Group variant (policy mode 1): G lanes per output.  SMEM: lhs and rhs are first copied into
+// shared memory by two bulk copies (they are re-read by every output of the block; the paper's
+// (2^8, 2^3) operands are 16 KB each).
 template <int D, int ESZ, bool SMEM>
 __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
     const __grid_constant__ Desc<uint32_t> d) {
@@ -1250,27 +1453,7 @@ __global__ void __launch_bounds__(TRIOT_CONV_BLOCK) conv_kernel(
   extern __shared__ __align__(128) unsigned char conv_smem[];
   T* sl = (T*)conv_smem;
   T* sr = sl + d.t[0].numel_pad;
-  if (SMEM) {
-    __shared__ __align__(8) uint64_t bar;
-    const uint32_t nl = (uint32_t)d.t[0].rho, nr = (uint32_t)d.t[1].rho;
-    const bool al = ((uintptr_t)lhs & 15u) == 0, ar = ((uintptr_t)rhs & 15u) == 0;
-    const uint32_t bl = al ? (nl * ESZ) & ~15u : 0u, br = ar ? (nr * ESZ) & ~15u : 0u;
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    pdl_wait();
-    if (threadIdx.x == 0 && bl + br) {
-      mbar_expect_tx(&bar, bl + br);
-      if (bl) bulk_g2s(sl, lhs, bl, &bar);
-      if (br) bulk_g2s(sr, rhs, br, &bar);
-    }
-    for (uint32_t i = bl / ESZ + threadIdx.x; i < nl; i += TRIOT_CONV_BLOCK) sl[i] = __ldg(lhs + i);
-    for (uint32_t i = br / ESZ + threadIdx.x; i < nr; i += TRIOT_CONV_BLOCK) sr[i] = __ldg(rhs + i);
-    if (bl + br) mbar_wait(&bar, 0);
-    __syncthreads();
-  }
+  if (SMEM) conv_stage<T, TRIOT_CONV_BLOCK>(d, lhs, rhs, sl, sr);
   // every lane stays to the end (the group shuffles need the full warp); past-the-end groups
   // compute nothing
   const bool active = u_flat < d.nvec;

@@ -478,9 +478,33 @@ def test_convolution_random(d, dtype):
         rs = random_shape(rng, d, 600 if d < 5 else 200, lo=1, hi=5 if d > 3 else 10)
         lhs = rng.standard_normal(ls).astype(dtype)
         rhs = rng.standard_normal(rs).astype(dtype)
+        # larger lhs: the lane kernel iterates rhs in reverse; swapped: lhs forward
+        for x, y in ((lhs, rhs), (rhs, lhs)):
+            ref = O.naive_convolve(x, y)
+            try:
+                for mode in (-1, 0, 1):   # automatic / lane per output / G-lane groups
+                    T.triot_set_launch_policy(mode, 0)
+                    got = T.naive_convolve(_dev(x, rep), _dev(y))
+                    assert_bits_equal(got, ref)
+            finally:
+                T.triot_set_launch_policy(-1, 0)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_convolution_global_operands(dtype):
+    """Operands too large for shared-memory staging (> 96 KB together): global loads."""
+    rng = np.random.default_rng(77)
+    m = 2 if dtype == np.float32 else 1
+    for ls, rs in (((300 * m, 41), (7, 9)), ((5, 6), (200 * m, 70))):
+        lhs = rng.standard_normal(ls).astype(dtype)
+        rhs = rng.standard_normal(rs).astype(dtype)
         ref = O.naive_convolve(lhs, rhs)
-        got = T.naive_convolve(_dev(lhs, rep), _dev(rhs))
-        assert_bits_equal(got, ref)
+        try:
+            for mode in (-1, 0, 1):
+                T.triot_set_launch_policy(mode, 0)
+                assert_bits_equal(T.naive_convolve(_dev(lhs), _dev(rhs)), ref)
+        finally:
+            T.triot_set_launch_policy(-1, 0)
 
 
 # ---------------------------------------------------------------- host-buffer streaming (P:607)

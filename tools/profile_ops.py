@@ -28,11 +28,12 @@ def main():
         mode, bpsm = (int(x) for x in a.policy.split(","))
         T.triot_set_launch_policy(mode, bpsm)
     for name in a.only.split(","):
-        if name == "B4":
+        if name in ("B4", "CONVBIG"):
             import numpy as np
             rng = np.random.default_rng(17)
-            l4 = torch.from_numpy(rng.random((256, 8))).to(dev)
-            r4 = torch.from_numpy(rng.random((256, 8))).to(dev)
+            sh = (256, 8) if name == "B4" else (48, 48, 8)   # CONVBIG: 135k outputs, 340M MACs
+            l4 = torch.from_numpy(rng.random(sh)).to(dev)
+            r4 = torch.from_numpy(rng.random(sh)).to(dev)
             for _ in range(a.reps):
                 T.naive_convolve(l4, r4)
             torch.cuda.synchronize()
