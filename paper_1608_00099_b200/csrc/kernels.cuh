@@ -1069,6 +1069,8 @@ __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__
     EvAcc<D> a;
     ev_acc_init<D, IDX>(a);
     const bool pvec = d.t[0].vec != 0;
+    const double nd = (double)d.ext[D - 1];
+    const uint32_t wmax = D > 1 ? (uint32_t)((IDX)V / d.ext[D - 1]) + 1u : 0u;  // wraps <= this
     for (IDX b = base0; b < vend; b += (IDX)K * dv) {
       uint32_t buf[K][NW];
 #pragma unroll
@@ -1091,21 +1093,50 @@ __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__
       }
 #pragma unroll
       for (int j = 0; j < K; ++j) {
+        // V elements, each followed by Alg 3's +1 with its weight events in closed
+        // form: every +1 of the innermost digit contributes -1 x (running mass), i.e.
+        // -(V S + sum of the V prefix sums) in total; a wrap (column n-1 -> 0) instead changes
+        // it by -(n-1), a correction of +n x (mass at the wrap), and carries into the outer
+        // digits with their own events.  Past the end the elements are +0.0.
+        double pfx[V + 1];  // pfx[e] = sum of the vector's first e elements
+        pfx[0] = 0.0;
+        double sumpre = 0.0;
 #pragma unroll
         for (int e = 0; e < V; ++e) {
-          a.S += (double)Elem<ESZ>::get(buf[j] + e * EW);  // +0.0 past the end
-          // +1 element with weight events (Alg 3 on the digits)
+          pfx[e + 1] = pfx[e] + (double)Elem<ESZ>::get(buf[j] + e * EW);
+          sumpre += pfx[e + 1];
+        }
+        const double pre = pfx[V];
+        // wraps (column n-1 -> 0) follow elements ew - 1 with ew = n - col, ew + n, ... <= V;
+        // the loop trip count is uniform (V / n + 1), so the warp stays converged
+        const IDX col = u[D - 1];
+        IDX ew = D > 1 ? d.ext[D - 1] - col : (IDX)(V + 1);
+        for (uint32_t w = 0; w < wmax; ++w, ew += d.ext[D - 1]) {
+          if (ew > (IDX)V) continue;
+          double pw = 0.0;  // pfx[ew] (a select chain: ew is per lane)
 #pragma unroll
-          for (int k = D - 1; k >= 0; --k) {
+          for (int e = 1; e <= V; ++e) pw = ((IDX)e == ew) ? pfx[e] : pw;
+          const double sc = a.S + pw;  // the running mass at this wrap
+          a.ev[D - 1] = fma(nd, sc, a.ev[D - 1]);
+#pragma unroll
+          for (int k = D - 2; k >= 0; --k) {
             const IDX old = u[k];
             IDX nu = old + 1;
             const bool carry = k > 0 && nu >= d.ext[k];
             if (carry) nu = 0;
             u[k] = nu;
-            a.ev[k] = fma(-((double)nu - (double)old), a.S, a.ev[k]);
+            a.ev[k] = fma(-(double)((int64_t)nu - (int64_t)old), sc, a.ev[k]);
             if (!carry) break;
           }
         }
+        {
+          // col + V - n * (number of wraps)
+          IDX c2 = col + (IDX)V;
+          while (D > 1 && c2 >= d.ext[D - 1]) c2 -= d.ext[D - 1];
+          u[D - 1] = c2;
+        }
+        a.ev[D - 1] -= fma((double)V, a.S, sumpre);
+        a.S += pre;
         digits_step_ev<D, IDX>(d, u, a);
         v += dv;
       }

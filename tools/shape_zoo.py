@@ -76,6 +76,17 @@ def ev_case(name, shape, dtype=torch.float64, off=0):
                       "gbs": round(nbytes / ms / 1e6, 1)}), flush=True)
 
 
+if "--big" in sys.argv:   # odd innermost extents at sizes past the launch-bound regime
+    embed_case("big: embed f32 (3000,3000,7) <- (2900,2900,5)", (3000, 3000, 7), (2900, 2900, 5))
+    embed_case("big: embed f32 (8192,4096,3) <- (8000,4000,3)", (8192, 4096, 3), (8000, 4000, 3))
+    embed_case("big: embed f64 (1000,1000,15) <- (1000,999,15)", (1000, 1000, 15), (1000, 999, 15),
+               dtype=torch.float64)
+    binary_case("big: binary f64 (3000,3001,7) x (3001,3000,7)", (3000, 3001, 7), (3001, 3000, 7))
+    binary_case("big: binary f32 (4000,4001,3) x (4001,4000,3)", (4000, 4001, 3), (4001, 4000, 3),
+                dtype=torch.float32)
+    ev_case("big: EV f64 (7,)*9", (7,) * 9)
+    ev_case("big: EV f32 (3000,3000,7)", (3000, 3000, 7), dtype=torch.float32)
+    sys.exit(0)
 embed_case("pad 2-D, innermost 999 (odd: 1-element vectors)", (1000, 1001), (900, 999))
 embed_case("pad 2-D, innermost 1000 (16-B vectors)", (1000, 1000), (900, 998))
 embed_case("pad 2-D, innermost 1024", (1000, 1024), (900, 1000))
