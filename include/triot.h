@@ -223,6 +223,16 @@ TRIOT_API int triot_apply_binary_view(const triot_view* c, const triot_view* a,
                                       const triot_view* b, const int64_t* iter_shape, int d,
                                       int dtype, int op, void* cuda_stream);
 
+/* triot_expected_value on a view (Alg 11 over the window, t relative to the window's start):
+ * out[k] = sum_t t_k p_view[t] for k < d, and out[d] = sum_t p_view[t] when with_mass != 0 (out
+ * holds d or d + 1 doubles, device, 8-byte aligned, outside the view's base buffer).  Workspace
+ * as triot_expected_value (triot_expected_value_workspace_size of the window's shape).  Same
+ * numerics and determinism as the dense call; a window equal to its base gives the dense
+ * call's value up to summation order. */
+TRIOT_API int triot_expected_value_view(double* out, const triot_view* p, int d, int dtype,
+                                        int with_mass, void* workspace, size_t workspace_bytes,
+                                        void* cuda_stream);
+
 /* ---- NEXT-2 / NEXT-3: the paper's Benchmarks 2 and 3 ----------------------------- */
 
 /* Workspace bytes triot_inner_product needs (zero-filled once; the call leaves it ready). */

@@ -23,14 +23,16 @@ from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED
                    triot_plan_describe, triot_set_launch_policy, triot_status_string,
                    LIB_PATH)
 from .api import (OPS, View, apply_binary, apply_binary_view, embed, embed_view,
-                  expected_value, fused_update, inner_product, naive_convolve, embed_host,
-                  apply_binary_host)
-from ._lib import (triot_apply_binary_view, triot_embed_view, triot_fused_update,
+                  expected_value, expected_value_view, fused_update, inner_product,
+                  naive_convolve, embed_host, apply_binary_host)
+from ._lib import (triot_apply_binary_view, triot_embed_view, triot_expected_value_view,
+                   triot_fused_update,
                    triot_inner_product, triot_inner_product_workspace_size, triot_naive_convolve)
 
 __all__ = [
     "embed", "apply_binary", "expected_value", "OPS", "TriotError", "View", "embed_view",
     "apply_binary_view", "triot_embed_view", "triot_apply_binary_view", "inner_product",
+    "expected_value_view", "triot_expected_value_view",
     "fused_update", "triot_inner_product", "triot_inner_product_workspace_size",
     "triot_fused_update", "naive_convolve", "triot_naive_convolve", "embed_host",
     "apply_binary_host",

@@ -28,6 +28,7 @@ STATUS = {
 EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "triot_embed",
            "triot_apply_binary", "triot_expected_value_workspace_size", "triot_expected_value",
            "triot_expected_value_mass", "triot_embed_view", "triot_apply_binary_view",
+           "triot_expected_value_view",
            "triot_inner_product_workspace_size", "triot_inner_product", "triot_fused_update",
            "triot_naive_convolve", "triot_embed_host", "triot_apply_binary_host",
            "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
@@ -81,6 +82,9 @@ _lib.triot_embed_view.argtypes = [_viewp, _viewp, ctypes.c_int, ctypes.c_int, ct
 _lib.triot_apply_binary_view.restype = ctypes.c_int
 _lib.triot_apply_binary_view.argtypes = [_viewp, _viewp, _viewp, _i64p, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, _vp]
+_lib.triot_expected_value_view.restype = ctypes.c_int
+_lib.triot_expected_value_view.argtypes = [_vp, _viewp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           _vp, ctypes.c_size_t, _vp]
 _lib.triot_inner_product_workspace_size.restype = ctypes.c_int
 _lib.triot_inner_product_workspace_size.argtypes = [ctypes.POINTER(ctypes.c_size_t)]
 _lib.triot_inner_product.restype = ctypes.c_int
@@ -187,6 +191,12 @@ def triot_apply_binary_view(c: triot_view, a: triot_view, b: triot_view, iter_sh
                             dtype: int, op: int, stream: int) -> int:
     return _lib.triot_apply_binary_view(ctypes.byref(c), ctypes.byref(a), ctypes.byref(b),
                                         _shape(iter_shape), d, dtype, op, stream)
+
+
+def triot_expected_value_view(out: int, p: triot_view, d: int, dtype: int, with_mass: int,
+                              workspace: int, workspace_bytes: int, stream: int) -> int:
+    return _lib.triot_expected_value_view(out, ctypes.byref(p), d, dtype, with_mass, workspace,
+                                          workspace_bytes, stream)
 
 
 def triot_inner_product_workspace_size() -> int:

@@ -87,6 +87,26 @@ def apply_binary_view(a: "View", b: "View", out: "View", op: str = "mul", iter_s
     return out
 
 
+def expected_value_view(p: "View", out=None, with_mass: bool = False):
+    """triot_expected_value_view: means[k] = sum_t t_k * p_view[t] over the window (t relative
+    to its start); (d+1,) with the window's mass last when with_mass."""
+    torch = _torch()
+    code = _dtype_code(p.base)
+    d = p.dim()
+    n = d + (1 if with_mass else 0)
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, device=p.base.device)
+    _check_tensor("out", out, p.base.device)
+    if out.dtype != torch.float64 or out.numel() < n:
+        raise ValueError(f"out must be a float64 tensor of >= {n} elements")
+    ws = workspace(tuple(p.shape), code, p.base.device)
+    pv, keep = p._c()
+    _lib.check(_lib.triot_expected_value_view(out.data_ptr(), pv, d, code, 1 if with_mass else 0,
+                                              ws.data_ptr(), ws.numel(),
+                                              _stream(p.base.device)))
+    return out
+
+
 def embed(dst, src, region_only: bool = False):
     """dst[t] = src[t] where t < src.shape, +0.0 elsewhere (or only the overlap if
     region_only).  In place on dst; returns dst."""

@@ -35,6 +35,8 @@ for _esz in (4, 8):
     UNITS.append((f"inst_2_{_esz}_0", "inst.cu", [f"-DTRIOT_INST_OP=2", f"-DTRIOT_INST_ESZ={_esz}"]))
     UNITS.append((f"inst_2_{_esz}_1", "inst.cu", [f"-DTRIOT_INST_OP=2", f"-DTRIOT_INST_ESZ={_esz}",
                                                   "-DTRIOT_INST_BOP=1"]))
+    UNITS.append((f"inst_2_{_esz}_2", "inst.cu", [f"-DTRIOT_INST_OP=2", f"-DTRIOT_INST_ESZ={_esz}",
+                                                  "-DTRIOT_INST_BOP=2"]))
     UNITS.append((f"inst_3_{_esz}_0", "inst.cu", ["-DTRIOT_INST_OP=3", f"-DTRIOT_INST_ESZ={_esz}"]))
     UNITS.append((f"inst_4_{_esz}_0", "inst.cu", ["-DTRIOT_INST_OP=4", f"-DTRIOT_INST_ESZ={_esz}"]))
     UNITS.append((f"inst_5_{_esz}_0", "inst.cu", ["-DTRIOT_INST_OP=5", f"-DTRIOT_INST_ESZ={_esz}"]))

@@ -34,6 +34,8 @@ const void* triot_table_3_4_0(int, int, int);
 const void* triot_table_3_8_0(int, int, int);
 const void* triot_table_4_4_0(int, int, int);
 const void* triot_table_4_8_0(int, int, int);
+const void* triot_table_2_4_2(int, int, int);
+const void* triot_table_2_8_2(int, int, int);
 const void* triot_table_5_4_0(int, int, int);
 const void* triot_table_5_8_0(int, int, int);
 }
@@ -46,6 +48,7 @@ typedef const void* (*TableFn)(int, int, int);
 TableFn table_for(const Geom& g) {
   const bool e8 = g.esz == 8;
   if (g.op == OP_EMBED) return e8 ? triot_table_0_8_0 : triot_table_0_4_0;
+  if (g.op == OP_EV && g.view) return e8 ? triot_table_2_8_2 : triot_table_2_4_2;
   if (g.op == OP_EV) return e8 ? triot_table_2_8_0 : triot_table_2_4_0;
   if (g.op == OP_DOT) return e8 ? triot_table_3_8_0 : triot_table_3_4_0;
   if (g.op == OP_UPDATE) return e8 ? triot_table_4_8_0 : triot_table_4_4_0;
@@ -189,7 +192,7 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
 // EV bulk-copy fast path: full 32-byte vectors, 32-B aligned p, one persistent block per SM
 int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, bool* used) {
   *used = false;
-  if (g.op != OP_EV || g.flat || g.V * g.esz != 32 || !g.t[0].vec) return TRIOT_OK;
+  if (g.op != OP_EV || g.view || g.flat || g.V * g.esz != 32 || !g.t[0].vec) return TRIOT_OK;
   // measured on B200 (ncu, cold cache, C3): the lean 32-B-load kernel at one full wave of 4
   // blocks/SM takes 30.2 us, the bulk-copy pipeline 33.1 us -> the bulk-copy path is opt-in
   if (g_override.mode != 2 && g_override.mode != 3) return TRIOT_OK;
@@ -473,10 +476,12 @@ int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, 
 
 static int expected_value_impl(double* means, const void* p, const int64_t* shape, int d,
                                int dtype, void* workspace, size_t workspace_bytes,
-                               void* cuda_stream, bool with_mass) {
+                               void* cuda_stream, bool with_mass,
+                               const triot_view* pv = nullptr) {
   Geom g;
-  int st = plan_ev(g, p, shape, d, dtype);
+  int st = pv ? plan_ev_view(g, pv, d, dtype) : plan_ev(g, p, shape, d, dtype);
   if (st) return st;
+  if (pv) p = g.t[0].ptr;
   g.with_mass = with_mass;
   const int nout = d + (with_mass ? 1 : 0);
   if (!means) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: means is NULL");
@@ -485,6 +490,12 @@ static int expected_value_impl(double* means, const void* p, const int64_t* shap
   {
     uintptr_t m0 = (uintptr_t)means, m1 = m0 + (uintptr_t)nout * 8;
     uintptr_t p0 = (uintptr_t)p, p1 = p0 + (uintptr_t)g.t[0].numel * (uintptr_t)g.esz;
+    if (pv) {  // the view's whole base buffer
+      uint64_t nb = 1;
+      for (int k = 0; k < d; ++k) nb *= (uint64_t)pv->base_shape[k];
+      p0 = (uintptr_t)pv->data;
+      p1 = p0 + (uintptr_t)nb * (uintptr_t)g.esz;
+    }
     if (g.t[0].numel && m0 < p1 && p0 < m1)
       return set_error(TRIOT_ERR_ALIASING, "Aliasing: means overlaps p");
   }
@@ -510,6 +521,13 @@ int triot_expected_value_mass(double* out, const void* p, const int64_t* shape, 
                               void* workspace, size_t workspace_bytes, void* cuda_stream) {
   return expected_value_impl(out, p, shape, d, dtype, workspace, workspace_bytes, cuda_stream,
                              true);
+}
+
+int triot_expected_value_view(double* out, const triot_view* p, int d, int dtype, int with_mass,
+                              void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  if (!p) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: view 'p' is NULL");
+  return expected_value_impl(out, nullptr, nullptr, d, dtype, workspace, workspace_bytes,
+                             cuda_stream, with_mass != 0, p);
 }
 
 int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* iter_shape, int d,

@@ -8,7 +8,7 @@
 //   TRIOT_INST_OP   0 = embed, 1 = binary, 2 = expected value, 3 = inner product,
 //                   4 = fused update, 5 = naive convolution
 //   TRIOT_INST_ESZ  4 or 8
-//   TRIOT_INST_BOP  binary op 0..3 (binary); 1 = bulk-copy variant (expected value)
+//   TRIOT_INST_BOP  binary op 0..3 (binary); 1 = bulk-copy variant, 2 = views (expected value)
 #include "kernels.cuh"
 
 #ifndef TRIOT_INST_OP
@@ -54,6 +54,9 @@ const void* kptr() {
   if (V == 1) return (const void*)&conv_kernel<D, ESZ, S>;
   if (V == 32 / ESZ) return (const void*)&conv_lane_kernel<D, ESZ, S, false>;
   return (const void*)&conv_lane_kernel<D, ESZ, S, true>;
+#elif TRIOT_INST_BOP == 2
+  // expected value of a view (strided p)
+  return (const void*)&ev_view_kernel<D, ESZ, V, IDX, KEV>;
 #elif TRIOT_INST_BOP == 1
   // EV bulk-copy fast path: only the 32-byte vector width exists; vi slot 1 (16 B) carries the
   // small-stage variant

@@ -902,6 +902,66 @@ __global__ void __launch_bounds__(kBlock, MINB) ev_kernel(const __grid_constant_
   TRIOT_TRACE(4);
 }
 
+// Expected value of a view (NEXT-1): as ev_kernel, but p is the window of a larger base, so
+// each lane tracks p's offset with the odometer (Alg 2 at the start, per-step carry deltas after
+// it).  Two copies of the digits: `uo` runs K steps ahead for the loads' offsets, `u` follows
+// the accumulation and records the telescoped weight events.
+template <int D, int ESZ, int V, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock, 4) ev_view_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  constexpr int NS = D + 2;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
+  const IDX base0 = warp * d.wmul;
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+  pdl_trigger();
+  pdl_wait();
+  if (base0 < d.nvec) {
+    const IDX vend = warp_end(d, base0);
+    const IDX dv = d.dv;
+    const uint32_t lgL = d.lgL;
+    IDX v = base0 + (IDX)lane;
+    IDX uo[D], off[1];
+    uint32_t oob;
+    odo_start<D, 1, false, IDX>(d, v, uo, off, oob);
+    IDX u[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) u[k] = uo[k];
+    EvAcc<D> a;
+    ev_acc_init<D, IDX>(a);
+    for (IDX b = base0; b < vend; b += (IDX)K * dv) {
+      uint32_t buf[K][NW];
+      IDX offj[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        offj[j] = off[0];
+        odo_step<D, 1, false, IDX>(d, uo, off, oob);
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (v + (IDX)j * dv < vend) {
+          load_vec<ESZ, V, IDX>(d.t[0], offj[j], lgL, buf[j]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NW; ++q) buf[j][q] = 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (v < vend) ev_accumulate<D, ESZ, V, IDX>(d, buf[j], a);
+        digits_step_ev<D, IDX>(d, u, a);
+        v += dv;
+      }
+    }
+    ev_finish<D, IDX>(d, u, a, acc);
+  }
+  ev_reduce<NS, kBlock, IDX>(d, acc);
+}
+
 // ---- Blackwell bulk-copy pipeline primitives (cp.async.bulk + mbarrier; SASS: UBLKCP, SYNCS)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

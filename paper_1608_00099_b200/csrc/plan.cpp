@@ -901,6 +901,39 @@ int plan_ev(Geom& g, const void* p, const int64_t* shape, int d, int dtype) {
   return TRIOT_OK;
 }
 
+// NEXT-1 for the third op: Alg 11 over a view's window (element t of the window is
+// base.flat[bias + Horner(t, base shape)]).  The counter is the window; p's offsets follow the
+// base strides, so the kernels track them with the odometer instead of assuming p is dense.
+// No flat vectors (their loads assume a dense p): odd innermost extents take 1-element vectors.
+int plan_ev_view(Geom& g, const triot_view* p, int d, int dtype) {
+  g = Geom();
+  int esz, st;
+  if ((st = check_common(d, dtype, &esz))) return st;
+  TArg tp;
+  if ((st = targ_view(tp, "p", p, d, esz))) return st;
+  g.op = OP_EV;
+  g.view = true;
+  g.flat_ok = false;
+  g.esz = esz;
+  g.dtype = dtype;
+  g.d = d;
+  g.ntensor = 1;
+  g.t[0].ptr = tp.ptr;
+  g.t[0].numel = tp.numel;
+  if (tp.numel == 0) {
+    g.empty = true;
+    clear_error();
+    return TRIOT_OK;
+  }
+  uint64_t n[TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) n[k] = (uint64_t)tp.shape[k];
+  uint64_t sig[TRIOT_MAXT][TRIOT_MAXD];
+  for (int k = 0; k < d; ++k) sig[0][k] = tp.sig[k];
+  build(g, n, sig, nullptr, /*allow_merge=*/false, /*bounds=*/false);
+  clear_error();
+  return TRIOT_OK;
+}
+
 // ------------------------------------------------------------------------------ describe
 
 static void arr(std::string& s, const char* key, const uint64_t* v, int n) {

@@ -49,6 +49,7 @@ struct Geom {
   bool with_mass = false;   // EV: also write sum(p) after the d means
   int nout = -1;            // reduction outputs if not d (+mass): the inner product writes 1
   bool split = false;       // reductions: partials summed by a second (PDL) kernel
+  bool view = false;        // EV of a view: p is strided (offsets tracked by the odometer)
   uint32_t zmask = 0;       // embed zero runs (desc.h)
   struct T {
     uint64_t sig[TRIOT_MAXD] = {}, kap[TRIOT_MAXD] = {};
@@ -77,6 +78,7 @@ int plan_conv(Geom& g, void* result, const void* lhs, const int64_t* lhs_shape, 
 // NEXT-1: the same ops on views
 int plan_embed_view(Geom& g, const triot_view* dst, const triot_view* src, int d, int dtype,
                     unsigned flags);
+int plan_ev_view(Geom& g, const triot_view* p, int d, int dtype);
 int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const triot_view* b,
                      const int64_t* iter_shape, int d, int dtype, int op);
 

@@ -33,7 +33,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     decl = declared_symbols()
-    assert len(decl) == 19, decl
+    assert len(decl) == 20, decl
     out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))
@@ -317,6 +317,23 @@ def test_view_validation():
     st = T.triot_apply_binary_view(v1, v1, v2, None, 2, F64, 0, 0)
     assert st == 7                                                 # c overlaps b
     del k1, k2, k3, k4, k5
+
+
+def test_ev_view_validation():
+    L_ = T._lib
+    good, k1 = L_.make_view(FAKE, (8, 9), (1, 2), (4, 5))
+    bad, k2 = L_.make_view(FAKE, (8, 9), (5, 2), (4, 5))           # 5 + 4 > 8 on axis 0
+    ws = FAKE * 3
+    st = T.triot_expected_value_view(FAKE * 2, bad, 2, F64, 0, ws, 1 << 20, 0)
+    assert st == 4 and "view 'p' axis 0" in T.triot_last_error()
+    # means inside the view's base buffer (not just its window) is refused
+    st = T.triot_expected_value_view(FAKE + 8, good, 2, F64, 0, ws, 1 << 20, 0)
+    assert st == 7
+    assert T.triot_expected_value_view(FAKE * 2 + 4, good, 2, F64, 0, ws, 1 << 20, 0) == 6
+    assert T.triot_expected_value_view(FAKE * 2, good, 2, 7, 0, ws, 1 << 20, 0) == 5
+    # a valid call reaches the launch, which fails without a GPU
+    assert T.triot_expected_value_view(FAKE * 2, good, 2, F64, 1, ws, 1 << 20, 0) == 9
+    del k1, k2
 
 
 @pytest.mark.parametrize("seed", range(6))

@@ -388,6 +388,49 @@ def test_views_vs_oracle(seed, dtype):
         assert_bits_equal(dt, refd)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("seed", range(8))
+def test_ev_view_vs_oracle(seed, dtype):
+    """triot_expected_value_view = Alg 11 on the materialised window (t relative to its start):
+    within 1e-12 for real data, exact for integer-valued data, deterministic, mass included."""
+    rng = np.random.default_rng(7500 + seed)
+    d = int(rng.integers(1, 9))
+    hi = 7 if d > 4 else 40
+    base = rng.random(random_shape(rng, d, 60000, lo=2, hi=hi)).astype(dtype)
+    win = tuple(int(rng.integers(1, s + 1)) for s in base.shape)
+    if seed % 3 == 0:   # tiny / odd innermost windows
+        win = win[:-1] + (min(base.shape[-1], int(rng.choice([1, 2, 3, 5]))),)
+    st = tuple(int(rng.integers(0, s - w + 1)) for s, w in zip(base.shape, win))
+    sl = tuple(slice(a, a + w) for a, w in zip(st, win))
+    window = np.ascontiguousarray(base[sl])
+    ref = O.expected_value(window)
+    bdev = _dev(base)
+    m1 = T.expected_value_view(T.View(bdev, st, win), with_mass=True).cpu().numpy()
+    m2 = T.expected_value_view(T.View(bdev, st, win), with_mass=True).cpu().numpy()
+    assert _bits(m1).tolist() == _bits(m2).tolist()
+    assert np.all(np.abs(m1[:d] - ref) <= 1e-12 * np.abs(ref) + 1e-300)
+    tot = float(window.astype(np.float64).sum())
+    assert abs(m1[d] - tot) <= 1e-12 * tot
+    # integer-valued: exact
+    q = rng.integers(0, 64, size=base.shape).astype(dtype)
+    refq = O.expected_value(np.ascontiguousarray(q[sl]))
+    np.testing.assert_array_equal(
+        T.expected_value_view(T.View(_dev(q), st, win)).cpu().numpy(), refq)
+
+
+def test_ev_view_whole_base_matches_dense():
+    p = make_inputs("C3")["p"]
+    dense = T.expected_value(_dev(p)).cpu().numpy()
+    view = T.expected_value_view(T.View(_dev(p))).cpu().numpy()
+    assert np.all(np.abs(view - dense) <= 1e-12 * np.abs(dense))
+    # an interior window of C3's p
+    st, win = (2, 0, 3, 1, 0, 4), (12, 16, 9, 15, 16, 7)
+    sl = tuple(slice(a, a + w) for a, w in zip(st, win))
+    ref = O.expected_value(np.ascontiguousarray(p[sl]))
+    got = T.expected_value_view(T.View(_dev(p), st, win)).cpu().numpy()
+    assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref))
+
+
 def test_view_centered_fft_padding():
     """The FFT-padding use with the signal placed at an offset: a (384)^3 f32 src embedded
     at (64,64,64) of a (512)^3 dst whose other elements must become +0.0: zero the dst with a
