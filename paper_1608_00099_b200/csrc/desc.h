@@ -72,6 +72,10 @@ struct Desc {
   // dense in the counter, so while a digit <= khi is out of bounds the warp stores zeros at
   // dst + r * step without touching the odometer (zmask = oob bits of digits 0..khi, 0 = off)
   uint32_t zmask;
+  // zero-run lengths: zn[m] = size of the sub-counter of digits m..khi (its value is the warp's
+  // step index mod zn[m]), with fast-division magics
+  uint32_t zdm[TRIOT_MAXD], zds[TRIOT_MAXD];
+  IDX zn[TRIOT_MAXD];
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
                                   // update: x, y, z
   void* out;             // EV: means (device)

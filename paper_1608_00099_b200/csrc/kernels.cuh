@@ -329,14 +329,9 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
     // significant out-of-bounds digit; it stays out of bounds until digits m..khi wrap, i.e.
     // for N - S more steps (N, S = size and mixed-radix value of the sub-counter m..khi).
     const int m = __ffs(oob & d.zmask) - 1;
-    IDX S = 0, N = 1;
-#pragma unroll
-    for (int k = 0; k < D - 1; ++k)
-      if (k >= m && k <= d.khi) {
-        S = S * d.ext[k] + u[k];
-        N = N * d.ext[k];
-      }
-    IDX run = N - S;
+    // N - S with S = the value of digits m..khi = (step index) mod N, the step index being b/32
+    const IDX N = d.zn[m], T = b >> 5;
+    IDX run = N - (T - divq<IDX>(T, N, d.zdm[m], d.zds[m]) * N);
     const IDX left = (vend - b + 31) / 32;
     if (run > left) run = left;
     const IDX full = (b + run * 32 <= vend) ? run : run - 1;

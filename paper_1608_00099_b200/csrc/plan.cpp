@@ -438,7 +438,15 @@ void set_step(Geom& g) {
     bool ok = true;
     for (int k = 0; k < D; ++k) ok = ok && (k == g.khi ? true : g.dlt[k] == 0);
     for (int k = 1; k <= g.khi; ++k) ok = ok && g.t[0].kap[k] == 0;
-    if (ok) g.zmask = (uint32_t)((2ull << g.khi) - 1ull);
+    if (ok) {
+      g.zmask = (uint32_t)((2ull << g.khi) - 1ull);
+      uint64_t nsub = 1;
+      for (int k = g.khi; k >= 0; --k) {
+        nsub *= g.ext[k];
+        g.zn[k] = nsub;
+        if (nsub < (1ull << 32)) fastdiv_magic((uint32_t)nsub, &g.zdm[k], &g.zds[k]);
+      }
+    }
   }
 }
 
@@ -986,6 +994,7 @@ std::string describe(const Geom& g) {
   arr(s, "ext", g.ext, g.D);
   arr(s, "dlt", g.dlt, g.D);
   arr(s, "bnd", g.bnd, g.D);
+  arr(s, "zn", g.zn, g.D);
   arr32(s, "fdm", g.fdm, g.D);
   arr32(s, "fds", g.fds, g.D);
   arri(s, "slot_of_axis", g.slot_of_axis, g.d + 1);

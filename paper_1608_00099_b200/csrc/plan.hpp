@@ -51,6 +51,8 @@ struct Geom {
   bool split = false;       // reductions: partials summed by a second (PDL) kernel
   bool view = false;        // EV of a view: p is strided (offsets tracked by the odometer)
   uint32_t zmask = 0;       // embed zero runs (desc.h)
+  uint64_t zn[TRIOT_MAXD] = {};
+  uint32_t zdm[TRIOT_MAXD] = {}, zds[TRIOT_MAXD] = {};
   struct T {
     uint64_t sig[TRIOT_MAXD] = {}, kap[TRIOT_MAXD] = {};
     uint64_t step = 0, rho = 0, tau = 1;
@@ -129,6 +131,11 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.op = g.binop;
   d.split = g.split ? 1 : 0;
   d.zmask = g.zmask;
+  for (int k = 0; k < TRIOT_MAXD; ++k) {
+    d.zn[k] = (IDX)g.zn[k];
+    d.zdm[k] = g.zdm[k];
+    d.zds[k] = g.zds[k];
+  }
   for (int x = 0; x < TRIOT_MAXT; ++x) {
     for (int k = 0; k < TRIOT_MAXD; ++k) {
       d.t[x].sig[k] = (IDX)g.t[x].sig[k];

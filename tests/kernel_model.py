@@ -91,6 +91,9 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
                     S, N = 0, 1
                     for k in range(m, khi + 1):
                         S, N = S * ext[k] + u[k], N * ext[k]
+                    # the kernel's form: N from the plan, S = (step index) mod N
+                    T_ = (v - lane) // 32
+                    assert desc["zn"][m] == N and T_ % N == S, (desc["zn"], m, N, S, T_)
                     run_ = min(N - S, (vend - (v - lane) + 31) // 32)
                     o = off[0]
                     for r in range(run_):
