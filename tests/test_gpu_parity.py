@@ -265,6 +265,48 @@ def test_u64_index_path():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.slow
+def test_u64_index_path_ev_and_binary():
+    """The 64-bit-index instances of the expected value and binary (> 2^32 elements): the EV of
+    an all-ones f32 p is exact in fp64, ((n_k - 1) / 2) * N for every axis, and the binary
+    product of two formula-generated tensors is checked on sampled elements."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip("needs ~55 GB free")
+    shape = (65537, 256, 256)          # 4,295,032,832 elements
+    n = math.prod(shape)
+    desc = T.triot_plan_describe(2, [shape], None, 3, T.TRIOT_F32, 0)
+    assert desc["idx64"]
+    p = torch.ones(shape, dtype=torch.float32, device=DEV)
+    m = T.expected_value(p, with_mass=True).cpu().numpy()
+    expect = [(e - 1) / 2 * n for e in shape] + [float(n)]
+    np.testing.assert_array_equal(m, np.array(expect))
+    del p
+    torch.cuda.empty_cache()
+    # binary: a[i] = (i mod 1021) / 8, b[i] = (i mod 509) / 16 (exact in f32), c = a * b
+    def formula(mod, scale):
+        out = torch.empty(n, dtype=torch.float32, device=DEV)
+        for s0 in range(0, n, 1 << 29):   # bounded int64 temporaries
+            s1 = min(n, s0 + (1 << 29))
+            out[s0:s1] = (torch.arange(s0, s1, dtype=torch.int64, device=DEV) % mod).to(
+                torch.float32).mul_(scale)
+        return out.view(shape)
+    a = formula(1021, 0.125)
+    b = formula(509, 0.0625)
+    c = torch.empty(shape, dtype=torch.float32, device=DEV)
+    assert T.triot_plan_describe(1, [shape, shape, shape], None, 3, T.TRIOT_F32, 2)["idx64"]
+    T.apply_binary(a, b, "mul", out=c)
+    torch.cuda.synchronize()
+    idx = np.concatenate([np.arange(64), np.random.default_rng(5).integers(0, n, 4096),
+                          np.arange(n - 64, n)])
+    got = c.view(-1)[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+    ref = ((idx % 1021).astype(np.float32) * np.float32(0.125)) * \
+          ((idx % 509).astype(np.float32) * np.float32(0.0625))
+    np.testing.assert_array_equal(got, ref)
+    del a, b, c
+    torch.cuda.empty_cache()
+
+
 def test_ev_mass_and_slab_amalgamation():
     """triot_expected_value_mass + the slab shift of parallel.py, emulating 3 ranks on one GPU."""
     from paper_1608_00099_b200 import parallel as P
