@@ -12,7 +12,8 @@ import json
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtriot.so")
+# TRIOT_LIB_PATH: an alternative build of the same library (A/B measurements in tools/ only)
+LIB_PATH = os.environ.get("TRIOT_LIB_PATH") or os.path.join(_PKG, "libtriot.so")
 
 TRIOT_F32, TRIOT_F64 = 0, 1
 TRIOT_ADD, TRIOT_SUB, TRIOT_MUL, TRIOT_DIV = 0, 1, 2, 3

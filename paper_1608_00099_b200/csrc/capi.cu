@@ -60,6 +60,7 @@ TableFn table_for(const Geom& g) {
 }
 
 int vindex(const Geom& g) {
+  if (g.rows) return 5;
   if (g.flat) return 3;
   if (g.V == 32 / g.esz) return 0;
   if (g.V == 16 / g.esz) return 1;
@@ -139,7 +140,12 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
       g_override.bpsm == 0 && pol.mode != 0)
     pol.q = 0;
   const uint64_t wpb = TRIOT_BLOCK / 32;
-  const uint64_t kMinSteps = 4;  // >= 4 steps per warp amortise the start decode
+  // >= 4 steps per warp amortise the start decode -- unless that leaves fewer than 8 blocks
+  // per SM: small ops (Benchmark 3's 27 MB) are latency-bound, and more warps with one step
+  // each keep more loads in flight than fewer warps with four
+  uint64_t kMinSteps = g.nsteps / ((uint64_t)sms * 8 * wpb);
+  if (kMinSteps > 4) kMinSteps = 4;
+  if (kMinSteps < 1) kMinSteps = 1;
   uint64_t grid = (uint64_t)sms * (uint64_t)(pol.bpsm > 0 ? pol.bpsm : occ);
   if (pol.bpsm <= 0 && pol.mode == 0 && pol.q > 0)
     grid = (g.nsteps + (uint64_t)pol.q * wpb - 1) / ((uint64_t)pol.q * wpb);
@@ -571,9 +577,12 @@ int triot_plan_describe(int op, const int64_t* const* shapes, const int64_t* ite
 }
 
 int triot_set_launch_policy(int mode, int blocks_per_sm) {
-  if (mode < -1 || mode > 4 || blocks_per_sm < 0 || blocks_per_sm > 1024)
+  if (mode < -1 || mode > 5 || blocks_per_sm < 0 || blocks_per_sm > 1024)
     return set_error(TRIOT_ERR_BAD_DTYPE_OR_OP, "BadPolicy: mode %d, blocks_per_sm %d", mode,
                      blocks_per_sm);
+  // mode 5: no row windows (short odd innermost rows take flat vectors), decomposition automatic
+  set_rows_enabled(mode != 5);
+  if (mode == 5) mode = -1;
   g_override.mode = mode;
   g_override.bpsm = mode < 0 ? 0 : blocks_per_sm;
   g_override.q = 0;

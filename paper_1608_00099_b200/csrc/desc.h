@@ -9,6 +9,8 @@
 //   flat       (odd innermost extents) vectors of V consecutive elements of the flattened
 //              counter that may cross rows: digits are then element digits (D = all axes) and
 //              the kernel walks the V elements with the +1 odometer.
+//   rows       (short odd innermost extents, embed / binary) a vector is one counter row; the
+//              digits are the outer axes and a warp sweeps its 32 rows' elements lane by lane.
 //   digits     u[0..D-1]: the mixed-radix coordinates of a vector.  Digits 0..D-2 are counter
 //              axes; digit D-1 (the "vector digit") is either the vector index inside a counter
 //              row (R == 1) or a group of R whole rows when rows are shorter than a vector
@@ -76,6 +78,11 @@ struct Desc {
   // step index mod zn[m]), with fast-division magics
   uint32_t zdm[TRIOT_MAXD], zds[TRIOT_MAXD];
   IDX zn[TRIOT_MAXD];
+  // row windows (short odd innermost extents, embed / binary): a vector is one counter row of
+  // rowlen elements; a warp sweeps groups of rwin windows of 32 rows, element e of a group in
+  // lane e % 32, row umulhi(e, rmag) = e / rowlen (rmag = 2^32 / rowlen + 1, exact for
+  // e < 2^13); scols = the embed bound of the column.
+  uint32_t rowlen, rmag, rwin;
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
                                   // update: x, y, z
   void* out;             // EV: means (device)

@@ -84,6 +84,19 @@ const void* kptr_flat() {
 #endif
 }
 
+// row-window instances (short odd innermost extents): embed, binary; K = 32 bytes of loads per
+// lane per batch (measured on B200: f32 K 8 > 4, f64 K 4 > 8)
+template <int D, typename IDX>
+const void* kptr_rows() {
+#if TRIOT_INST_OP == 0
+  return (const void*)&embed_rows_kernel<D, ESZ, IDX, 32 / ESZ>;
+#elif TRIOT_INST_OP == 1
+  return (const void*)&binary_rows_kernel<D, ESZ, IDX, 32 / ESZ, TRIOT_INST_BOP>;
+#else
+  return nullptr;
+#endif
+}
+
 // embed with zero runs (32-B vectors, dst dense in the counter; Desc::zmask)
 template <int D, typename IDX>
 const void* kptr_zero_runs() {
@@ -95,11 +108,13 @@ const void* kptr_zero_runs() {
 }
 
 // table index: ((D-1) * NVI + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
-// 3 = flat 32-B vectors, 4 = 32 B with embed zero runs
-constexpr int NVI = 5;
+// 3 = flat 32-B vectors, 4 = 32 B with embed zero runs, 5 = row windows
+constexpr int NVI = 6;
 template <int D>
 struct Fill {
   static void run(const void** t) {
+    t[((D - 1) * NVI + 5) * 2 + 0] = kptr_rows<D, uint32_t>();
+    t[((D - 1) * NVI + 5) * 2 + 1] = kptr_rows<D, uint64_t>();
     t[((D - 1) * NVI + 4) * 2 + 0] = kptr_zero_runs<D, uint32_t>();
     t[((D - 1) * NVI + 4) * 2 + 1] = kptr_zero_runs<D, uint64_t>();
     t[((D - 1) * NVI + 0) * 2 + 0] = kptr<D, 32 / ESZ, uint32_t>();

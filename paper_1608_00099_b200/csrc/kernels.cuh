@@ -85,6 +85,14 @@ struct Mem<8> {
   static __device__ __forceinline__ void ld(const void* p, uint32_t* w) {
     asm volatile("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(p));
   }
+  // w = pred ? *p : 0 (the address is formed unconditionally; only the load is predicated)
+  static __device__ __forceinline__ void ld_or0(const void* p, bool pred, uint32_t* w) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+        " @q ld.global.nc.v2.b32 {%0,%1}, [%2];\n}"
+        : "=r"(w[0]), "=r"(w[1])
+        : "l"(p), "r"((uint32_t)pred));
+  }
   static __device__ __forceinline__ void st(void* p, const uint32_t* w) {
     asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(p), "r"(w[0]), "r"(w[1]) : "memory");
   }
@@ -93,6 +101,13 @@ template <>
 struct Mem<4> {
   static __device__ __forceinline__ void ld(const void* p, uint32_t* w) {
     asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+  }
+  static __device__ __forceinline__ void ld_or0(const void* p, bool pred, uint32_t* w) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.b32 %0, 0;\n"
+        " @q ld.global.nc.b32 %0, [%1];\n}"
+        : "=r"(w[0])
+        : "l"(p), "r"((uint32_t)pred));
   }
   static __device__ __forceinline__ void st(void* p, const uint32_t* w) {
     asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(w[0]) : "memory");
@@ -567,6 +582,206 @@ __global__ void __launch_bounds__(kBlock) binary_flat_kernel(const __grid_consta
             Mem<ESZ>::st((void*)addr<ESZ>(d.t[0].ptr, coff[j][e]), r + e * EW);
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------ row windows (short odd rows)
+// When the innermost extent n is odd and short (3, 5, 7, ... <= 64), a vector is one counter
+// row.  A warp takes a group of W windows of 32 rows (W = d.rwin = 8, fewer for rows over 31
+// elements): lane i steps the odometer over rows b + i, b + 32 + i, ... (Alg 2 once,
+// then the carry deltas) and parks each row's offsets in the warp's shared-memory row table.
+// The warp then sweeps the group's rows * n elements lane by lane: element e = 32 j + lane
+// lies in row r = e / n (one multiply-high by the plan's magic rmag, exact for e < 2^13) and
+// column e - r n.  The table holds each tensor's offset rebased to the element index,
+// off'(r) = off(r) - r n tau, so element e sits at off'(r) + e tau, and (embed) the bound
+// lim(r) = r n + m (0 when the row is out of src bounds), so "column < m" is e < lim(r).
+// Consecutive lanes touch consecutive elements of every row-contiguous tensor, so accesses
+// coalesce at any alignment and no lane branches on a row end; a tensor dense in the counter
+// (dst, c) is addressed at the group base + e.  K elements per lane are loaded before any is
+// stored.  In stride decomposition (tuning only) groups are single windows.
+constexpr int kRowsWinMax = 8;                    // windows per group (plan: rwin <= this)
+constexpr int kRowsTab = 32 * kRowsWinMax;        // row-table entries per warp
+
+template <typename IDX>
+struct alignas(2 * sizeof(IDX)) RowSrc {
+  IDX off;   // rebased src offset
+  IDX lim;   // element bound: e < lim <=> the element's column reads src
+};
+
+template <int ESZ, typename IDX, int K, bool DD, bool T1>
+__device__ __forceinline__ void embed_rows_group(const Desc<IDX>& d, IDX gbase, uint32_t tot,
+                                                 const RowSrc<IDX>* ts, const IDX* td, int lane) {
+  constexpr int EW = ESZ / 4;
+  const uint32_t mg = d.rmag;
+  const IDX tau0 = T1 ? IDX(1) : d.t[0].tau, tau1 = T1 ? IDX(1) : d.t[1].tau;
+  const char* src = (const char*)d.t[1].ptr;
+  char* dst = (char*)d.t[0].ptr;
+  for (uint32_t e0 = 0; e0 < tot; e0 += 32 * K) {
+    uint32_t buf[K][EW];
+    IDX doff[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t e = e0 + 32u * j + (uint32_t)lane;
+      const uint32_t r = min(__umulhi(e, mg), (uint32_t)kRowsTab - 1u);  // past tot: any entry
+      const RowSrc<IDX> rs = ts[r];
+      if (!DD) doff[j] = td[r] + (IDX)e * tau0;
+      Mem<ESZ>::ld_or0(src + (uint64_t)(rs.off + (IDX)e * tau1) * ESZ, (IDX)e < rs.lim, buf[j]);
+    }
+    char* p = dst + (uint64_t)(gbase + (IDX)e0 + (IDX)lane) * ESZ;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (e0 + 32u * j + (uint32_t)lane < tot)
+        Mem<ESZ>::st(DD ? (void*)(p + 32 * ESZ * j) : (void*)(dst + (uint64_t)doff[j] * ESZ),
+                     buf[j]);
+  }
+}
+
+template <int D, int ESZ, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) embed_rows_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int EW = ESZ / 4;
+  __shared__ RowSrc<IDX> tsrc[kBlock / 32][kRowsTab];
+  __shared__ IDX tdst[kBlock / 32][kRowsTab];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[2];
+  uint32_t oob;
+  odo_start<D, 2, true, IDX, true>(d, base0 + (IDX)lane, u, off, oob);
+  const IDX n = (IDX)d.rowlen, m = d.scols;
+  const IDX tau0 = d.t[0].tau, tau1 = d.t[1].tau;
+  const bool ddense = d.t[0].vec != 0;
+  const bool t1 = tau0 == IDX(1) && tau1 == IDX(1);  // both rows contiguous
+  const int W = d.dv == (IDX)32 ? (int)d.rwin : 1;
+  RowSrc<IDX>* ts = tsrc[wib];
+  IDX* td = tdst[wib];
+  for (int i = lane; i < kRowsTab; i += 32) {  // entries no group fills read nothing
+    ts[i].off = 0;
+    ts[i].lim = 0;
+    td[i] = 0;
+  }
+  pdl_wait();
+  IDX b = base0;
+  while (b < vend) {
+    // fill the row table: W windows (fewer at the end of the warp's range)
+    uint32_t rows = 0;
+    bool any = false;
+    const IDX gb = b * n;  // counter element of the group's first row
+    for (int w = 0; w < W && b < vend; ++w, b += d.dv) {
+      const uint32_t nr = (vend - b) < (IDX)32 ? (uint32_t)(vend - b) : 32u;
+      const bool rd = (uint32_t)lane < nr && oob == 0;  // row reads src
+      any = any || (rd && m != 0);
+      const IDX r0 = (IDX)(32 * w + lane) * n;  // group element index of the row's first element
+      ts[32 * w + lane].off = off[1] - r0 * tau1;
+      ts[32 * w + lane].lim = rd ? r0 + m : IDX(0);
+      td[32 * w + lane] = off[0] - r0 * tau0;
+      rows = 32u * (uint32_t)w + nr;
+      odo_step<D, 2, true, IDX, true>(d, u, off, oob);
+    }
+    __syncwarp();
+    const uint32_t tot = rows * (uint32_t)n;
+    if (ddense) {
+      if (!__any_sync(0xffffffffu, any)) {
+        // every row of the group is out of src bounds: a plain zero stream
+        uint32_t z[EW];
+#pragma unroll
+        for (int q = 0; q < EW; ++q) z[q] = 0u;
+        for (uint32_t e = lane; e < tot; e += 32)
+          Mem<ESZ>::st((void*)addr<ESZ>(d.t[0].ptr, gb + (IDX)e), z);
+      } else if (t1) {
+        embed_rows_group<ESZ, IDX, K, true, true>(d, gb, tot, ts, td, lane);
+      } else {
+        embed_rows_group<ESZ, IDX, K, true, false>(d, gb, tot, ts, td, lane);
+      }
+    } else {
+      embed_rows_group<ESZ, IDX, K, false, false>(d, gb, tot, ts, td, lane);
+    }
+    __syncwarp();
+  }
+}
+
+// One group of the binary op: a and b offsets from the table, c dense (CD) or from the table.
+template <int ESZ, typename IDX, int K, int OP, bool CD, bool T1>
+__device__ __forceinline__ void binary_rows_group(const Desc<IDX>& d, IDX gbase, uint32_t tot,
+                                                  const IDX* tc, const RowSrc<IDX>* tab,
+                                                  int lane) {
+  constexpr int EW = ESZ / 4;
+  const uint32_t mg = d.rmag;
+  const IDX sc = T1 ? IDX(1) : d.t[0].tau, sa = T1 ? IDX(1) : d.t[1].tau;
+  const IDX sb = T1 ? IDX(1) : d.t[2].tau;
+  char* c = (char*)d.t[0].ptr;
+  const char* pa = (const char*)d.t[1].ptr;
+  const char* pb = (const char*)d.t[2].ptr;
+  for (uint32_t e0 = 0; e0 < tot; e0 += 32 * K) {
+    uint32_t ba[K][EW], bb[K][EW];
+    IDX coff[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t e = e0 + 32u * j + (uint32_t)lane;
+      const uint32_t r = min(__umulhi(e, mg), (uint32_t)kRowsTab - 1u);
+      const RowSrc<IDX> ab = tab[r];  // .off = a, .lim = b (rebased offsets)
+      if (!CD) coff[j] = tc[r] + (IDX)e * sc;
+      Mem<ESZ>::ld_or0(pa + (uint64_t)(ab.off + (IDX)e * sa) * ESZ, e < tot, ba[j]);
+      Mem<ESZ>::ld_or0(pb + (uint64_t)(ab.lim + (IDX)e * sb) * ESZ, e < tot, bb[j]);
+    }
+    char* p = c + (uint64_t)(gbase + (IDX)e0 + (IDX)lane) * ESZ;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (e0 + 32u * j + (uint32_t)lane >= tot) continue;
+      uint32_t r[EW];
+      Elem<ESZ>::put(r, bop<OP>(Elem<ESZ>::get(ba[j]), Elem<ESZ>::get(bb[j])));
+      Mem<ESZ>::st(CD ? (void*)(p + 32 * ESZ * j) : (void*)(c + (uint64_t)coff[j] * ESZ), r);
+    }
+  }
+}
+
+template <int D, int ESZ, typename IDX, int K, int OP>
+__global__ void __launch_bounds__(kBlock) binary_rows_kernel(const __grid_constant__ Desc<IDX> d) {
+  __shared__ RowSrc<IDX> tab[kBlock / 32][kRowsTab];
+  __shared__ IDX tcs[kBlock / 32][kRowsTab];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)wib;
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[3];
+  uint32_t oob;
+  odo_start<D, 3, false, IDX>(d, base0 + (IDX)lane, u, off, oob);
+  const IDX n = (IDX)d.rowlen;
+  const IDX sc = d.t[0].tau, sa = d.t[1].tau, sb = d.t[2].tau;
+  const bool cd = d.t[0].vec != 0;
+  const bool t1 = sc == IDX(1) && sa == IDX(1) && sb == IDX(1);
+  const int W = d.dv == (IDX)32 ? (int)d.rwin : 1;
+  pdl_wait();
+  IDX b = base0;
+  while (b < vend) {
+    uint32_t rows = 0;
+    const IDX gb = b * n;
+    for (int w = 0; w < W && b < vend; ++w, b += d.dv) {
+      const uint32_t nr = (vend - b) < (IDX)32 ? (uint32_t)(vend - b) : 32u;
+      const IDX r0 = (IDX)(32 * w + lane) * n;
+      tab[wib][32 * w + lane].off = off[1] - r0 * sa;
+      tab[wib][32 * w + lane].lim = off[2] - r0 * sb;
+      tcs[wib][32 * w + lane] = off[0] - r0 * sc;
+      rows = 32u * (uint32_t)w + nr;
+      odo_step<D, 3, false, IDX>(d, u, off, oob);
+    }
+    __syncwarp();
+    if (cd && t1)
+      binary_rows_group<ESZ, IDX, K, OP, true, true>(d, gb, rows * (uint32_t)n, tcs[wib],
+                                                     tab[wib], lane);
+    else if (cd)
+      binary_rows_group<ESZ, IDX, K, OP, true, false>(d, gb, rows * (uint32_t)n, tcs[wib],
+                                                      tab[wib], lane);
+    else
+      binary_rows_group<ESZ, IDX, K, OP, false, false>(d, gb, rows * (uint32_t)n, tcs[wib],
+                                                       tab[wib], lane);
+    __syncwarp();
   }
 }
 

@@ -162,6 +162,77 @@ static void plan_flat(Geom& g, const Axis* ax, int na, int nt, bool bounds, cons
   g.slot_of_axis[g.d] = na + 1;  // the mass
 }
 
+// Row windows: the longest innermost extent taken by row windows, per op (measured on B200,
+// embed rows of 33 stream faster as flat vectors, whose only gather is src;
+// binary rows up to 63 stream 1.7x faster as row windows, flat vectors gather both operands).
+// Thread-local switch so the tuning hook (triot_set_launch_policy mode 5) can turn them off.
+static const uint64_t kRowsMaxEmbed = 31, kRowsMaxBinary = 64;
+static thread_local bool g_rows_on = true;
+void set_rows_enabled(bool on) { g_rows_on = on; }
+
+// Row-window geometry: digits are the outer canonical axes (a single unit digit when there is
+// none); a "vector" is one counter row of n = rowlen elements; every tensor keeps its row
+// offset (Horner over the outer digits, Alg 2) and its innermost stride tau.  A tensor is
+// "dense" (vec) iff its offset of counter element f is f itself, so the kernel addresses it
+// from the window base without the row offset.
+static void plan_rows(Geom& g, const Axis* ax, int na, int nt, bool bounds) {
+  g.rows = true;
+  g.flat = false;
+  g.V = 1;
+  g.R = 1;
+  g.collapsed = false;
+  g.lgL = 0;
+  const Axis& in = ax[na - 1];
+  const uint64_t n = in.n;
+  g.rowlen = n;
+  g.rmag = (1ull << 32) / n + 1;  // n >= 3: fits 32 bits; umulhi(e, rmag) == e / n for e < 2^13
+  // windows per group: >= 16 elements per lane, at most 8 and at most 248 / n (the group's
+  // element indices stay below 2^13 for the magic).  Measured on B200 against fixed 1, 2, 4, 8
+  // windows per group (DESIGN.md §7 row windows): within 1-5 % of the best fixed choice.
+  g.rwin = (16 + n - 1) / n;
+  if (g.rwin > 8) g.rwin = 8;
+  if (g.rwin > 248 / n) g.rwin = 248 / n;
+  if (g.rwin < 1) g.rwin = 1;
+  uint64_t cstr[TRIOT_MAXD];
+  uint64_t hs = 1;
+  for (int k = na - 1; k >= 0; --k) {
+    cstr[k] = hs;
+    hs *= ax[k].n;
+  }
+  if (na == 1) {  // one row: a single unit digit
+    g.D = 1;
+    g.ext[0] = 1;
+    g.bnd[0] = 1;
+    for (int x = 0; x < nt; ++x) g.t[x].sig[0] = 0;
+  } else {
+    g.D = na - 1;
+    for (int k = 0; k < na - 1; ++k) {
+      g.ext[k] = ax[k].n;
+      g.bnd[k] = bounds ? ax[k].bnd : ax[k].n;
+      for (int x = 0; x < nt; ++x) g.t[x].sig[k] = ax[k].sig[x];
+    }
+  }
+  for (int x = 0; x < nt; ++x) {
+    bool dense = in.sig[x] == 1;
+    for (int k = 0; k < na; ++k)
+      if (ax[k].sig[x] != cstr[k]) dense = false;
+    g.t[x].vec = dense;
+    g.t[x].rho = 0;
+    g.t[x].tau = in.sig[x];
+  }
+  g.rowmul = g.colmul = 0;
+  g.srows = 1;
+  g.scols = g.all_oob ? 0 : (bounds ? in.bnd : n);
+  g.vfull = g.vany = 0;
+  g.N = 1;
+  for (int k = 0; k < na; ++k) g.N *= ax[k].n;
+  g.nvec = g.N / n;
+  g.nsteps = (g.nvec + 31) / 32;
+  finish_geometry(g, nt);
+  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  g.nslots = 0;
+}
+
 static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
                   const uint64_t* bnd, bool allow_merge, bool bounds) {
   const int d = g.d, nt = g.ntensor;
@@ -275,6 +346,11 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // flat vectors: when no vector width fits the innermost extent (odd extents: 3, 5, 7, 999),
   // take V consecutive elements of the flattened counter instead of one element per lane, for
   // the ops that have flat kernels.  The counter-dense tensors then still get full-width access.
+  const uint64_t rows_max = !g_rows_on ? 0 : g.op == OP_EMBED ? kRowsMaxEmbed : kRowsMaxBinary;
+  if (cc[best].V == 1 && vmax > 1 && g.rows_ok && nl >= 3 && nl <= rows_max) {
+    plan_rows(g, ax, na, nt, bounds);
+    return;
+  }
   if (cc[best].V == 1 && vmax > 1 && g.flat_ok) {
     plan_flat(g, ax, na, nt, bounds, n);
     return;
@@ -433,7 +509,7 @@ void set_step(Geom& g) {
   }
   // embed zero runs: a step of exactly one unit of digit khi < D-1 and dst offsets linear in it
   g.zmask = 0;
-  if (g.op == OP_EMBED && !g.flat && g.mode == 0 && g.dv == 32 && g.khi >= 0 && g.khi < D - 1 &&
+  if (g.op == OP_EMBED && !g.flat && !g.rows && g.mode == 0 && g.dv == 32 && g.khi >= 0 && g.khi < D - 1 &&
       g.dlt[g.khi] == 1 && g.t[0].vec && g.V * g.esz == 32) {
     bool ok = true;
     for (int k = 0; k < D; ++k) ok = ok && (k == g.khi ? true : g.dlt[k] == 0);
@@ -552,6 +628,7 @@ static int plan_embed_core(Geom& g, const TArg& dst, const TArg& src, int d, int
     return set_error(TRIOT_ERR_ALIASING, "Aliasing: dst and src overlap");
   g.op = OP_EMBED;
   g.flat_ok = true;
+  g.rows_ok = true;
   g.esz = esz;
   g.dtype = dtype;
   g.flags = flags;
@@ -634,6 +711,7 @@ static int plan_binary_core(Geom& g, const TArg& c, const TArg& a, const TArg& b
   }
   g.op = OP_BINARY;
   g.flat_ok = true;
+  g.rows_ok = true;
   g.esz = esz;
   g.dtype = dtype;
   g.binop = op;
@@ -979,14 +1057,17 @@ std::string describe(const Geom& g) {
            "\"op\":%d,\"esz\":%d,\"d\":%d,\"empty\":%s,\"idx64\":%s,\"all_oob\":%s,\"Dc\":%d,"
            "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"flat\":%s,\"N\":%llu,\"nvec\":%llu,"
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
-           "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,",
+           "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,"
+           "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
            (unsigned long long)g.nsteps, g.mode, (unsigned long long)g.wmul,
            (unsigned long long)g.wspan, (unsigned long long)g.dv, g.khi, g.klo, (unsigned long long)g.rowmul,
            (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,
-           (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots, g.zmask);
+           (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots, g.zmask,
+           g.rows ? "true" : "false", (unsigned long long)g.rowlen, (unsigned long long)g.rmag,
+           (unsigned long long)g.rwin);
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

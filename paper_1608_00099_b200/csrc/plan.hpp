@@ -36,6 +36,9 @@ struct Geom {
   bool collapsed = false;
   bool flat = false;   // flat vectors: V consecutive counter elements across rows (odd extents)
   bool flat_ok = false;  // the op has flat-vector kernels (embed, binary, expected value)
+  bool rows = false;     // row windows: a vector is one counter row (short odd innermost)
+  bool rows_ok = false;  // the op has row-window kernels (embed, binary)
+  uint64_t rowlen = 0, rmag = 0, rwin = 1;
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
@@ -88,6 +91,8 @@ int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const tr
 // 2 = contiguous chunk per block (EV bulk-copy kernel; `warps` is then the number of blocks).
 // Sets wmul/wspan/dv and the mixed-radix digits of the per-step advance (dlt, khi, klo, step).
 void set_decomposition(Geom& g, int mode, uint64_t warps);
+// Row windows on/off for this thread (tuning hook, triot_set_launch_policy mode 5).
+void set_rows_enabled(bool on);
 // (Re)compute the mixed-radix digits of the per-step advance for the current g.dv.
 void set_step(Geom& g);
 
@@ -131,6 +136,9 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.op = g.binop;
   d.split = g.split ? 1 : 0;
   d.zmask = g.zmask;
+  d.rowlen = (uint32_t)g.rowlen;
+  d.rmag = (uint32_t)g.rmag;
+  d.rwin = (uint32_t)g.rwin;
   for (int k = 0; k < TRIOT_MAXD; ++k) {
     d.zn[k] = (IDX)g.zn[k];
     d.zdm[k] = g.zdm[k];

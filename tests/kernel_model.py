@@ -68,6 +68,8 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
 
     if desc.get("flat"):
         return run_flat(desc, op, bufs, binop)
+    if desc.get("rows"):
+        return run_rows(desc, op, bufs, binop)
     wmul, wspan, dv = desc["wmul"], desc["wspan"], desc["dv"]
     # mode 0: warp chunks; 1: grid stride; 2: block chunks, thread t starts at vector t
     if desc["mode"] == 2:
@@ -253,4 +255,92 @@ def run_flat(desc: dict, op: str, bufs: list, binop: str = "mul"):
     if op == "ev":
         d = desc["d"]
         return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]
+    return None
+
+
+def run_rows(desc: dict, op: str, bufs: list, binop: str = "mul"):
+    """Row windows: lane i of warp step s holds counter row 32s+i (its tensor offsets and embed
+    bound, kept by the odometer); the warp sweeps the window's 32*n elements, element
+    e = 32j + lane in row umulhi(e, rmag) (== e // n, checked), column e - row*n, reading the
+    row's rebased offsets from the warp's row table as the kernel does."""
+    D, idx64 = desc["D"], desc["idx64"]
+    ext, dlt, bnd = desc["ext"], desc["dlt"], desc["bnd"]
+    khi, klo = desc["khi"], desc["klo"]
+    T = desc["t"]
+    nt = len(T)
+    n, mg, m = desc["rowlen"], desc["rmag"], desc["scols"]
+    nvec = desc["nvec"]
+    W = lambda x: _wrap(x, idx64)
+    fn = {"add": np.add, "sub": np.subtract, "mul": np.multiply, "div": np.divide}.get(binop)
+
+    def start(v):
+        u = [0] * D
+        for k in range(D - 1, 0, -1):
+            u[k] = v % ext[k]
+            v //= ext[k]
+        u[0] = v
+        off = [W(sum(u[k] * T[x]["sig"][k] for k in range(D))) for x in range(nt)]
+        oob = any(u[k] >= bnd[k] for k in range(D))
+        return u, off, oob
+
+    def step(u, off):
+        off = [W(off[x] + T[x]["step"]) for x in range(nt)]
+        carry = 0
+        for k in range(D - 1, -1, -1):
+            if k > khi:
+                continue
+            nu = u[k] + dlt[k] + carry
+            carry = int(nu >= ext[k])
+            if carry:
+                nu -= ext[k]
+                off = [W(off[x] + T[x]["kap"][k]) for x in range(nt)]
+            u[k] = nu
+            if k <= klo and not carry:
+                break
+        return u, off, any(u[k] >= bnd[k] for k in range(D))
+
+    wmul, wspan, dv = desc["wmul"], desc["wspan"], desc["dv"]
+    units = (nvec + wmul - 1) // wmul if desc["mode"] == 0 else dv // 32
+    Wg = desc["rwin"] if dv == 32 else 1
+    K = 32 // desc["esz"]
+    for w in range(units):
+        base0 = w * wmul
+        if base0 >= nvec:
+            continue
+        vend = min(base0 + wspan, nvec)
+        lanes = [start(base0 + i) for i in range(32)]
+        b = base0
+        while b < vend:
+            # the warp's row table: Wg windows of 32 rows (fewer at the end of its range); each
+            # entry holds the tensors' offsets rebased to the group's element index
+            # (off - r0*tau, r0 = the row's first element) and, for embed, the bound r0 + m
+            gb = b * n
+            tab, rows, wi = [], 0, 0
+            while wi < Wg and b < vend:
+                nr = min(32, vend - b)
+                for i in range(32):
+                    u, off, oob = lanes[i]
+                    r0 = (32 * wi + i) * n
+                    ent = [W(off[x] - r0 * T[x]["tau"]) for x in range(nt)]
+                    lim = r0 + m if (i < nr and not oob) else 0
+                    tab.append((ent, lim))
+                rows = 32 * wi + nr
+                lanes = [step(list(u), off) for (u, off, _) in lanes]
+                b += dv
+                wi += 1
+            tot = rows * n
+            for e in range(0, (tot + 32 * K - 1) // (32 * K) * 32 * K):
+                row = (e * mg) >> 32
+                assert row == e // n, (e, n, mg)
+                if e >= tot:
+                    continue
+                ent, lim = tab[row]
+                o = [W(ent[x] + e * T[x]["tau"]) for x in range(nt)]
+                if T[0]["vec"]:
+                    assert o[0] == gb + e
+                if op == "embed":
+                    bufs[0][o[0]] = bufs[1][o[1]] if e < lim else 0
+                else:
+                    with np.errstate(all="ignore"):
+                        bufs[0][o[0]] = fn(bufs[1][o[1]], bufs[2][o[2]])
     return None

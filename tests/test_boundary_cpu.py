@@ -56,12 +56,12 @@ def test_constants_and_status_strings():
 
 
 def test_launch_policy_range():
-    """Modes -1..4 and 0..1024 blocks per SM are accepted (host state only); others rejected."""
+    """Modes -1..5 and 0..1024 blocks per SM are accepted (host state only); others rejected."""
     lib = L.lib()
     try:
-        for mode in range(-1, 5):
+        for mode in range(-1, 6):
             assert lib.triot_set_launch_policy(mode, 16) == 0
-        for mode, bpsm in [(-2, 0), (5, 0), (0, -1), (0, 1025)]:
+        for mode, bpsm in [(-2, 0), (6, 0), (0, -1), (0, 1025)]:
             assert lib.triot_set_launch_policy(mode, bpsm) == 5
             assert "BadPolicy" in T.triot_last_error()
     finally:
@@ -407,9 +407,30 @@ def test_validation_conv():
     assert p["N"] == 511 * 15 and p["ext"] == [511, 15]
 
 
+@pytest.fixture
+def no_rows():
+    """Row windows off for this thread (triot_set_launch_policy mode 5): embed and binary with
+    short odd rows then take flat vectors."""
+    lib = L.lib()
+    assert lib.triot_set_launch_policy(5, 0) == 0
+    yield
+    lib.triot_set_launch_policy(-1, 0)
+
+
 @pytest.mark.parametrize("seed", range(8))
-def test_model_flat_vectors_vs_oracle(seed):
+def test_model_flat_vectors_vs_oracle(seed, no_rows):
     """Odd innermost extents take flat vectors (V consecutive counter elements across rows)."""
+    _odd_shapes_vs_oracle(seed, expect="flat")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_model_row_windows_vs_oracle(seed):
+    """Short odd innermost extents take row windows for embed and binary (a lane per row, the
+    warp sweeping the window's elements lane by lane); the expected value keeps flat vectors."""
+    _odd_shapes_vs_oracle(seed, expect="rows")
+
+
+def _odd_shapes_vs_oracle(seed, expect):
     rng = np.random.default_rng(6000 + seed)
     d = int(rng.integers(1, 6))
     odd = int(rng.choice([3, 5, 7, 9, 11]))
@@ -420,8 +441,14 @@ def test_model_flat_vectors_vs_oracle(seed):
     src = random_values(rng, src_shape, dtype, "normal")
     ref = np.full(dst_shape, -7.0, dtype=src.dtype)
     O.embed(ref, src)
-    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, dt, 0, mode=seed % 2,
-                                 warps=int(rng.integers(1, 6)))
+    region = seed % 3 == 2 and expect == "rows"
+    if region:
+        ref = np.full(dst_shape, -7.0, dtype=src.dtype)
+        O.embed(ref, src, region_only=True)
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, dt, 1 if region else 0,
+                                 mode=seed % 2, warps=int(rng.integers(1, 6)))
+    if not region or math.prod(min(a, b) for a, b in zip(dst_shape, src_shape)) > 1:
+        assert desc[expect] or desc["V"] > 1 or desc["R"] > 1, desc
     out = np.full(dst_shape, -7.0, dtype=src.dtype)
     kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
     np.testing.assert_array_equal(_bits(out), _bits(ref))
@@ -442,7 +469,7 @@ def test_model_flat_vectors_vs_oracle(seed):
     np.testing.assert_array_equal(np.array(got), O.expected_value(p))
 
 
-def test_flat_geometry_chosen_for_odd_innermost():
+def test_flat_geometry_chosen_for_odd_innermost(no_rows):
     p = T.triot_plan_describe(0, [(5, 7), (4, 6)], None, 2, F32, 0)
     assert p["flat"] and p["V"] == 8 and p["D"] == 2 and p["nvec"] == 5
     assert [t["vec"] for t in p["t"]] == [True, False]
@@ -450,3 +477,41 @@ def test_flat_geometry_chosen_for_odd_innermost():
     assert p["flat"] and p["V"] == 4 and p["nvec"] == (7 ** 5 + 3) // 4
     p = T.triot_plan_describe(0, [(4, 8), (3, 8)], None, 2, F32, 0)
     assert not p["flat"]                       # a vector width fits: regular geometry
+
+
+def test_row_window_geometry():
+    """Short odd rows (<= 64) take row windows for embed / binary: the outer axes are the digits,
+    one vector per row, dense tensors flagged; longer odd rows keep flat vectors."""
+    p = T.triot_plan_describe(0, [(5, 7), (4, 6)], None, 2, F32, 0)
+    assert p["rows"] and not p["flat"] and p["D"] == 1 and p["rowlen"] == 7
+    assert (p["rmag"], p["nvec"], p["scols"], p["bnd"]) == ((1 << 32) // 7 + 1, 5, 6, [4])
+    assert p["rwin"] == 3                                 # >= 16 elements per lane per group
+    for n, w in ((3, 6), (5, 4), (9, 2), (15, 2), (17, 1), (63, 1)):
+        q = T.triot_plan_describe(1, [None, (40, n), (39, n + 1)], (39, n), 2, F32, 2)
+        assert q["rows"] and q["rwin"] == w and 32 * w * n + 32 * 8 <= (1 << 13), (n, q["rwin"])
+    assert [t["vec"] for t in p["t"]] == [True, False]
+    assert [t["tau"] for t in p["t"]] == [1, 1]
+    p = T.triot_plan_describe(0, [(3000, 7), (2900, 5)], None, 2, F64, 0)
+    assert p["rows"] and p["ext"] == [3000] and p["t"][1]["sig"] == [5]
+    p = T.triot_plan_describe(0, [(11,), (4,)], None, 1, F32, 0)     # one row: a unit digit
+    assert p["rows"] and p["D"] == 1 and p["ext"] == [1] and p["nvec"] == 1 and p["scols"] == 4
+    p = T.triot_plan_describe(1, [None, (9, 65), (9, 66)], (9, 65), 2, F32, 2)
+    assert p["flat"] and not p["rows"]                    # binary rows longer than 64: flat
+    p = T.triot_plan_describe(0, [(9, 33), (8, 30)], None, 2, F32, 0)
+    assert p["flat"] and not p["rows"]                    # embed rows longer than 31: flat
+    p = T.triot_plan_describe(0, [(9, 31), (8, 30)], None, 2, F32, 0)
+    assert p["rows"]
+    p = T.triot_plan_describe(1, [None, (9, 63), (9, 66)], (9, 63), 2, F32, 2)
+    assert p["rows"] and [t["vec"] for t in p["t"]] == [True, True, False]
+    p = T.triot_plan_describe(2, [(7,) * 5], None, 5, F64, 0)
+    assert p["flat"] and not p["rows"]                    # the expected value keeps flat vectors
+
+
+def test_row_window_division_magic_exact():
+    """umulhi(e, 2^32 // n + 1) == e // n for every row length the row windows take (3..64) and
+    every element index a group of windows (plus a batch of overrun) can reach."""
+    e = np.arange(1 << 13, dtype=np.uint64)
+    for n in range(3, 65):
+        mg = (1 << 32) // n + 1
+        assert mg < (1 << 32)
+        assert np.array_equal((e * np.uint64(mg)) >> np.uint64(32), e // np.uint64(n)), n

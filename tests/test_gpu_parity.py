@@ -669,3 +669,65 @@ def test_results_independent_of_launch_policy():
                 assert abs(m1[-1] - p.sum()) <= 1e-12 * p.sum()
     finally:
         T.triot_set_launch_policy(-1, 0)
+
+
+# ---------------------------------------------------------------- row windows (short odd rows)
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("seed", range(8))
+def test_row_windows_vs_oracle(seed, dtype):
+    """Short odd innermost extents (row-window kernels) for embed (pad, crop, region only) and
+    every binary op (dense and strided c, element-aligned bases), bit-exact; the same calls with
+    row windows switched off (flat vectors, policy mode 5) give the same bits."""
+    rng = np.random.default_rng(700 + seed)
+    d = int(rng.integers(1, 8))
+    n = int(rng.choice([1, 3, 5, 7, 9, 13, 31, 33, 63]))
+    outer = random_shape(rng, d - 1, 40000 // max(n, 4), lo=1, hi=40 if d <= 3 else 7) if d > 1 else ()
+    dst_shape = outer + (n,)
+    src_shape = tuple(max(1, s + int(rng.integers(-2, 3))) for s in dst_shape)
+    src = rng.standard_normal(src_shape).astype(dtype)
+    a = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in dst_shape)).astype(dtype)
+    b = rng.standard_normal(tuple(s + int(rng.integers(0, 3)) for s in dst_shape)).astype(dtype)
+    op = ["add", "sub", "mul", "div"][seed % 4]
+    try:
+        for mode in (-1, 5):
+            T.triot_set_launch_policy(mode, 0)
+            for region, off in ((False, 0), (True, 1), (False, 3)):
+                ref = np.full(dst_shape, np.nan, dtype=dtype)
+                O.embed(ref, src, region_only=region)
+                dst = _poisoned(dst_shape, dtype, off)
+                T.embed(dst, _dev(src, off % 2), region_only=region)
+                assert_bits_equal(dst, ref)
+            for cs, off in ((dst_shape, 0), (tuple(s + 1 for s in dst_shape), 1)):
+                ref = np.full(cs, 9.0, dtype=dtype)
+                O.apply_binary(a, b, op, iter_shape=dst_shape, out=ref)
+                out = _dev(np.full(cs, 9.0, dtype=dtype), off)
+                T.apply_binary(_dev(a, off), _dev(b), op, out=out, iter_shape=dst_shape)
+                assert_bits_equal(out, ref)
+            x = rng.standard_normal(dst_shape).astype(dtype)
+            ref = O.apply_binary(x, b, op, iter_shape=dst_shape)
+            xt = _dev(x)
+            T.apply_binary(xt, _dev(b), op, out=xt, iter_shape=dst_shape)   # in place, c == a
+            assert_bits_equal(xt, ref)
+    finally:
+        T.triot_set_launch_policy(-1, 0)
+
+
+def test_row_windows_large_and_policies():
+    """A large short-odd-row embed / binary (many windows per warp, all-zero windows, ragged last
+    window) under every decomposition, bit-exact against the oracle."""
+    rng = np.random.default_rng(71)
+    src = rng.standard_normal((700, 300, 5)).astype(np.float32)
+    ref = np.empty((733, 310, 7), np.float32); O.embed(ref, src)
+    a = rng.standard_normal((701, 311, 7)); b = rng.standard_normal((700, 310, 9))
+    refb = O.apply_binary(a, b, "mul", iter_shape=(700, 310, 7))
+    try:
+        for mode, bpsm in [(-1, 0), (0, 1), (0, 5), (1, 1), (1, 7), (0, 300)]:
+            T.triot_set_launch_policy(mode, bpsm)
+            dst = _poisoned((733, 310, 7), np.float32)
+            T.embed(dst, _dev(src))
+            assert_bits_equal(dst, ref)
+            out = T.apply_binary(_dev(a), _dev(b), "mul", iter_shape=(700, 310, 7))
+            assert_bits_equal(out, refb)
+    finally:
+        T.triot_set_launch_policy(-1, 0)

@@ -39,6 +39,23 @@ def main():
             torch.cuda.synchronize()
             print(name, "ok", flush=True)
             continue
+        if name in ("ROWS7", "ROWS33", "ROWSB63"):   # short odd rows (row-window kernels)
+            if name == "ROWSB63":
+                a_ = torch.rand((2000, 2000, 63), device=dev)
+                b_ = torch.rand((2001, 2000, 64), device=dev)
+                c_ = torch.empty((2000, 2000, 63), device=dev)
+                fn = lambda: T.apply_binary(a_, b_, "mul", out=c_, iter_shape=(2000, 2000, 63))
+            else:
+                sh = ((3000, 3000, 7), (2900, 2900, 5)) if name == "ROWS7" else \
+                    ((3000, 1000, 33), (2900, 1000, 31))
+                src_ = torch.rand(sh[1], device=dev)
+                dst_ = torch.empty(sh[0], device=dev)
+                fn = lambda: T.embed(dst_, src_)
+            for _ in range(a.reps):
+                fn()
+            torch.cuda.synchronize()
+            print(name, "ok", flush=True)
+            continue
         if name in ("B2", "B3"):
             from triot_inputs import make_paper_inputs
             pin = make_paper_inputs(name)

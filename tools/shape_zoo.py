@@ -15,6 +15,9 @@ import torch  # noqa: E402
 import paper_1608_00099_b200 as T  # noqa: E402
 
 dev = torch.device("cuda:0")
+if "--policy" in sys.argv:   # e.g. --policy 5,0: row windows off (flat vectors), A/B runs
+    _m, _b = (int(x) for x in sys.argv[sys.argv.index("--policy") + 1].split(","))
+    T.triot_set_launch_policy(_m, _b)
 scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
 
@@ -47,6 +50,7 @@ def embed_case(name, dst_shape, src_shape, dtype=torch.float32, off=0):
                                  0 if dtype == torch.float32 else 1, 0, (off * esz % 32, 0, 0))
     print(json.dumps({"case": name, "op": "embed", "us": round(ms * 1e3, 1),
                       "gbs": round(nbytes / ms / 1e6, 1), "V": plan["V"], "D": plan["D"],
+                      "geom": "rows" if plan["rows"] else "flat" if plan["flat"] else "vec",
                       "vec": [t["vec"] for t in plan["t"]]}), flush=True)
 
 
@@ -62,6 +66,7 @@ def binary_case(name, a_shape, b_shape, dtype=torch.float64):
                                  0 if dtype == torch.float32 else 1, 2)
     print(json.dumps({"case": name, "op": "binary", "us": round(ms * 1e3, 1),
                       "gbs": round(nbytes / ms / 1e6, 1), "V": plan["V"], "D": plan["D"],
+                      "geom": "rows" if plan["rows"] else "flat" if plan["flat"] else "vec",
                       "vec": [t["vec"] for t in plan["t"]]}), flush=True)
 
 
@@ -76,6 +81,29 @@ def ev_case(name, shape, dtype=torch.float64, off=0):
                       "gbs": round(nbytes / ms / 1e6, 1)}), flush=True)
 
 
+if "--rows" in sys.argv:   # short odd rows: row windows vs flat vectors (run with --policy 5,0)
+    embed_case("rows: embed f32 (3000,3000,7) <- (2900,2900,5)", (3000, 3000, 7), (2900, 2900, 5))
+    embed_case("rows: embed f32 (8192,4096,3) <- (8000,4000,3)", (8192, 4096, 3), (8000, 4000, 3))
+    embed_case("rows: embed f64 (1000,1000,15) <- (1000,999,15)", (1000, 1000, 15), (1000, 999, 15),
+               dtype=torch.float64)
+    embed_case("rows: embed f32 (3000,1000,33) <- (2900,1000,31)", (3000, 1000, 33), (2900, 1000, 31))
+    embed_case("rows: embed f32 (3000,3000,15) <- (2900,2900,13)", (3000, 3000, 15), (2900, 2900, 13))
+    embed_case("rows: embed f32 (3000,1000,31) <- (2900,1000,29)", (3000, 1000, 31), (2900, 1000, 29))
+    embed_case("rows: embed f64 (3000,3000,7) <- (2900,2900,5)", (3000, 3000, 7), (2900, 2900, 5),
+               dtype=torch.float64)
+    embed_case("rows: embed f32 (7)^8 <- (5)^8", (7,) * 8, (5,) * 8)
+    embed_case("rows: embed f32 (5)^10 <- (4)^10", (5,) * 10, (4,) * 10)
+    embed_case("rows: crop f32 (4096,512,3) <- (4100,600,7)", (4096, 512, 3), (4100, 600, 7))
+    embed_case("rows: embed f32 (4096,4096,5) <- same, dst misaligned", (4096, 4096, 5),
+               (4096, 4096, 5), off=1)
+    binary_case("rows: binary f64 (3000,3001,7) x (3001,3000,7)", (3000, 3001, 7), (3001, 3000, 7))
+    binary_case("rows: binary f32 (4000,4001,3) x (4001,4000,3)", (4000, 4001, 3), (4001, 4000, 3),
+                dtype=torch.float32)
+    binary_case("rows: binary f64 (200,300,401,5) x (201,300,400,5)", (200, 300, 401, 5),
+                (201, 300, 400, 5))
+    binary_case("rows: binary f32 (2000,2000,63) x (2001,2000,64)", (2000, 2000, 63),
+                (2001, 2000, 64), dtype=torch.float32)
+    sys.exit(0)
 if "--big" in sys.argv:   # odd innermost extents at sizes past the launch-bound regime
     embed_case("big: embed f32 (3000,3000,7) <- (2900,2900,5)", (3000, 3000, 7), (2900, 2900, 5))
     embed_case("big: embed f32 (8192,4096,3) <- (8000,4000,3)", (8192, 4096, 3), (8000, 4000, 3))
