@@ -96,7 +96,9 @@ constexpr bool kEvSplitDefault = false;
 constexpr int kEvSplitBpsm = 16;
 Policy auto_policy(const Geom& g) {
   if (g.op == OP_EV) return kEvSplitDefault ? Policy{0, kEvSplitBpsm, 0} : Policy{0, 0, 0};
-  if (g.op == OP_DOT) return Policy{0, 8, 0};  // <= 2048 partials for the reduction
+  // inner product: one wave at occupancy, like the expected value (ncu, cold, Benchmark 2:
+  // 4 blocks per SM 26.2 us vs 8 per SM 27.1 us)
+  if (g.op == OP_DOT) return Policy{0, 0, 0};
   if (g.op == OP_EMBED) {
     // zero-run embeds (C5: 94 % of the steps are zero runs) keep improving up to the 4-step
     // minimum chunk (ncu, C5: 64 / 128 / 192 blocks per SM -> 160.4 / 156.6 / 156.3 us)
@@ -151,6 +153,11 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
     grid = (g.nsteps + (uint64_t)pol.q * wpb - 1) / ((uint64_t)pol.q * wpb);
   uint64_t need = (g.nsteps + kMinSteps * wpb - 1) / (kMinSteps * wpb);
   if (need < grid) grid = need;
+  // a small op (less than 4 steps per warp at 8 blocks per SM) is latency-bound: keep it to one
+  // wave of resident blocks (Benchmark 3's update kernel holds 2 blocks per SM at 94 registers:
+  // 839 one-step blocks ran in 2.8 waves)
+  if (kMinSteps < 4 && g_override.bpsm == 0 && grid > (uint64_t)sms * (uint64_t)occ)
+    grid = (uint64_t)sms * (uint64_t)occ;
   if (grid > (uint64_t)max_grid) grid = (uint64_t)max_grid;
   if (grid < 1) grid = 1;
   set_decomposition(g, pol.mode, grid * wpb);
