@@ -167,6 +167,9 @@ static void plan_flat(Geom& g, const Axis* ax, int na, int nt, bool bounds, cons
 // binary rows up to 63 stream 1.7x faster as row windows, flat vectors gather both operands).
 // Thread-local switch so the tuning hook (triot_set_launch_policy mode 5) can turn them off.
 static const uint64_t kRowsMaxEmbed = 31, kRowsMaxBinary = 64;
+// Rows up to this length take row windows when the output is misaligned (one window per group;
+// the kernel's multiply-high division stays exact while e * n < 2^32, e < 32 n + 256).
+static const uint64_t kRowsMaxLong = 4096;
 static thread_local bool g_rows_on = true;
 void set_rows_enabled(bool on) { g_rows_on = on; }
 
@@ -185,9 +188,10 @@ static void plan_rows(Geom& g, const Axis* ax, int na, int nt, bool bounds) {
   const Axis& in = ax[na - 1];
   const uint64_t n = in.n;
   g.rowlen = n;
-  g.rmag = (1ull << 32) / n + 1;  // n >= 3: fits 32 bits; umulhi(e, rmag) == e / n for e < 2^13
+  g.rmag = (1ull << 32) / n + 1;  // n >= 3: fits 32 bits; umulhi(e, rmag) == e / n (e n < 2^32)
   // windows per group: >= 16 elements per lane, at most 8 and at most 248 / n (the group's
-  // element indices stay below 2^13 for the magic).  Measured on B200 against fixed 1, 2, 4, 8
+  // element indices stay below 2^13 for the magic; rows over 248 take one window, e < 32 n + 256,
+  // where e * n < 2^32 keeps it exact up to kRowsMaxLong).  Measured on B200 against fixed 1, 2, 4, 8
   // windows per group (DESIGN.md §7 row windows): within 1-5 % of the best fixed choice.
   g.rwin = (16 + n - 1) / n;
   if (g.rwin > 8) g.rwin = 8;
@@ -348,6 +352,15 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // the ops that have flat kernels.  The counter-dense tensors then still get full-width access.
   const uint64_t rows_max = !g_rows_on ? 0 : g.op == OP_EMBED ? kRowsMaxEmbed : kRowsMaxBinary;
   if (cc[best].V == 1 && vmax > 1 && g.rows_ok && nl >= 3 && nl <= rows_max) {
+    plan_rows(g, ax, na, nt, bounds);
+    return;
+  }
+  // The output (dst / c) cannot take wide stores although a vector width fits its rows -- its
+  // base is only element-aligned (a view at an odd offset, a sliced buffer): element stores at a
+  // 32-byte lane stride write partial sectors (C2 with dst offset by 4 B: 1.4 TB/s), so rows up
+  // to kRowsMaxLong take row windows, whose lane-consecutive accesses coalesce at any alignment.
+  if (cc[best].V > 1 && !cc[best].vec[0] && g.rows_ok && g_rows_on && nl >= 3 &&
+      nl <= kRowsMaxLong) {
     plan_rows(g, ax, na, nt, bounds);
     return;
   }

@@ -194,9 +194,9 @@ def test_plans_of_the_five_configs():
     assert (p["Dc"], p["D"], p["V"], p["R"], p["collapsed"]) == (14, 13, 8, 2, True)
     assert [t["vec"] for t in p["t"]] == [True, False]
     assert all(not pl["idx64"] for pl in map(_plan, CONFIGS))
-    # misaligned output pointer: the plan falls back to narrower accesses, never faults
+    # misaligned output pointer: row windows (element accesses, lane-consecutive), never wide
     p = _plan("C2", mods=(4, 0, 0))
-    assert not p["t"][0]["vec"]
+    assert p["rows"] and p["V"] == 1
 
 
 def test_canonicalisation_drops_and_merges():
@@ -515,3 +515,42 @@ def test_row_window_division_magic_exact():
         mg = (1 << 32) // n + 1
         assert mg < (1 << 32)
         assert np.array_equal((e * np.uint64(mg)) >> np.uint64(32), e // np.uint64(n)), n
+    # long rows (misaligned outputs): one window per group, e < 32 n + 256, up to n = 4096
+    for n in list(range(249, 300)) + [383, 384, 511, 512, 999, 1000, 2047, 3001, 4095, 4096]:
+        e = np.arange(32 * n + 256, dtype=np.uint64)
+        mg = (1 << 32) // n + 1
+        assert np.array_equal((e * np.uint64(mg)) >> np.uint64(32), e // np.uint64(n)), n
+
+
+def test_row_windows_for_misaligned_outputs():
+    """An output whose base is only element-aligned takes row windows (rows <= 4096) instead of
+    element stores at a 32-byte lane stride; an aligned one keeps 32-byte vectors."""
+    p = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0, ptr_mod32=(4, 0, 0))
+    assert p["rows"] and p["rowlen"] == 512 and p["rwin"] == 1 and p["D"] == 2
+    p = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0)
+    assert not p["rows"] and p["V"] == 8
+    p = T.triot_plan_describe(1, [None, (64, 100), (64, 96)], (64, 96), 2, F64, 2,
+                              ptr_mod32=(8, 0, 0))
+    assert p["rows"]
+    p = T.triot_plan_describe(0, [(4, 8192), (4, 8000)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
+    assert not p["rows"]                                   # rows over 4096: vector plan
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_model_misaligned_output_rows_vs_oracle(seed):
+    """Row windows planned for misaligned outputs (long rows, one window per group) run through
+    the kernel model bit-exact against the oracle."""
+    rng = np.random.default_rng(8000 + seed)
+    d = int(rng.integers(1, 4))
+    n = int(rng.choice([8, 16, 40, 256, 300]))
+    dst_shape = random_shape(rng, d - 1, 4000 // n + 2, lo=1, hi=12) + (n,) if d > 1 else (n,)
+    src_shape = tuple(max(1, s + int(rng.integers(-2, 3))) for s in dst_shape)
+    src = random_values(rng, src_shape, "f32", "normal")
+    ref = np.full(dst_shape, -7.0, dtype=np.float32)
+    O.embed(ref, src)
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, F32, 0, ptr_mod32=(4, 0, 0),
+                                 mode=0, warps=int(rng.integers(1, 6)))
+    assert desc["rows"] or desc["V"] == 1, desc
+    out = np.full(dst_shape, -7.0, dtype=np.float32)
+    kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
+    np.testing.assert_array_equal(_bits(out), _bits(ref))

@@ -69,6 +69,17 @@ def test_C2_embed_full():
     assert_bits_equal(dst, ref)
 
 
+def test_C2_embed_misaligned_dst_and_src():
+    """C2 with dst (then src) based one element off 32-B alignment: the row-window plan for a
+    misaligned output, and the vector plan with element-wise src loads, both bit-exact."""
+    inp = make_inputs("C2")
+    ref = np.empty(inp["dst_shape"], np.float32); O.embed(ref, inp["src"])
+    for off_d, off_s in ((1, 0), (0, 3), (5, 1)):
+        dst = _poisoned(inp["dst_shape"], np.float32, off_d)
+        T.embed(dst, _dev(inp["src"], off_s))
+        assert_bits_equal(dst, ref)
+
+
 def test_C3_expected_value_full():
     p = make_inputs("C3")["p"]
     ref, plain = O.expected_value(p, with_plain=True)

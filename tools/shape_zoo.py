@@ -37,8 +37,8 @@ def timed(fn, reps=5):
     return sorted(ts)[len(ts) // 2]
 
 
-def embed_case(name, dst_shape, src_shape, dtype=torch.float32, off=0):
-    src = torch.rand(src_shape, dtype=dtype, device=dev)
+def embed_case(name, dst_shape, src_shape, dtype=torch.float32, off=0, soff=0):
+    src = torch.rand(math.prod(src_shape) + soff, dtype=dtype, device=dev)[soff:].view(src_shape)
     n = math.prod(dst_shape)
     buf = torch.empty(n + off, dtype=dtype, device=dev)
     dst = buf[off:].view(dst_shape)
@@ -47,23 +47,26 @@ def embed_case(name, dst_shape, src_shape, dtype=torch.float32, off=0):
     nbytes = (math.prod(min(a, b) for a, b in zip(src_shape, dst_shape)) + n) * esz
     d = len(dst_shape)
     plan = T.triot_plan_describe(0, [dst_shape, src_shape], None, d,
-                                 0 if dtype == torch.float32 else 1, 0, (off * esz % 32, 0, 0))
+                                 0 if dtype == torch.float32 else 1, 0,
+                                 (off * esz % 32, soff * esz % 32, 0))
     print(json.dumps({"case": name, "op": "embed", "us": round(ms * 1e3, 1),
                       "gbs": round(nbytes / ms / 1e6, 1), "V": plan["V"], "D": plan["D"],
                       "geom": "rows" if plan["rows"] else "flat" if plan["flat"] else "vec",
                       "vec": [t["vec"] for t in plan["t"]]}), flush=True)
 
 
-def binary_case(name, a_shape, b_shape, dtype=torch.float64):
-    a = torch.rand(a_shape, dtype=dtype, device=dev)
+def binary_case(name, a_shape, b_shape, dtype=torch.float64, aoff=0, coff=0):
+    a = torch.rand(math.prod(a_shape) + aoff, dtype=dtype, device=dev)[aoff:].view(a_shape)
     b = torch.rand(b_shape, dtype=dtype, device=dev)
     ish = tuple(min(x, y) for x, y in zip(a_shape, b_shape))
-    c = torch.empty(ish, dtype=dtype, device=dev)
+    c = torch.empty(math.prod(ish) + coff, dtype=dtype, device=dev)[coff:].view(ish)
     ms = timed(lambda: T.apply_binary(a, b, "mul", out=c))
     nbytes = 3 * math.prod(ish) * a.element_size()
     d = len(ish)
+    esz = a.element_size()
     plan = T.triot_plan_describe(1, [None, a_shape, b_shape], None, d,
-                                 0 if dtype == torch.float32 else 1, 2)
+                                 0 if dtype == torch.float32 else 1, 2,
+                                 (coff * esz % 32, aoff * esz % 32, 0))
     print(json.dumps({"case": name, "op": "binary", "us": round(ms * 1e3, 1),
                       "gbs": round(nbytes / ms / 1e6, 1), "V": plan["V"], "D": plan["D"],
                       "geom": "rows" if plan["rows"] else "flat" if plan["flat"] else "vec",
@@ -96,6 +99,12 @@ if "--rows" in sys.argv:   # short odd rows: row windows vs flat vectors (run wi
     embed_case("rows: crop f32 (4096,512,3) <- (4100,600,7)", (4096, 512, 3), (4100, 600, 7))
     embed_case("rows: embed f32 (4096,4096,5) <- same, dst misaligned", (4096, 4096, 5),
                (4096, 4096, 5), off=1)
+    embed_case("rows: C2 dst misaligned by 1 element", (512,) * 3, (384,) * 3, off=1)
+    embed_case("rows: C2 src misaligned by 1 element", (512,) * 3, (384,) * 3, soff=1)
+    embed_case("rows: f64 pad (128)^4 from (100)^4, dst misaligned", (128,) * 4, (100,) * 4,
+               dtype=torch.float64, off=1)
+    binary_case("rows: binary f64 (64)^4 vs (80)^4, c misaligned", (64,) * 4, (80,) * 4, coff=1)
+    binary_case("rows: binary f64 (64)^4 vs (80)^4, a misaligned", (64,) * 4, (80,) * 4, aoff=1)
     binary_case("rows: binary f64 (3000,3001,7) x (3001,3000,7)", (3000, 3001, 7), (3001, 3000, 7))
     binary_case("rows: binary f32 (4000,4001,3) x (4001,4000,3)", (4000, 4001, 3), (4001, 4000, 3),
                 dtype=torch.float32)
