@@ -306,7 +306,9 @@ TRIOT_API int triot_plan_describe(int op, const int64_t* const* shapes, const in
  * 1 = grid stride, 2 / 3 = the expected value's bulk-copy (cp.async.bulk + mbarrier) pipeline
  * with 32 KB / 16 KB stages (other ops treat 2 and 3 as automatic), 4 = chunk per warp with the
  * expected value's block partials summed by a second kernel instead of the last block (other
- * ops treat 4 as 0); blocks_per_sm: 0 = the default for the mode.  Results are bit-identical under every
+ * ops treat 4 as 0), 5 = automatic without row windows (short odd rows and misaligned outputs
+ * take flat vectors / element accesses instead; A/B measurements); blocks_per_sm: 0 = the
+ * default for the mode.  Results are bit-identical under every
  * policy for embed and binary; the expected value's summation order follows the policy (it
  * stays deterministic for a fixed policy).  Used by tools/tune.py; not needed otherwise.
  */
