@@ -350,7 +350,19 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // flat vectors: when no vector width fits the innermost extent (odd extents: 3, 5, 7, 999),
   // take V consecutive elements of the flattened counter instead of one element per lane, for
   // the ops that have flat kernels.  The counter-dense tensors then still get full-width access.
-  const uint64_t rows_max = !g_rows_on ? 0 : g.op == OP_EMBED ? kRowsMaxEmbed : kRowsMaxBinary;
+  // Flat vectors store 32 B at a time only into an output dense in the counter and 32-B
+  // aligned; any other output (a view window, a misaligned base) takes row windows up to
+  // kRowsMaxLong, whose lane-consecutive element stores coalesce at any alignment.
+  bool out_flat_vec = ((uintptr_t)g.t[0].ptr % 32) == 0;
+  {
+    uint64_t hs = 1;
+    for (int k = na - 1; k >= 0; --k) {
+      if (ax[k].sig[0] != hs) out_flat_vec = false;
+      hs *= ax[k].n;
+    }
+  }
+  uint64_t rows_max = !g_rows_on ? 0 : g.op == OP_EMBED ? kRowsMaxEmbed : kRowsMaxBinary;
+  if (g_rows_on && !out_flat_vec) rows_max = kRowsMaxLong;
   if (cc[best].V == 1 && vmax > 1 && g.rows_ok && nl >= 3 && nl <= rows_max) {
     plan_rows(g, ax, na, nt, bounds);
     return;

@@ -536,21 +536,37 @@ def test_row_windows_for_misaligned_outputs():
     assert not p["rows"]                                   # rows over 4096: vector plan
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(10))
 def test_model_misaligned_output_rows_vs_oracle(seed):
     """Row windows planned for misaligned outputs (long rows, one window per group) run through
     the kernel model bit-exact against the oracle."""
     rng = np.random.default_rng(8000 + seed)
     d = int(rng.integers(1, 4))
-    n = int(rng.choice([8, 16, 40, 256, 300]))
+    n = int(rng.choice([8, 16, 40, 45, 256, 300, 383]))
     dst_shape = random_shape(rng, d - 1, 4000 // n + 2, lo=1, hi=12) + (n,) if d > 1 else (n,)
     src_shape = tuple(max(1, s + int(rng.integers(-2, 3))) for s in dst_shape)
     src = random_values(rng, src_shape, "f32", "normal")
+    region = seed % 2 == 1
     ref = np.full(dst_shape, -7.0, dtype=np.float32)
-    O.embed(ref, src)
-    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, F32, 0, ptr_mod32=(4, 0, 0),
-                                 mode=0, warps=int(rng.integers(1, 6)))
+    O.embed(ref, src, region_only=region)
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, F32, 1 if region else 0,
+                                 ptr_mod32=(4, 0, 0), mode=0, warps=int(rng.integers(1, 6)))
     assert desc["rows"] or desc["V"] == 1, desc
     out = np.full(dst_shape, -7.0, dtype=np.float32)
     kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
     np.testing.assert_array_equal(_bits(out), _bits(ref))
+
+
+def test_row_windows_for_odd_rows_into_non_dense_outputs():
+    """Odd rows longer than the dense thresholds still take row windows when the output is not
+    dense in the counter (region-only embed, a c larger than the iteration) or misaligned."""
+    p = T.triot_plan_describe(0, [(40, 383), (40, 383)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
+    assert not p["rows"]                                   # same shapes merge: one long axis
+    p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 0)
+    assert p["flat"]                                       # dense aligned dst: flat vectors
+    p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
+    assert p["rows"]                                       # misaligned dst: row windows
+    p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 1)
+    assert p["rows"] and not p["t"][0]["vec"]              # region only: dst rows of 383 > 380
+    p = T.triot_plan_describe(1, [(40, 200), (40, 99), (40, 99)], (40, 99), 2, F64, 2)
+    assert p["rows"] and not p["t"][0]["vec"]              # c wider than the iteration

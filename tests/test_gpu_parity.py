@@ -381,6 +381,8 @@ def test_no_writes_outside_outputs(dtype):
         dst_shape = tuple(max(1, s + int(rng.integers(-2, 4))) for s in src_shape)
         if case % 3 == 0:
             dst_shape = dst_shape[:-1] + (int(rng.choice([1, 2, 3, 4])),)
+        elif case % 3 == 1:   # short odd rows: row windows (element-aligned bases too)
+            dst_shape = dst_shape[:-1] + (int(rng.choice([5, 7, 13, 31])),)
         if math.prod(dst_shape) > 100000:
             dst_shape = tuple(min(a, b) for a, b in zip(dst_shape, src_shape))
         src = rng.standard_normal(src_shape).astype(npdt)
@@ -742,3 +744,32 @@ def test_row_windows_large_and_policies():
             assert_bits_equal(out, refb)
     finally:
         T.triot_set_launch_policy(-1, 0)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_row_windows_long_odd_rows_non_dense_outputs(dtype):
+    """Odd rows past the dense thresholds into non-dense outputs (a view window at an odd
+    offset, region-only embed, c wider than the iteration), bit-exact against the oracle."""
+    rng = np.random.default_rng(97)
+    src = rng.standard_normal((41, 19, 383)).astype(dtype)
+    # view: src window (37,17,381) at (1,1,1) into dst base (45,23,401) at (3,5,7)
+    dbase = np.full((45, 23, 401), 3.0, dtype=dtype)
+    ref = dbase.copy()
+    ref[3:40, 5:22, 7:388] = src[1:38, 1:18, 1:382]
+    db = _dev(dbase)
+    T.embed_view(T.View(db, (3, 5, 7), (37, 17, 381)), T.View(_dev(src), (1, 1, 1), (37, 17, 381)))
+    assert_bits_equal(db, ref)
+    # region only, dst rows of 401 over src rows of 383 (pre-filled dst keeps its padding)
+    dst = _dev(np.full((45, 23, 401), 3.0, dtype=dtype), 1)
+    ref = np.full((45, 23, 401), 3.0, dtype=dtype)
+    O.embed(ref, src, region_only=True)
+    T.embed(dst, _dev(src), region_only=True)
+    assert_bits_equal(dst, ref)
+    # binary, c wider than the iteration (40, 17, 99)
+    a = rng.standard_normal((40, 17, 99)).astype(dtype)
+    b = rng.standard_normal((41, 18, 99)).astype(dtype)
+    ref = np.full((40, 17, 200), 9.0, dtype=dtype)
+    O.apply_binary(a, b, "sub", iter_shape=(40, 17, 99), out=ref)
+    c = _dev(np.full((40, 17, 200), 9.0, dtype=dtype))
+    T.apply_binary(_dev(a), _dev(b), "sub", out=c, iter_shape=(40, 17, 99))
+    assert_bits_equal(c, ref)

@@ -113,6 +113,37 @@ if "--rows" in sys.argv:   # short odd rows: row windows vs flat vectors (run wi
     binary_case("rows: binary f32 (2000,2000,63) x (2001,2000,64)", (2000, 2000, 63),
                 (2001, 2000, 64), dtype=torch.float32)
     sys.exit(0)
+if "--views" in sys.argv:   # NEXT-1 views: windows at aligned and odd offsets
+    def view_ev(name, base_shape, start, shape, dtype=torch.float64):
+        base = torch.rand(base_shape, dtype=dtype, device=dev)
+        v = T.View(base, start, shape)
+        out = torch.empty(len(shape), dtype=torch.float64, device=dev)
+        ms = timed(lambda: T.expected_value_view(v, out=out))
+        nbytes = math.prod(shape) * base.element_size()
+        print(json.dumps({"case": name, "op": "ev_view", "us": round(ms * 1e3, 1),
+                          "gbs": round(nbytes / ms / 1e6, 1)}), flush=True)
+
+    def view_embed(name, dbase, dstart, sbase, sstart, shape, dtype=torch.float32):
+        db = torch.zeros(dbase, dtype=dtype, device=dev)
+        sb = torch.rand(sbase, dtype=dtype, device=dev)
+        dv, sv = T.View(db, dstart, shape), T.View(sb, sstart, shape)
+        ms = timed(lambda: T.embed_view(dv, sv))
+        nbytes = 2 * math.prod(shape) * db.element_size()
+        print(json.dumps({"case": name, "op": "embed_view", "us": round(ms * 1e3, 1),
+                          "gbs": round(nbytes / ms / 1e6, 1)}), flush=True)
+
+    view_ev("views: EV f64 (256)^3 window of (264)^3 at (8,8,8)", (264,) * 3, (8, 8, 8), (256,) * 3)
+    view_ev("views: EV f64 (256)^3 window of (264)^3 at (5,5,5)", (264,) * 3, (5, 5, 5), (256,) * 3)
+    view_ev("views: EV f64 (255)^3 window of (264)^3 at (5,5,5)", (264,) * 3, (5, 5, 5), (255,) * 3)
+    view_ev("views: EV f32 (500)^3 window of (512)^3 at (3,3,3)", (512,) * 3, (3, 3, 3), (500,) * 3,
+            dtype=torch.float32)
+    view_embed("views: embed f32 (384)^3 into (512)^3 at (64,64,64)", (512,) * 3, (64,) * 3,
+               (384,) * 3, (0,) * 3, (384,) * 3)
+    view_embed("views: embed f32 (384)^3 into (512)^3 at (63,63,63)", (512,) * 3, (63,) * 3,
+               (384,) * 3, (0,) * 3, (384,) * 3)
+    view_embed("views: embed f32 window (383)^3 of (400)^3 at (1,1,1) into (512)^3 at (5,5,5)",
+               (512,) * 3, (5,) * 3, (400,) * 3, (1,) * 3, (383,) * 3)
+    sys.exit(0)
 if "--big" in sys.argv:   # odd innermost extents at sizes past the launch-bound regime
     embed_case("big: embed f32 (3000,3000,7) <- (2900,2900,5)", (3000, 3000, 7), (2900, 2900, 5))
     embed_case("big: embed f32 (8192,4096,3) <- (8000,4000,3)", (8192, 4096, 3), (8000, 4000, 3))
