@@ -773,3 +773,30 @@ def test_row_windows_long_odd_rows_non_dense_outputs(dtype):
     c = _dev(np.full((40, 17, 200), 9.0, dtype=dtype))
     T.apply_binary(_dev(a), _dev(b), "sub", out=c, iter_shape=(40, 17, 99))
     assert_bits_equal(c, ref)
+
+
+@pytest.mark.slow
+def test_u64_index_path_row_windows():
+    """The 64-bit-index row-window instance: embed f32 (613566757, 7) <- (613566757, 5), 4.3 G
+    destination elements, src generated by a formula, checked on the device in slabs."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 45e9:
+        pytest.skip("needs ~32 GB free")
+    rows = 613566757
+    desc = T.triot_plan_describe(0, [(rows, 7), (rows, 5)], None, 2, T.TRIOT_F32, 0)
+    assert desc["idx64"] and desc["rows"]
+    src = torch.empty((rows, 5), dtype=torch.float32, device=DEV)
+    flat = src.view(-1)
+    for s0 in range(0, flat.numel(), 1 << 29):
+        s1 = min(flat.numel(), s0 + (1 << 29))
+        flat[s0:s1] = (torch.arange(s0, s1, dtype=torch.int64, device=DEV) % 1021).to(
+            torch.float32) / 8
+    dst = torch.full((rows, 7), float("nan"), dtype=torch.float32, device=DEV)
+    T.embed(dst, src)
+    torch.cuda.synchronize()
+    for r0 in range(0, rows, 1 << 26):
+        r1 = min(rows, r0 + (1 << 26))
+        assert torch.equal(dst[r0:r1, :5], src[r0:r1])
+        assert int(torch.count_nonzero(dst[r0:r1, 5:])) == 0
+    del dst, src, flat
+    torch.cuda.empty_cache()
