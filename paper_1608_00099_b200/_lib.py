@@ -119,11 +119,21 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
+_SHAPES: dict = {}   # shape tuple -> its int64_t[] (the C side only reads it): ~2 us per call saved
+
+
 def _shape(s):
     if s is None:
         return None
-    s = [int(x) for x in s]
-    return (ctypes.c_int64 * max(1, len(s)))(*s)
+    try:
+        return _SHAPES[s]
+    except (KeyError, TypeError):
+        pass
+    t = tuple(int(x) for x in s)
+    arr = (ctypes.c_int64 * max(1, len(t)))(*t)
+    if len(_SHAPES) < 4096 and not isinstance(s, list):
+        _SHAPES[t] = arr
+    return arr
 
 
 def check(status: int) -> None:

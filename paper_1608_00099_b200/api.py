@@ -37,7 +37,12 @@ def _check_tensor(name: str, t, device=None):
 
 
 def _stream(device) -> int:
-    return _torch().cuda.current_stream(device).cuda_stream
+    torch = _torch()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)   # the same handle, ~1 us cheaper
+    if raw is not None:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        return raw(idx)
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 class View:
