@@ -800,3 +800,32 @@ def test_u64_index_path_row_windows():
         assert int(torch.count_nonzero(dst[r0:r1, 5:])) == 0
     del dst, src, flat
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("seed", range(6))
+def test_ev_odd_innermost_vs_oracle(seed, dtype):
+    """Expected value over short odd innermost extents (flat vectors, closed-form in-vector
+    weights): integer-valued p exact, real p within 1e-12, mass included, deterministic, and the
+    same under policy mode 5."""
+    rng = np.random.default_rng(900 + seed)
+    d = int(rng.integers(1, 7))
+    n = int(rng.choice([3, 5, 7, 9, 11, 13, 15]))
+    outer = random_shape(rng, d - 1, 200000 // n, lo=1, hi=30 if d <= 3 else 9) if d > 1 else ()
+    shape = outer + (n,)
+    pi = rng.integers(0, 256, size=shape).astype(dtype)
+    m = T.expected_value(_dev(pi), with_mass=True).cpu().numpy()
+    np.testing.assert_array_equal(m[:-1], O.expected_value(pi))
+    assert m[-1] == float(pi.astype(np.float64).sum())
+    pr = rng.random(shape).astype(dtype)
+    ref = O.expected_value(pr)
+    m1 = T.expected_value(_dev(pr)).cpu().numpy()
+    m2 = T.expected_value(_dev(pr)).cpu().numpy()
+    assert _bits(m1).tolist() == _bits(m2).tolist()
+    assert np.all(np.abs(m1 - ref) <= 1e-12 * np.abs(ref))
+    try:
+        T.triot_set_launch_policy(5, 0)
+        mf = T.expected_value(_dev(pr)).cpu().numpy()
+    finally:
+        T.triot_set_launch_policy(-1, 0)
+    assert np.all(np.abs(mf - ref) <= 1e-12 * np.abs(ref))
