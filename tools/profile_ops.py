@@ -39,6 +39,15 @@ def main():
             torch.cuda.synchronize()
             print(name, "ok", flush=True)
             continue
+        if name in ("EV7", "EVF32"):   # expected value over odd innermost extents
+            sh, dt = ((7,) * 9, torch.float64) if name == "EV7" else ((3000, 3000, 7), torch.float32)
+            p_ = torch.rand(sh, dtype=dt, device=dev)
+            o_ = torch.empty(len(sh), dtype=torch.float64, device=dev)
+            for _ in range(a.reps):
+                T.expected_value(p_, out=o_)
+            torch.cuda.synchronize()
+            print(name, "ok", flush=True)
+            continue
         if name in ("ROWS7", "ROWS33", "ROWSB63"):   # short odd rows (row-window kernels)
             if name == "ROWSB63":
                 a_ = torch.rand((2000, 2000, 63), device=dev)
