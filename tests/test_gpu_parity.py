@@ -829,3 +829,44 @@ def test_ev_odd_innermost_vs_oracle(seed, dtype):
     finally:
         T.triot_set_launch_policy(-1, 0)
     assert np.all(np.abs(mf - ref) <= 1e-12 * np.abs(ref))
+
+
+def test_fuzz_embed_binary_geometries():
+    """A randomized sweep over every geometry the planner can pick (32-B / 16-B / element
+    vectors, collapsed rows, flat vectors, row windows, zero runs, 64 dims of odd and even
+    extents), with element-aligned bases, region-only embeds, wide outputs and random launch
+    policies: every output bit-exact against the oracle."""
+    rng = np.random.default_rng(2024)
+    policies = [(-1, 0), (0, 1), (0, 3), (1, 2), (5, 0)]
+    try:
+        for case in range(160):
+            dtype = np.float32 if case % 2 else np.float64
+            d = int(rng.integers(1, 9))
+            shape = random_shape(rng, d, 20000, lo=1, hi=40 if d <= 2 else (12 if d <= 4 else 5))
+            if case % 5 == 0:
+                shape = shape[:-1] + (int(rng.choice([3, 5, 7, 9, 31, 33, 65])),)
+            src_shape = tuple(max(1, s + int(rng.integers(-2, 3))) for s in shape)
+            T.triot_set_launch_policy(*policies[case % len(policies)])
+            region = case % 3 == 1
+            off_d, off_s = int(rng.integers(0, 3)), int(rng.integers(0, 2))
+            src = rng.standard_normal(src_shape).astype(dtype)
+            ref = np.full(shape, np.nan, dtype=dtype)
+            O.embed(ref, src, region_only=region)
+            dst = _poisoned(shape, dtype, off_d)
+            T.embed(dst, _dev(src, off_s), region_only=region)
+            got = dst.cpu().numpy()
+            if region:   # untouched elements stay NaN-poisoned on both sides
+                assert np.array_equal(np.isnan(got), np.isnan(ref))
+                got, ref = np.nan_to_num(got), np.nan_to_num(ref)
+            assert np.array_equal(_bits(got), _bits(ref)), (case, shape, src_shape, region)
+            a = rng.standard_normal(tuple(s + int(rng.integers(0, 2)) for s in shape)).astype(dtype)
+            b = rng.standard_normal(tuple(s + int(rng.integers(0, 2)) for s in shape)).astype(dtype)
+            cs = tuple(s + int(rng.integers(0, 2)) for s in shape) if case % 4 == 0 else shape
+            op = ["add", "sub", "mul", "div"][case % 4]
+            refc = np.full(cs, 9.0, dtype=dtype)
+            O.apply_binary(a, b, op, iter_shape=shape, out=refc)
+            c = _dev(np.full(cs, 9.0, dtype=dtype), int(rng.integers(0, 2)))
+            T.apply_binary(_dev(a, int(rng.integers(0, 2))), _dev(b), op, out=c, iter_shape=shape)
+            assert_bits_equal(c, refc)
+    finally:
+        T.triot_set_launch_policy(-1, 0)
