@@ -50,6 +50,9 @@ struct Desc {
   IDX bnd[TRIOT_MAXD];   // embed: digit k (k < D-1) is in bounds iff u[k] < bnd[k]
   uint32_t fdm[TRIOT_MAXD];  // fast-division magic multiplier per digit extent (IDX = u32)
   uint32_t fds[TRIOT_MAXD];  // fast-division shifts: s1 | s2 << 8
+  uint32_t pow2;             // 1: every digit extent 1..D-1 is a power of two (decode by shifts)
+  uint8_t lg[TRIOT_MAXD];    // log2 of each digit extent when pow2
+  IDX lin0;                  // tensor 0 offset of digit vector index v is v * lin0 (0: use Horner)
   IDX nvec;              // number of vectors W
   IDX nelem;             // counter elements N (flat vectors: the last vector may be partial)
   // work decomposition: warp w starts at vector w*wmul + lane, owns

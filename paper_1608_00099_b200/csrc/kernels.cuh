@@ -145,22 +145,42 @@ __device__ __forceinline__ uint64_t divq<uint64_t>(uint64_t n, uint64_t e, uint3
   return n / e;
 }
 
-// Decode vector index v into digits, then Horner offsets per tensor (Alg 2).
+// Mixed-radix digits of v (P:139's %-and-/): a mask and a shift per digit when every extent
+// is a power of two (d.pow2, uniform), else the multiply-high division.
+template <int D, typename IDX>
+__device__ __forceinline__ void decode_digits(const Desc<IDX>& d, IDX v, IDX (&u)[D]) {
+  if (d.pow2) {
+#pragma unroll
+    for (int k = D - 1; k >= 1; --k) {
+      u[k] = v & (d.ext[k] - IDX(1));
+      v >>= d.lg[k];
+    }
+  } else {
+#pragma unroll
+    for (int k = D - 1; k >= 1; --k) {
+      IDX q = divq<IDX>(v, d.ext[k], d.fdm[k], d.fds[k]);
+      u[k] = v - q * d.ext[k];
+      v = q;
+    }
+  }
+  u[0] = v;
+}
+
+// Decode vector index v into digits, then Horner offsets per tensor (Alg 2) -- for a
+// tensor 0 dense in the digit space (d.lin0 != 0) Horner reduces to v * lin0.
 template <int D, int NT, bool BOUNDS, typename IDX, bool ALLB = false>
 __device__ __forceinline__ void odo_start(const Desc<IDX>& d, IDX v, IDX (&u)[D],
                                           IDX (&off)[NT], uint32_t& oob) {
-#pragma unroll
-  for (int k = D - 1; k >= 1; --k) {
-    IDX q = divq<IDX>(v, d.ext[k], d.fdm[k], d.fds[k]);
-    u[k] = v - q * d.ext[k];
-    v = q;
-  }
-  u[0] = v;
+  decode_digits<D, IDX>(d, v, u);
 #pragma unroll
   for (int x = 0; x < NT; ++x) {
     IDX o = 0;
+    if (x == 0 && d.lin0) {
+      o = v * d.lin0;
+    } else {
 #pragma unroll
-    for (int k = 0; k < D; ++k) o += u[k] * d.t[x].sig[k];
+      for (int k = 0; k < D; ++k) o += u[k] * d.t[x].sig[k];
+    }
     off[x] = o;
   }
   oob = 0;
@@ -853,13 +873,7 @@ __device__ __forceinline__ void ev_load(const TensorAcc<IDX>& t, IDX v, uint32_t
 
 template <int D, typename IDX>
 __device__ __forceinline__ void ev_decode(const Desc<IDX>& d, IDX v, IDX (&u)[D]) {
-#pragma unroll
-  for (int k = D - 1; k >= 1; --k) {
-    IDX q = divq<IDX>(v, d.ext[k], d.fdm[k], d.fds[k]);
-    u[k] = v - q * d.ext[k];
-    v = q;
-  }
-  u[0] = v;
+  decode_digits<D, IDX>(d, v, u);
 }
 
 // One vector: S += sum_e p_e; the in-vector row (e >> lgL) and column (e & (L-1)) weights

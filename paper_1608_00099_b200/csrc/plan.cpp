@@ -471,6 +471,17 @@ static void finish_geometry(Geom& g, int nt) {
     uint32_t e = g.ext[k] >= 1 && g.ext[k] <= 0xffffffffull ? (uint32_t)g.ext[k] : 1;
     fastdiv_magic(e, &g.fdm[k], &g.fds[k]);
   }
+  // decode by shifts when every digit extent the decode divides by is a power of two
+  g.pow2 = true;
+  for (int k = 1; k < D; ++k) {
+    const uint64_t e = g.ext[k];
+    if (e == 0 || (e & (e - 1)) != 0) g.pow2 = false;
+    g.lg[k] = (uint8_t)ilog2(e);
+  }
+  // tensor 0 dense in the digit space: its offset of digit vector v is v * (last digit stride)
+  g.lin0 = g.t[0].sig[D - 1];
+  for (int k = 0; k + 1 < D; ++k)
+    if (g.t[0].sig[k] != g.t[0].sig[k + 1] * g.ext[k + 1]) g.lin0 = 0;
   // 5. index width: 32-bit iff every offset, count and vector index fits, with room for the
   //    largest per-batch advance (K steps of up to 2^20 vectors)
   uint64_t mx = g.N + (1ull << 24) * V;
@@ -1083,7 +1094,7 @@ std::string describe(const Geom& g) {
            "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"flat\":%s,\"N\":%llu,\"nvec\":%llu,"
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,"
-           "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,",
+           "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,\"pow2\":%s,\"lin0\":%llu,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
@@ -1092,7 +1103,7 @@ std::string describe(const Geom& g) {
            (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,
            (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots, g.zmask,
            g.rows ? "true" : "false", (unsigned long long)g.rowlen, (unsigned long long)g.rmag,
-           (unsigned long long)g.rwin);
+           (unsigned long long)g.rwin, g.pow2 ? "true" : "false", (unsigned long long)g.lin0);
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

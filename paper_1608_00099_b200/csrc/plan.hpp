@@ -42,6 +42,9 @@ struct Geom {
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
+  bool pow2 = false;                // every digit extent 1..D-1 a power of two
+  uint8_t lg[TRIOT_MAXD] = {};
+  uint64_t lin0 = 0;                // tensor 0 dense in the digit space: offset = v * lin0
   uint64_t nvec = 0, nsteps = 0;
   uint64_t wmul = 32, wspan = 32, dv = 32;   // decomposition (set_decomposition)
   int mode = 0;                              // 0 = chunk, 1 = stride, 2 = block chunk
@@ -115,7 +118,10 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
     d.bnd[k] = (IDX)g.bnd[k];
     d.fdm[k] = g.fdm[k];
     d.fds[k] = g.fds[k];
+    d.lg[k] = g.lg[k];
   }
+  d.pow2 = g.pow2 ? 1u : 0u;
+  d.lin0 = (IDX)g.lin0;
   d.nvec = (IDX)g.nvec;
   d.nelem = (IDX)g.N;
   d.wmul = (IDX)g.wmul;

@@ -33,12 +33,15 @@ def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
     slots = [0.0] * (D + 1)
 
     def start(v):
+        v0 = v
         u = [0] * D
         for k in range(D - 1, 0, -1):
             u[k] = v % ext[k]
             v //= ext[k]
         u[0] = v
         off = [W(sum(u[k] * T[x]["sig"][k] for k in range(D))) for x in range(nt)]
+        if desc.get("lin0"):   # the kernel's shortcut for a tensor 0 dense in the digit space
+            assert off[0] == W(v0 * desc["lin0"]), (off[0], v0, desc["lin0"])
         oob = 0
         for k in range(D - 1):
             oob |= int(u[k] >= bnd[k]) << k

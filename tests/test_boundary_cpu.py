@@ -570,3 +570,20 @@ def test_row_windows_for_odd_rows_into_non_dense_outputs():
     assert p["rows"] and not p["t"][0]["vec"]              # region only: dst rows of 383 > 380
     p = T.triot_plan_describe(1, [(40, 200), (40, 99), (40, 99)], (40, 99), 2, F64, 2)
     assert p["rows"] and not p["t"][0]["vec"]              # c wider than the iteration
+
+
+def test_pow2_decode_and_linear_tensor0_flags():
+    """The plan flags shift decoding when every digit extent is a power of two, and the linear
+    offset of a tensor 0 dense in the digit space (C2, C3, C5 yes; C4's 24 is not a power of
+    two; a wide c is not dense)."""
+    c5 = T.triot_plan_describe(0, [(4,) * 14, (3,) * 14], None, 14, F32, 0)
+    assert c5["pow2"] and c5["lin0"] == 8
+    c2 = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0)
+    assert c2["pow2"] and c2["lin0"] == 8
+    c4 = T.triot_plan_describe(1, [None, (32, 48, 24, 40, 36), (40, 32, 32, 32, 32)],
+                               (32, 32, 24, 32, 32), 5, F64, 2)
+    assert not c4["pow2"] and c4["lin0"] == 4
+    wide = T.triot_plan_describe(1, [(8, 40), (8, 32), (8, 32)], (8, 32), 2, F64, 2)
+    assert wide["lin0"] == 0
+    ev = T.triot_plan_describe(2, [(16,) * 6], None, 6, F64, 0)
+    assert ev["pow2"]
