@@ -870,3 +870,32 @@ def test_fuzz_embed_binary_geometries():
             assert_bits_equal(c, refc)
     finally:
         T.triot_set_launch_policy(-1, 0)
+
+
+def test_sharded_expected_value_over_nccl():
+    """The slab-sharded expected value (paper_1608_00099_b200/parallel.py) with the real kernel
+    and the NCCL backend (world size 1 on this one-GPU box: the collective path runs for real),
+    equal to the single-call result within 1e-12 and exact on integer data."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1608_00099_b200 import parallel as P
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        p = make_inputs("C3")["p"]
+        pi = np.random.default_rng(3).integers(0, 256, size=(9, 7, 16, 8)).astype(np.float64)
+        for arr, exact in ((pi, True), (p, False)):
+            ref = O.expected_value(arr)
+            lo, hi = P.slab_rows(arr.shape[0], 1, 0)
+            got = P.expected_value_sharded(_dev(arr[lo:hi].copy()), lo).cpu().numpy()
+            if exact:
+                np.testing.assert_array_equal(got, ref)
+            else:
+                assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref))
+    finally:
+        dist.destroy_process_group()
