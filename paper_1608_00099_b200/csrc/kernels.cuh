@@ -606,10 +606,12 @@ __global__ void __launch_bounds__(kBlock) binary_flat_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ row windows (short odd rows)
-// When the innermost extent n is odd and short (3, 5, 7, ... <= 31 / 64), or the output's base is
-// only element-aligned (rows <= 4096), a vector is one counter row.  A warp takes a group of W windows of 32 rows (W = d.rwin = 8, fewer for rows over 31
-// elements): lane i steps the odometer over rows b + i, b + 32 + i, ... (Alg 2 once,
-// then the carry deltas) and parks each row's offsets in the warp's shared-memory row table.
+// When the innermost extent n is odd and short (3, 5, 7, ... up to 31 for embed, 64 for binary),
+// or the output is not dense-and-aligned (a view, a misaligned base; rows up to 4096), a vector
+// is one counter row.  A warp takes a group of W windows of 32 rows (W = d.rwin = ceil(16 / n)
+// <= 8, so a group holds >= 16 elements per lane): lane i steps the odometer over rows b + i,
+// b + 32 + i, ... (Alg 2 once, then the carry deltas) and parks each row's offsets in the
+// warp's shared-memory row table.
 // The warp then sweeps the group's rows * n elements lane by lane: element e = 32 j + lane
 // lies in row r = e / n (one multiply-high by the plan's magic rmag, exact while e n < 2^32) and
 // column e - r n.  The table holds each tensor's offset rebased to the element index,
