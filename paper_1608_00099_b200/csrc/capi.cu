@@ -170,11 +170,13 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   return TRIOT_OK;
 }
 
-// Every kernel is launched with programmatic stream serialization (PDL): it may be scheduled
-// while the previous kernel on the stream drains; it waits (griddepcontrol.wait) before its
-// first global memory access, so results are as with plain stream order.
+// Every streaming kernel is launched with programmatic stream serialization (PDL): it may be
+// scheduled while the previous kernel on the stream drains; it waits (griddepcontrol.wait)
+// before its first global memory access, so results are as with plain stream order.  (B200,
+// back to back in a CUDA graph: C3 5.40 vs 5.25 TB/s, C1 1.75 vs 2.03 us per op with / without;
+// the latency-bound convolution is launched without it, see triot_naive_convolve.)
 int launch_pdl(const void* fn, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-               void** args) {
+               void** args, bool pdl = true) {
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(grid);
@@ -185,7 +187,7 @@ int launch_pdl(const void* fn, unsigned grid, unsigned block, size_t smem, cudaS
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC");
   return TRIOT_OK;
@@ -472,7 +474,11 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   const unsigned block = group ? TRIOT_CONV_BLOCK : kConvLaneBlock;
   const uint64_t per_block = group ? TRIOT_CONV_BLOCK / TRIOT_CONV_GROUP : kConvLaneBlock;
   unsigned grid = (unsigned)((g.nvec + per_block - 1) / per_block);
-  st = launch_pdl(fn, grid, block, use_smem ? smem : 0, (cudaStream_t)cuda_stream, args);
+  // Plain stream order, not PDL: a successor's blocks made resident early by the programmatic
+  // launch slow this latency-bound kernel down (B200, 50 Benchmark-4 calls in a CUDA graph:
+  // 43.3 us per call with PDL, 24.0 us without); its griddepcontrol instructions are no-ops then.
+  st = launch_pdl(fn, grid, block, use_smem ? smem : 0, (cudaStream_t)cuda_stream, args,
+                  /*pdl=*/false);
   if (!st) clear_error();
   return st;
 }
