@@ -11,11 +11,13 @@ import sys
 WANT = [
     "Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "dram__bytes_read.sum",
     "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
-    "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
-    "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct",
+    # not in --set full: request them with --metrics (see profiles/README.md)
+    "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio",
+    "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio",
     "lts__d_sectors_fill_device.sum", "smsp__cycles_active.avg",
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
@@ -58,11 +60,12 @@ def evidence(res, configs):
         out.append({
             "config": cfg, "kernel": d.get("Kernel Name"), "us_cold": round(t_s * 1e6, 2),
             "dram_GBps": round((dr + dw) / t_s / 1e9, 1),
-            "dram_pct_of_peak": d.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "dram_pct_of_peak": d.get("dram__throughput.avg.pct_of_peak_sustained_elapsed") or
+            d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "overfetch_read": round(dr / rd, 3) if rd > 1000 else None,
             "write_completeness": round(dw / wr, 3) if wr > 1000 else None,
-            "bytes_per_sector_ld_pct": d.get("smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct"),
-            "bytes_per_sector_st_pct": d.get("smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct"),
+            "bytes_per_sector_ld": d.get("smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio"),
+            "bytes_per_sector_st": d.get("smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio"),
             "sectors_per_request_ld": round(sec_ld / req_ld, 2) if req_ld else None,
             "sectors_per_request_st": round(sec_st / req_st, 2) if req_st else None,
             "warp_inst_per_32B_vector": round(d["smsp__inst_executed.sum"] / nvec, 3),
