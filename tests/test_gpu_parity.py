@@ -839,10 +839,11 @@ def test_fuzz_embed_binary_geometries():
     rng = np.random.default_rng(2024)
     policies = [(-1, 0), (0, 1), (0, 3), (1, 2), (5, 0)]
     try:
-        for case in range(160):
+        for case in range(240):
             dtype = np.float32 if case % 2 else np.float64
-            d = int(rng.integers(1, 9))
-            shape = random_shape(rng, d, 20000, lo=1, hi=40 if d <= 2 else (12 if d <= 4 else 5))
+            d = int(rng.integers(1, 9)) if case % 8 else int(rng.integers(9, 17))
+            shape = random_shape(rng, d, 20000, lo=1, hi=40 if d <= 2 else (12 if d <= 4 else
+                                                                           (5 if d <= 8 else 3)))
             if case % 5 == 0:
                 shape = shape[:-1] + (int(rng.choice([3, 5, 7, 9, 31, 33, 65])),)
             src_shape = tuple(max(1, s + int(rng.integers(-2, 3))) for s in shape)
