@@ -86,6 +86,9 @@ struct Desc {
   // lane e % 32, row umulhi(e, rmag) = e / rowlen (rmag = 2^32 / rowlen + 1, exact for
   // e < 2^13); scols = the embed bound of the column.
   uint32_t rowlen, rmag, rwin;
+  // rows that are segments of a longer split axis (seglen = rowlen): the embed bound of the
+  // unsplit axis is segm, so segment s reads columns [0, clamp(segm - s rowlen, 0, rowlen))
+  IDX seglen, segm;
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
                                   // update: x, y, z
   void* out;             // EV: means (device)

@@ -695,10 +695,15 @@ __global__ void __launch_bounds__(kBlock) embed_rows_kernel(const __grid_constan
     for (int w = 0; w < W && b < vend; ++w, b += d.dv) {
       const uint32_t nr = (vend - b) < (IDX)32 ? (uint32_t)(vend - b) : 32u;
       const bool rd = (uint32_t)lane < nr && oob == 0;  // row reads src
-      any = any || (rd && m != 0);
+      IDX mr = m;  // columns of this row read from src
+      if (d.seglen) {  // a segment s of a split axis: clamp(segm - s n, 0, n)
+        const IDX s0 = u[D - 1] * n;
+        mr = d.segm > s0 ? (d.segm - s0 < n ? d.segm - s0 : n) : IDX(0);
+      }
+      any = any || (rd && mr != 0);
       const IDX r0 = (IDX)(32 * w + lane) * n;  // group element index of the row's first element
       ts[32 * w + lane].off = off[1] - r0 * tau1;
-      ts[32 * w + lane].lim = rd ? r0 + m : IDX(0);
+      ts[32 * w + lane].lim = rd ? r0 + mr : IDX(0);
       td[32 * w + lane] = off[0] - r0 * tau0;
       rows = 32u * (uint32_t)w + nr;
       odo_step<D, 2, true, IDX, true>(d, u, off, oob);

@@ -370,11 +370,40 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // The output (dst / c) cannot take wide stores although a vector width fits its rows -- its
   // base is only element-aligned (a view at an odd offset, a sliced buffer): element stores at a
   // 32-byte lane stride write partial sectors (C2 with dst offset by 4 B: 1.4 TB/s), so rows up
-  // to kRowsMaxLong take row windows, whose lane-consecutive accesses coalesce at any alignment.
-  if (cc[best].V > 1 && !cc[best].vec[0] && g.rows_ok && g_rows_on && nl >= 3 &&
-      nl <= kRowsMaxLong) {
-    plan_rows(g, ax, na, nt, bounds);
-    return;
+  // to kRowsMaxLong take row windows, whose lane-consecutive accesses coalesce at any alignment;
+  // longer rows (a fully merged copy) are cut into segments of a divisor L <= kRowsMaxLong.
+  const bool long_ok = g.rows_ok && g_rows_on && g.op != OP_EV && nl >= 3;
+  if ((cc[best].V > 1 && !cc[best].vec[0] && long_ok) ||
+      (cc[best].V == 1 && vmax > 1 && !out_flat_vec && long_ok)) {
+    // rows over 512 elements are cut into segments of a divisor L in [64, 512] when one
+    // exists: a warp step is 32 rows, so rows of thousands of elements leave too few warps
+    // (a merged 84 M-element copy in rows of 4,096: 640 warps, 1.3 TB/s)
+    uint64_t L = 0;
+    if (nl > 512)
+      for (uint64_t c = 512; c >= 64 && !L; --c)
+        if (nl % c == 0) L = c;
+    if (!L && nl <= kRowsMaxLong) {
+      plan_rows(g, ax, na, nt, bounds);
+      return;
+    }
+    if (L && na < TRIOT_MAXD) {
+      // split the innermost axis into (nl / L segments, L): a row is one segment; the embed
+      // bound m of the unsplit axis becomes a per-segment column bound (kernel: segm)
+      Axis sx[TRIOT_MAXD + 1];
+      for (int k = 0; k < na - 1; ++k) sx[k] = ax[k];
+      Axis seg = ax[na - 1], in = ax[na - 1];
+      seg.n = nl / L;
+      seg.bnd = seg.n;
+      for (int x = 0; x < nt; ++x) seg.sig[x] = ax[na - 1].sig[x] * L;
+      in.n = L;
+      in.bnd = L;
+      sx[na - 1] = seg;
+      sx[na] = in;
+      plan_rows(g, sx, na + 1, nt, bounds);
+      g.seglen = L;
+      g.segm = bounds ? ax[na - 1].bnd : nl;
+      return;
+    }
   }
   if (cc[best].V == 1 && vmax > 1 && g.flat_ok) {
     plan_flat(g, ax, na, nt, bounds, n);
@@ -1094,7 +1123,8 @@ std::string describe(const Geom& g) {
            "\"D\":%d,\"V\":%d,\"R\":%d,\"lgL\":%d,\"collapsed\":%s,\"flat\":%s,\"N\":%llu,\"nvec\":%llu,"
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,"
-           "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,\"pow2\":%s,\"lin0\":%llu,",
+           "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,\"pow2\":%s,\"lin0\":%llu,"
+           "\"seglen\":%llu,\"segm\":%llu,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
@@ -1103,7 +1133,8 @@ std::string describe(const Geom& g) {
            (unsigned long long)g.colmul, (unsigned long long)g.vfull, (unsigned long long)g.vany,
            (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots, g.zmask,
            g.rows ? "true" : "false", (unsigned long long)g.rowlen, (unsigned long long)g.rmag,
-           (unsigned long long)g.rwin, g.pow2 ? "true" : "false", (unsigned long long)g.lin0);
+           (unsigned long long)g.rwin, g.pow2 ? "true" : "false", (unsigned long long)g.lin0,
+           (unsigned long long)g.seglen, (unsigned long long)g.segm);
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

@@ -39,6 +39,7 @@ struct Geom {
   bool rows = false;     // row windows: a vector is one counter row (short odd innermost)
   bool rows_ok = false;  // the op has row-window kernels (embed, binary)
   uint64_t rowlen = 0, rmag = 0, rwin = 1;
+  uint64_t seglen = 0, segm = 0;   // rows are segments of a split axis; segm = its embed bound
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
@@ -145,6 +146,8 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.rowlen = (uint32_t)g.rowlen;
   d.rmag = (uint32_t)g.rmag;
   d.rwin = (uint32_t)g.rwin;
+  d.seglen = (IDX)g.seglen;
+  d.segm = (IDX)g.segm;
   for (int k = 0; k < TRIOT_MAXD; ++k) {
     d.zn[k] = (IDX)g.zn[k];
     d.zdm[k] = g.zdm[k];

@@ -325,7 +325,10 @@ def run_rows(desc: dict, op: str, bufs: list, binop: str = "mul"):
                     u, off, oob = lanes[i]
                     r0 = (32 * wi + i) * n
                     ent = [W(off[x] - r0 * T[x]["tau"]) for x in range(nt)]
-                    lim = r0 + m if (i < nr and not oob) else 0
+                    mr = m
+                    if desc.get("seglen"):   # a segment of a split axis: per-segment bound
+                        mr = max(0, min(desc["segm"] - u[D - 1] * n, n))
+                    lim = r0 + mr if (i < nr and not oob) else 0
                     tab.append((ent, lim))
                 rows = 32 * wi + nr
                 lanes = [step(list(u), off) for (u, off, _) in lanes]

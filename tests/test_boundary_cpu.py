@@ -533,7 +533,9 @@ def test_row_windows_for_misaligned_outputs():
                               ptr_mod32=(8, 0, 0))
     assert p["rows"]
     p = T.triot_plan_describe(0, [(4, 8192), (4, 8000)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
-    assert not p["rows"]                                   # rows over 4096: vector plan
+    assert p["rows"] and (p["seglen"], p["segm"], p["rowlen"]) == (512, 8000, 512)  # segments
+    p = T.triot_plan_describe(0, [(4, 8191), (4, 8000)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
+    assert not p["rows"]                                   # 8191 is prime: no segment length
 
 
 @pytest.mark.parametrize("seed", range(10))
@@ -561,7 +563,7 @@ def test_row_windows_for_odd_rows_into_non_dense_outputs():
     """Odd rows longer than the dense thresholds still take row windows when the output is not
     dense in the counter (region-only embed, a c larger than the iteration) or misaligned."""
     p = T.triot_plan_describe(0, [(40, 383), (40, 383)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
-    assert not p["rows"]                                   # same shapes merge: one long axis
+    assert p["rows"] and p["seglen"] == 383                # merged 15320 = 40 segments of 383
     p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 0)
     assert p["flat"]                                       # dense aligned dst: flat vectors
     p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
@@ -587,3 +589,33 @@ def test_pow2_decode_and_linear_tensor0_flags():
     assert wide["lin0"] == 0
     ev = T.triot_plan_describe(2, [(16,) * 6], None, 6, F64, 0)
     assert ev["pow2"]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_model_segmented_rows_vs_oracle(seed):
+    """Fully merged long rows into a misaligned output are cut into segments (rows of a divisor
+    L <= 4096 of the merged extent, per-segment embed bound): the kernel model is bit-exact
+    against the oracle for pads, crops and binary ops."""
+    rng = np.random.default_rng(9000 + seed)
+    n1 = int(rng.choice([2, 3, 5]))
+    inner = int(rng.choice([1024, 1500, 2048, 3000]))
+    dst_shape = (int(rng.integers(3, 7)), n1, inner)
+    src_shape = (dst_shape[0] + int(rng.integers(-2, 2)), n1, inner)   # inner axes merge
+    src = random_values(rng, src_shape, "f32", "normal")
+    ref = np.full(dst_shape, -7.0, dtype=np.float32)
+    O.embed(ref, src)
+    desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, 3, F32, 0,
+                                 ptr_mod32=(4, 0, 0), mode=0, warps=int(rng.integers(1, 5)))
+    assert desc["rows"] and desc["seglen"] > 0, desc
+    out = np.full(dst_shape, -7.0, dtype=np.float32)
+    kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
+    np.testing.assert_array_equal(_bits(out), _bits(ref))
+    a = random_values(rng, dst_shape, "f32", "normal")
+    b = random_values(rng, dst_shape, "f32", "normal")
+    refc = O.apply_binary(a, b, "add")
+    desc = T.triot_plan_describe(1, [dst_shape, dst_shape, dst_shape], None, 3, F32, 0,
+                                 ptr_mod32=(4, 0, 0), mode=0, warps=int(rng.integers(1, 5)))
+    assert desc["rows"] and desc["seglen"] > 0, desc
+    c = np.full(dst_shape, 5.0, dtype=np.float32)
+    kernel_model.run(desc, "binary", [c.reshape(-1), a.reshape(-1), b.reshape(-1)], binop="add")
+    np.testing.assert_array_equal(_bits(c), _bits(refc))

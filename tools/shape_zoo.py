@@ -100,6 +100,10 @@ if "--rows" in sys.argv:   # short odd rows: row windows vs flat vectors (run wi
     embed_case("rows: embed f32 (4096,4096,5) <- same, dst misaligned", (4096, 4096, 5),
                (4096, 4096, 5), off=1)
     embed_case("rows: C2 dst misaligned by 1 element", (512,) * 3, (384,) * 3, off=1)
+    embed_case("rows: merged copy (4096,4096,5) <- same, dst misaligned", (4096, 4096, 5),
+               (4096, 4096, 5), off=1)
+    embed_case("rows: merged pad (512)^3 <- (500,512,512), dst misaligned", (512,) * 3,
+               (500, 512, 512), off=1)
     embed_case("rows: C2 src misaligned by 1 element", (512,) * 3, (384,) * 3, soff=1)
     embed_case("rows: f64 pad (128)^4 from (100)^4, dst misaligned", (128,) * 4, (100,) * 4,
                dtype=torch.float64, off=1)
