@@ -60,7 +60,7 @@ TableFn table_for(const Geom& g) {
 }
 
 int vindex(const Geom& g) {
-  if (g.rows) return 5;
+  if (g.rows) return g.rwarp ? 6 : 5;
   if (g.flat) return 3;
   if (g.V == 32 / g.esz) return 0;
   if (g.V == 16 / g.esz) return 1;

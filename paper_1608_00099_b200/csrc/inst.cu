@@ -97,6 +97,18 @@ const void* kptr_rows() {
 #endif
 }
 
+// row windows, warp per row (long rows): embed, binary
+template <int D, typename IDX>
+const void* kptr_rowsw() {
+#if TRIOT_INST_OP == 0
+  return (const void*)&embed_rowsw_kernel<D, ESZ, IDX>;
+#elif TRIOT_INST_OP == 1
+  return (const void*)&binary_rowsw_kernel<D, ESZ, IDX, TRIOT_INST_BOP>;
+#else
+  return nullptr;
+#endif
+}
+
 // embed with zero runs (32-B vectors, dst dense in the counter; Desc::zmask)
 template <int D, typename IDX>
 const void* kptr_zero_runs() {
@@ -108,11 +120,14 @@ const void* kptr_zero_runs() {
 }
 
 // table index: ((D-1) * NVI + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
-// 3 = flat 32-B vectors, 4 = 32 B with embed zero runs, 5 = row windows
-constexpr int NVI = 6;
+// 3 = flat 32-B vectors, 4 = 32 B with embed zero runs, 5 = row windows, 6 = row windows with
+// a warp per row
+constexpr int NVI = 7;
 template <int D>
 struct Fill {
   static void run(const void** t) {
+    t[((D - 1) * NVI + 6) * 2 + 0] = kptr_rowsw<D, uint32_t>();
+    t[((D - 1) * NVI + 6) * 2 + 1] = kptr_rowsw<D, uint64_t>();
     t[((D - 1) * NVI + 5) * 2 + 0] = kptr_rows<D, uint32_t>();
     t[((D - 1) * NVI + 5) * 2 + 1] = kptr_rows<D, uint64_t>();
     t[((D - 1) * NVI + 4) * 2 + 0] = kptr_zero_runs<D, uint32_t>();

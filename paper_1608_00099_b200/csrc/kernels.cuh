@@ -658,6 +658,38 @@ __device__ __forceinline__ void embed_rows_group(const Desc<IDX>& d, IDX gbase, 
   }
 }
 
+template <typename IDX>
+__device__ __forceinline__ IDX shfl_idx(IDX v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+// Long rows (plan rwarp): a whole warp sweeps one row at a time -- lane i takes
+// columns i, i + 32, ... of that row, whose offsets and bound are uniform across the warp -- so
+// there is no per-element table lookup; KW columns per lane are loaded before any is stored.
+template <int ESZ, typename IDX, int KW, bool T1>
+__device__ __forceinline__ void embed_warp_row(const Desc<IDX>& d, IDX so, IDX dof, IDX mrow,
+                                               IDX n, int lane) {
+  constexpr int EW = ESZ / 4;
+  const IDX tau0 = T1 ? IDX(1) : d.t[0].tau, tau1 = T1 ? IDX(1) : d.t[1].tau;
+  const char* sp = (const char*)d.t[1].ptr + (uint64_t)so * ESZ;
+  char* dp = (char*)d.t[0].ptr + (uint64_t)dof * ESZ;
+  for (IDX c0 = (IDX)lane; c0 < n; c0 += 32 * KW) {
+    uint32_t buf[KW][EW];
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const IDX c = c0 + (IDX)(32 * j);
+#pragma unroll
+      for (int q = 0; q < EW; ++q) buf[j][q] = 0u;
+      if (c < mrow) Mem<ESZ>::ld(sp + (uint64_t)(c * tau1) * ESZ, buf[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const IDX c = c0 + (IDX)(32 * j);
+      if (c < n) Mem<ESZ>::st(dp + (uint64_t)(c * tau0) * ESZ, buf[j]);
+    }
+  }
+}
+
 template <int D, int ESZ, typename IDX, int K>
 __global__ void __launch_bounds__(kBlock) embed_rows_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
@@ -765,6 +797,36 @@ __device__ __forceinline__ void binary_rows_group(const Desc<IDX>& d, IDX gbase,
   }
 }
 
+template <int ESZ, typename IDX, int KW, int OP, bool T1>
+__device__ __forceinline__ void binary_warp_row(const Desc<IDX>& d, IDX oc, IDX oa, IDX ob, IDX n,
+                                                int lane) {
+  constexpr int EW = ESZ / 4;
+  const IDX sc = T1 ? IDX(1) : d.t[0].tau, sa = T1 ? IDX(1) : d.t[1].tau;
+  const IDX sb = T1 ? IDX(1) : d.t[2].tau;
+  char* cp = (char*)d.t[0].ptr + (uint64_t)oc * ESZ;
+  const char* ap = (const char*)d.t[1].ptr + (uint64_t)oa * ESZ;
+  const char* bp = (const char*)d.t[2].ptr + (uint64_t)ob * ESZ;
+  for (IDX c0 = (IDX)lane; c0 < n; c0 += 32 * KW) {
+    uint32_t ba[KW][EW], bb[KW][EW];
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const IDX c = c0 + (IDX)(32 * j);
+      if (c < n) {
+        Mem<ESZ>::ld(ap + (uint64_t)(c * sa) * ESZ, ba[j]);
+        Mem<ESZ>::ld(bp + (uint64_t)(c * sb) * ESZ, bb[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const IDX c = c0 + (IDX)(32 * j);
+      if (c >= n) continue;
+      uint32_t r[EW];
+      Elem<ESZ>::put(r, bop<OP>(Elem<ESZ>::get(ba[j]), Elem<ESZ>::get(bb[j])));
+      Mem<ESZ>::st(cp + (uint64_t)(c * sc) * ESZ, r);
+    }
+  }
+}
+
 template <int D, int ESZ, typename IDX, int K, int OP>
 __global__ void __launch_bounds__(kBlock) binary_rows_kernel(const __grid_constant__ Desc<IDX> d) {
   __shared__ RowSrc<IDX> tab[kBlock / 32][kRowsTab];
@@ -809,6 +871,72 @@ __global__ void __launch_bounds__(kBlock) binary_rows_kernel(const __grid_consta
       binary_rows_group<ESZ, IDX, K, OP, false, false>(d, gb, rows * (uint32_t)n, tcs[wib],
                                                        tab[wib], lane);
     __syncwarp();
+  }
+}
+
+// Row windows, warp per row (long rows, plan rwarp): the lane-per-row odometer of the row-window
+// kernels, then the warp sweeps each of its 32 rows in turn with uniform offsets and bound.
+template <int D, int ESZ, typename IDX>
+__global__ void __launch_bounds__(kBlock) embed_rowsw_kernel(const __grid_constant__ Desc<IDX> d) {
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[2];
+  uint32_t oob;
+  odo_start<D, 2, true, IDX, true>(d, base0 + (IDX)lane, u, off, oob);
+  const IDX n = (IDX)d.rowlen, m = d.scols;
+  const bool t1 = d.t[0].tau == IDX(1) && d.t[1].tau == IDX(1);
+  constexpr int KW = 64 / ESZ;  // 64 B of loads per lane in flight
+  pdl_wait();
+  for (IDX b = base0; b < vend; b += d.dv) {
+    const uint32_t nr = (vend - b) < (IDX)32 ? (uint32_t)(vend - b) : 32u;
+    IDX mr = m;  // columns of the lane's row read from src
+    if (d.seglen) {
+      const IDX s0 = u[D - 1] * n;
+      mr = d.segm > s0 ? (d.segm - s0 < n ? d.segm - s0 : n) : IDX(0);
+    }
+    if (oob != 0) mr = 0;
+    for (uint32_t i = 0; i < nr; ++i) {
+      const IDX so = shfl_idx(off[1], (int)i), dof = shfl_idx(off[0], (int)i);
+      const IDX mrow = shfl_idx(mr, (int)i);
+      if (t1)
+        embed_warp_row<ESZ, IDX, KW, true>(d, so, dof, mrow, n, lane);
+      else
+        embed_warp_row<ESZ, IDX, KW, false>(d, so, dof, mrow, n, lane);
+    }
+    odo_step<D, 2, true, IDX, true>(d, u, off, oob);
+  }
+}
+
+template <int D, int ESZ, typename IDX, int OP>
+__global__ void __launch_bounds__(kBlock) binary_rowsw_kernel(const __grid_constant__ Desc<IDX> d) {
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[3];
+  uint32_t oob;
+  odo_start<D, 3, false, IDX>(d, base0 + (IDX)lane, u, off, oob);
+  const IDX n = (IDX)d.rowlen;
+  const bool t1 = d.t[0].tau == IDX(1) && d.t[1].tau == IDX(1) && d.t[2].tau == IDX(1);
+  constexpr int KW = 32 / ESZ;  // two operands: 64 B of loads per lane in flight
+  pdl_wait();
+  for (IDX b = base0; b < vend; b += d.dv) {
+    const uint32_t nr = (vend - b) < (IDX)32 ? (uint32_t)(vend - b) : 32u;
+    for (uint32_t i = 0; i < nr; ++i) {
+      const IDX oc = shfl_idx(off[0], (int)i), oa = shfl_idx(off[1], (int)i);
+      const IDX ob = shfl_idx(off[2], (int)i);
+      if (t1)
+        binary_warp_row<ESZ, IDX, KW, OP, true>(d, oc, oa, ob, n, lane);
+      else
+        binary_warp_row<ESZ, IDX, KW, OP, false>(d, oc, oa, ob, n, lane);
+    }
+    odo_step<D, 3, false, IDX>(d, u, off, oob);
   }
 }
 

@@ -40,6 +40,7 @@ struct Geom {
   bool rows_ok = false;  // the op has row-window kernels (embed, binary)
   uint64_t rowlen = 0, rmag = 0, rwin = 1;
   uint64_t seglen = 0, segm = 0;   // rows are segments of a split axis; segm = its embed bound
+  bool rwarp = false;              // long rows: a warp per row instead of the row table
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};

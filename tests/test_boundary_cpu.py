@@ -619,3 +619,16 @@ def test_model_segmented_rows_vs_oracle(seed):
     c = np.full(dst_shape, 5.0, dtype=np.float32)
     kernel_model.run(desc, "binary", [c.reshape(-1), a.reshape(-1), b.reshape(-1)], binop="add")
     np.testing.assert_array_equal(_bits(c), _bits(refc))
+
+
+def test_warp_per_row_plan_rule():
+    """Long rows (>= 128) into an output not dense in the counter take a warp per row; dense
+    outputs and short rows keep the row table."""
+    p = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0, ptr_mod32=(4, 0, 0))
+    assert p["rows"] and not p["rwarp"]                   # dense misaligned dst: table
+    p = T.triot_plan_describe(0, [(41, 400), (40, 383)], None, 2, F32, 1)
+    assert p["rows"] and p["rwarp"]                       # region only, rows of 383
+    p = T.triot_plan_describe(1, [(40, 200), (40, 99), (40, 99)], (40, 99), 2, F64, 2)
+    assert p["rows"] and not p["rwarp"]                   # rows of 99 < 128: table
+    p = T.triot_plan_describe(1, [(40, 300), (40, 199), (40, 199)], (40, 199), 2, F64, 2)
+    assert p["rows"] and p["rwarp"]                       # wide c, rows of 199

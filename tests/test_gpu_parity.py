@@ -765,14 +765,15 @@ def test_row_windows_long_odd_rows_non_dense_outputs(dtype):
     O.embed(ref, src, region_only=True)
     T.embed(dst, _dev(src), region_only=True)
     assert_bits_equal(dst, ref)
-    # binary, c wider than the iteration (40, 17, 99)
-    a = rng.standard_normal((40, 17, 99)).astype(dtype)
-    b = rng.standard_normal((41, 18, 99)).astype(dtype)
-    ref = np.full((40, 17, 200), 9.0, dtype=dtype)
-    O.apply_binary(a, b, "sub", iter_shape=(40, 17, 99), out=ref)
-    c = _dev(np.full((40, 17, 200), 9.0, dtype=dtype))
-    T.apply_binary(_dev(a), _dev(b), "sub", out=c, iter_shape=(40, 17, 99))
-    assert_bits_equal(c, ref)
+    # binary, c wider than the iteration: rows of 99 (row table) and of 199 (a warp per row)
+    for n in (99, 199):
+        a = rng.standard_normal((40, 17, n)).astype(dtype)
+        b = rng.standard_normal((41, 18, n)).astype(dtype)
+        ref = np.full((40, 17, 300), 9.0, dtype=dtype)
+        O.apply_binary(a, b, "sub", iter_shape=(40, 17, n), out=ref)
+        c = _dev(np.full((40, 17, 300), 9.0, dtype=dtype), 1)
+        T.apply_binary(_dev(a), _dev(b), "sub", out=c, iter_shape=(40, 17, n))
+        assert_bits_equal(c, ref)
 
 
 @pytest.mark.slow
