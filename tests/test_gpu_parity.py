@@ -916,3 +916,30 @@ def test_segmented_rows_misaligned_merged_copy():
     dst = _poisoned((512, 512, 512), np.float32, 1)
     T.embed(dst, _dev(src))
     assert_bits_equal(dst, ref)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_ev_view_odd_windows(dtype):
+    """Expected value of view windows whose rows take no vector width (odd lengths >= 32, odd
+    starts): integer-valued data exact, real data within 1e-12, the mass, deterministic."""
+    rng = np.random.default_rng(61)
+    for base, start, win in [((40, 70, 300), (3, 5, 7), (33, 61, 255)),
+                             ((9, 300), (1, 1), (8, 297)),
+                             ((4, 5, 6, 200), (1, 0, 2, 3), (3, 5, 4, 33)),
+                             ((2000,), (3,), (1901,))]:
+        for kind in ("int", "real"):
+            if kind == "int":
+                b = rng.integers(0, 256, size=base).astype(dtype)
+            else:
+                b = rng.random(base).astype(dtype)
+            sl = tuple(slice(s, s + w) for s, w in zip(start, win))
+            ref = O.expected_value(np.ascontiguousarray(b[sl]))
+            bt = _dev(b)
+            m1 = T.expected_value_view(T.View(bt, start, win), with_mass=True).cpu().numpy()
+            m2 = T.expected_value_view(T.View(bt, start, win), with_mass=True).cpu().numpy()
+            assert _bits(m1).tolist() == _bits(m2).tolist()
+            if kind == "int":
+                np.testing.assert_array_equal(m1[:-1], ref)
+                assert m1[-1] == float(b[sl].astype(np.float64).sum())
+            else:
+                assert np.all(np.abs(m1[:-1] - ref) <= 1e-12 * np.abs(ref)), (m1, ref)
