@@ -60,6 +60,7 @@ TableFn table_for(const Geom& g) {
 }
 
 int vindex(const Geom& g) {
+  if (g.dshift) return 7;
   if (g.rows) return g.rwarp ? 6 : 5;
   if (g.flat) return 3;
   if (g.V == 32 / g.esz) return 0;

@@ -89,6 +89,9 @@ struct Desc {
   // rows that are segments of a longer split axis (seglen = rowlen): the embed bound of the
   // unsplit axis is segm, so segment s reads columns [0, clamp(segm - s rowlen, 0, rowlen))
   IDX seglen, segm;
+  // embed into a dst dense in the counter whose base is misaligned by dshift elements (> 0):
+  // aligned 32-byte stores of lane-shifted vectors (embed_shift_kernel)
+  uint32_t dshift;
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
                                   // update: x, y, z
   void* out;             // EV: means (device)

@@ -109,6 +109,16 @@ const void* kptr_rowsw() {
 #endif
 }
 
+// embed into a misaligned dst dense in the counter (shifted 32-B stores)
+template <int D, typename IDX>
+const void* kptr_shift() {
+#if TRIOT_INST_OP == 0
+  return (const void*)&embed_shift_kernel<D, ESZ, IDX, KEMBED>;
+#else
+  return nullptr;
+#endif
+}
+
 // embed with zero runs (32-B vectors, dst dense in the counter; Desc::zmask)
 template <int D, typename IDX>
 const void* kptr_zero_runs() {
@@ -121,11 +131,13 @@ const void* kptr_zero_runs() {
 
 // table index: ((D-1) * NVI + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
 // 3 = flat 32-B vectors, 4 = 32 B with embed zero runs, 5 = row windows, 6 = row windows with
-// a warp per row
-constexpr int NVI = 7;
+// a warp per row, 7 = 32 B with shifted stores (embed into a misaligned dense dst)
+constexpr int NVI = 8;
 template <int D>
 struct Fill {
   static void run(const void** t) {
+    t[((D - 1) * NVI + 7) * 2 + 0] = kptr_shift<D, uint32_t>();
+    t[((D - 1) * NVI + 7) * 2 + 1] = kptr_shift<D, uint64_t>();
     t[((D - 1) * NVI + 6) * 2 + 0] = kptr_rowsw<D, uint32_t>();
     t[((D - 1) * NVI + 6) * 2 + 1] = kptr_rowsw<D, uint64_t>();
     t[((D - 1) * NVI + 5) * 2 + 0] = kptr_rows<D, uint32_t>();

@@ -129,6 +129,11 @@ __device__ __forceinline__ const char* addr(const void* base, IDX off) {
   return (const char*)base + (uint64_t)off * ESZ;
 }
 
+template <typename IDX>
+__device__ __forceinline__ IDX shfl_idx(IDX v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
 // ------------------------------------------------------------------ index arithmetic
 
 // q = n / e for an invariant e: Granlund-Montgomery round-up multiply-high (u32), or hardware
@@ -399,6 +404,119 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   }
 }
 
+// Shifted stores for an output dense in the counter whose base is misaligned by s elements
+// (0 < s < V): a warp step's 32 vectors (one per lane, lane-ordered) are 1 KB contiguous of dst
+// starting s elements past a 32-byte boundary.  Lane l >= 1 stores the aligned 32-byte chunk l
+// made of lane l-1's last s elements (a shuffle) and its own first V - s; lane 0 stores its
+// head and lane 31 its tail element by element (the step's two partial chunks).
+template <int ESZ>
+__device__ __forceinline__ void store_shifted(char* a0, const uint32_t (&w)[8], int sw,
+                                              int lane) {
+  constexpr int EW = ESZ / 4;
+  uint32_t prev[8], out[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) prev[q] = __shfl_up_sync(0xffffffffu, w[q], 1);
+  switch (sw) {  // shift in 32-bit words (uniform)
+#define TRIOT_SHIFT_CASE(S)                                                      \
+  case S:                                                                        \
+    _Pragma("unroll") for (int q = 0; q < 8; ++q) out[q] = q < S ? prev[8 - S + q] : w[q - S]; \
+    break;
+    TRIOT_SHIFT_CASE(1)
+    TRIOT_SHIFT_CASE(2)
+    TRIOT_SHIFT_CASE(3)
+    TRIOT_SHIFT_CASE(4)
+    TRIOT_SHIFT_CASE(5)
+    TRIOT_SHIFT_CASE(6)
+    default:
+    TRIOT_SHIFT_CASE(7)
+#undef TRIOT_SHIFT_CASE
+  }
+  char* al = a0 - sw * 4;  // the 32-byte boundary below lane 0's vector
+  if (lane >= 1) {
+    Mem<32>::st(al + 32 * lane, out);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; q += EW)
+      if (q < 8 - sw) Mem<ESZ>::st(a0 + q * 4, w + q);
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < 8; q += EW)
+      if (q >= 8 - sw) Mem<ESZ>::st(al + 32 * 32 + (q - (8 - sw)) * 4, w + q);
+  }
+}
+
+// embed into a dst dense in the counter but misaligned (plan dshift): embed_kernel's loads,
+// store_shifted for every full warp step, element stores for a ragged last step.
+template <int D, int ESZ, typename IDX, int K>
+__global__ void __launch_bounds__(kBlock) embed_shift_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int V = 32 / ESZ;
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[2];
+  uint32_t oob;
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 2, true, IDX>(d, v, u, off, oob);
+  const uint32_t lgL = d.lgL;
+  const int sw = (int)d.dshift * EW;
+  pdl_wait();
+  for (IDX b = base0; b < vend; b += K * d.dv) {
+    uint32_t buf[K][NW];
+    IDX doff[K];
+    bool valid[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      valid[j] = v < vend;
+      v += d.dv;
+      doff[j] = off[0];
+      if (valid[j]) {
+        const IDX uv = u[D - 1];
+        const bool any = oob == 0 && uv < d.vany;
+        if (any && uv < d.vfull) {
+          load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, buf[j]);
+        } else if (!any) {
+#pragma unroll
+          for (int q = 0; q < NW; ++q) buf[j][q] = 0u;
+        } else {
+          const IDX row0 = uv * d.rowmul, col0 = uv * d.colmul;
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const IDX r = (IDX)((uint32_t)e >> lgL);
+            const IDX c = (IDX)((uint32_t)e & ((1u << lgL) - 1u));
+            if (row0 + r < d.srows && col0 + c < d.scols) {
+              Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1] + r * d.t[1].rho + c * d.t[1].tau),
+                           buf[j] + e * EW);
+            } else {
+#pragma unroll
+              for (int q = 0; q < EW; ++q) buf[j][e * EW + q] = 0u;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) buf[j][q] = 0u;
+      }
+      odo_step<D, 2, true, IDX>(d, u, off, oob);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (__all_sync(0xffffffffu, valid[j])) {
+        // lane 0's vector address: the step's first element (dst offsets are v * V)
+        char* a0 = (char*)d.t[0].ptr + (uint64_t)shfl_idx(doff[j], 0) * ESZ;
+        store_shifted<ESZ>(a0, buf[j], sw, lane);
+      } else if (valid[j]) {
+        store_vec<ESZ, V, IDX>(d.t[0], doff[j], lgL, buf[j]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ binary
 // c[t] = a[t] OP b[t] (Alg 9 apply_tensors).  Tensor 0 = c, 1 = a, 2 = b.
 // IEEE round-to-nearest, one rounding per element: explicit _rn intrinsics, no contraction.
@@ -656,11 +774,6 @@ __device__ __forceinline__ void embed_rows_group(const Desc<IDX>& d, IDX gbase, 
         Mem<ESZ>::st(DD ? (void*)(p + 32 * ESZ * j) : (void*)(dst + (uint64_t)doff[j] * ESZ),
                      buf[j]);
   }
-}
-
-template <typename IDX>
-__device__ __forceinline__ IDX shfl_idx(IDX v, int src) {
-  return __shfl_sync(0xffffffffu, v, src);
 }
 
 // Long rows (plan rwarp): a whole warp sweeps one row at a time -- lane i takes

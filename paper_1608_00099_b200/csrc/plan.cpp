@@ -360,6 +360,7 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // Flat vectors store 32 B at a time only into an output dense in the counter and 32-B
   // aligned; any other output (a view window, a misaligned base) takes row windows up to
   // kRowsMaxLong, whose lane-consecutive element stores coalesce at any alignment.
+  bool shift_build = false;
   bool out_flat_vec = ((uintptr_t)g.t[0].ptr % 32) == 0;
   {
     uint64_t hs = 1;
@@ -379,7 +380,23 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // 32-byte lane stride write partial sectors (C2 with dst offset by 4 B: 1.4 TB/s), so rows up
   // to kRowsMaxLong take row windows, whose lane-consecutive accesses coalesce at any alignment;
   // longer rows (a fully merged copy) are cut into segments of a divisor L <= kRowsMaxLong.
-  const bool long_ok = g.rows_ok && g_rows_on && g.op != OP_EV && nl >= 3;
+  // An embed whose dst is dense in the counter and only misaligned (a slice of a buffer) keeps
+  // the 32-byte vectors and stores them shifted to the 32-byte grid (embed_shift_kernel).
+  if (g.op == OP_EMBED && g_rows_on && cc[0].V == vmax && !cc[0].vec[0]) {
+    const uintptr_t mis = (uintptr_t)g.t[0].ptr % 32;
+    bool dense0 = mis % (uintptr_t)g.esz == 0;
+    uint64_t hs = 1;
+    for (int k = na - 1; k >= 0; --k) {
+      if (ax[k].sig[0] != hs) dense0 = false;
+      hs *= ax[k].n;
+    }
+    if (dense0 && mis != 0) {  // the 32-byte candidate, whatever the others scored
+      g.dshift = (uint32_t)(mis / (uintptr_t)g.esz);
+      shift_build = true;
+      best = 0;
+    }
+  }
+  const bool long_ok = g.rows_ok && g_rows_on && g.op != OP_EV && nl >= 3 && !shift_build;
   if ((cc[best].V > 1 && !cc[best].vec[0] && long_ok) ||
       (cc[best].V == 1 && vmax > 1 && !out_flat_vec && long_ok)) {
     // rows over 512 elements are cut into segments of a divisor L in [64, 512] when one
@@ -1131,7 +1148,7 @@ std::string describe(const Geom& g) {
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,"
            "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,\"pow2\":%s,\"lin0\":%llu,"
-           "\"seglen\":%llu,\"segm\":%llu,\"rwarp\":%s,",
+           "\"seglen\":%llu,\"segm\":%llu,\"rwarp\":%s,\"dshift\":%u,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
@@ -1141,7 +1158,8 @@ std::string describe(const Geom& g) {
            (unsigned long long)g.srows, (unsigned long long)g.scols, g.nslots, g.zmask,
            g.rows ? "true" : "false", (unsigned long long)g.rowlen, (unsigned long long)g.rmag,
            (unsigned long long)g.rwin, g.pow2 ? "true" : "false", (unsigned long long)g.lin0,
-           (unsigned long long)g.seglen, (unsigned long long)g.segm, g.rwarp ? "true" : "false");
+           (unsigned long long)g.seglen, (unsigned long long)g.segm, g.rwarp ? "true" : "false",
+           g.dshift);
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

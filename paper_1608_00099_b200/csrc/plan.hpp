@@ -41,6 +41,7 @@ struct Geom {
   uint64_t rowlen = 0, rmag = 0, rwin = 1;
   uint64_t seglen = 0, segm = 0;   // rows are segments of a split axis; segm = its embed bound
   bool rwarp = false;              // long rows: a warp per row instead of the row table
+  uint32_t dshift = 0;             // embed: dst dense but misaligned by this many elements
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
@@ -147,6 +148,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.rowlen = (uint32_t)g.rowlen;
   d.rmag = (uint32_t)g.rmag;
   d.rwin = (uint32_t)g.rwin;
+  d.dshift = g.dshift;
   d.seglen = (IDX)g.seglen;
   d.segm = (IDX)g.segm;
   for (int k = 0; k < TRIOT_MAXD; ++k) {

@@ -194,9 +194,9 @@ def test_plans_of_the_five_configs():
     assert (p["Dc"], p["D"], p["V"], p["R"], p["collapsed"]) == (14, 13, 8, 2, True)
     assert [t["vec"] for t in p["t"]] == [True, False]
     assert all(not pl["idx64"] for pl in map(_plan, CONFIGS))
-    # misaligned output pointer: row windows (element accesses, lane-consecutive), never wide
+    # misaligned output pointer: 32-B vectors stored shifted to the 32-byte grid
     p = _plan("C2", mods=(4, 0, 0))
-    assert p["rows"] and p["V"] == 1
+    assert p["dshift"] == 1 and p["V"] == 8 and not p["rows"]
 
 
 def test_canonicalisation_drops_and_merges():
@@ -526,16 +526,20 @@ def test_row_windows_for_misaligned_outputs():
     """An output whose base is only element-aligned takes row windows (rows <= 4096) instead of
     element stores at a 32-byte lane stride; an aligned one keeps 32-byte vectors."""
     p = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0, ptr_mod32=(4, 0, 0))
-    assert p["rows"] and p["rowlen"] == 512 and p["rwin"] == 1 and p["D"] == 2
+    assert p["dshift"] == 1 and not p["rows"]            # embed, dense dst: shifted 32-B stores
     p = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0)
-    assert not p["rows"] and p["V"] == 8
+    assert not p["rows"] and p["V"] == 8 and p["dshift"] == 0
+    p = T.triot_plan_describe(1, [(512,) * 3, (512,) * 3, (520,) * 3], (512,) * 3, 3, F32, 2,
+                              ptr_mod32=(4, 0, 0))
+    assert p["rows"] and p["rowlen"] == 512 and p["rwin"] == 1 and p["D"] == 2   # binary: rows
     p = T.triot_plan_describe(1, [None, (64, 100), (64, 96)], (64, 96), 2, F64, 2,
                               ptr_mod32=(8, 0, 0))
     assert p["rows"]
-    p = T.triot_plan_describe(0, [(4, 8192), (4, 8000)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
-    assert p["rows"] and (p["seglen"], p["segm"], p["rowlen"]) == (512, 8000, 512)  # segments
-    p = T.triot_plan_describe(0, [(4, 8191), (4, 8000)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
-    assert not p["rows"]                                   # 8191 is prime: no segment length
+    p = T.triot_plan_describe(0, [(4, 8192), (4, 8000)], None, 2, F32, 1, ptr_mod32=(4, 0, 0))
+    assert p["rows"] and (p["seglen"], p["segm"], p["rowlen"]) == (500, 8000, 500)  # segments
+    p = T.triot_plan_describe(1, [(4, 8191), (4, 8191), (4, 8191)], None, 2, F32, 2,
+                              ptr_mod32=(4, 0, 0))
+    assert not p["rows"]                 # merged 4 x 8191 (prime): no segment length in [64, 512]
 
 
 @pytest.mark.parametrize("seed", range(10))
@@ -553,7 +557,7 @@ def test_model_misaligned_output_rows_vs_oracle(seed):
     O.embed(ref, src, region_only=region)
     desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, d, F32, 1 if region else 0,
                                  ptr_mod32=(4, 0, 0), mode=0, warps=int(rng.integers(1, 6)))
-    assert desc["rows"] or desc["V"] == 1, desc
+    assert desc["rows"] or desc["dshift"] or desc["V"] == 1, desc
     out = np.full(dst_shape, -7.0, dtype=np.float32)
     kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
     np.testing.assert_array_equal(_bits(out), _bits(ref))
@@ -563,7 +567,7 @@ def test_row_windows_for_odd_rows_into_non_dense_outputs():
     """Odd rows longer than the dense thresholds still take row windows when the output is not
     dense in the counter (region-only embed, a c larger than the iteration) or misaligned."""
     p = T.triot_plan_describe(0, [(40, 383), (40, 383)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
-    assert p["rows"] and p["seglen"] == 383                # merged 15320 = 40 segments of 383
+    assert p["dshift"] == 1 and p["V"] == 8                # merged 15320, dense dst: shifted
     p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 0)
     assert p["flat"]                                       # dense aligned dst: flat vectors
     p = T.triot_plan_describe(0, [(40, 383), (30, 380)], None, 2, F32, 0, ptr_mod32=(4, 0, 0))
@@ -606,7 +610,7 @@ def test_model_segmented_rows_vs_oracle(seed):
     O.embed(ref, src)
     desc = T.triot_plan_describe(0, [dst_shape, src_shape], None, 3, F32, 0,
                                  ptr_mod32=(4, 0, 0), mode=0, warps=int(rng.integers(1, 5)))
-    assert desc["rows"] and desc["seglen"] > 0, desc
+    assert desc["dshift"] == 1, desc                        # embed: shifted 32-B stores
     out = np.full(dst_shape, -7.0, dtype=np.float32)
     kernel_model.run(desc, "embed", [out.reshape(-1), src.reshape(-1)])
     np.testing.assert_array_equal(_bits(out), _bits(ref))
@@ -624,11 +628,26 @@ def test_model_segmented_rows_vs_oracle(seed):
 def test_warp_per_row_plan_rule():
     """Long rows (>= 128) into an output not dense in the counter take a warp per row; dense
     outputs and short rows keep the row table."""
-    p = T.triot_plan_describe(0, [(512,) * 3, (384,) * 3], None, 3, F32, 0, ptr_mod32=(4, 0, 0))
-    assert p["rows"] and not p["rwarp"]                   # dense misaligned dst: table
+    p = T.triot_plan_describe(1, [(512,) * 3, (512,) * 3, (520,) * 3], (512,) * 3, 3, F32, 2,
+                              ptr_mod32=(4, 0, 0))
+    assert p["rows"] and not p["rwarp"]                   # dense misaligned c: table
     p = T.triot_plan_describe(0, [(41, 400), (40, 383)], None, 2, F32, 1)
     assert p["rows"] and p["rwarp"]                       # region only, rows of 383
     p = T.triot_plan_describe(1, [(40, 200), (40, 99), (40, 99)], (40, 99), 2, F64, 2)
     assert p["rows"] and not p["rwarp"]                   # rows of 99 < 128: table
     p = T.triot_plan_describe(1, [(40, 300), (40, 199), (40, 199)], (40, 199), 2, F64, 2)
     assert p["rows"] and p["rwarp"]                       # wide c, rows of 199
+
+
+def test_shifted_store_plan():
+    """An embed whose dst is dense in the counter but misaligned by whole elements keeps 32-B
+    vectors and stores them shifted (dshift = misalignment in elements); aligned, view and
+    region-only destinations do not."""
+    for esz, dt in ((4, F32), (8, F64)):
+        for k in range(1, 32 // esz):
+            p = T.triot_plan_describe(0, [(64, 64), (60, 60)], None, 2, dt, 0,
+                                      ptr_mod32=(k * esz, 0, 0))
+            assert p["dshift"] == k and p["V"] == 32 // esz, (esz, k, p["dshift"])
+    assert T.triot_plan_describe(0, [(64, 64), (60, 60)], None, 2, F32, 0)["dshift"] == 0
+    p = T.triot_plan_describe(0, [(64, 64), (60, 60)], None, 2, F32, 1, ptr_mod32=(4, 0, 0))
+    assert p["dshift"] == 0                               # region only: dst rows not dense

@@ -903,19 +903,29 @@ def test_sharded_expected_value_over_nccl():
         dist.destroy_process_group()
 
 
-def test_segmented_rows_misaligned_merged_copy():
-    """A fully merged pad into a misaligned output (one canonical axis of 134 M elements) is cut
-    into row segments of 512 with a per-segment bound; bit-exact against the oracle."""
+def test_misaligned_merged_outputs():
+    """A fully merged pad into a dst one element off the 32-byte grid (shifted 32-B stores), and
+    a merged binary into a misaligned c (row segments of 512), bit-exact against the oracle."""
     rng = np.random.default_rng(33)
     src = rng.standard_normal((500, 512, 512)).astype(np.float32)
     desc = T.triot_plan_describe(0, [(512, 512, 512), src.shape], None, 3, T.TRIOT_F32, 0,
                                  (4, 0, 0))
-    assert desc["rows"] and desc["seglen"] == 512 and desc["segm"] == 500 * 512 * 512
+    assert desc["dshift"] == 1
     ref = np.empty((512, 512, 512), np.float32)
     O.embed(ref, src)
     dst = _poisoned((512, 512, 512), np.float32, 1)
     T.embed(dst, _dev(src))
     assert_bits_equal(dst, ref)
+    del dst
+    a = rng.standard_normal((256, 512, 512)).astype(np.float32)
+    b = rng.standard_normal((256, 512, 512)).astype(np.float32)
+    desc = T.triot_plan_describe(1, [a.shape, a.shape, b.shape], None, 3, T.TRIOT_F32, 2,
+                                 (4, 0, 0))
+    assert desc["rows"] and desc["seglen"] == 512
+    refc = O.apply_binary(a, b, "mul")
+    c = _dev(np.zeros(a.shape, np.float32), 1)
+    T.apply_binary(_dev(a), _dev(b), "mul", out=c)
+    assert_bits_equal(c, refc)
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
@@ -943,3 +953,27 @@ def test_ev_view_odd_windows(dtype):
                 assert m1[-1] == float(b[sl].astype(np.float64).sum())
             else:
                 assert np.all(np.abs(m1[:-1] - ref) <= 1e-12 * np.abs(ref)), (m1, ref)
+
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_shifted_stores_every_offset(dtype):
+    """Embeds into a dense dst at every element offset from the 32-byte grid (shifted 32-B
+    stores: partial head / tail chunks per warp step, ragged last steps, collapsed rows, zero
+    vectors), bit-exact against the oracle under several decompositions."""
+    rng = np.random.default_rng(44)
+    V = 32 // np.dtype(dtype).itemsize
+    cases = [((37, 29, 16), (33, 30, 11)), ((9, 64), (8, 70)), ((5, 6, 4, 4), (4, 5, 3, 4)),
+             ((3, 1000), (3, 999))]
+    try:
+        for mode, bpsm in [(-1, 0), (0, 1), (1, 2)]:
+            T.triot_set_launch_policy(mode, bpsm)
+            for dst_shape, src_shape in cases:
+                src = rng.standard_normal(src_shape).astype(dtype)
+                ref = np.empty(dst_shape, dtype); O.embed(ref, src)
+                for off in range(1, V):
+                    dst = _poisoned(dst_shape, dtype, off)
+                    T.embed(dst, _dev(src, off % 2))
+                    assert_bits_equal(dst, ref)
+    finally:
+        T.triot_set_launch_policy(-1, 0)
