@@ -109,11 +109,13 @@ const void* kptr_rowsw() {
 #endif
 }
 
-// embed into a misaligned dst dense in the counter (shifted 32-B stores)
+// embed / binary into a misaligned output dense in the counter (shifted 32-B stores)
 template <int D, typename IDX>
 const void* kptr_shift() {
 #if TRIOT_INST_OP == 0
   return (const void*)&embed_shift_kernel<D, ESZ, IDX, KEMBED>;
+#elif TRIOT_INST_OP == 1
+  return (const void*)&binary_shift_kernel<D, ESZ, IDX, KBIN, TRIOT_INST_BOP>;
 #else
   return nullptr;
 #endif

@@ -600,6 +600,59 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
   }
 }
 
+// binary into a c dense in the counter but misaligned (plan dshift): binary_kernel with
+// store_shifted for every full warp step (in place is safe: a step's loads precede its stores,
+// and each element is loaded and stored by the same warp).
+template <int D, int ESZ, typename IDX, int K, int OP>
+__global__ void __launch_bounds__(kBlock) binary_shift_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int V = 32 / ESZ;
+  constexpr int EW = ESZ / 4;
+  constexpr int NW = V * EW;
+  const int lane = threadIdx.x & 31;
+  const IDX warp = (IDX)blockIdx.x * (kBlock / 32) + (IDX)(threadIdx.x >> 5);
+  const IDX base0 = warp * d.wmul;
+  pdl_trigger();
+  if (base0 >= d.nvec) return;
+  const IDX vend = warp_end(d, base0);
+  IDX u[D], off[3];
+  uint32_t oob;
+  IDX v = base0 + (IDX)lane;
+  odo_start<D, 3, false, IDX>(d, v, u, off, oob);
+  const uint32_t lgL = d.lgL;
+  const int sw = (int)d.dshift * EW;
+  pdl_wait();
+  for (IDX b = base0; b < vend; b += K * d.dv) {
+    uint32_t ba[K][NW], bb[K][NW];
+    IDX coff[K];
+    bool valid[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      valid[j] = v < vend;
+      v += d.dv;
+      coff[j] = off[0];
+      if (valid[j]) {
+        load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, ba[j]);
+        load_vec<ESZ, V, IDX>(d.t[2], off[2], lgL, bb[j]);
+      }
+      odo_step<D, 3, false, IDX>(d, u, off, oob);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      uint32_t r[NW];
+#pragma unroll
+      for (int e = 0; e < V; ++e)
+        Elem<ESZ>::put(r + e * EW,
+                       bop<OP>(Elem<ESZ>::get(ba[j] + e * EW), Elem<ESZ>::get(bb[j] + e * EW)));
+      if (__all_sync(0xffffffffu, valid[j])) {
+        char* a0 = (char*)d.t[0].ptr + (uint64_t)shfl_idx(coff[j], 0) * ESZ;
+        store_shifted<ESZ>(a0, r, sw, lane);
+      } else if (valid[j]) {
+        store_vec<ESZ, V, IDX>(d.t[0], coff[j], lgL, r);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ flat vectors (odd extents)
 // When no vector width divides the counter's innermost extent (3, 5, 7, 999, ...), a vector is
 // V consecutive elements of the flattened counter, crossing rows.  The lane decodes the tuple of

@@ -380,9 +380,11 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   // 32-byte lane stride write partial sectors (C2 with dst offset by 4 B: 1.4 TB/s), so rows up
   // to kRowsMaxLong take row windows, whose lane-consecutive accesses coalesce at any alignment;
   // longer rows (a fully merged copy) are cut into segments of a divisor L <= kRowsMaxLong.
-  // An embed whose dst is dense in the counter and only misaligned (a slice of a buffer) keeps
-  // the 32-byte vectors and stores them shifted to the 32-byte grid (embed_shift_kernel).
-  if (g.op == OP_EMBED && g_rows_on && cc[0].V == vmax && !cc[0].vec[0]) {
+  // An embed / binary op whose output is dense in the counter and only misaligned (a slice of a
+  // buffer) keeps the 32-byte vectors and stores them shifted to the 32-byte grid
+  // (embed_shift_kernel, binary_shift_kernel).
+  if ((g.op == OP_EMBED || g.op == OP_BINARY) && g_rows_on && cc[0].V == vmax &&
+      !cc[0].vec[0]) {
     const uintptr_t mis = (uintptr_t)g.t[0].ptr % 32;
     bool dense0 = mis % (uintptr_t)g.esz == 0;
     uint64_t hs = 1;

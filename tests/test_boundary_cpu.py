@@ -531,10 +531,10 @@ def test_row_windows_for_misaligned_outputs():
     assert not p["rows"] and p["V"] == 8 and p["dshift"] == 0
     p = T.triot_plan_describe(1, [(512,) * 3, (512,) * 3, (520,) * 3], (512,) * 3, 3, F32, 2,
                               ptr_mod32=(4, 0, 0))
-    assert p["rows"] and p["rowlen"] == 512 and p["rwin"] == 1 and p["D"] == 2   # binary: rows
-    p = T.triot_plan_describe(1, [None, (64, 100), (64, 96)], (64, 96), 2, F64, 2,
+    assert p["dshift"] == 1 and not p["rows"]            # binary, dense c: shifted stores
+    p = T.triot_plan_describe(1, [(64, 100), (64, 100), (64, 96)], (64, 96), 2, F64, 2,
                               ptr_mod32=(8, 0, 0))
-    assert p["rows"]
+    assert p["rows"] and p["rowlen"] == 96               # c wider than the iteration: rows
     p = T.triot_plan_describe(0, [(4, 8192), (4, 8000)], None, 2, F32, 1, ptr_mod32=(4, 0, 0))
     assert p["rows"] and (p["seglen"], p["segm"], p["rowlen"]) == (500, 8000, 500)  # segments
     p = T.triot_plan_describe(1, [(4, 8191), (4, 8191), (4, 8191)], None, 2, F32, 2,
@@ -616,11 +616,13 @@ def test_model_segmented_rows_vs_oracle(seed):
     np.testing.assert_array_equal(_bits(out), _bits(ref))
     a = random_values(rng, dst_shape, "f32", "normal")
     b = random_values(rng, dst_shape, "f32", "normal")
-    refc = O.apply_binary(a, b, "add")
-    desc = T.triot_plan_describe(1, [dst_shape, dst_shape, dst_shape], None, 3, F32, 0,
+    cs = dst_shape[:-1] + (dst_shape[-1] + 8,)            # c wider: not dense, rows > 512
+    refc = np.full(cs, 5.0, dtype=np.float32)
+    O.apply_binary(a, b, "add", out=refc)
+    desc = T.triot_plan_describe(1, [cs, dst_shape, dst_shape], dst_shape, 3, F32, 0,
                                  ptr_mod32=(4, 0, 0), mode=0, warps=int(rng.integers(1, 5)))
     assert desc["rows"] and desc["seglen"] > 0, desc
-    c = np.full(dst_shape, 5.0, dtype=np.float32)
+    c = np.full(cs, 5.0, dtype=np.float32)
     kernel_model.run(desc, "binary", [c.reshape(-1), a.reshape(-1), b.reshape(-1)], binop="add")
     np.testing.assert_array_equal(_bits(c), _bits(refc))
 
@@ -630,7 +632,7 @@ def test_warp_per_row_plan_rule():
     outputs and short rows keep the row table."""
     p = T.triot_plan_describe(1, [(512,) * 3, (512,) * 3, (520,) * 3], (512,) * 3, 3, F32, 2,
                               ptr_mod32=(4, 0, 0))
-    assert p["rows"] and not p["rwarp"]                   # dense misaligned c: table
+    assert p["dshift"] == 1 and not p["rows"]             # dense misaligned c: shifted stores
     p = T.triot_plan_describe(0, [(41, 400), (40, 383)], None, 2, F32, 1)
     assert p["rows"] and p["rwarp"]                       # region only, rows of 383
     p = T.triot_plan_describe(1, [(40, 200), (40, 99), (40, 99)], (40, 99), 2, F64, 2)

@@ -904,8 +904,8 @@ def test_sharded_expected_value_over_nccl():
 
 
 def test_misaligned_merged_outputs():
-    """A fully merged pad into a dst one element off the 32-byte grid (shifted 32-B stores), and
-    a merged binary into a misaligned c (row segments of 512), bit-exact against the oracle."""
+    """A fully merged pad into a dst one element off the 32-byte grid and a merged binary into a
+    misaligned c (both shifted 32-B stores), bit-exact against the oracle."""
     rng = np.random.default_rng(33)
     src = rng.standard_normal((500, 512, 512)).astype(np.float32)
     desc = T.triot_plan_describe(0, [(512, 512, 512), src.shape], None, 3, T.TRIOT_F32, 0,
@@ -921,7 +921,7 @@ def test_misaligned_merged_outputs():
     b = rng.standard_normal((256, 512, 512)).astype(np.float32)
     desc = T.triot_plan_describe(1, [a.shape, a.shape, b.shape], None, 3, T.TRIOT_F32, 2,
                                  (4, 0, 0))
-    assert desc["rows"] and desc["seglen"] == 512
+    assert desc["dshift"] == 1
     refc = O.apply_binary(a, b, "mul")
     c = _dev(np.zeros(a.shape, np.float32), 1)
     T.apply_binary(_dev(a), _dev(b), "mul", out=c)
@@ -977,3 +977,26 @@ def test_shifted_stores_every_offset(dtype):
                     assert_bits_equal(dst, ref)
     finally:
         T.triot_set_launch_policy(-1, 0)
+
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_binary_shifted_stores_every_offset(dtype):
+    """Binary ops into a dense c at every element offset from the 32-byte grid (shifted 32-B
+    stores), including exact in place (c == a), bit-exact against the oracle."""
+    rng = np.random.default_rng(45)
+    V = 32 // np.dtype(dtype).itemsize
+    for ish, ash, bsh in [((37, 29, 16), (37, 30, 16), (38, 29, 24)), ((9, 64), (9, 64), (9, 64)),
+                          ((3, 1000), (3, 1000), (4, 1000))]:
+        a = rng.standard_normal(ash).astype(dtype)
+        b = rng.standard_normal(bsh).astype(dtype)
+        for op in ("add", "div"):
+            ref = O.apply_binary(a, b, op, iter_shape=ish)
+            for off in range(1, V):
+                c = _dev(np.full(ish, 9.0, dtype=dtype), off)
+                T.apply_binary(_dev(a), _dev(b), op, out=c, iter_shape=ish)
+                assert_bits_equal(c, ref)
+                if ash == ish:   # in place: a misaligned by the same offset, c == a
+                    at = _dev(a, off)
+                    T.apply_binary(at, _dev(b), op, out=at, iter_shape=ish)
+                    assert_bits_equal(at, ref)
