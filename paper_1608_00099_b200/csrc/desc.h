@@ -92,6 +92,9 @@ struct Desc {
   // embed into a dst dense in the counter whose base is misaligned by dshift elements (> 0):
   // aligned 32-byte stores of lane-shifted vectors (embed_shift_kernel)
   uint32_t dshift;
+  // EV of a view with odd rows: vectors padded past the row end; elements at column >= scols
+  // (row length) read as +0
+  uint32_t evpad;
   TensorAcc<IDX> t[TRIOT_MAXT];   // embed: dst, src; binary: c, a, b; EV: p; dot: a, b;
                                   // update: x, y, z
   void* out;             // EV: means (device)

@@ -1461,16 +1461,30 @@ __global__ void __launch_bounds__(kBlock, 4) ev_view_kernel(const __grid_constan
     ev_acc_init<D, IDX>(a);
     for (IDX b = base0; b < vend; b += (IDX)K * dv) {
       uint32_t buf[K][NW];
-      IDX offj[K];
+      IDX offj[K], colj[K];
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         offj[j] = off[0];
+        colj[j] = uo[D - 1] * (IDX)V;  // the vector's first column (padded rows: masking)
         odo_step<D, 1, false, IDX>(d, uo, off, oob);
       }
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         if (v + (IDX)j * dv < vend) {
-          load_vec<ESZ, V, IDX>(d.t[0], offj[j], lgL, buf[j]);
+          if (V > 1 && d.evpad) {  // padded odd rows: columns past the row are +0
+            const IDX tau = d.t[0].tau;
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+              if (colj[j] + (IDX)e < d.scols) {
+                Mem<ESZ>::ld(addr<ESZ>(d.t[0].ptr, offj[j] + (IDX)e * tau), buf[j] + e * EW);
+              } else {
+#pragma unroll
+                for (int q = 0; q < EW; ++q) buf[j][e * EW + q] = 0u;
+              }
+            }
+          } else {
+            load_vec<ESZ, V, IDX>(d.t[0], offj[j], lgL, buf[j]);
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < NW; ++q) buf[j][q] = 0u;

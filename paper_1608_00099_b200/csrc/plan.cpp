@@ -435,6 +435,22 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
     plan_flat(g, ax, na, nt, bounds, n);
     return;
   }
+  // The expected value of a view window whose rows take no vector width (odd lengths): vectors
+  // of V elements padded past the row end (the vector digit runs to ceil(n / V)); the kernel
+  // loads element-wise and masks the padding (ev_view_kernel, evpad) -- instead of one element
+  // per lane and odometer step.
+  const bool evpad = g.op == OP_EV && g.view && g_rows_on && cc[best].V == 1 && vmax > 1 &&
+                     nl > (uint64_t)vmax;
+  if (evpad) {
+    Cand p;
+    p.V = vmax;
+    p.R = 1;
+    p.collapsed = false;
+    p.D = na;
+    for (int x = 0; x < nt; ++x) p.vec[x] = false;
+    cc[0] = p;
+    best = 0;
+  }
   const Cand& c = cc[best];
   g.V = c.V;
   g.R = c.R;
@@ -496,6 +512,13 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
   g.N = 1;
   for (int k = 0; k < na; ++k) g.N *= ax[k].n;
   g.nvec = g.N / V;
+  if (evpad) {
+    g.ext[D - 1] = (nl + V - 1) / V;
+    g.bnd[D - 1] = g.ext[D - 1];
+    g.scols = nl;  // elements of a row; the padding past it is masked
+    g.evpad = true;
+    g.nvec = g.N / nl * g.ext[D - 1];
+  }
   g.nsteps = (g.nvec + 31) / 32;
   finish_geometry(g, nt);
   // 6. expected-value weight slots: digit k<D-1 -> axis; vector digit -> last (a) or row axis (b)
@@ -1150,7 +1173,7 @@ std::string describe(const Geom& g) {
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,"
            "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,\"pow2\":%s,\"lin0\":%llu,"
-           "\"seglen\":%llu,\"segm\":%llu,\"rwarp\":%s,\"dshift\":%u,",
+           "\"seglen\":%llu,\"segm\":%llu,\"rwarp\":%s,\"dshift\":%u,\"evpad\":%s,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
@@ -1161,7 +1184,7 @@ std::string describe(const Geom& g) {
            g.rows ? "true" : "false", (unsigned long long)g.rowlen, (unsigned long long)g.rmag,
            (unsigned long long)g.rwin, g.pow2 ? "true" : "false", (unsigned long long)g.lin0,
            (unsigned long long)g.seglen, (unsigned long long)g.segm, g.rwarp ? "true" : "false",
-           g.dshift);
+           g.dshift, g.evpad ? "true" : "false");
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

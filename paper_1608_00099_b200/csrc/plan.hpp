@@ -42,6 +42,7 @@ struct Geom {
   uint64_t seglen = 0, segm = 0;   // rows are segments of a split axis; segm = its embed bound
   bool rwarp = false;              // long rows: a warp per row instead of the row table
   uint32_t dshift = 0;             // embed: dst dense but misaligned by this many elements
+  bool evpad = false;              // EV of a view: vectors padded past odd rows (scols = n)
   uint64_t N = 0;
   uint64_t ext[TRIOT_MAXD] = {}, dlt[TRIOT_MAXD] = {}, bnd[TRIOT_MAXD] = {};
   uint32_t fdm[TRIOT_MAXD] = {}, fds[TRIOT_MAXD] = {};
@@ -149,6 +150,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.rmag = (uint32_t)g.rmag;
   d.rwin = (uint32_t)g.rwin;
   d.dshift = g.dshift;
+  d.evpad = g.evpad ? 1u : 0u;
   d.seglen = (IDX)g.seglen;
   d.segm = (IDX)g.segm;
   for (int k = 0; k < TRIOT_MAXD; ++k) {
