@@ -1000,3 +1000,26 @@ def test_binary_shifted_stores_every_offset(dtype):
                     at = _dev(a, off)
                     T.apply_binary(at, _dev(b), op, out=at, iter_shape=ish)
                     assert_bits_equal(at, ref)
+
+
+@pytest.mark.slow
+def test_u64_index_path_shifted_stores():
+    """The 64-bit-index shifted-store instance: a 4.3 G-element f32 dst one element off the
+    32-byte grid, checked on the device."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40e9:
+        pytest.skip("needs ~20 GB free")
+    dst_shape = (65537, 65536)
+    src = np.random.default_rng(19).random((5, 70001)).astype(np.float32)
+    desc = T.triot_plan_describe(0, [dst_shape, src.shape], None, 2, T.TRIOT_F32, 0, (4, 0, 0))
+    assert desc["idx64"] and desc["dshift"] == 1
+    buf = torch.full((65537 * 65536 + 1,), float("nan"), dtype=torch.float32, device=DEV)
+    dst = buf[1:].view(dst_shape)
+    T.embed(dst, _dev(src))
+    torch.cuda.synchronize()
+    assert torch.isnan(buf[0])                      # the element before dst is untouched
+    assert torch.equal(dst[:5, :], torch.from_numpy(src[:, :65536]).to(DEV))
+    for r0 in range(5, 65537, 8192):
+        assert int(torch.count_nonzero(dst[r0:r0 + 8192])) == 0
+    del dst, buf
+    torch.cuda.empty_cache()
