@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
 // head and lane 31 its tail element by element (the step's two partial chunks).
 template <int ESZ>
 __device__ __forceinline__ void store_shifted(char* a0, const uint32_t (&w)[8], int sw,
-                                              int lane) {
+                                              int lane, int nvalid = 32) {
   constexpr int EW = ESZ / 4;
   uint32_t prev[8], out[8];
 #pragma unroll
@@ -432,17 +432,17 @@ __device__ __forceinline__ void store_shifted(char* a0, const uint32_t (&w)[8], 
 #undef TRIOT_SHIFT_CASE
   }
   char* al = a0 - sw * 4;  // the 32-byte boundary below lane 0's vector
-  if (lane >= 1) {
+  if (lane >= 1 && lane < nvalid) {
     Mem<32>::st(al + 32 * lane, out);
-  } else {
+  } else if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < 8; q += EW)
       if (q < 8 - sw) Mem<ESZ>::st(a0 + q * 4, w + q);
   }
-  if (lane == 31) {
+  if (lane == nvalid - 1) {  // the last valid lane's tail: the partial chunk past it
 #pragma unroll
     for (int q = 0; q < 8; q += EW)
-      if (q >= 8 - sw) Mem<ESZ>::st(al + 32 * 32 + (q - (8 - sw)) * 4, w + q);
+      if (q >= 8 - sw) Mem<ESZ>::st(al + 32 * nvalid + (q - (8 - sw)) * 4, w + q);
   }
 }
 
@@ -856,6 +856,55 @@ __device__ __forceinline__ void embed_warp_row(const Desc<IDX>& d, IDX so, IDX d
   }
 }
 
+// A long row whose src is 32-byte aligned and whose length is a multiple of V (rows of a view
+// window at an odd offset, say): lanes move 32-byte vectors -- aligned loads, and stores
+// shifted to the 32-byte grid when the dst row is not (store_shifted); two vectors per lane in
+// flight.  Columns >= mrow read as +0.
+template <int ESZ, typename IDX>
+__device__ __forceinline__ void embed_warp_row_vec(const Desc<IDX>& d, IDX so, IDX dof, IDX mrow,
+                                                   IDX n, int lane) {
+  constexpr int V = 32 / ESZ;
+  constexpr int EW = ESZ / 4;
+  constexpr int KV = 2;
+  const char* sp = (const char*)d.t[1].ptr + (uint64_t)so * ESZ;
+  char* dp = (char*)d.t[0].ptr + (uint64_t)dof * ESZ;
+  const int sw = (int)(((uintptr_t)dp & 31u) >> 2);
+  const IDX nv = n / (IDX)V;
+  for (IDX v0 = 0; v0 < nv; v0 += 32 * KV) {
+    uint32_t w[KV][8];
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      const IDX vi = v0 + (IDX)(32 * j + lane);
+      const IDX c0 = vi * (IDX)V;
+      if (vi < nv && c0 + (IDX)V <= mrow) {
+        Mem<32>::ld(sp + (uint64_t)c0 * ESZ, w[j]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if (vi < nv && c0 + (IDX)e < mrow) {
+            Mem<ESZ>::ld(sp + (uint64_t)(c0 + (IDX)e) * ESZ, w[j] + e * EW);
+          } else {
+#pragma unroll
+            for (int q = 0; q < EW; ++q) w[j][e * EW + q] = 0u;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      const IDX vb = v0 + (IDX)(32 * j);
+      if (vb >= nv) break;
+      const int nvalid = (nv - vb) < (IDX)32 ? (int)(nv - vb) : 32;
+      char* a0 = dp + (uint64_t)vb * 32;
+      if (sw == 0) {
+        if (lane < nvalid) Mem<32>::st(a0 + 32 * lane, w[j]);
+      } else {
+        store_shifted<ESZ>(a0, w[j], sw, lane, nvalid);
+      }
+    }
+  }
+}
+
 template <int D, int ESZ, typename IDX, int K>
 __global__ void __launch_bounds__(kBlock) embed_rows_kernel(const __grid_constant__ Desc<IDX> d) {
   constexpr int EW = ESZ / 4;
@@ -1068,7 +1117,12 @@ __global__ void __launch_bounds__(kBlock) embed_rowsw_kernel(const __grid_consta
     for (uint32_t i = 0; i < nr; ++i) {
       const IDX so = shfl_idx(off[1], (int)i), dof = shfl_idx(off[0], (int)i);
       const IDX mrow = shfl_idx(mr, (int)i);
-      if (t1)
+      const bool vec_ok = t1 && n % (IDX)(32 / ESZ) == 0 &&
+                          (((uintptr_t)d.t[1].ptr + (uint64_t)so * ESZ) & 31u) == 0 &&
+                          (((uintptr_t)d.t[0].ptr + (uint64_t)dof * ESZ) & (ESZ - 1)) == 0;
+      if (vec_ok)
+        embed_warp_row_vec<ESZ, IDX>(d, so, dof, mrow, n, lane);
+      else if (t1)
         embed_warp_row<ESZ, IDX, KW, true>(d, so, dof, mrow, n, lane);
       else
         embed_warp_row<ESZ, IDX, KW, false>(d, so, dof, mrow, n, lane);

@@ -1023,3 +1023,24 @@ def test_u64_index_path_shifted_stores():
         assert int(torch.count_nonzero(dst[r0:r0 + 8192])) == 0
     del dst, buf
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_view_embed_long_rows_vectorized(dtype):
+    """Embeds into view windows at odd offsets whose rows are long and a multiple of the vector
+    width (a warp per row moving 32-B vectors, stores shifted to the 32-byte grid; partial last
+    vector groups), including src windows narrower than dst (zero padding), bit-exact."""
+    rng = np.random.default_rng(64)
+    for dbase, dstart, win, sw in [((24, 36, 300), (1, 3, 5), (20, 30, 256), 256),
+                                   ((9, 1100), (2, 7), (6, 1024), 1000),
+                                   ((5, 7, 520), (0, 1, 3), (4, 5, 512), 512)]:
+        src = rng.standard_normal(win[:-1] + (sw,)).astype(dtype)
+        db = np.full(dbase, 3.0, dtype=dtype)
+        ref = db.copy()
+        sl = tuple(slice(a, a + w) for a, w in zip(dstart, win))
+        tmp = np.empty(win, dtype=dtype)
+        O.embed(tmp, src)
+        ref[sl] = tmp
+        dbt = _dev(db)
+        T.embed_view(T.View(dbt, dstart, win), T.View(_dev(src)))
+        assert_bits_equal(dbt, ref)
