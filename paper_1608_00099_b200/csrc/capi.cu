@@ -76,6 +76,17 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_error(TRIOT_ERR_CUDA, "CUDA: %s: %s", what, cudaGetErrorString(e));
 }
 
+// The SM count of device `dev`, queried once and cached; g_mu must be held.
+int sms_locked(int dev, int* sms) {
+  if (dev < 0 || dev >= 64) return set_error(TRIOT_ERR_CUDA, "CUDA: device id %d", dev);
+  if (!g_sms[dev]) {
+    cudaError_t e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  }
+  *sms = g_sms[dev];
+  return TRIOT_OK;
+}
+
 // ---- work decomposition policy ----------------------------------
 // mode 0 = each warp streams a contiguous chunk; mode 1 = grid stride (all warps sweep one
 // window of the tensors together, which the B200 DRAM schedules better: tools/membench.py).
@@ -117,12 +128,7 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   int sms, occ;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (dev < 0 || dev >= 64) return set_error(TRIOT_ERR_CUDA, "CUDA: device id %d", dev);
-    if (!g_sms[dev]) {
-      e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-    }
-    sms = g_sms[dev];
+    if (int st = sms_locked(dev, &sms)) return st;
     auto it = g_occ.find(fn);
     if (it == g_occ.end()) {
       int nb = 0;
@@ -226,12 +232,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   int sms;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (dev < 0 || dev >= 64) return set_error(TRIOT_ERR_CUDA, "CUDA: device id %d", dev);
-    if (!g_sms[dev]) {
-      e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-    }
-    sms = g_sms[dev];
+    if (int st = sms_locked(dev, &sms)) return st;
     if (g_occ.find(fn) == g_occ.end()) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -430,15 +431,13 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
   // of outputs per SM the lane-per-output kernel issues ~6x fewer instructions per term.  It
   // iterates the smaller operand's index space (reversed order when that is rhs: tensors 0/1
   // and their extents swap).  Policy mode 1 forces the group kernel, mode 0 the lane kernel.
-  int sms = 148;
+  int sms = 148;  // the B200's count if the query fails (only the kernel choice depends on it)
   {
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) {
       std::lock_guard<std::mutex> lk(g_mu);
-      if (dev >= 0 && dev < 64) {
-        if (!g_sms[dev]) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms[dev]) sms = g_sms[dev];
-      }
+      int q = 0;
+      if (sms_locked(dev, &q) == TRIOT_OK) sms = q;
     }
   }
   const bool group = g_override.mode == 1 ||
