@@ -17,6 +17,16 @@
 // with the odometer of Alg 3, unrolled over the compile-time digit count (Alg 6) with
 // an early exit once no carry remains (amortised O(1)); each carry adds a precomputed
 // per-tensor delta, so offsets stay exactly equal to Horner of the new tuple.
+//
+// Kernel families (the plan picks one per call):
+//   embed_kernel / binary_kernel          32-B (16-B, 1-element) vectors; embed zero runs
+//   embed_shift_kernel / binary_shift_..  the same with stores shifted to the 32-byte grid
+//   *_flat_kernel                         flat vectors across rows (longer odd extents; EV)
+//   *_rows_kernel / *_rowsw_kernel        row windows: a lane per row in a shared-memory row
+//                                         table, or a warp per row (short odd rows, views)
+//   ev_kernel / ev_view_kernel / ev_tma   expected value (+ view, + opt-in bulk-copy pipeline)
+//   dot_kernel / update_kernel            Benchmarks 2 and 3
+//   conv_kernel / conv_lane_kernel        Benchmark 4, Alg 15 naive convolution
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
