@@ -22,6 +22,8 @@
  *   - apply_binary             Alg 9 apply_tensors with body c = a OP b, each operand indexed
  *                              by its own shape.
  *   - expected_value           Alg 11 with one tensor: m_k = sum_t t_k * p[t].
+ *   - expected_value_abs       sum_t |t_k * p[t]|: the scale of the signed-input tolerance
+ *                               over Alg 11's terms.
  *
  * Every loop is the paper's: t starts at the zero tuple (Alg 6's memset), every tensor
  * offset is recomputed from the full tuple with Alg 2 (never the "offset is just i" shortcut of
@@ -31,8 +33,10 @@
  * flag would turn on FTZ/DAZ and FMA contraction and break bit parity).
  *
  * Parity pins: tests/test_oracle_pins.py checks every function here against values the paper
- * prints (651), closed forms, numpy library special cases and brute force.  No function
- * in this file is "parity unpinned".
+ * prints (651), closed forms, numpy library special cases and brute force;
+ * expected_value_abs by exact-rational brute force on signed inputs and the closed form
+ * p == -1 -> N (n_k - 1) / 2 (test_ev_abs_scale_*).  No function in this file is "parity
+ * unpinned".
  */
 #include <stdint.h>
 #include <string.h>

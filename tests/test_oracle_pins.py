@@ -329,6 +329,43 @@ def test_ev_fraction_brute_force():
             assert abs(Fraction(m[k]) - exact) <= Fraction(1, 10 ** 15) * max(abs(exact), 1)
 
 
+def test_ev_abs_scale_fraction_brute_force():
+    """oracle_expected_value_abs = sum_t |t_k * p[t]| (the scale of SURVEY Q12's signed-input
+    bound on Alg 11's terms), against itertools + the P:50 sum in exact rationals, on
+    signed inputs (a dropped abs, a dropped t_k weight or a wrong index fails), f64 and f32."""
+    rng = np.random.default_rng(161)
+    for d in (1, 2, 3, 4, 5):
+        for dt in (np.float64, np.float32):
+            shape = random_shape(rng, d, 500, lo=1, hi=7)
+            p = (rng.standard_normal(shape) * 3.0).astype(dt)
+            got = O.expected_value_abs(p)
+            pf = p.ravel()
+            for k in range(d):
+                exact = sum(abs(Fraction(t[k]) * Fraction(float(pf[p50_flat_index(t, shape)])))
+                            for t in brute_tuples(shape))
+                # a sum of <= 500 non-negative terms, each rounded once: rel error <= 1e-13
+                assert abs(Fraction(got[k]) - exact) <= Fraction(1, 10 ** 13) * max(exact, 1e-300)
+
+
+def test_ev_abs_scale_closed_form_minus_one():
+    """p == -1 everywhere: sum_t |t_k * p[t]| = sum_t t_k = N * (n_k - 1) / 2, an exact integer."""
+    for shape in [(5,), (3, 4), (2, 7, 3), (4, 1, 6, 2), (3, 3, 3, 3, 3)]:
+        for dt in (np.float64, np.float32):
+            p = np.full(shape, -1.0, dtype=dt)
+            got = O.expected_value_abs(p)
+            n = math.prod(shape)
+            assert list(got) == [float(n * (s - 1) // 2) for s in shape], (shape, got)
+            # and the signed sum is its negation (same terms, sign flipped)
+            assert list(O.expected_value(p)) == [-float(n * (s - 1) // 2) for s in shape]
+
+
+def test_ev_abs_scale_equals_ev_on_nonnegative_input():
+    """On p >= 0 every term t_k p[t] is non-negative, so the scale equals the integer-exact EV."""
+    rng = np.random.default_rng(162)
+    p = rng.integers(0, 256, size=(6, 5, 7, 4)).astype(np.float64)
+    assert list(O.expected_value_abs(p)) == list(O.expected_value(p))
+
+
 def test_ev_numpy_marginal_route_C3():
     """'marginalization': E[t_k] = sum_v v * (sum of p over axes != k)[v]."""
     p = make_inputs("C3")["p"]
