@@ -211,6 +211,19 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
   return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args);
 }
 
+// Reductions: blocks per first-level ticket group, the power of two nearest sqrt(grid) from
+// above (>= TRIOT_EV_MIN_GROUP), so the two ordered sums on the critical path (a group's
+// partials, then the group slots) have about the same length.  Returns the workspace bytes the
+// grid needs.
+size_t set_rgroup(Geom& g, uint64_t grid, int nslots) {
+  uint32_t G = TRIOT_EV_MIN_GROUP;
+  while ((uint64_t)G * G < grid) G <<= 1;
+  g.rgroup = G;
+  const uint64_t ngrp = (grid + G - 1) / G;
+  return TRIOT_EV_WS_HEADER + (size_t)(grid + (ngrp > 1 ? ngrp : 0)) *
+                                  (size_t)ev_slot_pad(nslots) * sizeof(double);
+}
+
 // EV bulk-copy fast path: full 32-byte vectors, 32-B aligned p, one persistent block per SM
 int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, bool* used) {
   *used = false;
@@ -249,7 +262,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   g.dv = (uint64_t)block;  // threads step by one block
   set_step(g);
   uint64_t grid = (g.nvec + g.wmul - 1) / g.wmul;
-  size_t need_ws = TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)ev_slot_pad(g.D + 2) * sizeof(double);
+  size_t need_ws = set_rgroup(g, grid, g.D + 2);
   if (!ws || ws_bytes < need_ws)
     return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                      need_ws);
@@ -285,8 +298,7 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
     if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no zero-run instance for D=%d", g.D);
   }
   if (g.op == OP_EV || g.op == OP_DOT) {
-    const size_t slots = (size_t)ev_slot_pad(g.op == OP_DOT ? 1 : g.D + 2);
-    size_t need = TRIOT_EV_WS_HEADER + (size_t)grid * slots * sizeof(double);
+    size_t need = set_rgroup(g, grid, g.op == OP_DOT ? 1 : g.D + 2);
     if (!ws || ws_bytes < need)
       return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                        need);
@@ -310,8 +322,9 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   return launch_pdl((const void*)&ev_final_kernel<kFinBlock>, 1, kFinBlock, 0, s, args);
 }
 
-size_t ev_ws_bytes(int d) {
-  return TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * (size_t)ev_slot_pad(d + 2) * sizeof(double);
+size_t ev_ws_bytes(int nslots) {
+  return TRIOT_EV_WS_HEADER + (size_t)(TRIOT_EV_MAX_GRID + TRIOT_EV_MAX_GROUPS) *
+                                  (size_t)ev_slot_pad(nslots) * sizeof(double);
 }
 
 }  // namespace
@@ -385,7 +398,7 @@ int triot_apply_binary_view(const triot_view* c, const triot_view* a, const trio
 
 int triot_inner_product_workspace_size(size_t* bytes) {
   if (!bytes) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: bytes is NULL");
-  *bytes = TRIOT_EV_WS_HEADER + (size_t)TRIOT_EV_MAX_GRID * sizeof(double);
+  *bytes = ev_ws_bytes(1);
   return TRIOT_OK;
 }
 
@@ -489,7 +502,7 @@ int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, 
   // validate the shape exactly like the real call (pointer checks skipped: no data yet)
   int st = plan_ev(g, (const void*)(uintptr_t)64, shape, d, dtype);
   if (st) return st;
-  *bytes = ev_ws_bytes(d);
+  *bytes = ev_ws_bytes(d + 2);
   return TRIOT_OK;
 }
 
@@ -599,6 +612,22 @@ int triot_set_launch_policy(int mode, int blocks_per_sm) {
   g_override.mode = mode;
   g_override.bpsm = mode < 0 ? 0 : blocks_per_sm;
   g_override.q = 0;
+  return TRIOT_OK;
+}
+
+int triot_fx_sum(const double* x, size_t n, double* out) {
+  if (!out || (n && !x)) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: x or out is NULL");
+  long long L[kFxNL];
+  memset(L, 0, sizeof(L));
+  unsigned fl = 0;
+  for (size_t i = 0; i < n; ++i) fx_add(L, x[i], &fl);
+  int lo = -1, hi = -1;
+  for (int i = 0; i < kFxNL; ++i)
+    if (L[i]) {
+      if (lo < 0) lo = i;
+      hi = i;
+    }
+  *out = fx_apply_flags(lo < 0 ? 0.0 : fx_round(L, lo, hi), fl);
   return TRIOT_OK;
 }
 

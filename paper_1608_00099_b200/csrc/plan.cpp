@@ -652,6 +652,9 @@ struct TArg {
   uint64_t sig[TRIOT_MAXD];    // Horner strides of the base shape
   uint64_t numel;              // window elements
   uint64_t span;               // elements from ptr through the window's last element (0 if empty)
+  const void* base;            // the base buffer (== ptr for a dense tensor)
+  int64_t start[TRIOT_MAXD];   // the window's start tuple in the base (0 for a dense tensor)
+  int d;
 };
 
 static void targ_span(TArg& t, int d) {
@@ -672,6 +675,9 @@ static int targ_dense(TArg& t, const char* name, const void* ptr, const int64_t*
   for (int k = 0; k < d; ++k) t.shape[k] = shape[k];
   strides_of(shape, d, t.sig);
   t.ptr = ptr;
+  t.base = ptr;
+  t.d = d;
+  for (int k = 0; k < d; ++k) t.start[k] = 0;
   targ_span(t, d);
   return TRIOT_OK;
 }
@@ -687,22 +693,42 @@ static int targ_view(TArg& t, const char* name, const triot_view* v, int d, int 
   uint64_t bias = 0;
   for (int k = 0; k < d; ++k) {
     const int64_t s0 = v->start ? v->start[k] : 0;
-    if (s0 < 0 || s0 + v->shape[k] > v->base_shape[k])
+    // shape and base_shape are >= 0 (check_shape), so the difference cannot overflow
+    if (s0 < 0 || s0 > v->base_shape[k] - v->shape[k])
       return set_error(TRIOT_ERR_AXIS_OUT_OF_BOUNDS,
                        "AxisOutOfBounds: view '%s' axis %d: start %lld + window %lld > base "
                        "extent %lld",
                        name, k, (long long)s0, (long long)v->shape[k],
                        (long long)v->base_shape[k]);
     t.shape[k] = v->shape[k];
+    t.start[k] = s0;
     bias += (uint64_t)s0 * t.sig[k];  // Horner of the start tuple
   }
   if ((st = check_ptr(name, v->data, t.numel, esz))) return st;
+  // a non-empty window has s0_k <= base_k - 1 on every axis, so bias <= nbase - 1 and
+  // bias * esz < 2^62 (check_shape); an empty window touches no memory and keeps bias 0 (its
+  // base may have zero extents, where the strides were never bounded)
+  if (t.numel == 0) bias = 0;
   t.ptr = (const char*)v->data + bias * (uint64_t)esz;
+  t.base = v->data;
+  t.d = d;
   targ_span(t, d);
   return TRIOT_OK;
 }
 
+// Two windows of one base laid out with the same strides share an element iff their boxes
+// [start, start + shape) intersect on every axis (a base tuple has one address: digits k >= 1
+// stay below their base extents); otherwise fall back to the conservative byte-span test.
 static bool targ_overlap(const TArg& a, const TArg& b, int esz) {
+  if (a.numel == 0 || b.numel == 0) return false;
+  bool same_layout = a.base == b.base && a.d == b.d;
+  for (int k = 0; same_layout && k < a.d; ++k) same_layout = a.sig[k] == b.sig[k];
+  if (same_layout) {
+    for (int k = 0; k < a.d; ++k)
+      if (a.start[k] >= b.start[k] + b.shape[k] || b.start[k] >= a.start[k] + a.shape[k])
+        return false;
+    return true;
+  }
   return overlap(a.ptr, a.span, b.ptr, b.span, esz);
 }
 
@@ -1119,7 +1145,7 @@ int plan_ev_view(Geom& g, const triot_view* p, int d, int dtype) {
   g.d = d;
   g.ntensor = 1;
   g.t[0].ptr = tp.ptr;
-  g.t[0].numel = tp.numel;
+  g.t[0].numel = tp.span;  // the index width must cover the window's span in the base
   if (tp.numel == 0) {
     g.empty = true;
     clear_error();
