@@ -320,12 +320,6 @@ TRIOT_API int triot_set_launch_policy(int mode, int blocks_per_sm);
  * equals n / divisor for every 32-bit n.  divisor must be >= 1. */
 TRIOT_API int triot_fastdiv_magic(uint32_t divisor, uint32_t* mul, uint32_t* shift);
 
-/* The exact-accumulation arithmetic the expected value's dynamic kernel uses to combine its
- * per-unit partial sums (so the result does not depend on which block took which unit):
- * *out = the double nearest (ties to even) to the exact sum of x[0..n-1]; NaN if any x is NaN or
- * both infinities occur, else +-inf if one does (or the exact sum overflows).  Host memory, host
- * computation (the same code the kernel runs); n may be 0 (*out = +0.0). */
-TRIOT_API int triot_fx_sum(const double* x, size_t n, double* out);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED
                    TriotError, check, lib, triot_apply_binary, triot_embed,
                    triot_expected_value, triot_expected_value_mass,
                    triot_expected_value_workspace_size,
-                   triot_fastdiv_magic, triot_fx_sum, triot_last_error, triot_max_dimension,
+                   triot_fastdiv_magic, triot_last_error, triot_max_dimension,
                    triot_plan_describe, triot_set_launch_policy, triot_status_string,
                    LIB_PATH)
 from .api import (OPS, View, apply_binary, apply_binary_view, embed, embed_view,
@@ -39,5 +39,5 @@ __all__ = [
     "triot_embed", "triot_apply_binary", "triot_expected_value", "triot_expected_value_mass",
     "triot_expected_value_workspace_size", "triot_max_dimension", "triot_status_string",
     "triot_last_error", "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic",
-    "triot_fx_sum", "LIB_PATH",
+    "LIB_PATH",
 ]

@@ -32,7 +32,7 @@ EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "tr
            "triot_expected_value_view",
            "triot_inner_product_workspace_size", "triot_inner_product", "triot_fused_update",
            "triot_naive_convolve", "triot_embed_host", "triot_apply_binary_host",
-           "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic", "triot_fx_sum")
+           "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
 
 
 class TriotError(RuntimeError):
@@ -110,8 +110,6 @@ _lib.triot_plan_describe.argtypes = [ctypes.c_int, ctypes.POINTER(_i64p), _i64p,
                                      ctypes.c_size_t]
 _lib.triot_set_launch_policy.restype = ctypes.c_int
 _lib.triot_set_launch_policy.argtypes = [ctypes.c_int, ctypes.c_int]
-_lib.triot_fx_sum.restype = ctypes.c_int
-_lib.triot_fx_sum.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double)]
 _lib.triot_fastdiv_magic.restype = ctypes.c_int
 _lib.triot_fastdiv_magic.argtypes = [ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_uint32)]
@@ -273,12 +271,3 @@ def triot_fastdiv_magic(divisor: int) -> tuple[int, int]:
     check(_lib.triot_fastdiv_magic(divisor, ctypes.byref(m), ctypes.byref(s)))
     return int(m.value), int(s.value)
 
-
-def triot_fx_sum(values) -> float:
-    """Host diagnostic: the exact sum of `values` (float64), rounded once to nearest even, by the
-    same fixed-point code the expected value's dynamic kernel runs on the device."""
-    import numpy as np
-    a = np.ascontiguousarray(values, dtype=np.float64)
-    out = ctypes.c_double(0.0)
-    check(_lib.triot_fx_sum(a.ctypes.data if a.size else None, a.size, ctypes.byref(out)))
-    return float(out.value)

@@ -211,17 +211,9 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
   return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args);
 }
 
-// Reductions: blocks per first-level ticket group, the power of two nearest sqrt(grid) from
-// above (>= TRIOT_EV_MIN_GROUP), so the two ordered sums on the critical path (a group's
-// partials, then the group slots) have about the same length.  Returns the workspace bytes the
-// grid needs.
-size_t set_rgroup(Geom& g, uint64_t grid, int nslots) {
-  uint32_t G = TRIOT_EV_MIN_GROUP;
-  while ((uint64_t)G * G < grid) G <<= 1;
-  g.rgroup = G;
-  const uint64_t ngrp = (grid + G - 1) / G;
-  return TRIOT_EV_WS_HEADER + (size_t)(grid + (ngrp > 1 ? ngrp : 0)) *
-                                  (size_t)ev_slot_pad(nslots) * sizeof(double);
+// Reductions: workspace bytes a grid needs (the counter header, one P-slot partial per block).
+size_t reduce_ws_bytes(uint64_t grid, int nslots) {
+  return TRIOT_EV_WS_HEADER + (size_t)grid * (size_t)ev_slot_pad(nslots) * sizeof(double);
 }
 
 // EV bulk-copy fast path: full 32-byte vectors, 32-B aligned p, one persistent block per SM
@@ -262,7 +254,7 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   g.dv = (uint64_t)block;  // threads step by one block
   set_step(g);
   uint64_t grid = (g.nvec + g.wmul - 1) / g.wmul;
-  size_t need_ws = set_rgroup(g, grid, g.D + 2);
+  size_t need_ws = reduce_ws_bytes(grid, g.D + 2);
   if (!ws || ws_bytes < need_ws)
     return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                      need_ws);
@@ -288,8 +280,11 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   }
   const void* fn = table_for(g)(g.D, vindex(g), g.idx64 ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no instance for D=%d V=%d", g.D, g.V);
+  const bool red = g.op == OP_EV || g.op == OP_DOT;
+  // EV: partials per block summed by ev_final_kernel (PDL) instead of the last block (mode 4)
+  g.split = g.op == OP_EV && (g_override.mode == 4 || (g_override.mode < 0 && kEvSplitDefault));
   int max_grid = 1 << 30;
-  if (g.op == OP_EV || g.op == OP_DOT) max_grid = TRIOT_EV_MAX_GRID;
+  if (red) max_grid = TRIOT_EV_MAX_GRID;
   unsigned grid;
   int st = launch_geometry(fn, g, max_grid, &grid);
   if (st) return st;
@@ -298,14 +293,11 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
     if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no zero-run instance for D=%d", g.D);
   }
   if (g.op == OP_EV || g.op == OP_DOT) {
-    size_t need = set_rgroup(g, grid, g.op == OP_DOT ? 1 : g.D + 2);
+    size_t need = reduce_ws_bytes(grid, g.op == OP_DOT ? 1 : g.D + 2);
     if (!ws || ws_bytes < need)
       return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes,
                        need);
   }
-  // EV: partials per block, summed by ev_final_kernel (PDL) -- no fence or atomic ticket per
-  // block, so many short blocks cost no serialised tail (mode 4, see auto_policy)
-  g.split = g.op == OP_EV && (g_override.mode == 4 || (g_override.mode < 0 && kEvSplitDefault));
   cudaStream_t s = (cudaStream_t)stream;
   int st2 = g.idx64 ? launch_t<uint64_t>(g, fn, grid, s, out, ws)
                     : launch_t<uint32_t>(g, fn, grid, s, out, ws);
@@ -322,10 +314,7 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   return launch_pdl((const void*)&ev_final_kernel<kFinBlock>, 1, kFinBlock, 0, s, args);
 }
 
-size_t ev_ws_bytes(int nslots) {
-  return TRIOT_EV_WS_HEADER + (size_t)(TRIOT_EV_MAX_GRID + TRIOT_EV_MAX_GROUPS) *
-                                  (size_t)ev_slot_pad(nslots) * sizeof(double);
-}
+size_t ev_ws_bytes(int nslots) { return reduce_ws_bytes(TRIOT_EV_MAX_GRID, nslots); }
 
 }  // namespace
 }  // namespace triot
@@ -612,22 +601,6 @@ int triot_set_launch_policy(int mode, int blocks_per_sm) {
   g_override.mode = mode;
   g_override.bpsm = mode < 0 ? 0 : blocks_per_sm;
   g_override.q = 0;
-  return TRIOT_OK;
-}
-
-int triot_fx_sum(const double* x, size_t n, double* out) {
-  if (!out || (n && !x)) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: x or out is NULL");
-  long long L[kFxNL];
-  memset(L, 0, sizeof(L));
-  unsigned fl = 0;
-  for (size_t i = 0; i < n; ++i) fx_add(L, x[i], &fl);
-  int lo = -1, hi = -1;
-  for (int i = 0; i < kFxNL; ++i)
-    if (L[i]) {
-      if (lo < 0) lo = i;
-      hi = i;
-    }
-  *out = fx_apply_flags(lo < 0 ? 0.0 : fx_round(L, lo, hi), fl);
   return TRIOT_OK;
 }
 

@@ -73,7 +73,6 @@ struct Desc {
   int32_t slot_of_axis[TRIOT_MAXD + 1];  // out[j] = slot >= 0 ? total[slot] : 0 (slot D+1 = mass)
   int32_t op;            // binary op
   int32_t split;         // reductions: 1 = write the block partial only; ev_final_kernel sums
-  uint32_t rgroup;       // reductions: blocks per first-level group (ev_reduce's two tickets)
   // embed zero runs: 32 vectors == one unit of digit khi (lanes share digits 0..khi) and dst is
   // dense in the counter, so while a digit <= khi is out of bounds the warp stores zeros at
   // dst + r * step without touching the odometer (zmask = oob bits of digits 0..khi, 0 = off)
@@ -103,13 +102,10 @@ struct Desc {
 };
 
 // Workspace layout of the reductions (expected value, inner product):
-//   [tickets: u32 [0] = the grid's, u32 [64 + g] = group g's | up to TRIOT_EV_WS_HEADER bytes]
-//   [grid x P block partials] [ceil(grid / rgroup) x P group partials]   (P = slots per block)
-// Zero-filled once by the caller; every call leaves all tickets at 0.
-#define TRIOT_EV_MAX_GRID 32768
-#define TRIOT_EV_MIN_GROUP 16
-#define TRIOT_EV_WS_HEADER 16384
-#define TRIOT_EV_MAX_GROUPS (TRIOT_EV_MAX_GRID / TRIOT_EV_MIN_GROUP)
+//   [arrival counter u32 | pad to 256 B] [grid x P block partials]   (P = slots per block)
+// Zero-filled once by the caller; every call leaves the counter at 0.
+#define TRIOT_EV_MAX_GRID 8192
+#define TRIOT_EV_WS_HEADER 256
 // EV bulk-copy pipeline: NSTAGE shared-memory stages of SVEC 32-byte vectors per block
 #define TRIOT_EV_NSTAGE 6
 #define TRIOT_EV_SVEC 1024

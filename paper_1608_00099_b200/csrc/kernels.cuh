@@ -30,7 +30,6 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <string.h>
 
 #include "desc.h"
 
@@ -1331,152 +1330,135 @@ __device__ __forceinline__ double warp_reduce_scatter(const double (&acc)[NS], i
   return a[0];
 }
 
-// Ordered sum of `total` partials laid out [block][P slots] (P divides BLOCK): thread t always
-// meets slot t % P and sums entries t, t + BLOCK, ... in order, 8 loads in flight; lanes with
-// the same slot are then combined by a butterfly and the warps' sums land in sm[warp][slot].  A
-// fixed function of the partials' values: whichever block runs it gets the same bits.
+// Ordered sum of `nparts` partials laid out [part][P slots] (P = ev_slot_pad(NS)), read as
+// 32-byte chunks, 4 chunks per thread in flight: chunk c holds the doubles 4c .. 4c+3, i.e. slots
+// (4c + q) % P, and since BLOCK * 4 is a multiple of P thread t always meets slots (4t + q) % P.
+// Lanes that meet the same slots are combined by a butterfly, warps in index order: a fixed
+// function of the partials, whichever block runs it.  Leaves the NS totals in sm[0][0..NS-1].
 template <int NS, int BLOCK>
-__device__ __forceinline__ void ordered_slot_sum(const double* src, unsigned total,
+__device__ __forceinline__ void ordered_slot_sum(const double* src, unsigned nparts,
                                                  double (&sm)[BLOCK / 32][NS]) {
   constexpr int P = ev_slot_pad(NS);
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  double f = 0.0;
-  for (unsigned i0 = threadIdx.x; i0 < total; i0 += 8 * BLOCK) {
-    double x[8];
+  static_assert((4 * BLOCK) % P == 0, "slots must tile the block");
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned total = nparts * (unsigned)P;
+  const unsigned nchunk = (total + 3u) / 4u;
+  double f[4] = {0.0, 0.0, 0.0, 0.0};
+  for (unsigned c0 = threadIdx.x; c0 < nchunk; c0 += 4u * BLOCK) {
+    uint32_t w[4][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const unsigned idx = i0 + (unsigned)i * BLOCK;
-      x[i] = idx < total ? __ldcg(src + idx) : 0.0;
+    for (int i = 0; i < 4; ++i) {
+      const unsigned c = c0 + (unsigned)i * BLOCK;
+      if (c < nchunk && 4u * c + 3u < total) {
+        asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3]), "=r"(w[i][4]),
+                       "=r"(w[i][5]), "=r"(w[i][6]), "=r"(w[i][7])
+                     : "l"(src + 4 * (size_t)c));
+      } else {  // past the end, or a ragged last chunk (P < 4): element by element
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double x = (c < nchunk && 4u * c + q < total) ? __ldcg(src + 4 * (size_t)c + q) : 0.0;
+          w[i][2 * q] = (uint32_t)__double2loint(x);
+          w[i][2 * q + 1] = (uint32_t)__double2hiint(x);
+        }
+      }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) f += x[i];
-  }
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-  for (int o = 16; o >= P; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
-  if (lane < NS) sm[wib][lane] = f;
+      for (int q = 0; q < 4; ++q) f[q] += __hiloint2double((int)w[i][2 * q + 1], (int)w[i][2 * q]);
+  }
+  if (P >= 4) {
+    constexpr int OMIN = P >= 4 ? P / 4 : 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int o = 16; o >= OMIN; o >>= 1) f[q] += __shfl_xor_sync(0xffffffffu, f[q], o);
+    if (lane < OMIN) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * lane + q < NS) sm[wib][4 * lane + q] = f[q];
+    }
+  } else {
+    double g[2] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) g[q % (P < 1 ? 1 : P)] += f[q];
+#pragma unroll
+    for (int q = 0; q < (P < 1 ? 1 : P); ++q) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) g[q] += __shfl_xor_sync(0xffffffffu, g[q], o);
+      if (lane == 0 && q < NS) sm[wib][q] = g[q];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < NS) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
+    sm[0][threadIdx.x] = t;  // each thread reads and writes its own column only
+  }
   __syncthreads();
 }
 
-__device__ __forceinline__ unsigned ticket_take(unsigned* t) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
-  return old;
-}
-
-// Fixed-order block reduction with two levels of tickets ("each thread computes its own
-// pre-result and these pre-results are amalgamated"):
-//   1. warp reduce-scatter, warps in index order -> one partial per block (slot blockIdx);
-//   2. blocks form groups of rgroup consecutive blocks; the last block of a group to arrive
-//      (acq_rel ticket) sums the group's partials in block order into the group's slot;
-//   3. the last group to finish sums the group slots in group order and writes the result.
-// Every sum runs in a fixed order over fixed operands, so the result is deterministic run to
-// run for a fixed grid; the critical path after the last load is two short ordered sums instead
-// of one over the whole grid (C3 at 16 blocks per SM: 2,368 x 8 partials serially in one block
-// was ~10 L2 round trips).  A grid of one group skips level 3.
+// Fixed-order block reduction ("each thread computes its own pre-result and these pre-results
+// are amalgamated"): warp reduce-scatter, warps in index order -> one partial per block
+// (slot blockIdx); then every block but the last-launched one *arrives* on a counter with a
+// release reduction and exits -- no block waits on an atomic's reply (a ticket per block held
+// its slot for ~0.5-1 us: profiles/r02_ev4_tail.jsonl, r02_ev7_k*) -- while the last-launched
+// block (dispatched last, so every other block is resident or done) has one thread poll the
+// counter until the grid - 1 arrivals are in, then sums the partials in block order
+// (ordered_slot_sum) and writes the result.  Deterministic for a fixed grid; the counter is left
+// at 0 for the next call.  (Measured alternatives: profiles/r02_ev*.)
 template <int NS, int BLOCK, typename IDX>
 __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS]) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   constexpr int GRP = NS <= 1 ? 32 : NS <= 2 ? 16 : NS <= 4 ? 8 : NS <= 8 ? 4 : NS <= 16 ? 2 : 1;
   __shared__ double sm[BLOCK / 32][NS];
-  __shared__ int is_last;
   {
     int slot;
     const double v = warp_reduce_scatter<NS>(acc, lane, slot);
     if ((lane & (GRP - 1)) == 0 && slot < NS) sm[wib][slot] = v;
   }
   __syncthreads();
-  unsigned* tickets = (unsigned*)d.ws;
+  unsigned* ctr = (unsigned*)d.ws;
   double* part = (double*)((char*)d.ws + TRIOT_EV_WS_HEADER);
   constexpr int P = ev_slot_pad(NS);
   static_assert(BLOCK % P == 0, "slots must tile the block");
-  // thread s < P: the block-order sum of slot s over the warps (padding slots carry +0.0)
-  auto warp_sum = [&]() {
+  if (threadIdx.x < P) {  // the block-order sum of slot t over the warps (padding slots: +0.0)
     double t = 0.0;
     if (threadIdx.x < NS) {
 #pragma unroll
       for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
     }
-    return t;
-  };
-  if (threadIdx.x < P) part[(size_t)blockIdx.x * P + threadIdx.x] = warp_sum();
+    part[(size_t)blockIdx.x * P + threadIdx.x] = t;
+  }
   if (d.split) return;  // ev_final_kernel sums the partials once this grid has completed
-#ifdef TRIOT_EV_TAIL  // diagnostic builds only (tools/ev_shot_probe): cost of the ticket tail
-  if (TRIOT_EV_TAIL == 1) return;
-  if (TRIOT_EV_TAIL == 2 || TRIOT_EV_TAIL == 3) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (TRIOT_EV_TAIL == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      unsigned old;
-      asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(tickets) : "memory");
-      is_last = old == gridDim.x - 1;
+  __syncthreads();      // this block's partial stores precede thread 0's release below
+  if (blockIdx.x != gridDim.x - 1) {
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    TRIOT_TRACE(3);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const unsigned target = gridDim.x - 1;
+    unsigned c;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
+    while (c < target) {
+      __nanosleep(64);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
     }
-    __syncthreads();
-    if (is_last && threadIdx.x == 0) *tickets = 0u;
-    return;
+    // synchronizes with every arrival's release (they form a release sequence on the counter)
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
+    *ctr = 0u;  // every arrival is in: leave the counter ready for the next call
   }
-  if (TRIOT_EV_TAIL == 4) {  // relaxed fire-and-forget arrival, nobody waits
-    if (threadIdx.x == 0) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(tickets) : "memory");
-    return;
-  }
-  if (TRIOT_EV_TAIL == 5) {  // release fire-and-forget arrival
-    __syncthreads();
-    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(tickets) : "memory");
-    return;
-  }
-  if (TRIOT_EV_TAIL == 6) {  // acq_rel ticket with the result waited on, nothing after
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = ticket_take(tickets) == gridDim.x - 1;
-    if (threadIdx.x == 0 && is_last) *tickets = 0u;
-    return;
-  }
-  if (TRIOT_EV_TAIL == 7) {  // as 6 but only warp 0 stays for the ticket
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
-    if (threadIdx.x == 0) is_last = ticket_take(tickets) == gridDim.x - 1;
-    if (threadIdx.x == 0 && is_last) *tickets = 0u;
-    return;
-  }
-#endif
-  // Tickets: the barrier orders this block's partial stores before thread 0's acq_rel atomic
-  // (release is cumulative over them); the last arriver's acquire + barrier orders its partial
-  // loads (L2, __ldcg) after every other block's release.
-  const unsigned G = d.rgroup;
-  const unsigned ngrp = (gridDim.x + G - 1) / G;
-  const unsigned grp = blockIdx.x / G;
-  const unsigned gn = min(G, gridDim.x - grp * G);
-  unsigned* gticket = ngrp > 1 ? tickets + 64 + grp : tickets;
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = ticket_take(gticket) == (ngrp > 1 ? gn : gridDim.x) - 1;
-  __syncthreads();
-  TRIOT_TRACE(3);
-  if (!is_last) return;
-  if (threadIdx.x == 0) *gticket = 0u;  // every arrival is in: leave it ready for the next call
-  if (ngrp > 1) {
-    double* gpart = part + (size_t)gridDim.x * P;
-    __syncthreads();  // sm is rewritten below
-    ordered_slot_sum<NS, BLOCK>(part + (size_t)grp * G * P, gn * (unsigned)P, sm);
-    if (threadIdx.x < P) gpart[(size_t)grp * P + threadIdx.x] = warp_sum();
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = ticket_take(tickets) == ngrp - 1;
-    __syncthreads();
-    if (!is_last) return;
-    if (threadIdx.x == 0) *tickets = 0u;
-    __syncthreads();
-    ordered_slot_sum<NS, BLOCK>(gpart, ngrp * (unsigned)P, sm);
-  } else {
-    __syncthreads();
-    ordered_slot_sum<NS, BLOCK>(part, gridDim.x * (unsigned)P, sm);
-  }
+  __syncthreads();  // the acquire (thread 0) orders every thread's partial loads below
+  TRIOT_TRACE(5);
+  ordered_slot_sum<NS, BLOCK>(part, gridDim.x, sm);
   TRIOT_TRACE(6);
   if (threadIdx.x < (unsigned)d.d_out) {
     const int sl = d.slot_of_axis[threadIdx.x];
-    double t = 0.0;
-    if (sl >= 0) {
-      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][sl];
-    }
-    ((double*)d.out)[threadIdx.x] = t;
+    ((double*)d.out)[threadIdx.x] = sl >= 0 ? sm[0][sl] : 0.0;
   }
 }
 
@@ -1566,589 +1548,6 @@ __global__ void __launch_bounds__(kBlock, MINB) ev_kernel(const __grid_constant_
   TRIOT_TRACE(2);
   ev_reduce<NS, kBlock, IDX>(d, acc);
   TRIOT_TRACE(4);
-}
-
-// ---- one-shot expected value (the default for a dense p)
-// Block b owns the contiguous unit of kBlock * J vectors starting at b * kBlock * J (units past
-// the grid are taken grid-stride); thread t loads vectors base + t + kBlock * j, j < J, all in
-// one batch (a warp instruction covers 1 KB contiguous of p), then weights each vector by its
-// own digits, decoded from the vector index (shifts when every extent is a power of two,
-// multiply-high division otherwise): acc_k += u_k * s for the outer digits, the vector digit's
-// first column / row times s plus the in-vector weights.  No odometer, no per-warp chunk: a
-// block lives for one batch of loads, so the hardware block scheduler balances the SMs to the
-// end of the stream (a one-wave split left a 5 us spread of finish times on C3), and a thread's
-// result is the plain sum of J vector terms (no telescoped running mass).
-template <int D, int ESZ, int V, typename IDX>
-__device__ __forceinline__ void ev_shot_acc(const Desc<IDX>& d, const IDX (&u)[D],
-                                            const uint32_t* w, double (&acc)[D + 2]) {
-  constexpr int EW = ESZ / 4;
-  double x[V];
-#pragma unroll
-  for (int e = 0; e < V; ++e) x[e] = (double)Elem<ESZ>::get(w + e * EW);
-  double s = x[0];
-#pragma unroll
-  for (int e = 1; e < V; ++e) s += x[e];
-#pragma unroll
-  for (int k = 0; k < D - 1; ++k) acc[k] = fma((double)u[k], s, acc[k]);
-  const double uv = (double)(u[D - 1] * (d.rowmul + d.colmul));  // exact: < 2^53
-  double wr = 0.0, wc = 0.0;
-  if (V > 1 && d.collapsed == 0) {
-#pragma unroll
-    for (int e = 1; e < V; ++e) wc = fma((double)e, x[e], wc);
-  } else if (V > 1) {
-    const uint32_t lgL = d.lgL;
-#pragma unroll
-    for (int e = 1; e < V; ++e) {
-      const uint32_t r = (uint32_t)e >> lgL, c = (uint32_t)e & ((1u << lgL) - 1u);
-      if (r) wr = fma((double)r, x[e], wr);
-      if (c) wc = fma((double)c, x[e], wc);
-    }
-  }
-  const bool coll = d.collapsed != 0;
-  acc[D - 1] += fma(uv, s, coll ? wr : wc);
-  if (coll) acc[D] += wc;
-  acc[D + 1] += s;  // the mass (slab-sharded amalgamation term)
-}
-
-template <int D, int ESZ, int V, typename IDX, int J, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) ev_shot_kernel(const __grid_constant__ Desc<IDX> d) {
-  constexpr int EW = ESZ / 4;
-  constexpr int NW = V * EW;
-  constexpr int NS = D + 2;  // D digit slots + collapsed column slot + mass
-  double acc[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-  pdl_trigger();
-  pdl_wait();
-  const IDX unit = (IDX)kBlock * (IDX)J;
-  const IDX nunits = (d.nvec + unit - 1) / unit;
-  for (IDX b = blockIdx.x; b < nunits; b += gridDim.x) {
-    const IDX v0 = b * unit + (IDX)threadIdx.x;
-    uint32_t buf[J][NW];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const IDX v = v0 + (IDX)j * (IDX)kBlock;
-      if (v < d.nvec) ev_load<ESZ, V, IDX>(d.t[0], v, buf[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const IDX v = v0 + (IDX)j * (IDX)kBlock;
-      if (v < d.nvec) {
-        IDX u[D];
-        decode_digits<D, IDX>(d, v, u);
-        ev_shot_acc<D, ESZ, V, IDX>(d, u, buf[j], acc);
-      }
-    }
-  }
-  ev_reduce<NS, kBlock, IDX>(d, acc);
-}
-
-// ---- expected value with dynamic units (the default for a dense p)
-// A static split of p over one wave of blocks leaves the block finish times spread over ~5 us of
-// C3's ~24 (per-block DRAM bandwidth varies +-10 % run to run), and a grid of many short blocks
-// pays a release fence + ticket per block (measured ~0.5 us of a block's lifetime each).  So:
-// persistent blocks (kDyn threads, one wave) take *units* of R rounds of kDyn * J vectors from
-// an atomic counter (the first B units of each block are static: blockIdx + j * grid; later
-// ones are fetched one unit ahead by thread 0 and published through shared memory at the
-// per-unit barrier), with the loads of the next B - 1 rounds in flight in a register ring while
-// the current round is weighted.  Each unit's contribution is reduced in a fixed order (warp
-// reduce-scatter, warps by a butterfly) and stored in the unit's own partial slot -- no fence
-// per unit: the block's single release (its end-of-work ticket) covers every partial it wrote.
-// The last block sums the units' partials in unit order (one batch of 32-byte loads), so the
-// result is a fixed function of p, independent of which block took which unit: deterministic
-// ("each thread computes its own pre-result and these pre-results are amalgamated").
-constexpr int kDyn = 1024;
-constexpr int kDynFinalDoubles = kDyn * 16;  // partial doubles the final sum reads in one batch
-
-// Workspace: tickets[0] = grid ticket, tickets[1] = unit counter (both left at 0).
-template <int NS, typename IDX>
-__device__ __forceinline__ void dyn_final_sum(const Desc<IDX>& d, const double* part, IDX nunits,
-                                              double (&sm)[kDyn / 32][NS]) {
-  constexpr int P = ev_slot_pad(NS);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  // thread t reads 32-byte chunks c = t, t + kDyn, ...: chunk c holds partial doubles 4c..4c+3,
-  // i.e. slots (4c + i) % P, and since kDyn * 4 is a multiple of P, (4t + i) % P
-  const unsigned nchunk = (unsigned)((nunits * (IDX)P + 3) / 4);
-  const unsigned total = (unsigned)(nunits * (IDX)P);
-  double f[4] = {0.0, 0.0, 0.0, 0.0};
-  for (unsigned c0 = threadIdx.x; c0 < nchunk; c0 += 4 * kDyn) {
-    uint32_t w[4][8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const unsigned c = c0 + (unsigned)i * kDyn;
-      if (c < nchunk && 4 * c + 3 < total) {
-        asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3]), "=r"(w[i][4]),
-                       "=r"(w[i][5]), "=r"(w[i][6]), "=r"(w[i][7])
-                     : "l"(part + 4 * (size_t)c));
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // a ragged last chunk (P < 4) element by element
-          const double x = (c < nchunk && 4 * c + q < total) ? __ldcg(part + 4 * (size_t)c + q) : 0.0;
-          w[i][2 * q] = (uint32_t)__double2loint(x);
-          w[i][2 * q + 1] = (uint32_t)__double2hiint(x);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) f[q] += Elem<8>::get(&w[i][2 * q]);
-  }
-  // fold f[q] into slots, fixed order: P >= 4 -> lanes with equal lane % (P/4) share the slots
-  // of f[0..3]; P < 4 -> slot q % P within the thread first, then every lane shares the slots
-  double g[4];
-  if (P >= 4) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      g[q] = f[q];
-#pragma unroll
-      for (int o = 16; o >= (P >= 4 ? P / 4 : 1) && o >= 1; o >>= 1)
-        g[q] += __shfl_xor_sync(0xffffffffu, g[q], o);
-    }
-    if (lane < P / 4) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (4 * lane + q < NS) sm[wib][4 * lane + q] = g[q];
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) g[q] = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) g[q % (P < 1 ? 1 : P)] += f[q];
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) g[q] += __shfl_xor_sync(0xffffffffu, g[q], o);
-      if (lane == 0 && q < NS) sm[wib][q] = g[q];
-    }
-  }
-  __syncthreads();
-  // warp s sums slot s over the kDyn / 32 warps (butterfly, fixed order)
-  if (wib < NS) {
-    double t = sm[lane][wib];
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) sm[0][wib] = t;  // row 0 is no longer read by other warps' lanes > 0 ...
-  }
-  __syncthreads();
-}
-
-template <int D, int ESZ, int V, typename IDX, int J, int B>
-__global__ void __launch_bounds__(kDyn, 1) ev_dyn_kernel(const __grid_constant__ Desc<IDX> d) {
-  constexpr int EW = ESZ / 4;
-  constexpr int NW = V * EW;
-  constexpr int NS = D + 2;
-  constexpr int P = ev_slot_pad(NS);
-  constexpr int QN = 16;  // unit queue ring (>= 2 B)
-  static_assert(B >= 2 && 2 * B <= QN, "ring depth");
-  __shared__ double sm[2][kDyn / 32][NS];
-  __shared__ IDX uq[QN];
-  __shared__ int is_last;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned* tickets = (unsigned*)d.ws;
-  double* part = (double*)((char*)d.ws + TRIOT_EV_WS_HEADER);
-  const IDX RV = (IDX)kDyn * (IDX)J;  // vectors per round
-  const IDX R = d.wmul;               // rounds per unit
-  const IDX NU = d.wspan;             // units
-  const IDX G = gridDim.x;
-  pdl_trigger();
-  pdl_wait();
-  // unit sequence of this block: U(j) = blockIdx + j G for j < B, then B G + fetched ticket
-  IDX pend = 0;
-  if (threadIdx.x == 0) {
-    unsigned t;
-    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(tickets + 1) : "memory");
-    pend = (IDX)B * G + (IDX)t;
-  }
-  if (threadIdx.x < B) uq[threadIdx.x] = (IDX)blockIdx.x + (IDX)threadIdx.x * G;
-  __syncthreads();
-
-  uint32_t buf[B][J][NW];
-  // lookahead position (lk: unit sequence index, lr: round) of the next issue; U(lk) is read
-  // when issuing (lk <= k + B - 1: already published)
-  int lk = 0;
-  IDX lr = 0;
-  auto issue = [&](uint32_t (&bb)[J][NW]) {
-    const IDX lu = uq[lk % QN];
-    if (lu < NU) {
-      const IDX base = (lu * R + lr) * RV + (IDX)threadIdx.x;
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const IDX v = base + (IDX)j * (IDX)kDyn;
-        if (v < d.nvec) ev_load<ESZ, V, IDX>(d.t[0], v, bb[j]);
-      }
-    }
-    if (++lr == R) {
-      lr = 0;
-      ++lk;
-    }
-  };
-#pragma unroll
-  for (int b = 0; b < B - 1; ++b) issue(buf[b]);
-
-  int k = 0;  // unit sequence index being computed
-  IDX cu = (IDX)blockIdx.x, cr = 0;
-  double acc[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-  while (cu < NU) {
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (cu >= NU) break;
-      issue(buf[(b + B - 1) % B]);
-      {
-        const IDX base = (cu * R + cr) * RV + (IDX)threadIdx.x;
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const IDX v = base + (IDX)j * (IDX)kDyn;
-          if (v < d.nvec) {
-            IDX u[D];
-            decode_digits<D, IDX>(d, v, u);
-            ev_shot_acc<D, ESZ, V, IDX>(d, u, buf[b][j], acc);
-          }
-        }
-      }
-      if (++cr == R) {  // unit cu complete: fixed-order reduction into its slot
-        const int sb = k & 1;
-        {
-          int slot;
-          constexpr int GRP = NS <= 1 ? 32 : NS <= 2 ? 16 : NS <= 4 ? 8 : NS <= 8 ? 4 : NS <= 16 ? 2 : 1;
-          const double v = warp_reduce_scatter<NS>(acc, lane, slot);
-          if ((lane & (GRP - 1)) == 0 && slot < NS) sm[sb][wib][slot] = v;
-        }
-        if (threadIdx.x == 0) {  // publish U(k + B), fetch U(k + B + 1)
-          uq[(k + B) % QN] = pend;
-          unsigned t;
-          asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(tickets + 1) : "memory");
-          pend = (IDX)B * G + (IDX)t;
-        }
-        __syncthreads();
-        if (wib < P) {  // warp s: slot s over the warps (padding slots store +0.0)
-          double t = wib < NS ? sm[sb][lane][wib < NS ? wib : 0] : 0.0;
-#pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-          if (lane == 0) part[(size_t)cu * P + wib] = t;
-        }
-#pragma unroll
-        for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-        ++k;
-        cu = uq[k % QN];
-        cr = 0;
-      }
-    }
-  }
-  // every unit partial of this block is stored: one release + ticket per block
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = ticket_take(tickets) == gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  if (threadIdx.x == 0) {
-    tickets[0] = 0u;
-    tickets[1] = 0u;
-  }
-  dyn_final_sum<NS, IDX>(d, part, NU, sm[0]);
-  if (threadIdx.x < (unsigned)d.d_out) {
-    const int sl = d.slot_of_axis[threadIdx.x];
-    ((double*)d.out)[threadIdx.x] = sl >= 0 ? sm[0][0][sl] : 0.0;
-  }
-}
-
-// ---- exact (fixed-point) accumulation of fp64 values: order-independent, hence deterministic
-// under dynamic scheduling.  A double x = +-m 2^(b - 1074) (m < 2^53, b in [0, 2045]) is added
-// into NL 64-bit limbs of radix 2^32 (limb i weighs 2^(32 i - 1074)): the 85-bit m << (b % 32)
-// is split into three 32-bit chunks added (or subtracted) into limbs b / 32 .. b / 32 + 2.  Each
-// limb keeps 31 bits of headroom, so 2^31 additions cannot overflow; carries are propagated once
-// at the end.  Integer addition is associative, so the accumulated value -- the exact sum of
-// everything added -- does not depend on the order of the additions, and the final rounding to
-// double (round to nearest even, once) is a fixed function of it.
-constexpr int kFxNL = 68;    // limbs: 2^-1074 .. 2^1102 (b / 32 + 2 <= 65, plus carry room)
-constexpr int kFxBlock = 256;
-constexpr int kFxWarps = kFxBlock / 32;
-constexpr int kFxCopies = 4;  // global accumulator copies (spreads the end-of-block atomics)
-// non-finite flags per slot
-constexpr unsigned kFxPosInf = 1u, kFxNegInf = 2u, kFxNaN = 4u;
-
-// host + device (the host copy is exported for the CPU tests: triot_fx_sum)
-__host__ __device__ inline unsigned long long fx_bits(double x) {
-#ifdef __CUDA_ARCH__
-  return (unsigned long long)__double_as_longlong(x);
-#else
-  unsigned long long b;
-  memcpy(&b, &x, 8);
-  return b;
-#endif
-}
-__host__ __device__ inline double fx_double(unsigned long long b) {
-#ifdef __CUDA_ARCH__
-  return __longlong_as_double((long long)b);
-#else
-  double x;
-  memcpy(&x, &b, 8);
-  return x;
-#endif
-}
-__host__ __device__ inline int fx_clz64(unsigned long long v) {
-#ifdef __CUDA_ARCH__
-  return __clzll((long long)v);
-#else
-  return v ? __builtin_clzll(v) : 64;
-#endif
-}
-__host__ __device__ inline void fx_flag(unsigned* flag, unsigned f) {
-#ifdef __CUDA_ARCH__
-  atomicOr(flag, f);
-#else
-  *flag |= f;
-#endif
-}
-
-__host__ __device__ inline void fx_add(long long* limbs, double x, unsigned* flag) {
-  const unsigned long long bits = fx_bits(x);
-  const bool neg = (bits >> 63) != 0;
-  const unsigned E = (unsigned)(bits >> 52) & 0x7ffu;
-  unsigned long long m = bits & ((1ull << 52) - 1ull);
-  if (E == 0x7ffu) {
-    fx_flag(flag, m ? kFxNaN : (neg ? kFxNegInf : kFxPosInf));
-    return;
-  }
-  if (E == 0 && m == 0) return;  // +-0
-  unsigned b = 0;                 // subnormal: m 2^-1074
-  if (E) {
-    m |= 1ull << 52;
-    b = E - 1u;
-  }
-  const unsigned i = b >> 5, r = b & 31u;
-  const unsigned long long lo = m << r;                     // low 64 bits of m << r
-  const unsigned long long hi = r ? (m >> (64u - r)) : 0ull;  // bits 64.. (< 2^21)
-  const long long c0 = (long long)(lo & 0xffffffffull), c1 = (long long)(lo >> 32),
-                  c2 = (long long)hi;
-  if (neg) {
-    limbs[i] -= c0;
-    limbs[i + 1] -= c1;
-    limbs[i + 2] -= c2;
-  } else {
-    limbs[i] += c0;
-    limbs[i + 1] += c1;
-    limbs[i + 2] += c2;
-  }
-}
-
-// The double nearest (ties to even) to the exact value held in L[0..kFxNL-1] (destroyed);
-// lo / hi: the lowest / highest nonzero limb.
-__host__ __device__ inline double fx_round(long long* L, int lo, int hi) {
-  // 1. carry-propagate upward from lo: limbs below the top become digits in [0, 2^32); the
-  //    top limb keeps the sign (the value is negative iff it is)
-  long long carry = 0;
-  bool done = false;
-  for (int i = lo; i < kFxNL - 1; ++i) {
-    const long long t = L[i] + carry;
-    carry = t >> 32;  // arithmetic shift: floor division by 2^32
-    L[i] = t & 0xffffffffll;
-    if (i >= hi && carry == 0) {
-      done = true;
-      break;
-    }
-  }
-  if (!done) L[kFxNL - 1] += carry;
-  // 2. magnitude: negate (two's complement over the digits) when the top limb is negative
-  const bool neg = L[kFxNL - 1] < 0;
-  if (neg) {
-    long long bor = 0;
-    for (int i = lo; i < kFxNL; ++i) {
-      long long v = -L[i] - bor;
-      if (i < kFxNL - 1) {
-        bor = v < 0 ? 1 : 0;
-        v += bor << 32;
-      }
-      L[i] = v;
-    }
-  }
-  int h = kFxNL - 1;
-  while (h > lo && L[h] == 0) --h;
-  if (L[h] == 0) return 0.0;
-  // 3. X = digits h .. h-3 as 128 bits (xh:xl), bit 0 of X at absolute position base = 32(h-3)
-  //    (units of 2^-1074); digits below h-3 only matter as a sticky bit
-  auto dig = [&](int i) -> unsigned long long {
-    return (i >= lo && i >= 0) ? (unsigned long long)L[i] : 0ull;
-  };
-  const unsigned long long xh = (dig(h) << 32) | dig(h - 1);
-  const unsigned long long xl = (dig(h - 2) << 32) | dig(h - 3);
-  bool sticky = false;
-  for (int i = lo; i < h - 3; ++i) sticky |= L[i] != 0;
-  const int base = 32 * (h - 3);
-  const int msb = base + 127 - (xh ? fx_clz64(xh) : 64 + fx_clz64(xl));
-  // 4. keep 53 bits from the msb (or down to 2^-1074 for subnormal results): LSB at q
-  const int q = msb - 52 > 0 ? msb - 52 : 0;
-  const int s = q - base;  // in [1, 75]: h >= 3 -> msb >= 32 h -> s >= 44; h < 3 -> s >= 32
-  unsigned long long mant;
-  bool up;
-  if (s < 64) {
-    mant = (xl >> s) | (xh << (64 - s));
-    const unsigned long long rem = xl & ((1ull << s) - 1ull), half = 1ull << (s - 1);
-    up = rem > half || (rem == half && (sticky || (mant & 1ull)));
-  } else if (s == 64) {
-    mant = xh;
-    const unsigned long long half = 1ull << 63;
-    up = xl > half || (xl == half && (sticky || (mant & 1ull)));
-  } else {
-    const int t = s - 64;
-    mant = xh >> t;
-    const unsigned long long remh = xh & ((1ull << t) - 1ull), halfh = 1ull << (t - 1);
-    const bool below = xl != 0 || sticky;
-    up = remh > halfh || (remh == halfh && (below || (mant & 1ull)));
-  }
-  int qq = q;
-  if (up && ++mant == (1ull << 53)) {  // rounding carried into a new bit
-    mant >>= 1;
-    ++qq;
-  }
-  // assemble the bits: value = mant 2^(qq - 1074); normal iff mant >= 2^52 (biased exponent
-  // qq + 1), else subnormal (qq == 0, exponent field 0)
-  unsigned long long bits;
-  if (mant >= (1ull << 52)) {
-    const unsigned long long E = (unsigned long long)(qq + 1);
-    bits = E >= 2047 ? (2047ull << 52) : ((E << 52) | (mant & ((1ull << 52) - 1ull)));
-  } else {
-    bits = mant;
-  }
-  if (neg) bits |= 1ull << 63;
-  return fx_double(bits);
-}
-
-// NaN / infinity flags override the finite sum (IEEE: inf + -inf = NaN)
-__host__ __device__ inline double fx_apply_flags(double r, unsigned fl) {
-  if ((fl & kFxNaN) || ((fl & kFxPosInf) && (fl & kFxNegInf))) return fx_double(0x7ff8000000000000ull);
-  if (fl & kFxPosInf) return fx_double(0x7ff0000000000000ull);
-  if (fl & kFxNegInf) return fx_double(0xfff0000000000000ull);
-  return r;
-}
-
-// Per warp, p is consumed in units of 32 * K vectors (lane l: vectors l + 32 j of the unit, all
-// K loads in one batch, 8 KB per warp for 32-byte vectors); a unit's contribution is weighted
-// with the telescoped digit weights (ev_accumulate / ev_finish), reduced over the warp in a
-// fixed order and added exactly into the warp's fixed-point accumulator in shared memory.  Units
-// are handed out by an atomic counter (fetched one unit ahead), so every SM streams to the end.
-// At the end each block adds its exact sums into one of kFxCopies global accumulators (integer
-// atomics, exact), takes a ticket, and the last block rounds the exact totals to double.
-template <int D, int ESZ, int V, typename IDX, int K, int DYN = 1>
-__global__ void __launch_bounds__(kFxBlock, 2) ev_fx_kernel(const __grid_constant__ Desc<IDX> d) {
-  constexpr int EW = ESZ / 4;
-  constexpr int NW = V * EW;
-  constexpr int NS = D + 2;
-  constexpr int GRP = NS <= 1 ? 32 : NS <= 2 ? 16 : NS <= 4 ? 8 : NS <= 8 ? 4 : NS <= 16 ? 2 : 1;
-  extern __shared__ long long fxs[];  // [kFxWarps][NS][kFxNL]
-  __shared__ unsigned fxflag[NS];
-  __shared__ int is_last;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned* tickets = (unsigned*)d.ws;  // [0] grid ticket, [1] unit counter, [8 + s] flags
-  long long* gacc = (long long*)((char*)d.ws + TRIOT_EV_WS_HEADER);
-  long long* mine = fxs + (size_t)wib * NS * kFxNL;
-  for (int w = lane; w < NS * kFxNL; w += 32) mine[w] = 0;
-  if (threadIdx.x < NS) fxflag[threadIdx.x] = 0u;
-  __syncthreads();
-  pdl_trigger();
-  pdl_wait();
-  const IDX US = (IDX)32 * (IDX)K;
-  const IDX NU = (d.nvec + US - 1) / US;
-  const IDX GW = (IDX)gridDim.x * (IDX)kFxWarps;
-  IDX u = (IDX)blockIdx.x * (IDX)kFxWarps + (IDX)wib;
-  IDX nxt = 0;
-  if (lane == 0) {
-    unsigned t;
-    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(tickets + 1) : "memory");
-    nxt = GW + (IDX)t;
-  }
-  while (u < NU) {
-    const IDX v0 = u * US + (IDX)lane;
-    uint32_t buf[K][NW];
-#pragma unroll
-    for (int j = 0; j < K; ++j)
-      if (v0 + (IDX)(32 * j) < d.nvec) ev_load<ESZ, V, IDX>(d.t[0], v0 + (IDX)(32 * j), buf[j]);
-    IDX dg[D];
-    ev_decode<D, IDX>(d, v0, dg);
-    EvAcc<D> a;
-    ev_acc_init<D, IDX>(a);
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (v0 + (IDX)(32 * j) < d.nvec) ev_accumulate<D, ESZ, V, IDX>(d, buf[j], a);
-      if (j + 1 < K) digits_step_ev<D, IDX>(d, dg, a);
-    }
-    double acc[NS];
-    ev_finish<D, IDX>(d, dg, a, acc);
-    int slot;
-    const double val = warp_reduce_scatter<NS>(acc, lane, slot);
-    if ((lane & (GRP - 1)) == 0 && slot < NS) fx_add(mine + slot * kFxNL, val, &fxflag[slot]);
-    __syncwarp();
-    if (!DYN) {
-      u += GW;
-      continue;
-    }
-    u = shfl_idx<IDX>(nxt, 0);
-    if (lane == 0 && u < NU) {
-      unsigned t;
-      asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(tickets + 1) : "memory");
-      nxt = GW + (IDX)t;
-    }
-  }
-  __syncthreads();
-  // the block's exact sums into global copy blockIdx % kFxCopies (integer atomics: exact)
-  long long* gmine = gacc + (size_t)(blockIdx.x % kFxCopies) * NS * kFxNL;
-  for (int w = threadIdx.x; w < NS * kFxNL; w += kFxBlock) {
-    long long s = 0;
-#pragma unroll
-    for (int q = 0; q < kFxWarps; ++q) s += fxs[(size_t)q * NS * kFxNL + w];
-    if (s) asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(gmine + w), "l"(s) : "memory");
-  }
-  if (threadIdx.x < NS && fxflag[threadIdx.x])
-    atomicOr(tickets + 8 + threadIdx.x, fxflag[threadIdx.x]);
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = ticket_take(tickets) == gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  // last block: sum the copies (and clear them for the next call), then round each slot
-  long long* tot = fxs;  // [NS][kFxNL]
-  for (int w = threadIdx.x; w < NS * kFxNL; w += kFxBlock) {
-    long long s = 0;
-#pragma unroll
-    for (int c = 0; c < kFxCopies; ++c) {
-      s += __ldcg(gacc + (size_t)c * NS * kFxNL + w);
-      gacc[(size_t)c * NS * kFxNL + w] = 0;
-    }
-    tot[w] = s;
-  }
-  __syncthreads();
-  __shared__ double res[NS];
-  for (int sl = wib; sl < NS; sl += kFxWarps) {
-    long long* L = tot + (size_t)sl * kFxNL;
-    unsigned nzb[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int i = lane + 32 * c;
-      nzb[c] = __ballot_sync(0xffffffffu, i < kFxNL && L[i] != 0);
-    }
-    int lo = -1, hi = -1;
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      if (nzb[c] && lo < 0) lo = 32 * c + __ffs(nzb[c]) - 1;
-#pragma unroll
-    for (int c = 2; c >= 0; --c)
-      if (nzb[c] && hi < 0) hi = 32 * c + 31 - __clz(nzb[c]);
-    if (lane == 0) {
-      const unsigned fl = __ldcg(tickets + 8 + sl);
-      res[sl] = fx_apply_flags(lo < 0 ? 0.0 : fx_round(L, lo, hi), fl);
-      tickets[8 + sl] = 0u;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < (unsigned)d.d_out) {
-    const int sl = d.slot_of_axis[threadIdx.x];
-    ((double*)d.out)[threadIdx.x] = sl >= 0 ? res[sl] : 0.0;
-  }
-  if (threadIdx.x == 0) {
-    tickets[0] = 0u;
-    tickets[1] = 0u;
-  }
 }
 
 // Expected value of a view (NEXT-1): as ev_kernel, but p is the window of a larger base, so

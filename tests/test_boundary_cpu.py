@@ -4,7 +4,6 @@ geometry, carry deltas, fast-division magics) is checked against the oracle thro
 of the kernel algorithm (tests/kernel_model.py).  No compute call reaches the device here."""
 import ctypes
 import math
-from fractions import Fraction
 import os
 import re
 import subprocess
@@ -34,7 +33,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     decl = declared_symbols()
-    assert len(decl) == 21, decl
+    assert len(decl) == 20, decl
     out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))
@@ -655,63 +654,3 @@ def test_shifted_store_plan():
     p = T.triot_plan_describe(0, [(64, 64), (60, 60)], None, 2, F32, 1, ptr_mod32=(4, 0, 0))
     assert p["dshift"] == 0                               # region only: dst rows not dense
 
-
-# ---------------------------------------------------------------- exact accumulation (host copy)
-
-def _exact_round(vals):
-    """The correctly rounded (ties to even) sum of doubles, by exact rational arithmetic."""
-    s = sum((Fraction(v) for v in vals), Fraction(0))
-    try:
-        return float(s)           # int / int true division: correctly rounded
-    except OverflowError:
-        return math.inf if s > 0 else -math.inf
-
-
-def test_fx_sum_exact_random_ranges():
-    """triot_fx_sum (the fixed-point code the dynamic EV kernel runs) equals the correctly
-    rounded exact sum for random doubles over the whole exponent range, both signs, subnormals."""
-    rng = np.random.default_rng(2024)
-    for trial in range(300):
-        n = int(rng.integers(1, 400))
-        kind = trial % 5
-        if kind == 0:     # one magnitude band
-            v = rng.random(n) * 2.0 ** int(rng.integers(-1070, 1000))
-        elif kind == 1:   # wide exponent spread, mixed signs
-            v = rng.standard_normal(n) * np.exp2(rng.integers(-1000, 1000, n).astype(np.float64))
-        elif kind == 2:   # subnormals and tiny normals
-            v = (rng.integers(-(1 << 52), 1 << 52, n).astype(np.float64)) * 2.0 ** -1074
-        elif kind == 3:   # near-cancellation
-            a = rng.standard_normal(n // 2 + 1)
-            v = np.concatenate([a, -a[:-1] * (1 + 2.0 ** -52)])
-        else:             # EV-like: probabilities times coordinates
-            v = rng.random(n) / n * rng.integers(0, 16, n)
-        v = v[np.isfinite(v)]
-        got = T.triot_fx_sum(v)
-        exp = _exact_round(v.tolist())
-        assert got == exp or (math.isnan(got) and math.isnan(exp)), (trial, got, exp)
-        assert math.copysign(1, got) == math.copysign(1, exp) or got != 0
-
-
-def test_fx_sum_ties_sticky_overflow_specials():
-    one, ulp_half = 1.0, 2.0 ** -53
-    assert T.triot_fx_sum([one, ulp_half]) == 1.0                       # tie -> even
-    assert T.triot_fx_sum([one + 2 ** -52, ulp_half]) == 1.0 + 2 ** -51  # tie -> even (up)
-    assert T.triot_fx_sum([one, ulp_half, 2.0 ** -1074]) == 1.0 + 2 ** -52  # sticky breaks it
-    assert T.triot_fx_sum([-one, -ulp_half, -(2.0 ** -1074)]) == -(1.0 + 2 ** -52)
-    assert T.triot_fx_sum([]) == 0.0 and math.copysign(1, T.triot_fx_sum([])) == 1
-    assert T.triot_fx_sum([1e300, -1e300, 2.0 ** -1074]) == 2.0 ** -1074
-    assert T.triot_fx_sum([1.7e308, 1.7e308]) == math.inf
-    assert T.triot_fx_sum([-1.7e308, -1.7e308]) == -math.inf
-    assert T.triot_fx_sum([1.7e308, 1.7e308, -1.7e308]) == 1.7e308     # exact: no overflow
-    assert T.triot_fx_sum([1.0, math.inf]) == math.inf
-    assert T.triot_fx_sum([1.0, -math.inf]) == -math.inf
-    assert math.isnan(T.triot_fx_sum([math.inf, -math.inf]))
-    assert math.isnan(T.triot_fx_sum([1.0, math.nan]))
-    big = [2.0 ** 1023] * 3 + [-(2.0 ** 1023)] * 2                   # exact intermediate > max
-    assert T.triot_fx_sum(big) == 2.0 ** 1023
-    # order independence, bit for bit
-    rng = np.random.default_rng(7)
-    v = rng.standard_normal(1000) * np.exp2(rng.integers(-60, 60, 1000).astype(np.float64))
-    ref = T.triot_fx_sum(v)
-    for _ in range(5):
-        assert T.triot_fx_sum(rng.permutation(v)) == ref
