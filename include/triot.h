@@ -170,6 +170,28 @@ TRIOT_API int triot_expected_value_mass(double* out, const void* p, const int64_
                                         int dtype, void* workspace, size_t workspace_bytes,
                                         void* cuda_stream);
 
+/* ---- blocks of a larger PMF and the amalgamation of pre-results ----------------
+ *
+ * P:607 splits the outer loops across processors: "each thread computes its own pre-result and
+ * these pre-results are amalgamated".  triot_expected_value_offset computes Alg 11
+ * for a block p of a larger PMF whose element t sits at the global tuple offset + t:
+ *   out[j] = sum_t (offset[j] + t_j) p[t]  (j < d),  out[d] = sum_t p[t] if with_mass,
+ * evaluated on the device as m_j + offset[j] * mass (one rounding).  offset: host array of d
+ * entries in [0, 2^53] (NULL = zeros); everything else as triot_expected_value (device buffers,
+ * the same workspace, asynchronous on cuda_stream).  Summing the outputs of the blocks of a
+ * partition with triot_sum_rows gives the expected value of the whole PMF.
+ */
+TRIOT_API int triot_expected_value_offset(double* out, const void* p, const int64_t* shape,
+                                          const int64_t* offset, int d, int dtype, int with_mass,
+                                          void* workspace, size_t workspace_bytes,
+                                          void* cuda_stream);
+
+/* out[j] = sum_{r < nrows} rows[r * ncols + j] for j < ncols, rows added in order (deterministic):
+ * the amalgamation step.  Device buffers (out must not overlap rows), asynchronous on
+ * cuda_stream; nrows == 0 writes zeros. */
+TRIOT_API int triot_sum_rows(double* out, const double* rows, int64_t nrows, int64_t ncols,
+                             void* cuda_stream);
+
 /* ---- host-buffer entry points: chunked streaming through device staging memory --------
  *
  * "a GPU speed-up is most likely when operating on a large, contiguous block of memory,
@@ -186,6 +208,16 @@ TRIOT_API int triot_expected_value_mass(double* out, const void* p, const int64_
 TRIOT_API int triot_embed_host(void* dst, const int64_t* dst_shape, const void* src,
                                const int64_t* src_shape, int d, int dtype, unsigned flags,
                                void* staging, size_t staging_bytes, void* cuda_stream);
+
+/* The expected value (Alg 11) of a PMF in HOST memory: p streamed through the staging
+ * buffer in chunks of its leading axes ("copied to the GPU in chunks"), each chunk's
+ * triot_expected_value_offset written to a row in staging, the rows summed in chunk order
+ * (triot_sum_rows) and the d (+1 with_mass) doubles copied to the host array `out`.  The staging
+ * buffer also holds the reduction workspace (cleared by the call itself); `cuda_stream`
+ * completes when `out` is written.  Deterministic for a fixed staging size. */
+TRIOT_API int triot_expected_value_host(double* out, const void* p, const int64_t* shape, int d,
+                                        int dtype, int with_mass, void* staging,
+                                        size_t staging_bytes, void* cuda_stream);
 
 /* c (host, dense in iter_shape, NULL = element-wise min) = a OP b, all host buffers. */
 TRIOT_API int triot_apply_binary_host(void* c, const void* a, const int64_t* a_shape,

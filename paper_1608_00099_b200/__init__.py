@@ -24,7 +24,9 @@ from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED
                    LIB_PATH)
 from .api import (OPS, View, apply_binary, apply_binary_view, embed, embed_view,
                   expected_value, expected_value_view, fused_update, inner_product,
-                  naive_convolve, embed_host, apply_binary_host)
+                  naive_convolve, embed_host, apply_binary_host, sum_rows,
+                  expected_value_host)
+from ._lib import (triot_expected_value_offset, triot_sum_rows, triot_expected_value_host)
 from ._lib import (triot_apply_binary_view, triot_embed_view, triot_expected_value_view,
                    triot_fused_update,
                    triot_inner_product, triot_inner_product_workspace_size, triot_naive_convolve)
@@ -35,7 +37,8 @@ __all__ = [
     "expected_value_view", "triot_expected_value_view",
     "fused_update", "triot_inner_product", "triot_inner_product_workspace_size",
     "triot_fused_update", "naive_convolve", "triot_naive_convolve", "embed_host",
-    "apply_binary_host",
+    "apply_binary_host", "sum_rows", "expected_value_host", "triot_expected_value_offset",
+    "triot_sum_rows", "triot_expected_value_host",
     "triot_embed", "triot_apply_binary", "triot_expected_value", "triot_expected_value_mass",
     "triot_expected_value_workspace_size", "triot_max_dimension", "triot_status_string",
     "triot_last_error", "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic",

@@ -32,7 +32,8 @@ EXPORTS = ("triot_max_dimension", "triot_status_string", "triot_last_error", "tr
            "triot_expected_value_view",
            "triot_inner_product_workspace_size", "triot_inner_product", "triot_fused_update",
            "triot_naive_convolve", "triot_embed_host", "triot_apply_binary_host",
-           "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic")
+           "triot_plan_describe", "triot_set_launch_policy", "triot_fastdiv_magic",
+           "triot_expected_value_offset", "triot_sum_rows", "triot_expected_value_host")
 
 
 class TriotError(RuntimeError):
@@ -71,6 +72,17 @@ _lib.triot_expected_value.argtypes = [_vp, _vp, _i64p, ctypes.c_int, ctypes.c_in
                                       ctypes.c_size_t, _vp]
 _lib.triot_expected_value_mass.restype = ctypes.c_int
 _lib.triot_expected_value_mass.argtypes = _lib.triot_expected_value.argtypes
+_lib.triot_expected_value_offset.restype = ctypes.c_int
+_lib.triot_expected_value_offset.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64p, _i64p,
+                                             ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+_lib.triot_sum_rows.restype = ctypes.c_int
+_lib.triot_sum_rows.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                ctypes.c_void_p]
+_lib.triot_expected_value_host.restype = ctypes.c_int
+_lib.triot_expected_value_host.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64p, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.c_size_t, ctypes.c_void_p]
 class triot_view(ctypes.Structure):
     """include/triot.h triot_view: a window of a dense base tensor."""
     _fields_ = [("data", ctypes.c_void_p), ("base_shape", _i64p), ("start", _i64p),
@@ -202,6 +214,24 @@ def triot_apply_binary_view(c: triot_view, a: triot_view, b: triot_view, iter_sh
                             dtype: int, op: int, stream: int) -> int:
     return _lib.triot_apply_binary_view(ctypes.byref(c), ctypes.byref(a), ctypes.byref(b),
                                         _shape(iter_shape), d, dtype, op, stream)
+
+
+def triot_expected_value_offset(out: int, p: int, shape, offset, d: int, dtype: int,
+                                with_mass: int, workspace: int, workspace_bytes: int,
+                                stream: int) -> int:
+    return _lib.triot_expected_value_offset(out, p, _shape(shape),
+                                            _shape(offset) if offset is not None else None, d,
+                                            dtype, with_mass, workspace, workspace_bytes, stream)
+
+
+def triot_sum_rows(out: int, rows: int, nrows: int, ncols: int, stream: int) -> int:
+    return _lib.triot_sum_rows(out, rows, nrows, ncols, stream)
+
+
+def triot_expected_value_host(out: int, p: int, shape, d: int, dtype: int, with_mass: int,
+                              staging: int, staging_bytes: int, stream: int) -> int:
+    return _lib.triot_expected_value_host(out, p, _shape(shape), d, dtype, with_mass, staging,
+                                          staging_bytes, stream)
 
 
 def triot_expected_value_view(out: int, p: triot_view, d: int, dtype: int, with_mass: int,

@@ -36,6 +36,29 @@ def _check_tensor(name: str, t, device=None):
         raise ValueError(f"{name} is on {t.device}, expected {device}")
 
 
+class _NoSwitch:
+    __slots__ = ()
+
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
+_NO_SWITCH = _NoSwitch()
+
+
+def _device(device):
+    """Make `device` current for the C call (the library sizes grids from cudaGetDevice() and
+    launches on the tensor's stream): a no-op when it already is, which is the common case."""
+    torch = _torch()
+    idx = device.index
+    if idx is None or idx == torch.cuda.current_device():
+        return _NO_SWITCH
+    return torch.cuda.device(idx)
+
+
 def _stream(device) -> int:
     torch = _torch()
     raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)   # the same handle, ~1 us cheaper
@@ -75,8 +98,9 @@ def embed_view(dst: "View", src: "View", region_only: bool = False):
         raise ValueError("dst and src must be on one device")
     (dv, keep1), (sv, keep2) = dst._c(), src._c()
     flags = _lib.TRIOT_EMBED_REGION_ONLY if region_only else _lib.TRIOT_EMBED_FULL
-    _lib.check(_lib.triot_embed_view(dv, sv, dst.dim(), _dtype_code(dst.base), flags,
-                                     _stream(dst.base.device)))
+    with _device(dst.base.device):
+        _lib.check(_lib.triot_embed_view(dv, sv, dst.dim(), _dtype_code(dst.base), flags,
+                                         _stream(dst.base.device)))
     return dst
 
 
@@ -85,10 +109,13 @@ def apply_binary_view(a: "View", b: "View", out: "View", op: str = "mul", iter_s
     for v in (a, b, out):
         if v.base.dtype != a.base.dtype or v.dim() != a.dim():
             raise ValueError("views must share dtype and dimension")
+        if v.base.device != a.base.device:
+            raise ValueError("views must be on one device")
     (cv, k1), (av, k2), (bv, k3) = out._c(), a._c(), b._c()
-    _lib.check(_lib.triot_apply_binary_view(cv, av, bv, iter_shape, a.dim(),
-                                            _dtype_code(a.base), OPS[op],
-                                            _stream(a.base.device)))
+    with _device(a.base.device):
+        _lib.check(_lib.triot_apply_binary_view(cv, av, bv, iter_shape, a.dim(),
+                                                _dtype_code(a.base), OPS[op],
+                                                _stream(a.base.device)))
     return out
 
 
@@ -106,9 +133,10 @@ def expected_value_view(p: "View", out=None, with_mass: bool = False):
         raise ValueError(f"out must be a float64 tensor of >= {n} elements")
     ws = workspace(tuple(p.shape), code, p.base.device)
     pv, keep = p._c()
-    _lib.check(_lib.triot_expected_value_view(out.data_ptr(), pv, d, code, 1 if with_mass else 0,
-                                              ws.data_ptr(), ws.numel(),
-                                              _stream(p.base.device)))
+    with _device(p.base.device):
+        _lib.check(_lib.triot_expected_value_view(out.data_ptr(), pv, d, code, 1 if with_mass else 0,
+                                                  ws.data_ptr(), ws.numel(),
+                                                  _stream(p.base.device)))
     return out
 
 
@@ -120,9 +148,10 @@ def embed(dst, src, region_only: bool = False):
     if src.dtype != dst.dtype or src.dim() != dst.dim():
         raise ValueError("dst and src must have the same dtype and dimension")
     flags = _lib.TRIOT_EMBED_REGION_ONLY if region_only else _lib.TRIOT_EMBED_FULL
-    _lib.check(_lib.triot_embed(dst.data_ptr(), tuple(dst.shape), src.data_ptr(),
-                                tuple(src.shape), dst.dim(), _dtype_code(dst), flags,
-                                _stream(dst.device)))
+    with _device(dst.device):
+        _lib.check(_lib.triot_embed(dst.data_ptr(), tuple(dst.shape), src.data_ptr(),
+                                    tuple(src.shape), dst.dim(), _dtype_code(dst), flags,
+                                    _stream(dst.device)))
     return dst
 
 
@@ -142,9 +171,10 @@ def apply_binary(a, b, op: str = "mul", out=None, iter_shape=None):
     _check_tensor("out", out, a.device)
     if out.dtype != a.dtype:
         raise ValueError("out must have the dtype of a and b")
-    _lib.check(_lib.triot_apply_binary(out.data_ptr(), tuple(out.shape), a.data_ptr(),
-                                       tuple(a.shape), b.data_ptr(), tuple(b.shape), iter_shape,
-                                       a.dim(), _dtype_code(a), OPS[op], _stream(a.device)))
+    with _device(a.device):
+        _lib.check(_lib.triot_apply_binary(out.data_ptr(), tuple(out.shape), a.data_ptr(),
+                                           tuple(a.shape), b.data_ptr(), tuple(b.shape), iter_shape,
+                                           a.dim(), _dtype_code(a), OPS[op], _stream(a.device)))
     return out
 
 
@@ -161,9 +191,11 @@ def workspace(p_shape, dtype_code: int, device):
     return ws
 
 
-def expected_value(p, out=None, with_mass: bool = False):
+def expected_value(p, out=None, with_mass: bool = False, offset=None):
     """means[k] = sum_t t_k * p[t] (fp64), k = 0..d-1.  Returns a (d,) float64 CUDA tensor, or
-    (d+1,) with out[d] = sum_t p[t] when with_mass (triot_expected_value_mass)."""
+    (d+1,) with out[d] = sum_t p[t] when with_mass (triot_expected_value_mass).  offset: p is
+    the block of a larger PMF whose element t sits at offset + t; the weights are then the
+    global coordinates (triot_expected_value_offset, P:607 slabs)."""
     torch = _torch()
     _check_tensor("p", p)
     code = _dtype_code(p)
@@ -175,9 +207,56 @@ def expected_value(p, out=None, with_mass: bool = False):
     if out.dtype != torch.float64 or out.numel() < n:
         raise ValueError(f"out must be a float64 tensor of >= {n} elements")
     ws = workspace(tuple(p.shape), code, p.device)
-    fn = _lib.triot_expected_value_mass if with_mass else _lib.triot_expected_value
-    _lib.check(fn(out.data_ptr(), p.data_ptr(), tuple(p.shape), d, code, ws.data_ptr(),
-                  ws.numel(), _stream(p.device)))
+    with _device(p.device):
+        if offset is not None:
+            off = tuple(int(x) for x in offset)
+            if len(off) != d:
+                raise ValueError(f"offset must have {d} entries")
+            _lib.check(_lib.triot_expected_value_offset(
+                out.data_ptr(), p.data_ptr(), tuple(p.shape), off, d, code,
+                1 if with_mass else 0, ws.data_ptr(), ws.numel(), _stream(p.device)))
+        else:
+            fn = _lib.triot_expected_value_mass if with_mass else _lib.triot_expected_value
+            _lib.check(fn(out.data_ptr(), p.data_ptr(), tuple(p.shape), d, code, ws.data_ptr(),
+                          ws.numel(), _stream(p.device)))
+    return out
+
+
+def sum_rows(rows, out=None):
+    """out[j] = sum_r rows[r, j], rows added in order (triot_sum_rows): the deterministic
+    amalgamation of per-slab / per-rank results.  rows: a 2-D float64 CUDA tensor."""
+    torch = _torch()
+    _check_tensor("rows", rows)
+    if rows.dtype != torch.float64 or rows.dim() != 2:
+        raise ValueError("rows must be a 2-D float64 tensor")
+    nr, nc = int(rows.shape[0]), int(rows.shape[1])
+    if out is None:
+        out = torch.empty(nc, dtype=torch.float64, device=rows.device)
+    _check_tensor("out", out, rows.device)
+    with _device(rows.device):
+        _lib.check(_lib.triot_sum_rows(out.data_ptr(), rows.data_ptr(), nr, nc,
+                                       _stream(rows.device)))
+    return out
+
+
+def expected_value_host(p, staging, out=None, with_mass: bool = False):
+    """triot_expected_value_host: the expected value of a (pinned) host tensor p, streamed in
+    chunks through the device `staging` buffer (a uint8 CUDA tensor, 256-byte aligned); returns
+    a host float64 tensor (pinned when allocated here).  Synchronous: waits for the result."""
+    torch = _torch()
+    if p.is_cuda or not p.is_contiguous():
+        raise ValueError("p must be a contiguous host tensor")
+    code = _dtype_code(p)
+    d = p.dim()
+    n = d + (1 if with_mass else 0)
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    dev = staging.device
+    with _device(dev):
+        _lib.check(_lib.triot_expected_value_host(out.data_ptr(), p.data_ptr(), tuple(p.shape), d,
+                                                  code, 1 if with_mass else 0,
+                                                  staging.data_ptr(), staging.numel(),
+                                                  _stream(dev)))
     return out
 
 
@@ -198,10 +277,11 @@ def inner_product(a, b, iter_shape=None, out=None):
         if ws is None or ws.numel() < need:
             ws = torch.zeros(need, dtype=torch.uint8, device=a.device)
             _ws_cache[key] = ws
-    _lib.check(_lib.triot_inner_product(out.data_ptr(), a.data_ptr(), tuple(a.shape),
-                                        b.data_ptr(), tuple(b.shape), iter_shape, a.dim(),
-                                        _dtype_code(a), ws.data_ptr(), ws.numel(),
-                                        _stream(a.device)))
+    with _device(a.device):
+        _lib.check(_lib.triot_inner_product(out.data_ptr(), a.data_ptr(), tuple(a.shape),
+                                            b.data_ptr(), tuple(b.shape), iter_shape, a.dim(),
+                                            _dtype_code(a), ws.data_ptr(), ws.numel(),
+                                            _stream(a.device)))
     return out
 
 
@@ -212,9 +292,10 @@ def fused_update(x, y, z):
     _check_tensor("z", z, x.device)
     if not (x.dtype == y.dtype == z.dtype) or not (x.dim() == y.dim() == z.dim()):
         raise ValueError("x, y, z must share dtype and dimension")
-    _lib.check(_lib.triot_fused_update(x.data_ptr(), tuple(x.shape), y.data_ptr(), tuple(y.shape),
-                                       z.data_ptr(), tuple(z.shape), x.dim(), _dtype_code(x),
-                                       _stream(x.device)))
+    with _device(x.device):
+        _lib.check(_lib.triot_fused_update(x.data_ptr(), tuple(x.shape), y.data_ptr(), tuple(y.shape),
+                                           z.data_ptr(), tuple(z.shape), x.dim(), _dtype_code(x),
+                                           _stream(x.device)))
     return x
 
 
@@ -231,9 +312,10 @@ def naive_convolve(lhs, rhs, out=None):
     _check_tensor("out", out, lhs.device)
     if tuple(out.shape) != shape or out.dtype != lhs.dtype:
         raise ValueError(f"out must be {lhs.dtype} of shape {shape}")
-    _lib.check(_lib.triot_naive_convolve(out.data_ptr(), lhs.data_ptr(), tuple(lhs.shape),
-                                         rhs.data_ptr(), tuple(rhs.shape), lhs.dim(),
-                                         _dtype_code(lhs), _stream(lhs.device)))
+    with _device(lhs.device):
+        _lib.check(_lib.triot_naive_convolve(out.data_ptr(), lhs.data_ptr(), tuple(lhs.shape),
+                                             rhs.data_ptr(), tuple(rhs.shape), lhs.dim(),
+                                             _dtype_code(lhs), _stream(lhs.device)))
     return out
 
 

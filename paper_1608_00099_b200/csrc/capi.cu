@@ -70,7 +70,19 @@ int vindex(const Geom& g) {
 
 std::mutex g_mu;
 int g_sms[64] = {0};
-std::unordered_map<const void*, int> g_occ;
+// per (device, kernel): occupancy in blocks per SM, or 1 once the kernel's dynamic shared
+// memory attribute has been set on that device (attributes are per device)
+struct OccKey {
+  int dev;
+  const void* fn;
+  bool operator==(const OccKey& o) const { return dev == o.dev && fn == o.fn; }
+};
+struct OccHash {
+  size_t operator()(const OccKey& k) const {
+    return std::hash<const void*>()(k.fn) ^ ((size_t)k.dev * 0x9e3779b97f4a7c15ull);
+  }
+};
+std::unordered_map<OccKey, int, OccHash> g_occ;
 
 int cuda_fail(cudaError_t e, const char* what) {
   return set_error(TRIOT_ERR_CUDA, "CUDA: %s: %s", what, cudaGetErrorString(e));
@@ -129,13 +141,13 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (int st = sms_locked(dev, &sms)) return st;
-    auto it = g_occ.find(fn);
+    auto it = g_occ.find(OccKey{dev, fn});
     if (it == g_occ.end()) {
       int nb = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, TRIOT_BLOCK, 0);
       if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
       if (nb < 1) nb = 1;
-      it = g_occ.emplace(fn, nb).first;
+      it = g_occ.emplace(OccKey{dev, fn}, nb).first;
     }
     occ = it->second;
   }
@@ -238,10 +250,10 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (int st = sms_locked(dev, &sms)) return st;
-    if (g_occ.find(fn) == g_occ.end()) {
+    if (g_occ.find(OccKey{dev, fn}) == g_occ.end()) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-      g_occ.emplace(fn, 1);
+      g_occ.emplace(OccKey{dev, fn}, 1);
     }
   }
   uint64_t blocks = (uint64_t)sms * (uint64_t)(g_override.bpsm > 0 ? g_override.bpsm : 1);
@@ -310,6 +322,8 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   f.ns = g.D + 2;
   f.d_out = g.nout >= 0 ? g.nout : g.d + (g.with_mass ? 1 : 0);
   for (int k = 0; k <= TRIOT_MAXD; ++k) f.slot_of_axis[k] = g.slot_of_axis[k];
+  f.nax = g.nax;
+  for (int k = 0; k < TRIOT_MAXD; ++k) f.offd[k] = g.offd[k];
   void* args[1] = {&f};
   return launch_pdl((const void*)&ev_final_kernel<kFinBlock>, 1, kFinBlock, 0, s, args);
 }
@@ -457,12 +471,14 @@ int triot_naive_convolve(void* result, const void* lhs, const int64_t* lhs_shape
       g.D, group ? 2 : (rev ? 1 : 0), use_smem ? 1 : 0);
   if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no convolution instance for d=%d", d);
   if (use_smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     std::lock_guard<std::mutex> lk(g_mu);
-    if (g_occ.find(fn) == g_occ.end()) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           96 * 1024);
+    if (g_occ.find(OccKey{dev, fn}) == g_occ.end()) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-      g_occ.emplace(fn, 1);
+      g_occ.emplace(OccKey{dev, fn}, 1);
     }
   }
   Desc<uint32_t> desc;
@@ -498,12 +514,21 @@ int triot_expected_value_workspace_size(const int64_t* shape, int d, int dtype, 
 static int expected_value_impl(double* means, const void* p, const int64_t* shape, int d,
                                int dtype, void* workspace, size_t workspace_bytes,
                                void* cuda_stream, bool with_mass,
-                               const triot_view* pv = nullptr) {
+                               const triot_view* pv = nullptr, const int64_t* offset = nullptr) {
   Geom g;
   int st = pv ? plan_ev_view(g, pv, d, dtype) : plan_ev(g, p, shape, d, dtype);
   if (st) return st;
   if (pv) p = g.t[0].ptr;
   g.with_mass = with_mass;
+  if (offset) {  // the coordinates of p's element 0 in a larger PMF (P:607 slabs)
+    for (int k = 0; k < d; ++k) {
+      if (offset[k] < 0 || offset[k] > (int64_t)(1ll << 53))
+        return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: offset[%d] = %lld outside [0, 2^53]", k,
+                         (long long)offset[k]);
+      g.offd[k] = (double)offset[k];
+    }
+    g.nax = d;
+  }
   const int nout = d + (with_mass ? 1 : 0);
   if (!means) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: means is NULL");
   if (((uintptr_t)means) % 8)
@@ -520,7 +545,7 @@ static int expected_value_impl(double* means, const void* p, const int64_t* shap
     if (g.t[0].numel && m0 < p1 && p0 < m1)
       return set_error(TRIOT_ERR_ALIASING, "Aliasing: means overlaps p");
   }
-  if (g.empty) {
+  if (g.empty) {  // empty sums: 0 (the offsets multiply a zero mass)
     cudaError_t e =
         cudaMemsetAsync(means, 0, (size_t)nout * sizeof(double), (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
@@ -542,6 +567,38 @@ int triot_expected_value_mass(double* out, const void* p, const int64_t* shape, 
                               void* workspace, size_t workspace_bytes, void* cuda_stream) {
   return expected_value_impl(out, p, shape, d, dtype, workspace, workspace_bytes, cuda_stream,
                              true);
+}
+
+int triot_expected_value_offset(double* out, const void* p, const int64_t* shape,
+                                const int64_t* offset, int d, int dtype, int with_mass,
+                                void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  return expected_value_impl(out, p, shape, d, dtype, workspace, workspace_bytes, cuda_stream,
+                             with_mass != 0, nullptr, offset);
+}
+
+int triot_sum_rows(double* out, const double* rows, int64_t nrows, int64_t ncols,
+                   void* cuda_stream) {
+  if (ncols < 0 || nrows < 0)
+    return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: nrows %lld, ncols %lld", (long long)nrows,
+                     (long long)ncols);
+  if (ncols == 0) return TRIOT_OK;
+  if (!out || (nrows && !rows)) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: out/rows");
+  if (((uintptr_t)out) % 8 || ((uintptr_t)rows) % 8)
+    return set_error(TRIOT_ERR_MISALIGNED, "Misaligned: out/rows not 8-byte aligned");
+  {
+    uintptr_t o0 = (uintptr_t)out, o1 = o0 + (uintptr_t)ncols * 8;
+    uintptr_t r0 = (uintptr_t)rows, r1 = r0 + (uintptr_t)(nrows * ncols) * 8;
+    if (nrows && o0 < r1 && r0 < o1) return set_error(TRIOT_ERR_ALIASING, "Aliasing: out overlaps rows");
+  }
+  const unsigned grid = (unsigned)((ncols + 255) / 256);
+  const double* r = rows;
+  double* o = out;
+  uint64_t nr = (uint64_t)nrows, nc = (uint64_t)ncols;
+  void* args[4] = {&o, &r, &nr, &nc};
+  int st = launch_pdl((const void*)&sum_rows_kernel<256>, grid, 256, 0, (cudaStream_t)cuda_stream,
+                      args);
+  if (!st) clear_error();
+  return st;
 }
 
 int triot_expected_value_view(double* out, const triot_view* p, int d, int dtype, int with_mass,

@@ -242,6 +242,119 @@ int triot_embed_host(void* dst, const int64_t* dst_shape, const void* src,
                       });
 }
 
+int triot_expected_value_host(double* out, const void* p, const int64_t* shape, int d, int dtype,
+                              int with_mass, void* staging, size_t staging_bytes,
+                              void* cuda_stream) {
+  Geom g;
+  int st = plan_ev(g, p, shape, d, dtype);
+  if (st) return st;
+  if (!out) return set_error(TRIOT_ERR_NULL_POINTER, "NullPointer: out is NULL");
+  if (!staging) return set_error(TRIOT_ERR_WORKSPACE, "Workspace: staging is NULL");
+  if (((uintptr_t)staging) % 256)
+    return set_error(TRIOT_ERR_MISALIGNED, "Misaligned: staging is not 256-byte aligned");
+  const int esz = esz_of(dtype);
+  const int nout = d + (with_mass ? 1 : 0);
+  size_t ws_bytes = 0;
+  if ((st = triot_expected_value_workspace_size(shape, d, dtype, &ws_bytes))) return st;
+  auto align = [](uint64_t x) { return (x + 255) & ~255ull; };
+  cudaStream_t cs = (cudaStream_t)cuda_stream;
+  Pipe* pp;
+  if ((st = pipe_for(cs, &pp))) return st;
+  Pipe& P = *pp;
+  std::lock_guard<std::mutex> lk(P.mu);
+  if ((st = pipe_init(P))) return st;
+  // staging: [workspace][final: nout][rows: nchunk x nout][slot 0][slot 1]
+  const uint64_t fixed = align(ws_bytes) + align((uint64_t)nout * 8);
+  if (staging_bytes <= fixed + 512)
+    return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu staging bytes, need > %llu", staging_bytes,
+                     (unsigned long long)(fixed + 512));
+  if (g.empty) {  // empty sums: zeros
+    double* fin0 = (double*)((char*)staging + align(ws_bytes));
+    cudaError_t e0 = cudaMemsetAsync(fin0, 0, (size_t)nout * 8, cs);
+    if (e0 == cudaSuccess)
+      e0 = cudaMemcpyAsync(out, fin0, (size_t)nout * 8, cudaMemcpyDeviceToHost, cs);
+    if (e0 != cudaSuccess) return cuda_err(e0, "empty expected value");
+    clear_error();
+    return TRIOT_OK;
+  }
+  // choose the chunk axis k (the first whose single index fits a slot, with room for the rows)
+  int k = 0;
+  uint64_t rows = 0, nchunk = 0, row_bytes = 0, npre = 1;
+  for (; k < d; ++k) {
+    row_bytes = sub_elems(shape, d, k) * (uint64_t)esz;
+    const uint64_t nk = (uint64_t)shape[k];
+    // rows per chunk r: 2 * align(r row_bytes) + align(chunks(r) * nout * 8) <= avail
+    const uint64_t avail = staging_bytes - fixed;
+    uint64_t r = (avail / 2) / (row_bytes ? row_bytes : 1);
+    if (r > nk) r = nk;
+    while (r >= 1) {
+      const uint64_t nc = npre * ((nk + r - 1) / r);
+      if (2 * align(r * row_bytes) + align(nc * (uint64_t)nout * 8) <= avail) break;
+      r = r > 1 ? r / 2 : 0;
+    }
+    if (r >= 1) {
+      rows = r;
+      nchunk = npre * ((nk + r - 1) / r);
+      break;
+    }
+    npre *= nk;
+  }
+  if (k == d)
+    return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu staging bytes cannot hold two chunks",
+                     staging_bytes);
+  char* base = (char*)staging;
+  void* ws = base;
+  double* fin = (double*)(base + align(ws_bytes));
+  double* rowsbuf = (double*)(base + fixed);
+  char* slot[2];
+  slot[0] = base + fixed + align(nchunk * (uint64_t)nout * 8);
+  slot[1] = slot[0] + align(rows * row_bytes);
+  cudaError_t e;
+  // the workspace must start zeroed (the reduction leaves it zeroed afterwards)
+  if ((e = cudaMemsetAsync(ws, 0, ws_bytes, cs)) != cudaSuccess) return cuda_err(e, "memset");
+  if ((e = cudaEventRecord(P.computed[0], cs)) != cudaSuccess) return cuda_err(e, "record");
+  if ((e = cudaStreamWaitEvent(P.h2d, P.computed[0], 0)) != cudaSuccess) return cuda_err(e, "wait");
+  const uint64_t nk = (uint64_t)shape[k];
+  int64_t csh[TRIOT_MAXD], off[TRIOT_MAXD];
+  uint64_t prefix[TRIOT_MAXD] = {0};
+  uint64_t chunk = 0;
+  for (uint64_t pi = 0; pi < npre; ++pi) {
+    uint64_t pbase = 0;  // Horner of the prefix, in units of axis-k index rows
+    for (int j = 0; j < k; ++j) pbase = pbase * (uint64_t)shape[j] + prefix[j];
+    pbase *= nk;
+    for (uint64_t a = 0; a < nk; a += rows, ++chunk) {
+      const int s = (int)(chunk & 1);
+      const uint64_t r = a + rows <= nk ? rows : nk - a;
+      if (chunk >= 2)  // the slot's previous chunk has been consumed
+        if ((e = cudaStreamWaitEvent(P.h2d, P.computed[s], 0)) != cudaSuccess)
+          return cuda_err(e, "wait");
+      e = cudaMemcpyAsync(slot[s], (const char*)p + (pbase + a) * row_bytes, r * row_bytes,
+                          cudaMemcpyHostToDevice, P.h2d);
+      if (e != cudaSuccess) return cuda_err(e, "cudaMemcpyAsync H2D");
+      if ((e = cudaEventRecord(P.loaded[s], P.h2d)) != cudaSuccess) return cuda_err(e, "record");
+      if ((e = cudaStreamWaitEvent(cs, P.loaded[s], 0)) != cudaSuccess) return cuda_err(e, "wait");
+      // the chunk as a d-dimensional block (1, .., 1, r, s_{k+1}, ..) at (prefix, a, 0, ..)
+      for (int j = 0; j < d; ++j) {
+        csh[j] = j < k ? 1 : j == k ? (int64_t)r : shape[j];
+        off[j] = j < k ? (int64_t)prefix[j] : j == k ? (int64_t)a : 0;
+      }
+      if ((st = triot_expected_value_offset(rowsbuf + chunk * (uint64_t)nout, slot[s], csh, off, d,
+                                            dtype, with_mass, ws, ws_bytes, cs)))
+        return st;
+      if ((e = cudaEventRecord(P.computed[s], cs)) != cudaSuccess) return cuda_err(e, "record");
+    }
+    for (int j = k - 1; j >= 0; --j) {  // Alg 3 on the prefix
+      if (++prefix[j] < (uint64_t)shape[j]) break;
+      prefix[j] = 0;
+    }
+  }
+  if ((st = triot_sum_rows(fin, rowsbuf, (int64_t)nchunk, nout, cs))) return st;
+  e = cudaMemcpyAsync(out, fin, (size_t)nout * 8, cudaMemcpyDeviceToHost, cs);
+  if (e != cudaSuccess) return cuda_err(e, "cudaMemcpyAsync D2H");
+  clear_error();
+  return TRIOT_OK;
+}
+
 int triot_apply_binary_host(void* c, const void* a, const int64_t* a_shape, const void* b,
                             const int64_t* b_shape, const int64_t* iter_shape, int d, int dtype,
                             int op, void* staging, size_t staging_bytes, void* cuda_stream) {

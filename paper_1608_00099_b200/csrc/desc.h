@@ -73,6 +73,10 @@ struct Desc {
   int32_t slot_of_axis[TRIOT_MAXD + 1];  // out[j] = slot >= 0 ? total[slot] : 0 (slot D+1 = mass)
   int32_t op;            // binary op
   int32_t split;         // reductions: 1 = write the block partial only; ev_final_kernel sums
+  // expected value of a block of a larger PMF (slab / chunk / shard): output axis j < nax
+  // gets offd[j] * mass added (global coordinate = offset + local), mass = slot_of_axis[nax]
+  int32_t nax;
+  double offd[TRIOT_MAXD];
   // embed zero runs: 32 vectors == one unit of digit khi (lanes share digits 0..khi) and dst is
   // dense in the counter, so while a digit <= khi is out of bounds the warp stores zeros at
   // dst + r * step without touching the odometer (zmask = oob bits of digits 0..khi, 0 = off)

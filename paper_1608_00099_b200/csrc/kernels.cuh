@@ -1458,8 +1458,27 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
   TRIOT_TRACE(6);
   if (threadIdx.x < (unsigned)d.d_out) {
     const int sl = d.slot_of_axis[threadIdx.x];
-    ((double*)d.out)[threadIdx.x] = sl >= 0 ? sm[0][sl] : 0.0;
+    double v = sl >= 0 ? sm[0][sl] : 0.0;
+    // a block of a larger PMF: sum_t (off_j + t_j) p[t] = m_j + off_j * mass (one rounding)
+    if ((int)threadIdx.x < d.nax && d.offd[threadIdx.x] != 0.0)
+      v = fma(d.offd[threadIdx.x], sm[0][d.slot_of_axis[d.nax]], v);
+    ((double*)d.out)[threadIdx.x] = v;
   }
+}
+
+// Amalgamation of pre-results: out[j] = sum_r rows[r][j], rows in order (fixed order:
+// deterministic).  Sums the per-slab results of the host-streamed expected value and the
+// per-rank results of the sharded one.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) sum_rows_kernel(double* out, const double* rows,
+                                                         uint64_t nrows, uint64_t ncols) {
+  pdl_trigger();
+  pdl_wait();
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  double t = 0.0;
+  for (uint64_t r = 0; r < nrows; ++r) t += __ldcg(rows + r * ncols + j);
+  out[j] = t;
 }
 
 // Second half of a split reduction: launched after the reduction kernel with programmatic
@@ -1473,6 +1492,8 @@ struct EvFin {
   uint32_t nblk;
   int32_t ns, d_out;
   int32_t slot_of_axis[TRIOT_MAXD + 1];
+  int32_t nax;
+  double offd[TRIOT_MAXD];
 };
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) ev_final_kernel(const __grid_constant__ EvFin f) {
@@ -1498,11 +1519,18 @@ __global__ void __launch_bounds__(BLOCK) ev_final_kernel(const __grid_constant__
   for (unsigned o = 16; o >= P; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   if (lane < f.ns) sm[wib][lane] = a;
   __syncthreads();
+  __shared__ double tot[NSMAX];
+  if ((int)threadIdx.x < f.ns) {
+    double t = 0.0;
+    for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
   if ((int)threadIdx.x < f.d_out) {
     const int sl = f.slot_of_axis[threadIdx.x];
-    double t = 0.0;
-    if (sl >= 0)
-      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][sl];
+    double t = sl >= 0 ? tot[sl] : 0.0;
+    if ((int)threadIdx.x < f.nax && f.offd[threadIdx.x] != 0.0)
+      t = fma(f.offd[threadIdx.x], tot[f.slot_of_axis[f.nax]], t);
     f.out[threadIdx.x] = t;
   }
 }

@@ -59,6 +59,8 @@ struct Geom {
   bool with_mass = false;   // EV: also write sum(p) after the d means
   int nout = -1;            // reduction outputs if not d (+mass): the inner product writes 1
   bool split = false;       // reductions: partials summed by a second (PDL) kernel
+  int nax = 0;              // EV of a block of a larger PMF: per-axis coordinate offsets
+  double offd[TRIOT_MAXD] = {};
   bool view = false;        // EV of a view: p is strided (offsets tracked by the odometer)
   uint32_t zmask = 0;       // embed zero runs (desc.h)
   uint64_t zn[TRIOT_MAXD] = {};
@@ -145,6 +147,8 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.d_out = g.nout >= 0 ? g.nout : g.d + (g.with_mass ? 1 : 0);
   d.op = g.binop;
   d.split = g.split ? 1 : 0;
+  d.nax = g.nax;
+  for (int k = 0; k < TRIOT_MAXD; ++k) d.offd[k] = g.offd[k];
   d.zmask = g.zmask;
   d.rowlen = (uint32_t)g.rowlen;
   d.rmag = (uint32_t)g.rmag;

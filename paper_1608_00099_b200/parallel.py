@@ -9,15 +9,15 @@ Here the partition is a slab of axis 0 (the outermost loop):
 
 * embed and apply_binary need NO collective: rank r owns rows [lo, hi) of the output and reads
   only the matching rows of the inputs (`slab_rows`, `embed_slab`, `apply_binary_slab`);
-* the expected value is the one exchange: each rank computes its slab's means and mass with
-  `triot_expected_value_mass`, shifts the axis-0 weight by its row offset (t_0 = lo + local t_0,
-  so m_0 += lo * mass), and the d-vectors are all-gathered and summed in rank order, so the result
-  is identical on every rank and deterministic run to run (an all-reduce would leave the
-  summation order to the collective's algorithm).
+* the expected value is the one exchange: each rank runs `triot_expected_value_offset` on its
+  slab with the slab's origin (lo, 0, ..., 0) -- the kernel weights axis 0 by the global
+  coordinate lo + t_0 -- the d-vectors are all-gathered (NCCL over NVLink for CUDA tensors, gloo
+  in the CPU tests) and summed in rank order by `triot_sum_rows`, so the result is identical on
+  every rank and deterministic run to run (an all-reduce would leave the summation order to the
+  collective's algorithm).  No arithmetic happens outside the library's kernels.
 
-The collective is over whatever process group the caller passes (NCCL for CUDA tensors across
-GPUs over NVLink; gloo for the CPU tests).  `local_ev` lets the host logic run with a stand-in
-for the GPU kernel (the CPU tests pass one); the default is the library's kernel.
+`local_ev` / `sum_rows` let the host logic run with stand-ins for the GPU kernels (the CPU tests
+pass the oracle); the defaults are the library's kernels.
 """
 from __future__ import annotations
 
@@ -51,19 +51,17 @@ def apply_binary_slab(a, b, lo: int, hi: int, op: str = "mul", out_slab=None, it
                             op, out=out_slab, iter_shape=ish)
 
 
-def _default_local_ev(p_slab):
+def _default_local_ev(p_slab, offset):
     from . import api
-    return api.expected_value(p_slab, with_mass=True)
+    return api.expected_value(p_slab, offset=offset)
 
 
-def amalgamate(local_means_mass, lo: int):
-    """Shift a slab's (d means, mass) so axis 0 counts from the global origin: m_0 += lo*mass."""
-    v = local_means_mass.clone()
-    v[0] = v[0] + float(lo) * v[-1]
-    return v[:-1]
+def _default_sum_rows(rows):
+    from . import api
+    return api.sum_rows(rows)
 
 
-def expected_value_sharded(p_slab, lo: int, group=None, local_ev=None):
+def expected_value_sharded(p_slab, lo: int, group=None, local_ev=None, sum_rows=None):
     """Global expected value of a p whose axis-0 rows [lo, lo + p_slab.shape[0]) this rank holds.
 
     Returns the same (d,) float64 tensor on every rank of `group`."""
@@ -71,11 +69,10 @@ def expected_value_sharded(p_slab, lo: int, group=None, local_ev=None):
     import torch.distributed as dist
 
     local_ev = local_ev or _default_local_ev
-    part = amalgamate(local_ev(p_slab), lo)
+    sum_rows = sum_rows or _default_sum_rows
+    d = p_slab.dim()
+    part = local_ev(p_slab, (lo,) + (0,) * (d - 1))
     world = dist.get_world_size(group)
-    parts = [torch.empty_like(part) for _ in range(world)]
-    dist.all_gather(parts, part, group=group)
-    total = parts[0].clone()
-    for r in range(1, world):        # rank order: deterministic
-        total += parts[r]
-    return total
+    flat = torch.empty(world * d, dtype=torch.float64, device=part.device)
+    dist.all_gather_into_tensor(flat, part.reshape(-1)[:d].contiguous(), group=group)
+    return sum_rows(flat.view(world, d))

@@ -33,7 +33,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     decl = declared_symbols()
-    assert len(decl) == 20, decl
+    assert len(decl) == 23, decl
     out = subprocess.run(["nm", "-D", "--defined-only", T.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = sorted(set(re.findall(r"\bT (triot_\w+)", out)))

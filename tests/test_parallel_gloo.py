@@ -24,10 +24,21 @@ def _free_port():
     return port
 
 
-def _oracle_ev_with_mass(p_slab):
+def _oracle_ev_offset(p_slab, offset):
+    """Stand-in for triot_expected_value_offset: the oracle's sums, each weight shifted by the
+    slab's origin (sum_t (off_k + t_k) p[t] = m_k + off_k * mass)."""
     p = p_slab.numpy()
     m = O.expected_value(p)
-    return torch.tensor(list(m) + [float(np.sum(p, dtype=np.float64))], dtype=torch.float64)
+    mass = float(np.sum(p, dtype=np.float64))
+    return torch.tensor([m[k] + offset[k] * mass for k in range(p.ndim)], dtype=torch.float64)
+
+
+def _rank_order_sum(rows):
+    """Stand-in for triot_sum_rows: rows added in order."""
+    out = torch.zeros(rows.shape[1], dtype=torch.float64)
+    for r in range(rows.shape[0]):
+        out += rows[r]
+    return out
 
 
 def _worker(rank, world, port, q):
@@ -42,7 +53,7 @@ def _worker(rank, world, port, q):
         for name, p in (("int", p_int), ("c3", p_c3)):
             lo, hi = P.slab_rows(p.shape[0], world, rank)
             got = P.expected_value_sharded(torch.from_numpy(p[lo:hi].copy()), lo,
-                                           local_ev=_oracle_ev_with_mass)
+                                           local_ev=_oracle_ev_offset, sum_rows=_rank_order_sum)
             res[name] = got.numpy()
         # embed slab: each rank's slab of dst from the global src, oracle as the local kernel
         src = make_inputs("C1")["src"]
@@ -93,8 +104,3 @@ def test_slab_rows_cover_once():
             spans = [P.slab_rows(n0, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n0
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
-
-
-def test_amalgamate_shift():
-    v = torch.tensor([2.0, 3.0, 10.0], dtype=torch.float64)    # m0, m1, mass
-    np.testing.assert_array_equal(P.amalgamate(v, 4).numpy(), [42.0, 3.0])
