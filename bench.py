@@ -11,8 +11,13 @@ of the K timed steps / device time; inputs are resident in HBM before the timed 
 step moves 2.6 GB, ≫ the 126 MB L2, so each op's inputs were evicted by its predecessor
 (no extra flush).  Device time = CUDA events on the launching stream, max over ranks.
 
-N > 1 (torchrun): every rank runs the full step on its own GPU (independent problem
-instances, weak scaling, no collective on the data path); value = all ranks' bytes / max time.
+N > 1 (torchrun): ONE global instance of each config is partitioned over the ranks along its
+outermost loops (parallel.leading_box: axis-0 slabs, or axis-0 indices shared by rank
+groups that split axis 1 when there are more ranks than indices -- C5's (4)^14 at 8 GPUs).
+Embed and product need no collective; the expected value is each rank's triot_expected_value_
+offset on its slab (global coordinates), an NCCL all_gather of the d doubles and triot_sum_rows
+in rank order (deterministic).  Strong scaling: value = the global instance's bytes per step x K
+/ max-over-ranks time.
 
 --impl reference: the CPU oracle (oracle/, plain C, 1 thread) on a bounded slab of the same
 workload per step (rank 0 only).
@@ -151,29 +156,46 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        print(f"[bench rank {rank}/{world}] NCCL process group up on {dev} "
+              f"(backend {dist.get_backend()}, NCCL {'.'.join(map(str, torch.cuda.nccl.version()))})",
+              file=sys.stderr, flush=True)
 
-    # ---- inputs resident in HBM (init excluded from timing)
+    # ---- inputs resident in HBM (init excluded from timing): this rank's box of each
+    # config (the whole config at N = 1)
     host = {n: make_inputs(n) for n in ("C1",) + STEP_OPS}
+    sl = slab_plan(host, world, rank)
     g = {}
-    g["src2"] = torch.from_numpy(host["C2"]["src"]).to(dev)
-    g["dst2"] = torch.empty(host["C2"]["dst_shape"], dtype=torch.float32, device=dev)
-    g["p3"] = torch.from_numpy(host["C3"]["p"]).to(dev)
+    g["src2"] = torch.from_numpy(sl["C2"]["src"]).to(dev)
+    g["dst2"] = torch.empty(sl["C2"]["dst_shape"], dtype=torch.float32, device=dev)
+    g["p3"] = torch.from_numpy(sl["C3"]["p"]).to(dev)
     g["m3"] = torch.empty(6, dtype=torch.float64, device=dev)
-    g["a4"] = torch.from_numpy(host["C4"]["a"]).to(dev)
-    g["b4"] = torch.from_numpy(host["C4"]["b"]).to(dev)
-    g["c4"] = torch.empty(host["C4"]["iter_shape"], dtype=torch.float64, device=dev)
-    g["src5"] = torch.from_numpy(host["C5"]["src"]).to(dev)
-    g["dst5"] = torch.empty(host["C5"]["dst_shape"], dtype=torch.float32, device=dev)
+    g["a4"] = torch.from_numpy(sl["C4"]["a"]).to(dev)
+    g["b4"] = torch.from_numpy(sl["C4"]["b"]).to(dev)
+    g["c4"] = torch.empty(sl["C4"]["iter_shape"], dtype=torch.float64, device=dev)
+    g["src5"] = torch.from_numpy(sl["C5"]["src"]).to(dev)
+    g["dst5"] = torch.empty(sl["C5"]["dst_shape"], dtype=torch.float32, device=dev)
+    if world > 1:
+        g["g3"] = torch.empty(world * 6, dtype=torch.float64, device=dev)
+        g["r3"] = torch.empty(6, dtype=torch.float64, device=dev)
+    off3 = sl["C3"]["offset"]
     stream = torch.cuda.current_stream(dev)
+
+    def ev_step():
+        if world == 1:
+            T.expected_value(g["p3"], out=g["m3"])
+        else:  # the one exchange: d doubles per rank, summed in rank order
+            T.expected_value(g["p3"], out=g["m3"], offset=off3)
+            dist.all_gather_into_tensor(g["g3"], g["m3"])
+            T.sum_rows(g["g3"].view(world, 6), out=g["r3"])
 
     def step(evs=None):
         T.embed(g["dst2"], g["src2"])
         if evs is not None:
             evs[0].record(stream)
-        T.expected_value(g["p3"], out=g["m3"])
+        ev_step()
         if evs is not None:
             evs[1].record(stream)
-        T.apply_binary(g["a4"], g["b4"], "mul", out=g["c4"])
+        T.apply_binary(g["a4"], g["b4"], "mul", out=g["c4"], iter_shape=sl["C4"]["iter_shape"])
         if evs is not None:
             evs[2].record(stream)
         T.embed(g["dst5"], g["src5"])
@@ -214,6 +236,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
 
+    extras = world == 1   # the single-GPU diagnostics below are not repeated per rank
     # ---- C1: latency-bound; us per call over back-to-back launches
     c1src = torch.from_numpy(host["C1"]["src"]).to(dev)
     c1dst = torch.empty(host["C1"]["dst_shape"], dtype=torch.float64, device=dev)
@@ -275,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- each op alone after a clean L2 scrub (write a 512 MB buffer, then read another so
     # every dirty line is written back before the timed launch): median of 5 single launches
     iso, graph20 = {}, {}
-    if not args.no_isolated:
+    if extras and not args.no_isolated:
         scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
         clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
         fns = {"C2": lambda: T.embed(g["dst2"], g["src2"]),
@@ -315,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- the paper's own Benchmarks 1-3 (§8(f) NEXT-2/3), same isolated protocol
     paper = {}
-    if not args.no_isolated:
+    if extras and not args.no_isolated:
         from triot_inputs import make_paper_inputs
         scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
         clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
@@ -370,7 +393,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e: same step through the public API with pinned HOST buffers; every step copies
     # its inputs H2D and reads its results back D2H inside the timed region
-    e2e = run_e2e(args, host, dev, stream, T, world)
+    e2e = run_e2e(args, sl, dev, stream, T, world, rank)
     sampler.stop()
 
     peak, peak_kind = measured_peak()
@@ -402,10 +425,13 @@ def run_ours(args, rank, world, local_rank):
             row["graph20_gbs"] = round(b / (g20 * 1e-3) / 1e9, 1)
         per_op_iso.append(row)
     dom = max(per_op, key=lambda r: r["us"])
-    traffic = None
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dom["config"])
+            tj = json.load(f)
+        traffic = tj.get(dom["config"])
+        traffic_src = ("profiles/traffic.json: " + str(tj.get("_source", "")) +
+                       " (not this run: ncu replays kernels and is never run inside the bench)")
     except Exception:
         traffic = None
     cpu = None
@@ -416,7 +442,8 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(total_ms / K, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "f32+f64 (embed: raw 32-bit words; binary f64; EV f64 accumulate)",
         "data": "synthetic (numpy PCG64 seeds 1..5, BASELINE.json configs)",
         "config": {"workload": WORKLOAD, "bytes_per_step": step_bytes,
@@ -425,7 +452,10 @@ def run_ours(args, rank, world, local_rank):
                           "(3)^14->(4)^14",
                    "l2": "no flush: 2.6 GB per step >> 126 MB L2, each op's inputs evicted "
                          "by its predecessor",
-                   "parallelism": f"replicas x{world} (weak; no data-path collective)"},
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"outer-loop partition over {world} GPUs (P:607): embed / "
+                                   "binary boxes with no collective, EV all_gather of 6 doubles "
+                                   "+ rank-order triot_sum_rows")},
         "per_op": per_op,
         "per_op_isolated": {"note": f"each op alone after a clean L2 scrub, {args.iso_reps} "
                                     "launches: us = median (event timestamps are quantised to "
@@ -445,10 +475,10 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": f"{dom['op']} ({dom['config']})",
                      "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
                      "frac": round(dom["gbs"] / peak, 3), "peak_kind": peak_kind,
-                     "traffic": traffic},
+                     "traffic": traffic, "traffic_source": traffic_src},
         "clocks": sampler.summary(),
         "e2e": e2e,
-        "gpu_launches": 4 * K,
+        "gpu_launches": (4 if world == 1 else 5) * K,
         "cpu_baseline": cpu,
     }
     if world > 1:
@@ -457,33 +487,111 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(out), flush=True)
 
 
-def run_e2e(args, host, dev, stream, T, world):
+def slab_plan(host, world, rank):
+    """This rank's part of one global instance of each step config: its box of the counter
+    (paper_1608_00099_b200.parallel.leading_box) and the matching input blocks.  At
+    world == 1 the box is the whole config."""
+    from paper_1608_00099_b200.parallel import leading_box
+
+    def take(arr, box):
+        idx = tuple(slice(min(lo, n), min(hi, n)) for (lo, hi), n in zip(box, arr.shape))
+        return np.ascontiguousarray(arr[idx])
+
+    plan = {}
+    for n in ("C2", "C5"):
+        dsh = host[n]["dst_shape"]
+        box = leading_box(dsh, world, rank)
+        plan[n] = {"box": box, "dst_shape": tuple(hi - lo for lo, hi in box),
+                   "src": take(host[n]["src"], box)}
+    p = host["C3"]["p"]
+    box = leading_box(p.shape, world, rank)
+    plan["C3"] = {"box": box, "p": take(p, box), "offset": tuple(lo for lo, _ in box)}
+    ish = host["C4"]["iter_shape"]
+    box = leading_box(ish, world, rank)
+    ab = [(lo, hi) for lo, hi in box]
+    a4, b4 = host["C4"]["a"], host["C4"]["b"]
+    # a and b keep their own extents outside the box's cut axes (each indexed by its own shape)
+    cut = [k for k, (lo, hi) in enumerate(ab) if (lo, hi) != (0, ish[k])]
+    boxa = [ab[k] if k in cut else (0, a4.shape[k]) for k in range(a4.ndim)]
+    boxb = [ab[k] if k in cut else (0, b4.shape[k]) for k in range(b4.ndim)]
+    plan["C4"] = {"box": box, "iter_shape": tuple(hi - lo for lo, hi in box),
+                  "a": take(a4, boxa), "b": take(b4, boxb)}
+    return plan
+
+
+def pcie_floors(dev, h2d_bytes, d2h_bytes):
+    """PCIe copy rates of this box in the same run (pinned host <-> device, torch copies): H2D
+    alone, D2H alone and both at once on two streams; floor_ms = the step's copies at those
+    rates (the e2e value cannot beat it)."""
     import torch
+    n = 256 << 20
+    hs = torch.empty(n, dtype=torch.uint8).pin_memory()
+    hd = torch.empty(n, dtype=torch.uint8).pin_memory()
+    ds = torch.empty(n, dtype=torch.uint8, device=dev)
+    dd = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn, reps=4):
+        fn()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize(dev)
+        return (time.perf_counter() - t) / reps
+
+    t_h2d = timed(lambda: ds.copy_(hs, non_blocking=True))
+    t_d2h = timed(lambda: hd.copy_(dd, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(s1):
+            ds.copy_(hs, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hd.copy_(dd, non_blocking=True)
+    t_both = timed(both)
+    h2d_gbs, d2h_gbs, both_gbs = n / t_h2d / 1e9, n / t_d2h / 1e9, 2 * n / t_both / 1e9
+    floor_ms = 1e3 * max(h2d_bytes / (h2d_gbs * 1e9), d2h_bytes / (d2h_gbs * 1e9),
+                         (h2d_bytes + d2h_bytes) / (both_gbs * 1e9))
+    del hs, hd, ds, dd
+    return {"h2d_gbs": round(h2d_gbs, 1), "d2h_gbs": round(d2h_gbs, 1),
+            "both_gbs": round(both_gbs, 1), "floor_ms_per_step": round(floor_ms, 2),
+            "how": "256 MiB pinned<->device torch copies, wall clock over 4 reps after 1"}
+
+
+def run_e2e(args, sl, dev, stream, T, world, rank):
+    import torch
+    import torch.distributed as dist
     pin = {
-        "src2": torch.from_numpy(host["C2"]["src"]).pin_memory(),
-        "p3": torch.from_numpy(host["C3"]["p"]).pin_memory(),
-        "a4": torch.from_numpy(host["C4"]["a"]).pin_memory(),
-        "b4": torch.from_numpy(host["C4"]["b"]).pin_memory(),
-        "src5": torch.from_numpy(host["C5"]["src"]).pin_memory(),
+        "src2": torch.from_numpy(sl["C2"]["src"]).pin_memory(),
+        "p3": torch.from_numpy(sl["C3"]["p"]).pin_memory(),
+        "a4": torch.from_numpy(sl["C4"]["a"]).pin_memory(),
+        "b4": torch.from_numpy(sl["C4"]["b"]).pin_memory(),
+        "src5": torch.from_numpy(sl["C5"]["src"]).pin_memory(),
     }
     outs = {
-        "dst2": torch.empty(host["C2"]["dst_shape"], dtype=torch.float32).pin_memory(),
+        "dst2": torch.empty(sl["C2"]["dst_shape"], dtype=torch.float32).pin_memory(),
         "m3": torch.empty(6, dtype=torch.float64).pin_memory(),
-        "c4": torch.empty(host["C4"]["iter_shape"], dtype=torch.float64).pin_memory(),
-        "dst5": torch.empty(host["C5"]["dst_shape"], dtype=torch.float32).pin_memory(),
+        "c4": torch.empty(sl["C4"]["iter_shape"], dtype=torch.float64).pin_memory(),
+        "dst5": torch.empty(sl["C5"]["dst_shape"], dtype=torch.float32).pin_memory(),
     }
-    # bytes that cross PCIe per step: every input in full (b's 8 rows beyond the iteration shape
-    # are not sent by the slab pipeline: b rows [0, 32) only)
+    ish = sl["C4"]["iter_shape"]
+    # bytes that cross PCIe per step on this rank: the input blocks (b's rows beyond the
+    # iteration shape are not sent by the slab pipeline) and the results
+    b4 = sl["C4"]["b"]
     h2d = sum(t.numel() * t.element_size() for t in pin.values()) - \
-        (host["C4"]["b"].shape[0] - host["C4"]["iter_shape"][0]) * \
-        (host["C4"]["b"][0].size * 8)
+        (b4.shape[0] - ish[0]) * (b4[0].size * 8 if b4.shape[0] else 0)
     d2h = sum(t.numel() * t.element_size() for t in outs.values())
+    staging3 = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+    if world > 1:
+        m3d = torch.empty(6, dtype=torch.float64, device=dev)
+        g3 = torch.empty(world * 6, dtype=torch.float64, device=dev)
+        r3 = torch.empty(6, dtype=torch.float64, device=dev)
+        res3 = torch.empty(6, dtype=torch.float64).pin_memory()
 
-    # host-buffer entry points (triot_embed_host / triot_apply_binary_host): axis-0 slabs
-    # streamed through a device staging buffer with H2D, kernel and D2H overlapped
-    # Each op is issued on its own stream (the user-level concurrency the API allows), so one
-    # op's device-to-host drain overlaps the next op's host-to-device feed; the step ends when
-    # every stream has finished (the timed region joins them).
+    # every leg through the C-ABI host-buffer entry points (triot_embed_host, triot_expected_
+    # value_host, triot_apply_binary_host): slabs streamed through device staging with H2D,
+    # kernel and D2H overlapped (P:607), each op on its own stream so one op's device-to-host
+    # drain overlaps the next op's host-to-device feed; the step ends when every stream is done
     side = [torch.cuda.Stream(dev) for _ in range(4)]
 
     def e2e_step():
@@ -492,10 +600,16 @@ def run_e2e(args, host, dev, stream, T, world):
         with torch.cuda.stream(side[0]):
             T.embed_host(outs["dst2"], pin["src2"], device=dev)
         with torch.cuda.stream(side[1]):
-            m3 = T.expected_value(pin["p3"].to(dev, non_blocking=True))
-            outs["m3"].copy_(m3, non_blocking=True)
+            T.expected_value_host(pin["p3"], staging3, out=outs["m3"],
+                                  offset=sl["C3"]["offset"] if world > 1 else None)
+            if world > 1:   # amalgamate the ranks' results: 48 bytes each way
+                m3d.copy_(outs["m3"], non_blocking=True)
+                dist.all_gather_into_tensor(g3, m3d)
+                T.sum_rows(g3.view(world, 6), out=r3)
+                res3.copy_(r3, non_blocking=True)
         with torch.cuda.stream(side[2]):
-            T.apply_binary_host(pin["a4"], pin["b4"], "mul", out=outs["c4"], device=dev)
+            T.apply_binary_host(pin["a4"], pin["b4"], "mul", out=outs["c4"], iter_shape=ish,
+                                device=dev)
         with torch.cuda.stream(side[3]):
             T.embed_host(outs["dst5"], pin["src5"], device=dev)
         for sd in side:
@@ -505,20 +619,33 @@ def run_e2e(args, host, dev, stream, T, world):
     torch.cuda.synchronize(dev)
     k = max(1, min(args.steps, args.e2e_steps))
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
     ea.record(stream)
     for _ in range(k):
         e2e_step()
     eb.record(stream)
     torch.cuda.synchronize(dev)
     ms = ea.elapsed_time(eb) / k
+    if world > 1:
+        import torch as _t
+        v = _t.tensor([ms, float(h2d), float(d2h)], dtype=_t.float64, device=dev)
+        mx = v[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        ms, h2d, d2h = float(mx.item()), int(v[1].item()), int(v[2].item())
     step_bytes = sum(algorithmic_bytes(n) for n in STEP_OPS)
-    return {"value": round(world * step_bytes / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": k,
-            "ms_per_step": round(ms, 3),
-            "note": "public API from pinned host buffers: embed_host / apply_binary_host "
-                    "(slab-streamed, H2D / kernel / D2H overlapped) and expected_value on a "
-                    "copied p, one stream per op; every input's H2D and every result's D2H "
-                    "inside the timed region"}
+    out = {"value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": k,
+           "ms_per_step": round(ms, 3),
+           "note": "public C-ABI host-buffer entry points from pinned host memory: "
+                   "triot_embed_host, triot_expected_value_host, triot_apply_binary_host "
+                   "(chunk-streamed, H2D / kernel / D2H overlapped), one stream per op; every "
+                   "input's H2D and every result's D2H inside the timed region"}
+    if world == 1:
+        out["pcie_same_run"] = pcie_floors(dev, h2d, d2h)
+    return out
 
 
 # ----------------------------------------------------------------------------- oracle arms
@@ -575,13 +702,15 @@ def _calibrate(seconds: float) -> float:
     return min(1.0, seconds / max(full_s, 1e-9))
 
 
-def cpu_baseline(budget_s: float = 20.0, frac: float | None = None):
-    """The oracle as it stands, 1 thread, on a slab of each op sized to ~budget_s seconds."""
+def cpu_baseline(budget_s: float = 20.0, frac: float | None = None, reps: int = 3):
+    """The oracle as it stands, 1 thread, on a slab of each op sized to ~budget_s seconds in
+    all: `reps` repetitions (init excluded), min / mean / max reported, value = median."""
     if frac is None:
-        frac = _calibrate(budget_s)
+        frac = _calibrate(budget_s / reps)
     slabs = [_slab(n, frac) for n in STEP_OPS]
-    secs = sum(_run_slab(k, a) for k, a, _ in slabs)
     nbytes = sum(b for _, _, b in slabs)
+    runs = [sum(_run_slab(k, a) for k, a, _ in slabs) for _ in range(reps)]
+    secs = statistics.median(runs)
     # Benchmark 4 (naive convolution) on the same host thread, for the paper-benchmark line
     from oracle import oracle as O
     rng4 = np.random.default_rng(17)
@@ -591,8 +720,14 @@ def cpu_baseline(budget_s: float = 20.0, frac: float | None = None):
     b4_us = (time.perf_counter() - t0) * 1e6
     return {"value": round(nbytes / secs / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"leading {frac:.3f} of axis 0 of each of C2,C3,C4,C5 (one slab per op), "
-                      f"{nbytes} algorithmic bytes in {secs:.2f} s, single thread",
-            "seconds": round(secs, 3), "b4_oracle_us": round(b4_us, 1), "host": host_info()}
+                      f"{nbytes} algorithmic bytes, median of {reps} reps, single thread",
+            "reps": reps,
+            "seconds_min_mean_max": [round(min(runs), 3), round(statistics.fmean(runs), 3),
+                                     round(max(runs), 3)],
+            "gbs_min_mean_max": [round(nbytes / max(runs) / 1e9, 4),
+                                 round(nbytes / statistics.fmean(runs) / 1e9, 4),
+                                 round(nbytes / min(runs) / 1e9, 4)],
+            "b4_oracle_us": round(b4_us, 1), "host": host_info()}
 
 
 def host_info():
@@ -636,6 +771,9 @@ def run_reference(args, rank, world):
         "ms_per_step": round(1000 * total / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "bytes_per_step": step_bytes,
+                   "slab": f"leading {frac:.4f} of axis 0 of each of C2, C3, C4, C5 per step "
+                           "(a bounded sample of the same configs: the full step would take "
+                           "~6 s of oracle time per step)",
                    "parallelism": "CPU oracle, rank 0 only"},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": sample, "host": host_info()},

@@ -212,12 +212,14 @@ TRIOT_API int triot_embed_host(void* dst, const int64_t* dst_shape, const void* 
 /* The expected value (Alg 11) of a PMF in HOST memory: p streamed through the staging
  * buffer in chunks of its leading axes ("copied to the GPU in chunks"), each chunk's
  * triot_expected_value_offset written to a row in staging, the rows summed in chunk order
- * (triot_sum_rows) and the d (+1 with_mass) doubles copied to the host array `out`.  The staging
- * buffer also holds the reduction workspace (cleared by the call itself); `cuda_stream`
- * completes when `out` is written.  Deterministic for a fixed staging size. */
-TRIOT_API int triot_expected_value_host(double* out, const void* p, const int64_t* shape, int d,
-                                        int dtype, int with_mass, void* staging,
-                                        size_t staging_bytes, void* cuda_stream);
+ * (triot_sum_rows) and the d (+1 with_mass) doubles copied to the host array `out`.  offset
+ * (host, d entries, NULL = zeros): p is the block of a larger PMF at that tuple, as in
+ * triot_expected_value_offset.  The staging buffer (device, 256-byte aligned) also holds the
+ * reduction workspace (cleared by the call itself); `cuda_stream` completes when `out` is
+ * written.  Deterministic for a fixed staging size. */
+TRIOT_API int triot_expected_value_host(double* out, const void* p, const int64_t* shape,
+                                        const int64_t* offset, int d, int dtype, int with_mass,
+                                        void* staging, size_t staging_bytes, void* cuda_stream);
 
 /* c (host, dense in iter_shape, NULL = element-wise min) = a OP b, all host buffers. */
 TRIOT_API int triot_apply_binary_host(void* c, const void* a, const int64_t* a_shape,

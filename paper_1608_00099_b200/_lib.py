@@ -80,9 +80,9 @@ _lib.triot_sum_rows.restype = ctypes.c_int
 _lib.triot_sum_rows.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                 ctypes.c_void_p]
 _lib.triot_expected_value_host.restype = ctypes.c_int
-_lib.triot_expected_value_host.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64p, ctypes.c_int,
-                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
-                                           ctypes.c_size_t, ctypes.c_void_p]
+_lib.triot_expected_value_host.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64p, _i64p,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
 class triot_view(ctypes.Structure):
     """include/triot.h triot_view: a window of a dense base tensor."""
     _fields_ = [("data", ctypes.c_void_p), ("base_shape", _i64p), ("start", _i64p),
@@ -228,10 +228,12 @@ def triot_sum_rows(out: int, rows: int, nrows: int, ncols: int, stream: int) -> 
     return _lib.triot_sum_rows(out, rows, nrows, ncols, stream)
 
 
-def triot_expected_value_host(out: int, p: int, shape, d: int, dtype: int, with_mass: int,
-                              staging: int, staging_bytes: int, stream: int) -> int:
-    return _lib.triot_expected_value_host(out, p, _shape(shape), d, dtype, with_mass, staging,
-                                          staging_bytes, stream)
+def triot_expected_value_host(out: int, p: int, shape, offset, d: int, dtype: int,
+                              with_mass: int, staging: int, staging_bytes: int,
+                              stream: int) -> int:
+    return _lib.triot_expected_value_host(out, p, _shape(shape),
+                                          _shape(offset) if offset is not None else None, d,
+                                          dtype, with_mass, staging, staging_bytes, stream)
 
 
 def triot_expected_value_view(out: int, p: triot_view, d: int, dtype: int, with_mass: int,

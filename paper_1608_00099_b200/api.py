@@ -239,10 +239,12 @@ def sum_rows(rows, out=None):
     return out
 
 
-def expected_value_host(p, staging, out=None, with_mass: bool = False):
+def expected_value_host(p, staging=None, out=None, with_mass: bool = False, offset=None,
+                        device=None):
     """triot_expected_value_host: the expected value of a (pinned) host tensor p, streamed in
     chunks through the device `staging` buffer (a uint8 CUDA tensor, 256-byte aligned); returns
-    a host float64 tensor (pinned when allocated here).  Synchronous: waits for the result."""
+    a host float64 tensor (pinned when allocated here), valid once the current stream has
+    completed.  offset: p is the block at that tuple of a larger PMF (global weights)."""
     torch = _torch()
     if p.is_cuda or not p.is_contiguous():
         raise ValueError("p must be a contiguous host tensor")
@@ -251,10 +253,15 @@ def expected_value_host(p, staging, out=None, with_mass: bool = False):
     n = d + (1 if with_mass else 0)
     if out is None:
         out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    if staging is None:
+        dev = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        staging = globals()["staging"](dev)
     dev = staging.device
     with _device(dev):
-        _lib.check(_lib.triot_expected_value_host(out.data_ptr(), p.data_ptr(), tuple(p.shape), d,
-                                                  code, 1 if with_mass else 0,
+        off = tuple(int(x) for x in offset) if offset is not None else None
+        _lib.check(_lib.triot_expected_value_host(out.data_ptr(), p.data_ptr(), tuple(p.shape),
+                                                  off, d, code, 1 if with_mass else 0,
                                                   staging.data_ptr(), staging.numel(),
                                                   _stream(dev)))
     return out

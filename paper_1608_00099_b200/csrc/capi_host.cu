@@ -242,9 +242,9 @@ int triot_embed_host(void* dst, const int64_t* dst_shape, const void* src,
                       });
 }
 
-int triot_expected_value_host(double* out, const void* p, const int64_t* shape, int d, int dtype,
-                              int with_mass, void* staging, size_t staging_bytes,
-                              void* cuda_stream) {
+int triot_expected_value_host(double* out, const void* p, const int64_t* shape,
+                              const int64_t* offset, int d, int dtype, int with_mass,
+                              void* staging, size_t staging_bytes, void* cuda_stream) {
   Geom g;
   int st = plan_ev(g, p, shape, d, dtype);
   if (st) return st;
@@ -268,6 +268,11 @@ int triot_expected_value_host(double* out, const void* p, const int64_t* shape, 
   if (staging_bytes <= fixed + 512)
     return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu staging bytes, need > %llu", staging_bytes,
                      (unsigned long long)(fixed + 512));
+  if (offset)
+    for (int j = 0; j < d; ++j)
+      if (offset[j] < 0 || offset[j] + shape[j] > (int64_t)(1ll << 53))
+        return set_error(TRIOT_ERR_BAD_SHAPE, "BadShape: offset[%d] = %lld outside [0, 2^53)", j,
+                         (long long)offset[j]);
   if (g.empty) {  // empty sums: zeros
     double* fin0 = (double*)((char*)staging + align(ws_bytes));
     cudaError_t e0 = cudaMemsetAsync(fin0, 0, (size_t)nout * 8, cs);
@@ -336,7 +341,7 @@ int triot_expected_value_host(double* out, const void* p, const int64_t* shape, 
       // the chunk as a d-dimensional block (1, .., 1, r, s_{k+1}, ..) at (prefix, a, 0, ..)
       for (int j = 0; j < d; ++j) {
         csh[j] = j < k ? 1 : j == k ? (int64_t)r : shape[j];
-        off[j] = j < k ? (int64_t)prefix[j] : j == k ? (int64_t)a : 0;
+        off[j] = (offset ? offset[j] : 0) + (j < k ? (int64_t)prefix[j] : j == k ? (int64_t)a : 0);
       }
       if ((st = triot_expected_value_offset(rowsbuf + chunk * (uint64_t)nout, slot[s], csh, off, d,
                                             dtype, with_mass, ws, ws_bytes, cs)))

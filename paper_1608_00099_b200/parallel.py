@@ -29,6 +29,29 @@ def slab_rows(n0: int, world: int, rank: int) -> tuple[int, int]:
     return (rank * n0) // world, ((rank + 1) * n0) // world
 
 
+def leading_box(shape, world: int, rank: int) -> list[tuple[int, int]]:
+    """This rank's box [lo_k, hi_k) per axis of a partition of the outermost loops:
+    axis 0 in balanced slabs when it has at least as many indices as ranks; otherwise each
+    axis-0 index goes to a contiguous group of ranks (rank r takes index r * n0 // world), which
+    split the next axis the same way.  Boxes are disjoint and cover the shape."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    box = [(0, int(n)) for n in shape]
+    r, nr = rank, world
+    for k, n in enumerate(shape):
+        n = int(n)
+        if nr <= 1:
+            break
+        if n >= nr or k == len(shape) - 1:
+            box[k] = slab_rows(n, nr, r)
+            break
+        i = (r * n) // nr
+        box[k] = (i, i + 1)
+        first, last = -(-i * nr // n), -(-(i + 1) * nr // n)   # ranks sharing index i
+        r, nr = r - first, last - first
+    return box
+
+
 def embed_slab(dst_slab, src, lo: int, region_only: bool = False):
     """Rows [lo, lo + dst_slab.shape[0]) of embed(dst, src): dst_slab is this rank's slab of the
     global dst; src is the global src (or at least its rows from lo on) on this device."""

@@ -104,3 +104,63 @@ def test_slab_rows_cover_once():
             spans = [P.slab_rows(n0, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n0
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def test_leading_box_partition_covers_once():
+    """Every element of the shape lies in exactly one rank's box (C2/C3/C4/C5 shapes at 1..8
+    ranks, including (4,)*14 with more ranks than axis-0 indices)."""
+    for shape in [(512, 512, 512), (16,) * 6, (32, 32, 24, 32, 32), (4,) * 14, (3, 5), (2, 2, 2),
+                  (1, 7), (5,)]:
+        for world in range(1, 9):
+            lead = shape[:3]
+            cover = np.zeros(lead, dtype=np.int32)
+            for r in range(world):
+                box = P.leading_box(shape, world, r)
+                assert all(0 <= lo <= hi <= n for (lo, hi), n in zip(box, shape))
+                assert all(box[k] == (0, shape[k]) for k in range(3, len(shape)))
+                cover[tuple(slice(lo, hi) for lo, hi in box[:3])] += 1
+            assert np.all(cover == 1), (shape, world)
+
+
+def test_bench_slab_plan_reassembles_the_global_step():
+    """bench.slab_plan at 1..8 ranks: every rank's blocks, run through the oracle, reassemble the
+    global C2/C4/C5 outputs exactly, and the rank results of C3 (offset EVs, rank-order sum)
+    equal the global oracle EV -- on shrunken copies of the configs (same dimensions, smaller
+    extents) so the oracle finishes fast."""
+    import bench
+    rng = np.random.default_rng(11)
+    host = {
+        "C2": {"src": rng.standard_normal((6, 5, 7)).astype(np.float32), "dst_shape": (9, 8, 8)},
+        "C3": {"p": rng.random((5, 4, 3, 4))},
+        "C4": {"a": rng.random((4, 6, 3, 5)), "b": rng.random((6, 4, 4, 4)),
+               "iter_shape": (4, 4, 3, 4)},
+        "C5": {"src": rng.random((3,) * 6).astype(np.float32), "dst_shape": (4,) * 6},
+    }
+    ref2 = np.empty(host["C2"]["dst_shape"], np.float32); O.embed(ref2, host["C2"]["src"])
+    ref5 = np.empty(host["C5"]["dst_shape"], np.float32); O.embed(ref5, host["C5"]["src"])
+    ref4 = O.apply_binary(host["C4"]["a"], host["C4"]["b"], "mul", iter_shape=(4, 4, 3, 4))
+    ref3 = O.expected_value(host["C3"]["p"])
+    for world in range(1, 9):
+        out2 = np.full(ref2.shape, np.nan, np.float32)
+        out5 = np.full(ref5.shape, np.nan, np.float32)
+        out4 = np.full(ref4.shape, np.nan)
+        tot3 = np.zeros(4)
+        for r in range(world):
+            sl = bench.slab_plan(host, world, r)
+            for n, out in (("C2", out2), ("C5", out5)):
+                blk = np.empty(sl[n]["dst_shape"], np.float32)
+                if blk.size:
+                    O.embed(blk, sl[n]["src"])
+                out[tuple(slice(lo, hi) for lo, hi in sl[n]["box"])] = blk
+            if all(e > 0 for e in sl["C4"]["iter_shape"]):
+                blk = O.apply_binary(sl["C4"]["a"], sl["C4"]["b"], "mul",
+                                     iter_shape=sl["C4"]["iter_shape"])
+                out4[tuple(slice(lo, hi) for lo, hi in sl["C4"]["box"])] = blk
+            p = sl["C3"]["p"]
+            if p.size:
+                m, mass = O.expected_value(p), p.sum()
+                tot3 = tot3 + np.array([m[k] + sl["C3"]["offset"][k] * mass for k in range(4)])
+        np.testing.assert_array_equal(out2, ref2)
+        np.testing.assert_array_equal(out5, ref5)
+        np.testing.assert_array_equal(out4, ref4)
+        assert np.all(np.abs(tot3 - ref3) <= 1e-12 * np.abs(ref3)), world
