@@ -25,8 +25,10 @@ LIB = os.path.join(PKG, "libtriot.so")
 INCLUDE = os.path.join(ROOT, "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# --compress-mode=size: the SASS of the ~1,500 kernel instances is stored compressed in the
+# fatbins (decompressed by the driver when a kernel is first loaded): 2.6x smaller objects
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fvisibility=hidden",
-           "-I", CSRC, "-I", INCLUDE, "-diag-suppress", "177"]
+           "-I", CSRC, "-I", INCLUDE, "-diag-suppress", "177", "--compress-mode=size"]
 
 # (object name, source, extra defines)
 UNITS = [("plan", "plan.cpp", []), ("capi", "capi.cu", []), ("capi_host", "capi_host.cu", [])]

@@ -39,6 +39,19 @@ constexpr int KEV = 2;
 
 template <int D, int V, typename IDX>
 const void* kptr() {
+  // One-element vectors are never planned for embed, binary or the dense expected value: an
+  // innermost extent no vector width divides takes flat vectors (plan.cpp: flat_ok) or row
+  // windows instead -- so those instances are not compiled (tests/test_boundary_cpu.py
+  // test_planner_never_selects_uncompiled_instances).  Dot, update, convolution and the EV of
+  // a view keep them.
+#if TRIOT_INST_OP == 0 || TRIOT_INST_OP == 1 || (TRIOT_INST_OP == 2 && TRIOT_INST_BOP == 0)
+  constexpr bool kSkip = V == 1;
+#else
+  constexpr bool kSkip = false;
+#endif
+  if constexpr (kSkip) {
+    return nullptr;
+  } else {
 #if TRIOT_INST_OP == 0
   return (const void*)&embed_kernel<D, ESZ, V, IDX, KEMBED, false>;
 #elif TRIOT_INST_OP == 1
@@ -68,6 +81,7 @@ const void* kptr() {
 #else
   return (const void*)&ev_kernel<D, ESZ, V, IDX, KEV>;
 #endif
+  }
 }
 
 // flat-vector instances (odd innermost extents): embed, binary, expected value
@@ -125,7 +139,11 @@ const void* kptr_shift() {
 template <int D, typename IDX>
 const void* kptr_zero_runs() {
 #if TRIOT_INST_OP == 0
-  return (const void*)&embed_kernel<D, ESZ, 32 / ESZ, IDX, KEMBED, true>;
+  if constexpr (D < 2) {  // zero runs need an outer digit khi < D - 1 (plan.cpp set_step)
+    return nullptr;
+  } else {
+    return (const void*)&embed_kernel<D, ESZ, 32 / ESZ, IDX, KEMBED, true>;
+  }
 #else
   return nullptr;
 #endif

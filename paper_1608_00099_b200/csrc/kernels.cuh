@@ -124,6 +124,65 @@ struct Mem<4> {
   }
 };
 
+// Coherent (non-.nc) loads for operands that may alias the kernel's own output: PTX defines
+// ld.global.nc only for data read-only for the kernel's lifetime, and apply_binary allows c == a
+// (in place), the fused update writes x in place.  The binary and update kernels load
+// through these; embed (src may never overlap dst) and the reductions keep .nc.
+template <int NB>
+struct MemC;
+template <>
+struct MemC<32> {
+  static __device__ __forceinline__ void ld(const void* p, uint32_t* w) {
+    asm volatile(
+        "ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7])
+        : "l"(p));
+  }
+};
+template <>
+struct MemC<16> {
+  static __device__ __forceinline__ void ld(const void* p, uint32_t* w) {
+    asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p));
+  }
+};
+template <>
+struct MemC<8> {
+  static __device__ __forceinline__ void ld(const void* p, uint32_t* w) {
+    asm volatile("ld.global.v2.b32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(p));
+  }
+  static __device__ __forceinline__ void ld_or0(const void* p, bool pred, uint32_t* w) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+        " @q ld.global.v2.b32 {%0,%1}, [%2];\n}"
+        : "=r"(w[0]), "=r"(w[1])
+        : "l"(p), "r"((uint32_t)pred));
+  }
+};
+template <>
+struct MemC<4> {
+  static __device__ __forceinline__ void ld(const void* p, uint32_t* w) {
+    asm volatile("ld.global.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+  }
+  static __device__ __forceinline__ void ld_or0(const void* p, bool pred, uint32_t* w) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.b32 %0, 0;\n"
+        " @q ld.global.b32 %0, [%1];\n}"
+        : "=r"(w[0])
+        : "l"(p), "r"((uint32_t)pred));
+  }
+};
+template <bool NC, int NB>
+struct MemSel {
+  using T = Mem<NB>;
+};
+template <int NB>
+struct MemSel<false, NB> {
+  using T = MemC<NB>;
+};
+
 // Programmatic dependent launch (sm_90+): every kernel is launched with programmatic stream
 // serialization, so it may be scheduled while its predecessor on the stream drains.  It lets
 // its own successor be scheduled as soon as all its blocks have started (pdl_trigger), and it
@@ -285,15 +344,16 @@ __device__ __forceinline__ IDX elem_off(IDX off, int e, uint32_t lgL, IDX rho, I
   return off + r * rho + c * tau;
 }
 
-template <int ESZ, int V, typename IDX>
+template <int ESZ, int V, typename IDX, bool NC = true>
 __device__ __forceinline__ void load_vec(const TensorAcc<IDX>& t, IDX off, uint32_t lgL,
                                          uint32_t* w) {
   constexpr int EW = ESZ / 4;
   if (V > 1 && t.vec) {
-    Mem<V * ESZ>::ld(addr<ESZ>(t.ptr, off), w);
+    MemSel<NC, V * ESZ>::T::ld(addr<ESZ>(t.ptr, off), w);
   } else {
 #pragma unroll
-    for (int e = 0; e < V; ++e) Mem<ESZ>::ld(addr<ESZ>(t.ptr, elem_off(off, e, lgL, t.rho, t.tau)), w + e * EW);
+    for (int e = 0; e < V; ++e)
+      MemSel<NC, ESZ>::T::ld(addr<ESZ>(t.ptr, elem_off(off, e, lgL, t.rho, t.tau)), w + e * EW);
   }
 }
 
@@ -592,8 +652,8 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
       v += d.dv;
       coff[j] = off[0];
       if (valid[j]) {
-        load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, ba[j]);
-        load_vec<ESZ, V, IDX>(d.t[2], off[2], lgL, bb[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[1], off[1], lgL, ba[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[2], off[2], lgL, bb[j]);
       }
       odo_step<D, 3, false, IDX>(d, u, off, oob);
     }
@@ -641,8 +701,8 @@ __global__ void __launch_bounds__(kBlock) binary_shift_kernel(const __grid_const
       v += d.dv;
       coff[j] = off[0];
       if (valid[j]) {
-        load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, ba[j]);
-        load_vec<ESZ, V, IDX>(d.t[2], off[2], lgL, bb[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[1], off[1], lgL, ba[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[2], off[2], lgL, bb[j]);
       }
       odo_step<D, 3, false, IDX>(d, u, off, oob);
     }
@@ -753,13 +813,13 @@ __global__ void __launch_bounds__(kBlock) binary_flat_kernel(const __grid_consta
       v += d.dv;
       const IDX f0 = vj[j] * (IDX)V;
       const bool full = vj[j] < vend && f0 + (IDX)V <= d.nelem;
-      if (full && avec) Mem<32>::ld(addr<ESZ>(d.t[1].ptr, f0), ba[j]);
-      if (full && bvec) Mem<32>::ld(addr<ESZ>(d.t[2].ptr, f0), bb[j]);
+      if (full && avec) MemC<32>::ld(addr<ESZ>(d.t[1].ptr, f0), ba[j]);
+      if (full && bvec) MemC<32>::ld(addr<ESZ>(d.t[2].ptr, f0), bb[j]);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         const bool in = vj[j] < vend && f0 + (IDX)e < d.nelem;
-        if (in && !(full && avec)) Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1]), ba[j] + e * EW);
-        if (in && !(full && bvec)) Mem<ESZ>::ld(addr<ESZ>(d.t[2].ptr, off[2]), bb[j] + e * EW);
+        if (in && !(full && avec)) MemC<ESZ>::ld(addr<ESZ>(d.t[1].ptr, off[1]), ba[j] + e * EW);
+        if (in && !(full && bvec)) MemC<ESZ>::ld(addr<ESZ>(d.t[2].ptr, off[2]), bb[j] + e * EW);
         coff[j][e] = off[0];
         odo_inc1<D, 3, false, IDX>(d, u, off, oob);
       }
@@ -1008,8 +1068,8 @@ __device__ __forceinline__ void binary_rows_group(const Desc<IDX>& d, IDX gbase,
       const uint32_t r = min(__umulhi(e, mg), (uint32_t)kRowsTab - 1u);
       const RowSrc<IDX> ab = tab[r];  // .off = a, .lim = b (rebased offsets)
       if (!CD) coff[j] = tc[r] + (IDX)e * sc;
-      Mem<ESZ>::ld_or0(pa + (uint64_t)(ab.off + (IDX)e * sa) * ESZ, e < tot, ba[j]);
-      Mem<ESZ>::ld_or0(pb + (uint64_t)(ab.lim + (IDX)e * sb) * ESZ, e < tot, bb[j]);
+      MemC<ESZ>::ld_or0(pa + (uint64_t)(ab.off + (IDX)e * sa) * ESZ, e < tot, ba[j]);
+      MemC<ESZ>::ld_or0(pb + (uint64_t)(ab.lim + (IDX)e * sb) * ESZ, e < tot, bb[j]);
     }
     char* p = c + (uint64_t)(gbase + (IDX)e0 + (IDX)lane) * ESZ;
 #pragma unroll
@@ -1037,8 +1097,8 @@ __device__ __forceinline__ void binary_warp_row(const Desc<IDX>& d, IDX oc, IDX 
     for (int j = 0; j < KW; ++j) {
       const IDX c = c0 + (IDX)(32 * j);
       if (c < n) {
-        Mem<ESZ>::ld(ap + (uint64_t)(c * sa) * ESZ, ba[j]);
-        Mem<ESZ>::ld(bp + (uint64_t)(c * sb) * ESZ, bb[j]);
+        MemC<ESZ>::ld(ap + (uint64_t)(c * sa) * ESZ, ba[j]);
+        MemC<ESZ>::ld(bp + (uint64_t)(c * sb) * ESZ, bb[j]);
       }
     }
 #pragma unroll
@@ -1771,9 +1831,9 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
       v += d.dv;
       xoff[j] = off[0];
       if (valid[j]) {
-        load_vec<ESZ, V, IDX>(d.t[0], off[0], lgL, bx[j]);
-        load_vec<ESZ, V, IDX>(d.t[1], off[1], lgL, by[j]);
-        load_vec<ESZ, V, IDX>(d.t[2], off[2], lgL, bz[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[0], off[0], lgL, bx[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[1], off[1], lgL, by[j]);
+        load_vec<ESZ, V, IDX, false>(d.t[2], off[2], lgL, bz[j]);
       }
       odo_step<D, 3, false, IDX>(d, u, off, oob);
     }

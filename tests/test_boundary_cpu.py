@@ -654,3 +654,27 @@ def test_shifted_store_plan():
     p = T.triot_plan_describe(0, [(64, 64), (60, 60)], None, 2, F32, 1, ptr_mod32=(4, 0, 0))
     assert p["dshift"] == 0                               # region only: dst rows not dense
 
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_planner_never_selects_uncompiled_instances(seed):
+    """inst.cu compiles no one-element-vector instances for embed, binary and the dense expected
+    value, and no zero-run instance for D = 1: over random shapes, alignments and policies the
+    planner never selects them (a V = 1 plan is always flat vectors or row windows)."""
+    rng = np.random.default_rng(900 + seed)
+    for trial in range(300):
+        d = int(rng.integers(1, 9))
+        dt = [F32, F64][trial % 2]
+        a = random_shape(rng, d, 4000, lo=1, hi=9)
+        b = tuple(int(x) + int(rng.integers(0, 3)) for x in a)
+        mods = [int(rng.integers(0, 8)) * (4 if dt == F32 else 8) % 32 for _ in range(3)]
+        plans = [T.triot_plan_describe(0, [b, a], None, d, dt, 0, mods),
+                 T.triot_plan_describe(0, [a, b], None, d, dt, 0, mods),
+                 T.triot_plan_describe(1, [None, a, b], None, d, dt, 2, mods),
+                 T.triot_plan_describe(1, [b, a, b], a, d, dt, 0, mods),
+                 T.triot_plan_describe(2, [a], None, d, dt, 0, mods)]
+        for pl in plans:
+            if pl["empty"]:
+                continue
+            assert pl["V"] > 1 or pl["flat"] or pl["rows"], pl
+            assert not (pl["zmask"] and pl["D"] < 2), pl
