@@ -13,18 +13,30 @@ _ws_lock = threading.Lock()
 _ws_cache: dict = {}
 
 
+_T = None          # torch, imported on first use (the package imports without it)
+_DT = {}           # torch dtype -> triot dtype code
+_RAW_STREAM = None  # torch._C._cuda_getCurrentRawStream
+_GET_DEV = None     # torch._C._cuda_getDevice
+
+
 def _torch():
-    import torch
-    return torch
+    global _T, _RAW_STREAM, _GET_DEV
+    if _T is None:
+        import torch
+        _DT[torch.float32] = _lib.TRIOT_F32
+        _DT[torch.float64] = _lib.TRIOT_F64
+        _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        _GET_DEV = getattr(torch._C, "_cuda_getDevice", None)
+        _T = torch
+    return _T
 
 
 def _dtype_code(t) -> int:
-    torch = _torch()
-    if t.dtype == torch.float32:
-        return _lib.TRIOT_F32
-    if t.dtype == torch.float64:
-        return _lib.TRIOT_F64
-    raise TypeError(f"triot supports float32 and float64 tensors, got {t.dtype}")
+    _torch()
+    code = _DT.get(t.dtype)
+    if code is None:
+        raise TypeError(f"triot supports float32 and float64 tensors, got {t.dtype}")
+    return code
 
 
 def _check_tensor(name: str, t, device=None):
@@ -54,18 +66,34 @@ def _device(device):
     launches on the tensor's stream): a no-op when it already is, which is the common case."""
     torch = _torch()
     idx = device.index
-    if idx is None or idx == torch.cuda.current_device():
+    if idx is None or idx == (_GET_DEV() if _GET_DEV else torch.cuda.current_device()):
         return _NO_SWITCH
     return torch.cuda.device(idx)
 
 
 def _stream(device) -> int:
     torch = _torch()
-    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)   # the same handle, ~1 us cheaper
-    if raw is not None:
+    if _RAW_STREAM is not None:   # the same handle as current_stream().cuda_stream, ~1 us cheaper
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        return raw(idx)
+        return _RAW_STREAM(idx)
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def _fast_pair(x, y):
+    """The common case of the two-operand entry points in one pass: both contiguous CUDA tensors
+    of one dtype, dimension and device.  Returns (device index, dtype code, stream) or None (the
+    caller then runs the full checks, which raise the precise error)."""
+    _torch()
+    if not (x.is_cuda and y.is_cuda and x.is_contiguous() and y.is_contiguous()):
+        return None
+    idx = x.get_device()            # an int: cheaper than comparing torch.device objects
+    dt = x.dtype
+    code = _DT.get(dt)
+    if code is None or y.dtype != dt or y.get_device() != idx or y.dim() != x.dim():
+        return None
+    if _RAW_STREAM is None or _GET_DEV is None or idx != _GET_DEV():
+        return None
+    return idx, code, _RAW_STREAM(idx)
 
 
 class View:
@@ -143,15 +171,26 @@ def expected_value_view(p: "View", out=None, with_mass: bool = False):
 def embed(dst, src, region_only: bool = False):
     """dst[t] = src[t] where t < src.shape, +0.0 elsewhere (or only the overlap if
     region_only).  In place on dst; returns dst."""
+    fast = _fast_pair(dst, src)
+    if fast is not None:   # the tensors are on the current device: no guard needed
+        st = _lib._lib.triot_embed(dst.data_ptr(), _lib._shape(dst.shape), src.data_ptr(),
+                                   _lib._shape(src.shape), dst.dim(), fast[1],
+                                   _lib.TRIOT_EMBED_REGION_ONLY if region_only else 0, fast[2])
+        if st:
+            _lib.check(st)
+        return dst
+    dev = dst.device
     _check_tensor("dst", dst)
-    _check_tensor("src", src, dst.device)
+    _check_tensor("src", src, dev)
     if src.dtype != dst.dtype or src.dim() != dst.dim():
         raise ValueError("dst and src must have the same dtype and dimension")
     flags = _lib.TRIOT_EMBED_REGION_ONLY if region_only else _lib.TRIOT_EMBED_FULL
-    with _device(dst.device):
-        _lib.check(_lib.triot_embed(dst.data_ptr(), tuple(dst.shape), src.data_ptr(),
-                                    tuple(src.shape), dst.dim(), _dtype_code(dst), flags,
-                                    _stream(dst.device)))
+    with _device(dev):
+        st = _lib.lib().triot_embed(dst.data_ptr(), _lib._shape(dst.shape), src.data_ptr(),
+                                    _lib._shape(src.shape), dst.dim(), _dtype_code(dst), flags,
+                                    _stream(dev))
+    if st:
+        _lib.check(st)
     return dst
 
 
@@ -159,6 +198,16 @@ def apply_binary(a, b, op: str = "mul", out=None, iter_shape=None):
     """out[t] = a[t] OP b[t] for t in iter_shape (default: element-wise min of the shapes).
     `out` defaults to a new tensor dense in iter_shape."""
     torch = _torch()
+    fast = _fast_pair(a, b)
+    if fast is not None and out is not None and iter_shape is None and out.is_cuda and \
+            out.is_contiguous() and out.dtype == a.dtype and out.get_device() == fast[0]:
+        st = _lib._lib.triot_apply_binary(out.data_ptr(), _lib._shape(out.shape), a.data_ptr(),
+                                          _lib._shape(a.shape), b.data_ptr(),
+                                          _lib._shape(b.shape), None, a.dim(), fast[1],
+                                          OPS[op], fast[2])
+        if st:
+            _lib.check(st)
+        return out
     _check_tensor("a", a)
     _check_tensor("b", b, a.device)
     if a.dtype != b.dtype or a.dim() != b.dim():

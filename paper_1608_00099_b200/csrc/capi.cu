@@ -330,6 +330,107 @@ int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
 
 size_t ev_ws_bytes(int nslots) { return reduce_ws_bytes(TRIOT_EV_MAX_GRID, nslots); }
 
+// ---- plan cache (dense embed / apply_binary): repeated calls on the same shapes skip the
+// planner and the launch geometry (P:266 calls the dispatch "already a prerequisite cost"; on a
+// 75 KB op it is most of the host time).  The plan depends on the pointers only through their
+// alignment (modulo 32) and null-ness -- both in the key -- and through the aliasing checks,
+// which are re-run on every hit: any overlap between the tensors (allowed in-place binary calls
+// included) takes the full planner, so every error is reported exactly as without the cache.
+struct PlanKey {
+  int32_t op, d, dtype, sub, dev, pmode, pbpsm, rows_on;
+  int64_t sh[4][TRIOT_MAXD];  // tensor shapes (+ the iteration shape for binary)
+  uint8_t has[4], mod[3];
+  bool operator==(const PlanKey& o) const { return memcmp(this, &o, sizeof(PlanKey)) == 0; }
+};
+struct PlanEntry {
+  PlanKey key;
+  bool valid = false;
+  Geom g;
+  const void* fn = nullptr;
+  unsigned grid = 0;
+};
+constexpr int kPlanCache = 8;
+thread_local PlanEntry g_plans[kPlanCache];
+
+uint64_t key_hash(const PlanKey& k) {
+  const unsigned char* b = (const unsigned char*)&k;
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < sizeof(PlanKey); ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+bool make_key(PlanKey& k, int op, int d, int dtype, int sub, const void* const* ptrs,
+              const int64_t* const* shapes, int nt, const int64_t* iter) {
+  if (d < 1 || d > TRIOT_MAXD) return false;
+  memset(&k, 0, sizeof(k));
+  k.op = op;
+  k.d = d;
+  k.dtype = dtype;
+  k.sub = sub;
+  if (cudaGetDevice(&k.dev) != cudaSuccess) return false;
+  k.pmode = g_override.mode;
+  k.pbpsm = g_override.bpsm;
+  k.rows_on = rows_enabled() ? 1 : 0;
+  for (int x = 0; x < nt; ++x) {
+    k.has[x] = shapes[x] ? 1 : 0;
+    if (shapes[x]) memcpy(k.sh[x], shapes[x], sizeof(int64_t) * d);
+    k.mod[x] = (uint8_t)(((uintptr_t)ptrs[x] & 31u) | (ptrs[x] ? 0x80u : 0u));
+  }
+  k.has[3] = iter ? 1 : 0;
+  if (iter) memcpy(k.sh[3], iter, sizeof(int64_t) * d);
+  return true;
+}
+
+// A hit with no overlap among the tensors: the cached plan with this call's pointers.
+bool plan_hit(const PlanKey& k, const void* const* ptrs, int nt, Geom& g, const void** fn,
+              unsigned* grid) {
+  PlanEntry& e = g_plans[key_hash(k) % kPlanCache];
+  if (!e.valid || !(e.key == k)) return false;
+  for (int x = 0; x < nt; ++x)
+    for (int y = x + 1; y < nt; ++y)
+      if (ptrs[x] && ptrs[y]) {
+        const uintptr_t a0 = (uintptr_t)ptrs[x], a1 = a0 + e.g.t[x].numel * (uint64_t)e.g.esz;
+        const uintptr_t b0 = (uintptr_t)ptrs[y], b1 = b0 + e.g.t[y].numel * (uint64_t)e.g.esz;
+        if (e.g.t[x].numel && e.g.t[y].numel && a0 < b1 && b0 < a1) return false;
+      }
+  g = e.g;
+  for (int x = 0; x < nt; ++x) g.t[x].ptr = ptrs[x];
+  *fn = e.fn;
+  *grid = e.grid;
+  return true;
+}
+
+void plan_store(const PlanKey& k, const Geom& g, const void* fn, unsigned grid) {
+  PlanEntry& e = g_plans[key_hash(k) % kPlanCache];
+  e.key = k;
+  e.g = g;
+  e.fn = fn;
+  e.grid = grid;
+  e.valid = true;
+}
+
+// embed / binary: choose the instance and the grid (the part of launch() a plan-cache hit skips)
+int prepare_stream_op(Geom& g, const void** fn_out, unsigned* grid_out) {
+  const void* fn = table_for(g)(g.D, vindex(g), g.idx64 ? 1 : 0);
+  if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no instance for D=%d V=%d", g.D, g.V);
+  unsigned grid;
+  int st = launch_geometry(fn, g, 1 << 30, &grid);
+  if (st) return st;
+  if (g.zmask) {  // embed with zero runs (set_step): its own instance, same geometry
+    fn = table_for(g)(g.D, 4, g.idx64 ? 1 : 0);
+    if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no zero-run instance for D=%d", g.D);
+  }
+  *fn_out = fn;
+  *grid_out = grid;
+  return TRIOT_OK;
+}
+
+int launch_stream_op(const Geom& g, const void* fn, unsigned grid, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return g.idx64 ? launch_t<uint64_t>(g, fn, grid, s, nullptr, nullptr)
+                 : launch_t<uint32_t>(g, fn, grid, s, nullptr, nullptr);
+}
+
 }  // namespace
 }  // namespace triot
 
@@ -359,10 +460,24 @@ const char* triot_last_error(void) { return last_error(); }
 
 int triot_embed(void* dst, const int64_t* dst_shape, const void* src, const int64_t* src_shape,
                 int d, int dtype, unsigned flags, void* cuda_stream) {
+  const void* ptrs[2] = {dst, src};
+  const int64_t* shapes[2] = {dst_shape, src_shape};
+  PlanKey key;
+  const bool keyed = dst_shape && src_shape && make_key(key, OP_EMBED, d, dtype, (int)flags, ptrs,
+                                                        shapes, 2, nullptr);
   Geom g;
+  const void* fn;
+  unsigned grid;
+  if (keyed && plan_hit(key, ptrs, 2, g, &fn, &grid)) {
+    const int st0 = launch_stream_op(g, fn, grid, cuda_stream);
+    if (!st0) clear_error();
+    return st0;
+  }
   int st = plan_embed(g, dst, dst_shape, src, src_shape, d, dtype, flags);
   if (st || g.empty) return st;
-  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if ((st = prepare_stream_op(g, &fn, &grid))) return st;
+  if (keyed) plan_store(key, g, fn, grid);
+  st = launch_stream_op(g, fn, grid, cuda_stream);
   if (!st) clear_error();
   return st;
 }
@@ -370,10 +485,24 @@ int triot_embed(void* dst, const int64_t* dst_shape, const void* src, const int6
 int triot_apply_binary(void* c, const int64_t* c_shape, const void* a, const int64_t* a_shape,
                        const void* b, const int64_t* b_shape, const int64_t* iter_shape, int d,
                        int dtype, int op, void* cuda_stream) {
+  const void* ptrs[3] = {c, a, b};
+  const int64_t* shapes[3] = {c_shape, a_shape, b_shape};
+  PlanKey key;
+  const bool keyed = a_shape && b_shape &&
+                     make_key(key, OP_BINARY, d, dtype, op, ptrs, shapes, 3, iter_shape);
   Geom g;
+  const void* fn;
+  unsigned grid;
+  if (keyed && plan_hit(key, ptrs, 3, g, &fn, &grid)) {
+    const int st0 = launch_stream_op(g, fn, grid, cuda_stream);
+    if (!st0) clear_error();
+    return st0;
+  }
   int st = plan_binary(g, c, c_shape, a, a_shape, b, b_shape, iter_shape, d, dtype, op);
   if (st || g.empty) return st;
-  st = launch(g, cuda_stream, nullptr, nullptr, 0);
+  if ((st = prepare_stream_op(g, &fn, &grid))) return st;
+  if (keyed) plan_store(key, g, fn, grid);
+  st = launch_stream_op(g, fn, grid, cuda_stream);
   if (!st) clear_error();
   return st;
 }

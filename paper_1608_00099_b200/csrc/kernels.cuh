@@ -428,7 +428,8 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
             }
           }
         }
-        odo_step<D, 2, true, IDX>(d, u, off, oob);
+        // past the warp's range the odometer is never read again (the loop ends): skip it
+        if (valid[j]) odo_step<D, 2, true, IDX>(d, u, off, oob);
       }
 #pragma unroll
       for (int j = 0; j < K; ++j)

@@ -174,6 +174,7 @@ static const uint64_t kRowsMaxLong = 4096;
 static const uint64_t kRowsWarpMin = 128;
 static thread_local bool g_rows_on = true;
 void set_rows_enabled(bool on) { g_rows_on = on; }
+bool rows_enabled() { return g_rows_on; }
 
 // Row-window geometry: digits are the outer canonical axes (a single unit digit when there is
 // none); a "vector" is one counter row of n = rowlen elements; every tensor keeps its row

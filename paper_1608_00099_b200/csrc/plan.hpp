@@ -102,6 +102,7 @@ int plan_binary_view(Geom& g, const triot_view* c, const triot_view* a, const tr
 void set_decomposition(Geom& g, int mode, uint64_t warps);
 // Row windows on/off for this thread (tuning hook, triot_set_launch_policy mode 5).
 void set_rows_enabled(bool on);
+bool rows_enabled();
 // (Re)compute the mixed-radix digits of the per-step advance for the current g.dv.
 void set_step(Geom& g);
 

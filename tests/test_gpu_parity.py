@@ -1182,3 +1182,44 @@ def test_view_embed_long_rows_vectorized(dtype):
         dbt = _dev(db)
         T.embed_view(T.View(dbt, dstart, win), T.View(_dev(src)))
         assert_bits_equal(dbt, ref)
+
+
+def test_plan_cache_pointers_alignment_and_aliasing():
+    """The host plan cache (dense embed / binary) keys on shapes, dtype, op, alignment and
+    policy: repeated calls with new buffers stay bit-exact, a call whose buffers overlap after a
+    cached disjoint call is still refused (or run in place when allowed), and a misaligned call
+    after an aligned one takes its own plan."""
+    inp = make_inputs("C1")
+    ref = np.empty(inp["dst_shape"]); O.embed(ref, inp["src"])
+    src = _dev(inp["src"])
+    for _ in range(3):                       # fresh dst buffers, same key: cached plan
+        dst = _poisoned(inp["dst_shape"], np.float64)
+        T.embed(dst, src)
+        assert_bits_equal(dst, ref)
+    for off in (1, 2, 0):                    # alignment changes the key
+        dst = _poisoned(inp["dst_shape"], np.float64, off)
+        T.embed(dst, _dev(inp["src"], (off + 1) % 3))
+        assert_bits_equal(dst, ref)
+    # overlap after a cached disjoint call: dst over src's buffer is refused
+    buf = torch.zeros(2 * 8 * 16 * 8 * 8 + 4 * 9 * 7 * 5, dtype=torch.float64, device=DEV)
+    d1 = buf[:8192].view(8, 16, 8, 8)
+    s1 = buf[8192:8192 + 1260].view(4, 9, 7, 5)
+    s1.copy_(src)
+    T.embed(d1, s1)                           # disjoint: cached
+    assert_bits_equal(d1, ref)
+    s2 = buf[100:100 + 1260].view(4, 9, 7, 5)     # elements [100, 1360)
+    with pytest.raises(T.TriotError, match="ALIASING"):   # dst [1000, 9192) overlaps it
+        T.embed(buf[1000:1000 + 8192].view(8, 16, 8, 8), s2)
+    # binary: out-of-place (cached), then exact in place on the same shapes (allowed)
+    rng = np.random.default_rng(4)
+    a = rng.random((7, 9, 16)); b = rng.random((7, 9, 16))
+    refc = O.apply_binary(a, b, "mul")
+    ta, tb = _dev(a), _dev(b)
+    for _ in range(2):
+        c = T.apply_binary(ta, tb, "mul")
+        assert_bits_equal(c, refc)
+    T.apply_binary(ta, tb, "mul", out=ta)     # c == a: in place
+    assert_bits_equal(ta, refc)
+    with pytest.raises(T.TriotError, match="ALIASING"):   # partial overlap: refused
+        big = torch.zeros(2 * 7 * 9 * 16, dtype=torch.float64, device=DEV)
+        T.apply_binary(big[:1008].view(7, 9, 16), tb, "mul", out=big[8:1016].view(7, 9, 16))
