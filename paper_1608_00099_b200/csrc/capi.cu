@@ -60,6 +60,7 @@ TableFn table_for(const Geom& g) {
 }
 
 int vindex(const Geom& g) {
+  if (g.evrows) return 5;
   if (g.dshift) return 7;
   if (g.rows) return g.rwarp ? 6 : 5;
   if (g.flat) return 3;
@@ -75,11 +76,13 @@ int g_sms[64] = {0};
 struct OccKey {
   int dev;
   const void* fn;
-  bool operator==(const OccKey& o) const { return dev == o.dev && fn == o.fn; }
+  size_t smem = 0;  // dynamic shared memory per block the occupancy was computed for
+  bool operator==(const OccKey& o) const { return dev == o.dev && fn == o.fn && smem == o.smem; }
 };
 struct OccHash {
   size_t operator()(const OccKey& k) const {
-    return std::hash<const void*>()(k.fn) ^ ((size_t)k.dev * 0x9e3779b97f4a7c15ull);
+    return std::hash<const void*>()(k.fn) ^ ((size_t)k.dev * 0x9e3779b97f4a7c15ull) ^
+           (k.smem * 0xbf58476d1ce4e5b9ull);
   }
 };
 std::unordered_map<OccKey, int, OccHash> g_occ;
@@ -284,7 +287,74 @@ int launch_ev_tma(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes, b
   return g.idx64 ? go(uint64_t(0)) : go(uint32_t(0));
 }
 
+// Dense EV with a short odd innermost extent (plan_ev_rows): tiles of whole rows staged in
+// shared memory by bulk copies, one wave of blocks at occupancy, contiguous tiles per block.
+int launch_ev_rows(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
+  const void* fn = table_for(g)(g.D, 5, g.idx64 ? 1 : 0);
+  if (!fn) return set_error(TRIOT_ERR_CUDA, "internal: no EV row-tile instance for D=%d", g.D);
+  const uint64_t rb = (uint64_t)g.rowlen * (uint64_t)g.esz;
+  uint64_t rpt = TRIOT_EVROWS_STAGE / ((uint64_t)TRIOT_BLOCK * rb);  // ~16 KB stages
+  if (rpt < 1) rpt = 1;
+  if (rpt > 8) rpt = 8;
+  const uint64_t stage = ((uint64_t)TRIOT_BLOCK * rpt * rb + 127) & ~127ull;
+  const size_t smem = (size_t)(kEvRowsStages * stage + 8 * kEvRowsStages);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int sms, occ = 1;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (int st = sms_locked(dev, &sms)) return st;
+    // the attribute is the largest stage set any row length can ask for (n <= 31, f64: one
+    // row per thread, 3 x 63.5 KB), set once per device; the occupancy per stage size
+    if (g_occ.find(OccKey{dev, fn, 1}) == g_occ.end()) {
+      const int maxsmem = kEvRowsStages * TRIOT_BLOCK * 31 * 8 + 8 * kEvRowsStages + 128;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+      g_occ.emplace(OccKey{dev, fn, 1}, 1);
+    }
+    auto it = g_occ.find(OccKey{dev, fn, smem});
+    if (it == g_occ.end()) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TRIOT_BLOCK, smem);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      if (occ < 1) occ = 1;
+      it = g_occ.emplace(OccKey{dev, fn, smem}, occ).first;
+    }
+    occ = it->second;
+  }
+  const uint64_t tr = (uint64_t)TRIOT_BLOCK * rpt;
+  const uint64_t ntiles = (g.nvec + tr - 1) / tr;
+  uint64_t blocks = (uint64_t)sms * (uint64_t)(g_override.bpsm > 0 ? g_override.bpsm : occ);
+  if (blocks > TRIOT_EV_MAX_GRID) blocks = TRIOT_EV_MAX_GRID;
+  if (blocks > ntiles) blocks = ntiles;
+  if (blocks < 1) blocks = 1;
+  const uint64_t per = (ntiles + blocks - 1) / blocks;
+  const uint64_t grid = (ntiles + per - 1) / per;
+  g.mode = 0;
+  g.dv = TRIOT_BLOCK;  // a thread's rows advance by one block's worth
+  set_step(g);
+  g.wmul = tr;
+  g.wspan = per;
+  g.rwin = (uint32_t)rpt;
+  g.rmag = (uint32_t)stage;
+  const size_t need = reduce_ws_bytes(grid, g.D + 2);
+  if (!ws || ws_bytes < need)
+    return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes, need);
+  auto go = [&](auto tag) -> int {
+    using IDX = decltype(tag);
+    Desc<IDX> d;
+    memset(&d, 0, sizeof(d));
+    fill_desc<IDX>(g, d);
+    d.out = out;
+    d.ws = ws;
+    void* args[1] = {&d};
+    return launch_pdl(fn, (unsigned)grid, TRIOT_BLOCK, smem, (cudaStream_t)stream, args);
+  };
+  return g.idx64 ? go(uint64_t(0)) : go(uint32_t(0));
+}
+
 int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
+  if (g.op == OP_EV && g.evrows) return launch_ev_rows(g, stream, out, ws, ws_bytes);
   if (g.op == OP_EV) {
     bool used = false;
     int st = launch_ev_tma(g, stream, out, ws, ws_bytes, &used);

@@ -99,13 +99,20 @@ const void* kptr_flat() {
 }
 
 // row-window instances (short odd innermost extents): embed, binary; K = 32 bytes of loads per
-// lane per batch (measured on B200: f32 K 8 > 4, f64 K 4 > 8)
+// lane per batch (measured on B200: f32 K 8 > 4, f64 K 4 > 8); the dense expected value's
+// shared-memory row tiles (D = the outer axes, at most 15)
 template <int D, typename IDX>
 const void* kptr_rows() {
 #if TRIOT_INST_OP == 0
   return (const void*)&embed_rows_kernel<D, ESZ, IDX, 32 / ESZ>;
 #elif TRIOT_INST_OP == 1
   return (const void*)&binary_rows_kernel<D, ESZ, IDX, 32 / ESZ, TRIOT_INST_BOP>;
+#elif TRIOT_INST_OP == 2 && TRIOT_INST_BOP == 0
+  if constexpr (D >= TRIOT_MAXD) {
+    return nullptr;
+  } else {
+    return (const void*)&ev_rows_kernel<D, ESZ, IDX>;
+  }
 #else
   return nullptr;
 #endif

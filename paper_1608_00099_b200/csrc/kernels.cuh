@@ -1391,12 +1391,20 @@ __device__ __forceinline__ double warp_reduce_scatter(const double (&acc)[NS], i
   return a[0];
 }
 
+// 32-byte chunks per thread in flight in the final ordered sum, and the poll's sleep (ns)
+#ifndef TRIOT_EV_FINAL_CHUNKS
+#define TRIOT_EV_FINAL_CHUNKS 4
+#endif
+#ifndef TRIOT_EV_POLL_SLEEP
+#define TRIOT_EV_POLL_SLEEP 64
+#endif
+
 // Ordered sum of `nparts` partials laid out [part][P slots] (P = ev_slot_pad(NS)), read as
 // 32-byte chunks, 4 chunks per thread in flight: chunk c holds the doubles 4c .. 4c+3, i.e. slots
 // (4c + q) % P, and since BLOCK * 4 is a multiple of P thread t always meets slots (4t + q) % P.
 // Lanes that meet the same slots are combined by a butterfly, warps in index order: a fixed
 // function of the partials, whichever block runs it.  Leaves the NS totals in sm[0][0..NS-1].
-template <int NS, int BLOCK>
+template <int NS, int BLOCK, int CH = TRIOT_EV_FINAL_CHUNKS>
 __device__ __forceinline__ void ordered_slot_sum(const double* src, unsigned nparts,
                                                  double (&sm)[BLOCK / 32][NS]) {
   constexpr int P = ev_slot_pad(NS);
@@ -1405,10 +1413,10 @@ __device__ __forceinline__ void ordered_slot_sum(const double* src, unsigned npa
   const unsigned total = nparts * (unsigned)P;
   const unsigned nchunk = (total + 3u) / 4u;
   double f[4] = {0.0, 0.0, 0.0, 0.0};
-  for (unsigned c0 = threadIdx.x; c0 < nchunk; c0 += 4u * BLOCK) {
-    uint32_t w[4][8];
+  for (unsigned c0 = threadIdx.x; c0 < nchunk; c0 += (unsigned)CH * BLOCK) {
+    uint32_t w[CH][8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < CH; ++i) {
       const unsigned c = c0 + (unsigned)i * BLOCK;
       if (c < nchunk && 4u * c + 3u < total) {
         asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -1425,7 +1433,7 @@ __device__ __forceinline__ void ordered_slot_sum(const double* src, unsigned npa
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < CH; ++i)
 #pragma unroll
       for (int q = 0; q < 4; ++q) f[q] += __hiloint2double((int)w[i][2 * q + 1], (int)w[i][2 * q]);
   }
@@ -1506,7 +1514,9 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
     unsigned c;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
     while (c < target) {
-      __nanosleep(64);
+#if TRIOT_EV_POLL_SLEEP
+      __nanosleep(TRIOT_EV_POLL_SLEEP);
+#endif
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
     }
     // synchronizes with every arrival's release (they form a release sequence on the counter)
@@ -1747,6 +1757,99 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// ---- expected value, dense p with a short odd innermost extent n: rows through shared memory
+// A vector is one row of n contiguous elements (plan.cpp plan_ev_rows); the digits are the outer
+// axes.  Block b owns the contiguous tiles [b * wspan, (b+1) * wspan) of TR = kBlock * RPT rows;
+// thread 0 keeps NST - 1 tiles in flight with 1-D bulk copies (cp.async.bulk, one mbarrier per
+// stage completing on the transferred bytes) while all threads sum the current tile's rows from
+// shared memory: thread t takes rows t, t + kBlock, ... -- one arithmetic progression of rows
+// per thread across the block's tiles, so the digits advance by a fixed +kBlock rows step
+// (digits_step_ev: the telescoped weights of ev_kernel, P:129's amortised carries).  Per row:
+// mass s = sum_c x_c and column moment sum_c c x_c by suffix sums (T += x_c; m += T for c
+// from n-1 down to 1), no per-element weight or odometer -- ~4 instructions per element
+// against the flat kernel's ~10.  Bytes = p + d doubles.
+#ifndef TRIOT_EVROWS_MINB
+#define TRIOT_EVROWS_MINB 2
+#endif
+#ifndef TRIOT_EVROWS_STAGE
+#define TRIOT_EVROWS_STAGE 16384
+#endif
+constexpr int kEvRowsStages = 3;
+template <int D, int ESZ, typename IDX>
+__global__ void __launch_bounds__(kBlock, TRIOT_EVROWS_MINB)
+    ev_rows_kernel(const __grid_constant__ Desc<IDX> d) {
+  constexpr int NS = D + 2;  // D outer digits, the column moment, the mass
+  constexpr int NST = kEvRowsStages;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t n = d.rowlen;
+  const uint32_t RPT = d.rwin;       // rows per thread per tile
+  const uint32_t stage = d.rmag;     // bytes per stage (multiple of 16)
+  const IDX TR = (IDX)kBlock * (IDX)RPT;
+  uint64_t* full = (uint64_t*)(smem + (size_t)NST * stage);
+  const int tid = threadIdx.x;
+  const IDX ntiles = (d.nvec + TR - 1) / TR;
+  const IDX t0 = (IDX)blockIdx.x * d.wspan;
+  IDX t1 = t0 + d.wspan;
+  if (t1 > ntiles || t1 < t0) t1 = ntiles;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_trigger();
+  pdl_wait();
+  __syncthreads();
+  const char* pbase = (const char*)d.t[0].ptr;
+  const uint64_t row_bytes = (uint64_t)n * ESZ;
+  auto issue = [&](IDX tile, int s) {
+    const IDX r0 = tile * TR;
+    const IDX nr = (d.nvec - r0) < TR ? (d.nvec - r0) : TR;
+    // round the last tile up to 16 bytes: the extra bytes lie in the same 16-byte granule as
+    // p's last element (p is 16-byte aligned), are never summed, and cannot cross a page
+    const uint32_t bytes = (uint32_t)(((uint64_t)nr * row_bytes + 15u) & ~15ull);
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(smem + (size_t)s * stage, pbase + (uint64_t)r0 * row_bytes, bytes, &full[s]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < NST - 1; ++s)
+      if (t0 + (IDX)s < t1) issue(t0 + (IDX)s, s);
+  IDX u[D];
+  decode_digits<D, IDX>(d, t0 * TR + (IDX)tid, u);
+  EvAcc<D> a;
+  ev_acc_init<D, IDX>(a);
+  for (IDX i = t0; i < t1; ++i) {
+    const int s = (int)((i - t0) % NST);
+    const uint32_t par = (uint32_t)(((i - t0) / NST) & 1);
+    if (tid == 0 && i + (IDX)(NST - 1) < t1)  // its stage was released at the last barrier
+      issue(i + (IDX)(NST - 1), (int)((i - t0 + NST - 1) % NST));
+    mbar_wait(&full[s], par);
+    const unsigned char* st = smem + (size_t)s * stage;
+    for (uint32_t r = 0; r < RPT; ++r) {
+      const IDX row = i * TR + (IDX)(r * kBlock + tid);
+      if (row < d.nvec) {
+        const unsigned char* rp = st + (size_t)(r * kBlock + tid) * row_bytes;
+        double T = 0.0, m = 0.0;
+#pragma unroll 4
+        for (int c = (int)n - 1; c >= 1; --c) {
+          T += (double)Elem<ESZ>::get((const uint32_t*)(rp + (size_t)c * ESZ));
+          m += T;
+        }
+        T += (double)Elem<ESZ>::get((const uint32_t*)rp);
+        a.S += T;
+        a.Wc += m;
+      }
+      digits_step_ev<D, IDX>(d, u, a);
+    }
+    __syncthreads();  // every thread is done with stage s before thread 0 refills it
+  }
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < D; ++k) acc[k] = fma((double)u[k], a.S, a.ev[k]);
+  acc[D] = a.Wc;
+  acc[D + 1] = a.S;
+  ev_reduce<NS, kBlock, IDX>(d, acc);
 }
 
 // ------------------------------------------------------------------ NEXT-2: inner product

@@ -162,6 +162,53 @@ static void plan_flat(Geom& g, const Axis* ax, int na, int nt, bool bounds, cons
   g.slot_of_axis[g.d] = na + 1;  // the mass
 }
 
+// Dense expected value with a short odd innermost extent n (no vector width divides it): a
+// vector is one row of n contiguous elements, the digits are the outer axes (D = na - 1), and
+// ev_rows_kernel stages tiles of whole rows in shared memory with bulk copies -- each thread
+// sums its rows from shared memory (mass + column moment by suffix sums, ~4 instructions per
+// element instead of the flat kernel's per-element odometer).  Needs a 16-byte aligned p (the
+// bulk copies) and 3 <= n <= kEvRowsMax.
+static const uint64_t kEvRowsMax = 31;
+static void plan_ev_rows(Geom& g, const Axis* ax, int na, const uint64_t* n0) {
+  const uint64_t n = ax[na - 1].n;
+  g.evrows = true;
+  g.flat = g.rows = false;
+  g.V = 1;
+  g.R = 1;
+  g.collapsed = false;
+  g.lgL = 0;
+  g.D = na - 1;
+  for (int k = 0; k < na - 1; ++k) {
+    g.ext[k] = ax[k].n;
+    g.bnd[k] = ax[k].n;
+    g.t[0].sig[k] = ax[k].sig[0];
+  }
+  g.rowlen = (uint32_t)n;
+  g.Dc = na;
+  for (int k = 0; k < na; ++k) {
+    g.cn[k] = ax[k].n;
+    g.corig[k] = ax[k].orig;
+    g.cmerged[k] = ax[k].merged;
+  }
+  g.t[0].vec = false;
+  g.t[0].rho = 0;
+  g.t[0].tau = ax[na - 1].sig[0];
+  g.rowmul = g.colmul = 0;
+  g.srows = g.scols = 0;
+  g.vfull = g.vany = 0;
+  g.N = 1;
+  for (int k = 0; k < na; ++k) g.N *= ax[k].n;
+  g.nvec = g.N / n;  // rows
+  g.nsteps = (g.nvec + 31) / 32;
+  finish_geometry(g, 1);
+  for (int j = 0; j <= TRIOT_MAXD; ++j) g.slot_of_axis[j] = -1;
+  for (int k = 0; k < na - 1; ++k) g.slot_of_axis[ax[k].orig] = k;  // outer axes
+  g.slot_of_axis[ax[na - 1].orig] = na - 1;                          // the column moment
+  g.nslots = na;
+  g.slot_of_axis[g.d] = na;                                          // the mass (slot D + 1)
+  (void)n0;
+}
+
 // Row windows: the longest innermost extent taken by row windows, per op (measured on B200,
 // embed rows of 33 stream faster as flat vectors, whose only gather is src;
 // binary rows up to 63 stream 1.7x faster as row windows, flat vectors gather both operands).
@@ -431,6 +478,11 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
       g.segm = bounds ? ax[na - 1].bnd : nl;
       return;
     }
+  }
+  if (cc[best].V == 1 && vmax > 1 && g.op == OP_EV && !g.view && g_rows_on && na >= 2 &&
+      nl >= 3 && nl <= kEvRowsMax && ((uintptr_t)g.t[0].ptr % 16) == 0) {
+    plan_ev_rows(g, ax, na, n);
+    return;
   }
   if (cc[best].V == 1 && vmax > 1 && g.flat_ok) {
     plan_flat(g, ax, na, nt, bounds, n);
@@ -1200,7 +1252,8 @@ std::string describe(const Geom& g) {
            "\"nsteps\":%llu,\"mode\":%d,\"wmul\":%llu,\"wspan\":%llu,\"dv\":%llu,\"khi\":%d,\"klo\":%d,\"rowmul\":%llu,\"colmul\":%llu,\"vfull\":%llu,"
            "\"vany\":%llu,\"srows\":%llu,\"scols\":%llu,\"nslots\":%d,\"zmask\":%u,"
            "\"rows\":%s,\"rowlen\":%llu,\"rmag\":%llu,\"rwin\":%llu,\"pow2\":%s,\"lin0\":%llu,"
-           "\"seglen\":%llu,\"segm\":%llu,\"rwarp\":%s,\"dshift\":%u,\"evpad\":%s,",
+           "\"seglen\":%llu,\"segm\":%llu,\"rwarp\":%s,\"dshift\":%u,\"evpad\":%s,"
+           "\"evrows\":%s,",
            g.op, g.esz, g.d, g.empty ? "true" : "false", g.idx64 ? "true" : "false",
            g.all_oob ? "true" : "false", g.Dc, g.D, g.V, g.R, g.lgL,
            g.collapsed ? "true" : "false", g.flat ? "true" : "false", (unsigned long long)g.N, (unsigned long long)g.nvec,
@@ -1211,7 +1264,7 @@ std::string describe(const Geom& g) {
            g.rows ? "true" : "false", (unsigned long long)g.rowlen, (unsigned long long)g.rmag,
            (unsigned long long)g.rwin, g.pow2 ? "true" : "false", (unsigned long long)g.lin0,
            (unsigned long long)g.seglen, (unsigned long long)g.segm, g.rwarp ? "true" : "false",
-           g.dshift, g.evpad ? "true" : "false");
+           g.dshift, g.evpad ? "true" : "false", g.evrows ? "true" : "false");
   s += b;
   arr(s, "cn", g.cn, g.Dc);
   arri(s, "corig", g.corig, g.Dc);

@@ -37,6 +37,8 @@ struct Geom {
   bool flat = false;   // flat vectors: V consecutive counter elements across rows (odd extents)
   bool flat_ok = false;  // the op has flat-vector kernels (embed, binary, expected value)
   bool rows = false;     // row windows: a vector is one counter row (short odd innermost)
+  bool evrows = false;   // dense EV with a short odd innermost extent: rows staged in shared
+                         // memory by bulk copies (ev_rows_kernel); digits = the outer axes
   bool rows_ok = false;  // the op has row-window kernels (embed, binary)
   uint64_t rowlen = 0, rmag = 0, rwin = 1;
   uint64_t seglen = 0, segm = 0;   // rows are segments of a split axis; segm = its embed bound

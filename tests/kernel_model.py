@@ -19,9 +19,33 @@ def _wrap(x, idx64):
     return x if idx64 else (x & M32)
 
 
+def run_ev_rows(desc: dict, p):
+    """The dense EV's shared-memory row tiles (ev_rows_kernel): rows of rowlen elements, the
+    outer digits of row index r (decoded over `ext`) weight the row's mass, the column moment
+    goes to slot D, the mass to slot D + 1 -- checks the plan's digits and slot mapping."""
+    D, ext, n = desc["D"], desc["ext"], desc["rowlen"]
+    slots = [0.0] * (D + 2)
+    for r in range(desc["nvec"]):
+        row = p[r * n:(r + 1) * n]
+        u, v = [0] * D, r
+        for k in range(D - 1, 0, -1):
+            u[k] = v % ext[k]
+            v //= ext[k]
+        u[0] = v
+        mass = float(np.sum(row, dtype=np.float64))
+        for k in range(D):
+            slots[k] += u[k] * mass
+        slots[D] += float(sum(c * float(row[c]) for c in range(n)))
+        slots[D + 1] += mass
+    d = desc["d"]
+    return [slots[sl] if sl >= 0 else 0.0 for sl in desc["slot_of_axis"][:d]]
+
+
 def run(desc: dict, op: str, bufs: list, binop: str = "mul"):
     """bufs: flat numpy arrays in tensor order (embed: dst, src; binary: c, a, b; ev: p).
     Writes outputs in place; for 'ev' returns the weight-slot totals (list of floats)."""
+    if op == "ev" and desc.get("evrows"):
+        return run_ev_rows(desc, bufs[0])
     D, V, idx64 = desc["D"], desc["V"], desc["idx64"]
     ext, dlt, bnd = desc["ext"], desc["dlt"], desc["bnd"]
     khi, klo, lgL = desc["khi"], desc["klo"], desc["lgL"]

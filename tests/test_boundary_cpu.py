@@ -504,7 +504,14 @@ def test_row_window_geometry():
     p = T.triot_plan_describe(1, [None, (9, 63), (9, 66)], (9, 63), 2, F32, 2)
     assert p["rows"] and [t["vec"] for t in p["t"]] == [True, True, False]
     p = T.triot_plan_describe(2, [(7,) * 5], None, 5, F64, 0)
-    assert p["flat"] and not p["rows"]                    # the expected value keeps flat vectors
+    # the dense expected value of short odd rows: shared-memory row tiles over the outer digits
+    assert p["evrows"] and not p["flat"] and not p["rows"] and p["D"] == 4 and p["rowlen"] == 7
+    assert p["nvec"] == 7 ** 4 and p["slot_of_axis"] == [0, 1, 2, 3, 4, 5]
+    # ... unless p is not 16-byte aligned (the bulk copies) or the row is too long: flat vectors
+    p = T.triot_plan_describe(2, [(7,) * 5], None, 5, F64, 0, [8, 0, 0])
+    assert p["flat"] and not p["evrows"]
+    p = T.triot_plan_describe(2, [(40, 33)], None, 2, F32, 0)
+    assert p["flat"] and not p["evrows"]
 
 
 def test_row_window_division_magic_exact():
@@ -676,5 +683,5 @@ def test_planner_never_selects_uncompiled_instances(seed):
         for pl in plans:
             if pl["empty"]:
                 continue
-            assert pl["V"] > 1 or pl["flat"] or pl["rows"], pl
+            assert pl["V"] > 1 or pl["flat"] or pl["rows"] or pl["evrows"], pl
             assert not (pl["zmask"] and pl["D"] < 2), pl

@@ -148,6 +148,15 @@ if "--views" in sys.argv:   # NEXT-1 views: windows at aligned and odd offsets (
     view_embed("views: embed f32 window (383)^3 of (400)^3 at (1,1,1) into (512)^3 at (5,5,5)",
                (512,) * 3, (5,) * 3, (400,) * 3, (1,) * 3, (383,) * 3)
     sys.exit(0)
+if "--evodd" in sys.argv:   # dense EV with odd innermost extents (row tiles vs --policy 5,0 flat)
+    ev_case("evodd: EV f64 (7,)*9", (7,) * 9)
+    ev_case("evodd: EV f32 (3000,3000,7)", (3000, 3000, 7), dtype=torch.float32)
+    ev_case("evodd: EV f64 (3000,3000,7)", (3000, 3000, 7))
+    ev_case("evodd: EV f32 (2000,2000,15)", (2000, 2000, 15), dtype=torch.float32)
+    ev_case("evodd: EV f64 (1000,1000,31)", (1000, 1000, 31))
+    ev_case("evodd: EV f32 (4000,4000,3)", (4000, 4000, 3), dtype=torch.float32)
+    ev_case("evodd: EV f64 (5,)*11", (5,) * 11)
+    sys.exit(0)
 if "--big" in sys.argv:   # odd innermost extents at sizes past the launch-bound regime
     embed_case("big: embed f32 (3000,3000,7) <- (2900,2900,5)", (3000, 3000, 7), (2900, 2900, 5))
     embed_case("big: embed f32 (8192,4096,3) <- (8000,4000,3)", (8192, 4096, 3), (8000, 4000, 3))
