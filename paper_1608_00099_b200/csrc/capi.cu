@@ -353,6 +353,147 @@ int launch_ev_rows(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) 
   return g.idx64 ? go(uint64_t(0)) : go(uint32_t(0));
 }
 
+// ---- EV of a view window with rows of 32..256 elements: TMA tensor tiles (ev_view_tma_kernel)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  return fn;
+}
+
+// Returns TRIOT_OK with *used = false when the view does not qualify (the regular view kernel
+// then runs): rank of the window's non-unit axes 2..5, its innermost axis the base's innermost
+// with 32..256 elements, a 16-byte aligned base whose row pitch and outer strides are multiples
+// of 16 bytes.
+int launch_ev_view_tma(const Geom& g, const triot_view* v, int d, int dtype, bool with_mass,
+                       void* out, void* ws, size_t ws_bytes, void* stream, bool* used) {
+  *used = false;
+  if (g_override.mode >= 0 || !rows_enabled()) return TRIOT_OK;  // tuning runs keep the old path
+  const int esz = dtype == TRIOT_F32 ? 4 : 8;
+  int ax[TRIOT_MAXD], m = 0;
+  for (int k = 0; k < d; ++k)
+    if (v->shape[k] > 1) ax[m++] = k;
+  if (m < 2 || m > 5 || ax[m - 1] != d - 1) return TRIOT_OK;
+  const uint64_t n = (uint64_t)v->shape[d - 1];
+  if (n < 32 || n > 256) return TRIOT_OK;
+  if (((uintptr_t)v->data) % 16) return TRIOT_OK;
+  uint64_t bstride[TRIOT_MAXD];  // base strides in bytes
+  uint64_t acc = (uint64_t)esz;
+  for (int k = d - 1; k >= 0; --k) {
+    bstride[k] = acc;
+    acc *= (uint64_t)v->base_shape[k];
+  }
+  for (int j = 0; j < m - 1; ++j)
+    if (bstride[ax[j]] % 16 || bstride[ax[j]] >= (1ull << 40)) return TRIOT_OK;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return TRIOT_OK;
+  // the unit axes of the window fold into the map's base address (multiples of 16 bytes)
+  uint64_t bias = 0;
+  for (int k = 0; k < d; ++k)
+    if (v->shape[k] == 1 && v->start) bias += (uint64_t)v->start[k] * bstride[k];
+  // the box starts on a 16-byte boundary at or before the window's first column
+  const uint64_t s_in = v->start ? (uint64_t)v->start[d - 1] : 0;
+  const uint32_t cshift = (uint32_t)((s_in * esz % 16) / esz);
+  const uint32_t nbox = (uint32_t)(((n + cshift) * esz + 15) / 16 * 16 / esz);
+  if (nbox > 256) return TRIOT_OK;
+  const int D = m - 1;
+  EvTmaGeo G;
+  memset(&G, 0, sizeof(G));
+  G.m = (uint32_t)m;
+  G.n = (uint32_t)n;
+  G.nbox = nbox;
+  G.cshift = cshift;
+  cuuint64_t gdim[5], gstr[4];
+  cuuint32_t box[5], estr[5];
+  for (int j = 0; j < m; ++j) {  // TMA dim j = window axis ax[m-1-j]
+    const int k = ax[m - 1 - j];
+    gdim[j] = (cuuint64_t)v->base_shape[k];
+    if (j) gstr[j - 1] = (cuuint64_t)bstride[k];
+    G.coord0[j] = (int32_t)(v->start ? v->start[k] : 0) - (j == 0 ? (int32_t)cshift : 0);
+    box[j] = 1;
+    estr[j] = 1;
+  }
+  for (int j = 0; j < D; ++j) G.ext[j] = (uint64_t)v->shape[ax[j]];
+  uint64_t R = 16384 / ((uint64_t)nbox * esz);
+  if (R < 1) R = 1;
+  if (R > 256) R = 256;
+  if (R > G.ext[D - 1]) R = G.ext[D - 1];
+  box[0] = nbox;
+  box[1] = (cuuint32_t)R;
+  G.R = (uint32_t)R;
+  G.stage = (uint32_t)(((uint64_t)nbox * R * esz + 127) & ~127ull);
+  G.tpa = (G.ext[D - 1] + R - 1) / R;
+  G.ntiles = G.tpa;
+  for (int j = 0; j < D - 1; ++j) G.ntiles *= G.ext[j];
+  if (G.ntiles >= (1ull << 32) || G.ext[D - 1] >= (1ull << 31)) return TRIOT_OK;  // 32-bit tiles
+  CUtensorMap map;
+  CUresult cr = enc(&map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                    (cuuint32_t)m, (char*)v->data + bias, gdim, gstr, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return TRIOT_OK;  // not encodable: the regular kernel
+  const void* fns4[4] = {(const void*)&ev_view_tma_kernel<1, 4>, (const void*)&ev_view_tma_kernel<2, 4>,
+                         (const void*)&ev_view_tma_kernel<3, 4>, (const void*)&ev_view_tma_kernel<4, 4>};
+  const void* fns8[4] = {(const void*)&ev_view_tma_kernel<1, 8>, (const void*)&ev_view_tma_kernel<2, 8>,
+                         (const void*)&ev_view_tma_kernel<3, 8>, (const void*)&ev_view_tma_kernel<4, 8>};
+  const void* fn = (esz == 4 ? fns4 : fns8)[D - 1];
+  const size_t smem = (size_t)kEvRowsStages * G.stage + 8 * kEvRowsStages;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int sms, occ = 1;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (int st = sms_locked(dev, &sms)) return st;
+    if (g_occ.find(OccKey{dev, fn, 1}) == g_occ.end()) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kEvRowsStages * 20480 + 8 * kEvRowsStages);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+      g_occ.emplace(OccKey{dev, fn, 1}, 1);
+    }
+    auto it = g_occ.find(OccKey{dev, fn, smem});
+    if (it == g_occ.end()) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TRIOT_BLOCK, smem);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      if (occ < 1) occ = 1;
+      it = g_occ.emplace(OccKey{dev, fn, smem}, occ).first;
+    }
+    occ = it->second;
+  }
+  uint64_t blocks = (uint64_t)sms * (uint64_t)occ;
+  if (blocks > TRIOT_EV_MAX_GRID) blocks = TRIOT_EV_MAX_GRID;
+  if (blocks > G.ntiles) blocks = G.ntiles;
+  if (blocks < 1) blocks = 1;
+  G.per = (G.ntiles + blocks - 1) / blocks;
+  const uint64_t grid = (G.ntiles + G.per - 1) / G.per;
+  const size_t need = reduce_ws_bytes(grid, D + 2);
+  if (!ws || ws_bytes < need)
+    return set_error(TRIOT_ERR_WORKSPACE, "Workspace: %zu bytes given, %zu needed", ws_bytes, need);
+  Desc<uint32_t> desc;
+  memset(&desc, 0, sizeof(desc));
+  desc.out = out;
+  desc.ws = ws;
+  desc.d_out = d + (with_mass ? 1 : 0);
+  for (int k = 0; k <= TRIOT_MAXD; ++k) desc.slot_of_axis[k] = -1;
+  for (int j = 0; j < m; ++j) desc.slot_of_axis[ax[j]] = j;  // outer digits j < D; inner D
+  desc.slot_of_axis[d] = D + 1;                              // the mass
+  void* args[3] = {&desc, &map, &G};
+  *used = true;
+  (void)g;
+  return launch_pdl(fn, (unsigned)grid, TRIOT_BLOCK, smem, (cudaStream_t)stream, args);
+}
+
 int launch(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) {
   if (g.op == OP_EV && g.evrows) return launch_ev_rows(g, stream, out, ws, ws_bytes);
   if (g.op == OP_EV) {
@@ -743,6 +884,15 @@ static int expected_value_impl(double* means, const void* p, const int64_t* shap
     }
     if (g.t[0].numel && m0 < p1 && p0 < m1)
       return set_error(TRIOT_ERR_ALIASING, "Aliasing: means overlaps p");
+  }
+  if (pv && !g.empty && !offset) {  // long view rows: TMA tensor tiles
+    bool used = false;
+    st = launch_ev_view_tma(g, pv, d, dtype, with_mass, means, workspace, workspace_bytes,
+                            cuda_stream, &used);
+    if (st || used) {
+      if (!st) clear_error();
+      return st;
+    }
   }
   if (g.empty) {  // empty sums: 0 (the offsets multiply a zero mass)
     cudaError_t e =

@@ -28,6 +28,7 @@
 //   dot_kernel / update_kernel            Benchmarks 2 and 3
 //   conv_kernel / conv_lane_kernel        Benchmark 4, Alg 15 naive convolution
 #pragma once
+#include <cuda.h>  // CUtensorMap (the struct only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -1850,6 +1851,183 @@ __global__ void __launch_bounds__(kBlock, TRIOT_EVROWS_MINB)
   acc[D] = a.Wc;
   acc[D + 1] = a.S;
   ev_reduce<NS, kBlock, IDX>(d, acc);
+}
+
+// ---- expected value of a view window with long rows (n in 32..256): TMA tensor tiles
+// A window of a base tensor has contiguous rows at the base's strides; a TMA tensor map over the
+// base (rank m = the window's axes of extent > 1, at most 5) moves boxes of R rows x nbox
+// columns (nbox = n rounded up to 16 bytes; columns past the base are zero-filled by the TMA,
+// columns past the window masked) into a 3-stage shared-memory ring, thread 0 issuing
+// `cp.async.bulk.tensor` for tile i + 2 while the block consumes tile i.  Thread t owns column
+// t of every row: per element one shared load and one fp64 add into its running column mass S;
+// the outer digits' weights are telescoped over its row sequence (+1 row inside a tile, a jump
+// between tiles: one FMA per change, P:129's argument) and the column weight t multiplies S
+// once at the end -- no per-element weight, odometer or offset arithmetic.
+struct EvTmaGeo {
+  uint64_t ext[4];    // window extents of the outer axes (digits 0..D-1; digit D-1 = the row axis)
+  int32_t coord0[5];  // base coordinate of the window start per TMA dim (dim 0 = innermost)
+  uint32_t m;         // TMA rank (D + 1)
+  uint32_t n, nbox, R, stage;
+  uint32_t cshift;    // columns the box starts before the window (16-byte aligned box start)
+  uint64_t tpa;       // tiles along the row axis: ceil(ext[D-1] / R)
+  uint64_t ntiles, per;
+};
+
+__device__ __forceinline__ void tma_load_tile(void* dst, const void* map, int m, const int32_t* c,
+                                              uint64_t* bar) {
+  const uint32_t sd = smem_u32(dst), sb = smem_u32(bar);
+  const uint64_t mp = (uint64_t)map;
+  switch (m) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(sd), "l"(mp), "r"(c[0]), "r"(c[1]), "r"(sb)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sd), "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+          "r"(sb)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sd), "l"(mp), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(sb)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(sd), "l"(mp), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sb)
+          : "memory");
+      break;
+  }
+}
+
+template <int D, int ESZ>
+__global__ void __launch_bounds__(kBlock, 4)
+    ev_view_tma_kernel(const __grid_constant__ Desc<uint32_t> d,
+                       const __grid_constant__ CUtensorMap map, const __grid_constant__ EvTmaGeo G) {
+  constexpr int NS = D + 2;  // the outer digits, the column moment, the mass
+  constexpr int NST = kEvRowsStages;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)(smem + (size_t)NST * G.stage);
+  const int tid = threadIdx.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * G.per;
+  uint64_t t1 = t0 + G.per;
+  if (t1 > G.ntiles) t1 = G.ntiles;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map) : "memory");
+  }
+  pdl_trigger();
+  pdl_wait();
+  __syncthreads();
+  // tile position as an odometer: a = tile index along the row axis, pre[] = the digits of the
+  // axes above it (32-bit: ntiles < 2^32 is checked on the host); one division per thread at
+  // the start, then +1 tile steps -- 64-bit divisions per tile cost more than the tile's work
+  struct Pos {
+    uint32_t a;
+    uint32_t pre[D > 1 ? D - 1 : 1];
+  };
+  auto pos_of = [&](uint64_t tile) {
+    Pos q;
+    uint32_t t = (uint32_t)tile;
+    q.a = t % (uint32_t)G.tpa;
+    t /= (uint32_t)G.tpa;
+#pragma unroll
+    for (int k = D - 2; k >= 0; --k) {
+      q.pre[k] = t % (uint32_t)G.ext[k];
+      t /= (uint32_t)G.ext[k];
+    }
+    return q;
+  };
+  auto advance = [&](Pos& q) {
+    if (++q.a == (uint32_t)G.tpa) {
+      q.a = 0;
+#pragma unroll
+      for (int k = D - 2; k >= 0; --k) {
+        if (++q.pre[k] < (uint32_t)G.ext[k]) break;
+        q.pre[k] = 0;
+      }
+    }
+  };
+  auto issue = [&](const Pos& q, int s) {
+    int32_t c[5];
+    c[0] = G.coord0[0];
+    c[1] = G.coord0[1] + (int32_t)(q.a * G.R);
+#pragma unroll
+    for (int j = 2; j <= D; ++j) c[j] = G.coord0[j] + (int32_t)q.pre[D - j];
+    mbar_expect_tx(&full[s], G.nbox * G.R * ESZ);
+    tma_load_tile(smem + (size_t)s * G.stage, &map, (int)G.m, c, &full[s]);
+  };
+  Pos ip;  // thread 0: the next tile to issue
+  if (tid == 0 && t0 < t1) {
+    ip = pos_of(t0);
+    for (int s = 0; s < NST - 1; ++s)
+      if (t0 + (uint64_t)s < t1) {
+        issue(ip, s);
+        advance(ip);
+      }
+  }
+  const bool active = (uint32_t)tid < G.n;
+  Pos cp = pos_of(t0 < t1 ? t0 : 0);  // the tile being consumed
+  uint32_t u[D];
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) u[k] = cp.pre[k];
+  u[D - 1] = cp.a * G.R;
+  double S = 0.0, ev[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ev[k] = 0.0;
+  for (uint64_t i = t0; i < t1; ++i) {
+    const int s = (int)((i - t0) % NST);
+    const uint32_t par = (uint32_t)(((i - t0) / NST) & 1);
+    if (tid == 0 && i + (uint64_t)(NST - 1) < t1) {
+      issue(ip, (int)((i - t0 + NST - 1) % NST));
+      advance(ip);
+    }
+    // jump to the tile's first row: one event per changed digit
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k)
+      if (cp.pre[k] != u[k]) {
+        ev[k] = fma(-((double)cp.pre[k] - (double)u[k]), S, ev[k]);
+        u[k] = cp.pre[k];
+      }
+    {
+      const uint32_t r0 = cp.a * G.R;
+      if (r0 != u[D - 1]) {
+        ev[D - 1] = fma(-((double)r0 - (double)u[D - 1]), S, ev[D - 1]);
+        u[D - 1] = r0;
+      }
+    }
+    const uint32_t left = (uint32_t)G.ext[D - 1] - cp.a * G.R;
+    const uint32_t rows = left < G.R ? left : G.R;
+    mbar_wait(&full[s], par);
+    const unsigned char* st = smem + (size_t)s * G.stage + (size_t)(tid + G.cshift) * ESZ;
+    const uint32_t pitch = G.nbox * ESZ;
+    if (active) {
+      S += (double)Elem<ESZ>::get((const uint32_t*)st);
+      for (uint32_t r = 1; r < rows; ++r) {  // next row: the row digit + 1
+        ev[D - 1] -= S;
+        S += (double)Elem<ESZ>::get((const uint32_t*)(st + r * pitch));
+      }
+    }
+    u[D - 1] += rows - 1;
+    advance(cp);
+    __syncthreads();  // stage s consumed before thread 0 refills it
+  }
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < D; ++k) acc[k] = fma((double)u[k], S, ev[k]);
+  acc[D] = (double)tid * S;  // column weight t times the column's mass
+  acc[D + 1] = S;
+  ev_reduce<NS, kBlock, uint32_t>(d, acc);
 }
 
 // ------------------------------------------------------------------ NEXT-2: inner product

@@ -1252,3 +1252,38 @@ def test_ev_row_tiles_vs_oracle(dtype):
                 assert np.all(np.abs(mis - ref) <= 1e-12 * np.abs(ref))
             m = T.expected_value(_dev(p), with_mass=True).cpu().numpy()
             assert abs(m[-1] - math.fsum(p.astype(np.float64).ravel())) <= 1e-12 * m[-1] + 1e-300
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_ev_view_tma_tiles_vs_oracle(dtype):
+    """EV of view windows with rows of 32..256 elements (TMA tensor tiles, ev_view_tma_kernel):
+    window ranks 2..5 (+ unit axes folded into the map address), odd and even row lengths,
+    windows ending at the base edge (TMA zero fill past it) and inside it (masked columns and
+    rows) -- exact on integer data, 1e-12 on real data, deterministic."""
+    rng = np.random.default_rng(3301 if dtype == np.float32 else 3302)
+    cases = [((264, 264, 264), (5, 5, 5), (255, 255, 255)),
+             ((40, 300), (3, 20), (37, 255)),
+             ((20, 30, 256), (1, 2, 0), (19, 27, 256)),
+             ((6, 7, 8, 64), (1, 0, 2, 32), (5, 7, 6, 32)),
+             ((3, 4, 5, 6, 100), (1, 1, 1, 1, 4), (2, 3, 4, 5, 96)),
+             ((4, 9, 1, 96), (2, 0, 0, 8), (1, 9, 1, 88)),       # unit axes in the window
+             ((50, 64), (7, 0), (43, 64))]
+    for base_shape, start, shape in cases:
+        esz = np.dtype(dtype).itemsize
+        if (base_shape[-1] * esz) % 16:
+            continue
+        for kind in ("int", "real"):
+            base = (rng.integers(0, 256, size=base_shape).astype(dtype) if kind == "int"
+                    else rng.random(base_shape).astype(dtype))
+            win = base[tuple(slice(s0, s0 + w) for s0, w in zip(start, shape))].copy()
+            ref = O.expected_value(win)
+            tb = _dev(base)
+            got = T.expected_value_view(T.View(tb, start, shape)).cpu().numpy()
+            if kind == "int":
+                np.testing.assert_array_equal(got, ref)
+            else:
+                assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref) + 1e-300), (shape, got, ref)
+                again = T.expected_value_view(T.View(tb, start, shape)).cpu().numpy()
+                np.testing.assert_array_equal(got, again)
+            m = T.expected_value_view(T.View(tb, start, shape), with_mass=True).cpu().numpy()
+            assert abs(m[-1] - math.fsum(win.astype(np.float64).ravel())) <= 1e-12 * abs(m[-1]) + 1e-300

@@ -39,6 +39,16 @@ def main():
             torch.cuda.synchronize()
             print(name, "ok", flush=True)
             continue
+        if name in ("EVVIEW255", "EVVIEW256"):   # EV of a view window (TMA tensor tiles)
+            base_ = torch.rand((264,) * 3, dtype=torch.float64, device=dev)
+            st_, sh_ = ((5,) * 3, (255,) * 3) if name == "EVVIEW255" else ((8,) * 3, (256,) * 3)
+            v_ = T.View(base_, st_, sh_)
+            o_ = torch.empty(3, dtype=torch.float64, device=dev)
+            for _ in range(a.reps):
+                T.expected_value_view(v_, out=o_)
+            torch.cuda.synchronize()
+            print(name, "ok", flush=True)
+            continue
         if name in ("EV7", "EVF32"):   # expected value over odd innermost extents
             sh, dt = ((7,) * 9, torch.float64) if name == "EV7" else ((3000, 3000, 7), torch.float32)
             p_ = torch.rand(sh, dtype=dt, device=dev)
