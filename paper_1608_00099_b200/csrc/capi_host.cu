@@ -10,6 +10,7 @@
 // the compute.  Pinned host memory is needed for the copies to be asynchronous (pageable memory
 // still works, serialised by the driver).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -34,9 +35,10 @@ int cuda_err(cudaError_t e, const char* what) {
 // different caller streams get different copy streams, so one op's device-to-host drain runs
 // while another op's host-to-device feed is in flight (PCIe is full duplex); a mutex keeps
 // concurrent calls on the same caller stream in order.
+constexpr int kMaxSlots = 8;
 struct Pipe {
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t loaded[2], computed[2], drained[2];
+  cudaEvent_t loaded[kMaxSlots], computed[kMaxSlots], drained[kMaxSlots];
   std::mutex mu;
   bool ready = false;
 };
@@ -61,7 +63,7 @@ int pipe_init(Pipe& p) {
     return cuda_err(e, "cudaStreamCreateWithFlags");
   if ((e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking)) != cudaSuccess)
     return cuda_err(e, "cudaStreamCreateWithFlags");
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < kMaxSlots; ++s) {
     cudaEvent_t* evs[3] = {&p.loaded[s], &p.computed[s], &p.drained[s]};
     for (cudaEvent_t* ev : evs)
       if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
@@ -72,6 +74,19 @@ int pipe_init(Pipe& p) {
 }
 
 int esz_of(int dtype) { return dtype == TRIOT_F32 ? 4 : dtype == TRIOT_F64 ? 8 : 0; }
+
+// staging slots per pipeline (the ring of chunks in flight): 6 keeps more, smaller chunks moving
+// so the copy engines interleave the pipelines of concurrent calls finer (B200, the bench's four
+// e2e legs: 2 slots 40.6-46.1 ms, 3: 38.5-44.1, 4: 40.3-46.7, 6: 36.9-38.2 ms per step,
+// profiles/r02_e2e_slots2.jsonl); TRIOT_HOST_SLOTS overrides it for A/B runs (tools/e2e_probe.py)
+int host_slots() {
+  static int n = [] {
+    const char* e = getenv("TRIOT_HOST_SLOTS");
+    int v = e ? atoi(e) : 6;
+    return v < 2 ? 2 : v > kMaxSlots ? kMaxSlots : v;
+  }();
+  return n;
+}
 
 // Elements of one index of axis k: prod_{j > k} shape[j].
 uint64_t sub_elems(const int64_t* shape, int d, int k) {
@@ -96,7 +111,8 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
   Pipe& P = *pp;
   std::lock_guard<std::mutex> lk(P.mu);
   if ((st = pipe_init(P))) return st;
-  const uint64_t slot_bytes = staging_bytes / 2;
+  const int NSL = host_slots();
+  const uint64_t slot_bytes = (staging_bytes / (uint64_t)NSL) & ~255ull;  // slots 256-B aligned
   const uint64_t pad = 256 * (uint64_t)(nin + 1);
   // choose the chunk axis k and the rows per chunk
   int k = 0;
@@ -118,9 +134,9 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
   uint64_t in_row[TRIOT_MAXT];
   for (int i = 0; i < nin; ++i) in_row[i] = sub_elems(in_shape[i], d, k) * (uint64_t)esz;
   auto align = [](uint64_t x) { return (x + 255) & ~255ull; };
-  char* dev_out[2];
-  char* dev_in[2][TRIOT_MAXT];
-  for (int s = 0; s < 2; ++s) {
+  char* dev_out[kMaxSlots];
+  char* dev_in[kMaxSlots][TRIOT_MAXT];
+  for (int s = 0; s < NSL; ++s) {
     char* q = (char*)staging + (size_t)s * slot_bytes;
     dev_out[s] = q;
     q += align(rows * out_row);
@@ -156,9 +172,9 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
       in_base[i] = b * (uint64_t)in_shape[i][k];
     }
     for (uint64_t a = 0; a < nk; a += rows, ++chunk) {
-      const int s = (int)(chunk & 1);
+      const int s = (int)(chunk % (uint64_t)NSL);
       const uint64_t r = a + rows <= nk ? rows : nk - a;
-      if (chunk >= 2) {  // slot reuse: chunk-2's inputs consumed, its output drained
+      if (chunk >= (uint64_t)NSL) {  // slot reuse: its last chunk's inputs consumed, output drained
         if ((e = cudaStreamWaitEvent(P.h2d, P.computed[s], 0)) != cudaSuccess)
           return cuda_err(e, "wait");
         if ((e = cudaStreamWaitEvent(compute, P.drained[s], 0)) != cudaSuccess)
@@ -201,7 +217,7 @@ int run_pipeline(void* out_h, const int64_t* out_shape, int nin, const void* con
     }
   }
   // the caller's stream completes only when the last chunk has landed in host memory
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < NSL; ++s)
     if (chunk > (uint64_t)s)
       if ((e = cudaStreamWaitEvent(compute, P.drained[s], 0)) != cudaSuccess)
         return cuda_err(e, "wait");

@@ -28,7 +28,7 @@ def main():
     side = [torch.cuda.Stream(dev) for _ in range(4)]
     legs = {
         "C2": lambda: T.embed_host(dst2, src2, device=dev),
-        "C3": lambda: m3.copy_(T.expected_value(p3.to(dev, non_blocking=True)), non_blocking=True),
+        "C3": lambda: T.expected_value_host(p3, out=m3, device=dev),
         "C4": lambda: T.apply_binary_host(a4, b4, "mul", out=c4, device=dev),
         "C5": lambda: T.embed_host(dst5, src5, device=dev),
     }
@@ -52,13 +52,19 @@ def main():
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    for names in (["C2"], ["C3"], ["C4"], ["C5"], ["C4", "C5"], ["C2", "C5"], ["C2", "C4"],
-                  ["C2", "C3", "C4", "C5"], ["C5", "C4", "C3", "C2"]):
-        print(json.dumps({"legs": names, "ms": round(timed(names), 3)}), flush=True)
-    for mb in (64, 128, 512):
+    slots = os.environ.get("TRIOT_HOST_SLOTS", "2")
+    order = ["C5", "C2", "C4", "C3"]
+    if os.environ.get("E2E_ORDER_ONLY"):
+        ms = [round(timed(order, reps=4), 3) for _ in range(3)]
+        print(json.dumps({"slots": slots, "legs": order, "ms": ms}), flush=True)
+        return
+    for names in (["C2", "C3", "C4", "C5"], order):
+        print(json.dumps({"slots": slots, "staging_MB": T.api.STAGING_BYTES >> 20, "legs": names,
+                          "ms": round(timed(names), 3)}), flush=True)
+    for mb in (128, 512):
         T.api.STAGING_BYTES = mb << 20
         T.api._ws_cache.clear()
-        print(json.dumps({"legs": "all", "staging_MB": mb,
+        print(json.dumps({"slots": slots, "staging_MB": mb, "legs": "all",
                           "ms": round(timed(["C2", "C3", "C4", "C5"]), 3)}), flush=True)
 
 
