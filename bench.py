@@ -156,9 +156,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        try:
+            nv = ".".join(map(str, torch.cuda.nccl.version()))
+        except Exception:
+            nv = "?"
         print(f"[bench rank {rank}/{world}] NCCL process group up on {dev} "
-              f"(backend {dist.get_backend()}, NCCL {'.'.join(map(str, torch.cuda.nccl.version()))})",
-              file=sys.stderr, flush=True)
+              f"(backend {dist.get_backend()}, NCCL {nv})", file=sys.stderr, flush=True)
 
     # ---- inputs resident in HBM (init excluded from timing): this rank's box of each
     # config (the whole config at N = 1)
@@ -398,7 +401,8 @@ def run_ours(args, rank, world, local_rank):
 
     peak, peak_kind = measured_peak()
     step_bytes = sum(algorithmic_bytes(n) for n in STEP_OPS)
-    value = world * K * step_bytes / (total_ms * 1e-3) / 1e9
+    # strong scaling: the ranks together process ONE global instance per step
+    value = K * step_bytes / (total_ms * 1e-3) / 1e9
     per_op = []
     for n in STEP_OPS:
         b = algorithmic_bytes(n)
