@@ -150,12 +150,22 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
+    # the partitioned (multi-GPU) path; --split-test runs it at world size 1 (a one-rank NCCL
+    # group, the offset EV + all_gather + sum_rows) so a one-GPU box exercises every line of it
+    split = world > 1 or args.split_test
     import paper_1608_00099_b200 as T
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if split:
+        if "MASTER_ADDR" not in os.environ:   # --split-test without torchrun: a one-rank group
+            import socket
+            so = socket.socket()
+            so.bind(("127.0.0.1", 0))
+            os.environ["MASTER_ADDR"] = "127.0.0.1"
+            os.environ["MASTER_PORT"] = str(so.getsockname()[1])
+            so.close()
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
         try:
             nv = ".".join(map(str, torch.cuda.nccl.version()))
         except Exception:
@@ -177,14 +187,14 @@ def run_ours(args, rank, world, local_rank):
     g["c4"] = torch.empty(sl["C4"]["iter_shape"], dtype=torch.float64, device=dev)
     g["src5"] = torch.from_numpy(sl["C5"]["src"]).to(dev)
     g["dst5"] = torch.empty(sl["C5"]["dst_shape"], dtype=torch.float32, device=dev)
-    if world > 1:
+    if split:
         g["g3"] = torch.empty(world * 6, dtype=torch.float64, device=dev)
         g["r3"] = torch.empty(6, dtype=torch.float64, device=dev)
     off3 = sl["C3"]["offset"]
     stream = torch.cuda.current_stream(dev)
 
     def ev_step():
-        if world == 1:
+        if not split:
             T.expected_value(g["p3"], out=g["m3"])
         else:  # the one exchange: d doubles per rank, summed in rank order
             T.expected_value(g["p3"], out=g["m3"], offset=off3)
@@ -215,7 +225,7 @@ def run_ours(args, rank, world, local_rank):
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     e_start = torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if split:
         dist.barrier()
     torch.cuda.synchronize(dev)
     sampler.mark()
@@ -224,7 +234,7 @@ def run_ours(args, rank, world, local_rank):
         step(evs[k])
     torch.cuda.synchronize(dev)
     sampler.mark()
-    if world > 1:
+    if split:
         dist.barrier()
     total_ms = e_start.elapsed_time(evs[-1][3])
     per_op_ms = {n: 0.0 for n in STEP_OPS}
@@ -234,7 +244,7 @@ def run_ours(args, rank, world, local_rank):
         for i, n in enumerate(STEP_OPS):
             per_op_ms[n] += marks[i].elapsed_time(marks[i + 1])
     per_op_ms = {n: v / K for n, v in per_op_ms.items()}
-    if world > 1:
+    if split:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -396,7 +406,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e: same step through the public API with pinned HOST buffers; every step copies
     # its inputs H2D and reads its results back D2H inside the timed region
-    e2e = run_e2e(args, sl, dev, stream, T, world, rank)
+    e2e = run_e2e(args, sl, dev, stream, T, world, rank, split)
     sampler.stop()
 
     peak, peak_kind = measured_peak()
@@ -482,10 +492,10 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "traffic_source": traffic_src},
         "clocks": sampler.summary(),
         "e2e": e2e,
-        "gpu_launches": (4 if world == 1 else 5) * K,
+        "gpu_launches": (5 if split else 4) * K,
         "cpu_baseline": cpu,
     }
-    if world > 1:
+    if split:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -562,7 +572,7 @@ def pcie_floors(dev, h2d_bytes, d2h_bytes):
             "how": "256 MiB pinned<->device torch copies, wall clock over 4 reps after 1"}
 
 
-def run_e2e(args, sl, dev, stream, T, world, rank):
+def run_e2e(args, sl, dev, stream, T, world, rank, split):
     import torch
     import torch.distributed as dist
     pin = {
@@ -586,7 +596,7 @@ def run_e2e(args, sl, dev, stream, T, world, rank):
         (b4.shape[0] - ish[0]) * (b4[0].size * 8 if b4.shape[0] else 0)
     d2h = sum(t.numel() * t.element_size() for t in outs.values())
     staging3 = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
-    if world > 1:
+    if split:
         m3d = torch.empty(6, dtype=torch.float64, device=dev)
         g3 = torch.empty(world * 6, dtype=torch.float64, device=dev)
         r3 = torch.empty(6, dtype=torch.float64, device=dev)
@@ -613,8 +623,8 @@ def run_e2e(args, sl, dev, stream, T, world, rank):
                                 device=dev)
         with torch.cuda.stream(side[1]):
             T.expected_value_host(pin["p3"], staging3, out=outs["m3"],
-                                  offset=sl["C3"]["offset"] if world > 1 else None)
-            if world > 1:   # amalgamate the ranks' results: 48 bytes each way
+                                  offset=sl["C3"]["offset"] if split else None)
+            if split:   # amalgamate the ranks' results: 48 bytes each way
                 m3d.copy_(outs["m3"], non_blocking=True)
                 dist.all_gather_into_tensor(g3, m3d)
                 T.sum_rows(g3.view(world, 6), out=r3)
@@ -626,7 +636,7 @@ def run_e2e(args, sl, dev, stream, T, world, rank):
     torch.cuda.synchronize(dev)
     k = max(1, min(args.steps, args.e2e_steps))
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if split:
         dist.barrier()
     torch.cuda.synchronize(dev)
     ea.record(stream)
@@ -635,7 +645,7 @@ def run_e2e(args, sl, dev, stream, T, world, rank):
     eb.record(stream)
     torch.cuda.synchronize(dev)
     ms = ea.elapsed_time(eb) / k
-    if world > 1:
+    if split:
         import torch as _t
         v = _t.tensor([ms, float(h2d), float(d2h)], dtype=_t.float64, device=dev)
         mx = v[:1].clone()
@@ -802,6 +812,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-isolated", action="store_true")
     ap.add_argument("--iso-reps", type=int, default=50)
+    ap.add_argument("--split-test", action="store_true",
+                    help="run the multi-GPU partition path at world size 1 (testing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1287,3 +1287,25 @@ def test_ev_view_tma_tiles_vs_oracle(dtype):
                 np.testing.assert_array_equal(got, again)
             m = T.expected_value_view(T.View(tb, start, shape), with_mass=True).cpu().numpy()
             assert abs(m[-1] - math.fsum(win.astype(np.float64).ravel())) <= 1e-12 * abs(m[-1]) + 1e-300
+
+
+@pytest.mark.slow
+def test_bench_partition_path_runs():
+    """bench.py's multi-GPU partition path (outer-loop boxes, offset EV, NCCL all_gather,
+    triot_sum_rows in rank order) end to end at world size 1 (--split-test): one JSON line with
+    the step's metric -- so a one-GPU box exercises every line the N-GPU run takes."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("MASTER_ADDR", "MASTER_PORT", "RANK",
+                                                             "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--split-test",
+                        "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-isolated",
+                        "--e2e-steps", "1"], capture_output=True, text=True, timeout=600, env=env,
+                       cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["value"] > 1000 and line["gpu_launches"] == 25 and line["e2e"]["value"] > 0
+    assert "NCCL process group up" in r.stderr
