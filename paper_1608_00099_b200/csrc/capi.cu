@@ -396,6 +396,8 @@ int launch_ev_view_tma(const Geom& g, const triot_view* v, int d, int dtype, boo
   }
   for (int j = 0; j < m - 1; ++j)
     if (bstride[ax[j]] % 16 || bstride[ax[j]] >= (1ull << 40)) return TRIOT_OK;
+  for (int j = 0; j < m; ++j)  // TMA coordinates are 32-bit signed
+    if (v->base_shape[ax[j]] >= (1ll << 31)) return TRIOT_OK;
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return TRIOT_OK;
   // the unit axes of the window fold into the map's base address (multiples of 16 bytes)
