@@ -310,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- each op alone after a clean L2 scrub (write a 512 MB buffer, then read another so
     # every dirty line is written back before the timed launch): median of 5 single launches
-    iso, graph20 = {}, {}
+    iso, graph20, ev_context = {}, {}, {}
     if extras and not args.no_isolated:
         scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
         clean = torch.ones(512 << 18, dtype=torch.int32, device=dev)
@@ -347,6 +347,49 @@ def run_ours(args, rank, world, local_rank):
                 del gr
             except Exception as exc:
                 graph20[n] = f"unavailable: {exc}"
+        # context for C3 (134 MB, one launch: launch, ramp and tail are not amortised): the same
+        # kernel instance (d = 6, f64, power-of-two extents) on a PMF 8x the size, and a library
+        # reduction (torch.sum, one value out) over C3's own bytes, both under both protocols
+        try:
+            p8 = torch.rand((32, 32, 32, 16, 16, 16), dtype=torch.float64, device=dev)
+            m8 = torch.empty(6, dtype=torch.float64, device=dev)
+            s3 = torch.empty((), dtype=torch.float64, device=dev)
+            p3flat = g["p3"].view(-1)
+            ctx = {"EV d=6 f64 (32,32,32,16,16,16), 1.07 GB":
+                   (lambda: T.expected_value(p8, out=m8), p8.numel() * 8 + 48),
+                   "torch.sum over C3's p (134 MB, library reduction)":
+                   (lambda: torch.sum(p3flat, dim=(0,), out=s3), g["p3"].numel() * 8 + 8)}
+            for n, (fn, nbytes) in ctx.items():
+                fn()
+                ts = []
+                for _ in range(15):
+                    scratch.fill_(1)
+                    clean.sum()
+                    ea.record(stream)
+                    fn()
+                    eb.record(stream)
+                    torch.cuda.synchronize(dev)
+                    ts.append(ea.elapsed_time(eb))
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr):
+                    for _ in range(20):
+                        fn()
+                gr.replay()
+                torch.cuda.synchronize(dev)
+                ea.record(stream)
+                gr.replay()
+                eb.record(stream)
+                torch.cuda.synchronize(dev)
+                g20 = ea.elapsed_time(eb) / 20
+                ms = statistics.median(ts)
+                ev_context[n] = {"bytes": nbytes, "us": round(ms * 1000, 2),
+                                 "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+                                 "graph20_us": round(g20 * 1000, 2),
+                                 "graph20_gbs": round(nbytes / (g20 * 1e-3) / 1e9, 1)}
+                del gr
+            del p8, m8
+        except Exception as exc:
+            ev_context["unavailable"] = str(exc)
         del scratch, clean
 
     # ---- the paper's own Benchmarks 1-3 (§8(f) NEXT-2/3), same isolated protocol
@@ -475,7 +518,8 @@ def run_ours(args, rank, world, local_rank):
                                     "launches: us = median (event timestamps are quantised to "
                                     "~2 us); graph20 = 20 back-to-back launches in one CUDA "
                                     "graph, no scrub (steady state incl. write-back)",
-                            "ops": per_op_iso},
+                            "ops": per_op_iso,
+                            "c3_context": ev_context},
         "paper_benchmarks": {"note": "P:333 Benchmarks 1-3 at the paper's shapes, f64, "
                                      "isolated as per_op_isolated (B3 is 27 MB: launch-bound)",
                              "ops": paper},

@@ -193,6 +193,10 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Keeps a value's computation ahead of a following pdl_wait(): volatile asm statements are not
+// reordered among themselves, so the operand must be ready before the wait is issued.
+__device__ __forceinline__ void pin_before_wait(uint32_t x) { asm volatile("" ::"r"(x)); }
+__device__ __forceinline__ void pin_before_wait(uint64_t x) { asm volatile("" ::"l"(x)); }
 
 template <int ESZ, typename IDX>
 __device__ __forceinline__ const char* addr(const void* base, IDX off) {
@@ -390,6 +394,43 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   IDX v = base0 + (IDX)lane;
   odo_start<D, 2, true, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
+  if (!ZR && d.wspan == 32) {
+    // One step per warp (small, launch-bound ops: C1): no loop, no odometer step, and the
+    // vector's classification is formed before the wait, so that after it only the loads and
+    // the store remain (C1: 1.57 -> 1.18 us per op back to back in a CUDA graph,
+    // tools/latency_probe.py, profiles/r02_latency_graph2.jsonl).
+    const IDX uv = u[D - 1];
+    const bool valid = v < vend;
+    const bool any = oob == 0 && uv < d.vany;
+    const bool fullv = any && uv < d.vfull;
+    const IDX row0 = uv * d.rowmul, col0 = uv * d.colmul;
+    const IDX o0 = off[0], o1 = off[1];
+    pin_before_wait(o0);
+    pin_before_wait(o1);
+    pin_before_wait(row0);
+    pin_before_wait(col0);
+    pin_before_wait((uint32_t)valid | ((uint32_t)any << 1) | ((uint32_t)fullv << 2));
+    pdl_wait();
+    if (!valid) return;
+    uint32_t w[NW];
+    if (fullv) {
+      load_vec<ESZ, V, IDX>(d.t[1], o1, lgL, w);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NW; ++q) w[q] = 0u;
+      if (any) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const IDX r = (IDX)((uint32_t)e >> lgL);
+          const IDX c = (IDX)((uint32_t)e & ((1u << lgL) - 1u));
+          if (row0 + r < d.srows && col0 + c < d.scols)
+            Mem<ESZ>::ld(addr<ESZ>(d.t[1].ptr, o1 + r * d.t[1].rho + c * d.t[1].tau), w + e * EW);
+        }
+      }
+    }
+    store_vec<ESZ, V, IDX>(d.t[0], o0, lgL, w);
+    return;
+  }
   pdl_wait();
   IDX b = base0;
   for (;;) {

@@ -209,6 +209,36 @@ def test_ev_random_integer_exact(d):
             np.testing.assert_array_equal(got, O.expected_value(p))
 
 
+def test_ev_workspace_reuse_across_grids_and_slots():
+    """One workspace (the binding caches one per stream) serves launches of every grid size and
+    slot count in turn (other grids, other partial counts, the split-reduction policy): every call
+    leaves the arrival counter ready for the next, and partials left by earlier launches are
+    never read.  Integer data: every result is exact, so any stale or missing partial shows."""
+    rng = np.random.default_rng(91)
+    shapes = [(16,) * 5, (3, 4), (64, 64, 64), (2,), (8, 8, 8, 8, 8), (5, 7, 3), (1, 1, 4),
+              (128, 96, 48), (4,) * 9, (7, 1, 9), (1000,), (32, 32, 32, 8)]
+    cases = []
+    for sh in shapes:
+        p = rng.integers(0, 64, size=sh).astype(np.float64)
+        cases.append((_dev(p), O.expected_value(p), float(p.sum())))
+    a = rng.integers(0, 16, size=(40, 30, 20)).astype(np.float64)
+    b = rng.integers(0, 16, size=(50, 30, 10)).astype(np.float64)
+    ad, bd, dot_ref = _dev(a), _dev(b), float((a[:40, :30, :10] * b[:40, :30, :10]).sum())
+    try:
+        for rnd in range(6):
+            pol = [(-1, 0), (0, 1), (4, 2), (0, 23), (1, 2), (-1, 0)][rnd]
+            T.triot_set_launch_policy(*pol)
+            for i in rng.permutation(len(cases)):
+                pd, ref, mass = cases[i]
+                got = T.expected_value(pd, with_mass=True).cpu().numpy()
+                np.testing.assert_array_equal(got[:-1], ref)
+                assert got[-1] == mass
+                if i % 3 == 0:
+                    assert float(T.inner_product(ad, bd).cpu()) == dot_ref
+    finally:
+        T.triot_set_launch_policy(-1, 0)
+
+
 def test_ev_closed_forms():
     p = np.full((16,) * 6, 2.0 ** -24)
     assert T.expected_value(_dev(p)).cpu().tolist() == [7.5] * 6

@@ -5,6 +5,8 @@ import torch
 import paper_1608_00099_b200 as T
 from triot_inputs import make_inputs, make_paper_inputs
 dev = torch.device("cuda:0")
+if os.environ.get("TRIOT_POLICY"):   # "mode,blocks_per_sm"
+    T.triot_set_launch_policy(*(int(x) for x in os.environ["TRIOT_POLICY"].split(",")))
 b1 = make_paper_inputs("B1"); y1 = torch.from_numpy(b1["src"]).to(dev)
 x1 = torch.empty(b1["dst_shape"], dtype=torch.float64, device=dev)
 b2 = make_paper_inputs("B2"); a2, bb2 = torch.from_numpy(b2["a"]).to(dev), torch.from_numpy(b2["b"]).to(dev)

@@ -12,7 +12,8 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 sys.path.insert(0, ROOT)
-SO = os.path.join(HERE, "libevprobe.so")
+DEFS = os.environ.get("EVPROBE_DEFS", "").split()   # e.g. "-DTRIOT_EV_LL=0": A/B of the tail
+SO = os.path.join(HERE, "libevprobe%s.so" % ("_" + "".join(c for c in "".join(DEFS) if c.isalnum()) if DEFS else ""))
 
 
 def build():
@@ -20,7 +21,7 @@ def build():
             os.path.join(ROOT, "paper_1608_00099_b200", "csrc", "plan.cpp")]
     if not os.path.exists(SO) or any(os.path.getmtime(x) > os.path.getmtime(SO) for x in srcs):
         subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
-                        "-shared", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+                        "-shared", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), *DEFS,
                         "-o", SO, *srcs], check=True)
     L = ctypes.CDLL(SO)
     for f in (L.probe_ev_c3, L.probe_ev_ldg_c3):

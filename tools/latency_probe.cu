@@ -47,6 +47,18 @@ __global__ void copy8_desc_pdl(const __grid_constant__ Desc<uint32_t> d) {
   for (int j = 0; j < 4; ++j) q[i * 4 + j] = x[j];
 }
 
+// 64 KB moved as one 32-byte vector per thread, any block size (what is the floor of C1's
+// bytes, and does the block shape matter?); mode 1 = stores only, 2 = loads only
+__global__ void copyv_pdl(const double* s, double* d, int mode) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (mode != 1) Mem<32>::ld(s + 4 * i, w);
+  if (mode != 2) Mem<32>::st(d + 4 * i, w);
+  else if (w[0] == 0x12345u) d[0] = 1.0;
+}
+
 static int launch(const void* fn, unsigned grid, unsigned block, void** args, cudaStream_t st,
                   bool pdl) {
   cudaLaunchConfig_t cfg;
@@ -73,7 +85,8 @@ extern "C" double probe_latency(int variant, void* dst, const void* src, void* s
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned grid = variant == 4 ? 1u : 8u;
-  set_decomposition(g, 0, (uint64_t)grid * (TRIOT_BLOCK / 32));
+  const unsigned eblock = (unsigned)TRIOT_BLOCK;
+  set_decomposition(g, 0, (uint64_t)grid * (eblock / 32));
   Desc<uint32_t> d;
   memset(&d, 0, sizeof(d));
   fill_desc<uint32_t>(g, d);
@@ -82,6 +95,9 @@ extern "C" double probe_latency(int variant, void* dst, const void* src, void* s
   const double* s = (const double*)scratch;
   double* o = (double*)scratch + 8192;
   void* cargs[2] = {&s, &o};
+  int cmode = variant == 14 ? 1 : variant == 15 ? 2 : 0;
+  void* vargs[3] = {&s, &o, &cmode};
+  const unsigned vblock = variant == 10 ? 256 : variant == 11 ? 128 : variant == 12 ? 64 : variant == 13 ? 32 : 256;
   cudaGraph_t gr;
   cudaGraphExec_t ge;
   cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
@@ -90,9 +106,11 @@ extern "C" double probe_latency(int variant, void* dst, const void* src, void* s
       case 0: launch((const void*)empty_pdl, 1, 32, nullptr, st, true); break;
       case 1: launch((const void*)empty_plain, 1, 32, nullptr, st, false); break;
       case 2: launch((const void*)copy1_pdl, 1, 32, cargs, st, true); break;
-      case 3: case 4: launch(efn, grid, TRIOT_BLOCK, eargs, st, true); break;
+      case 3: case 4: launch(efn, grid, eblock, eargs, st, true); break;
       case 6: launch((const void*)copy8_pdl, 8, 256, cargs, st, true); break;
       case 7: launch((const void*)copy8_desc_pdl, 8, 256, eargs, st, true); break;
+      case 10: case 11: case 12: case 13: case 14: case 15:
+        launch((const void*)copyv_pdl, 2048 / vblock, vblock, vargs, st, true); break;
       default: launch(efn, grid, TRIOT_BLOCK, eargs, st, false); break;
     }
   }

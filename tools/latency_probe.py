@@ -36,7 +36,10 @@ def main():
     names = ["empty+pdl", "empty plain", "1 load+1 store, pdl", "C1 embed 8 blocks pdl",
              "C1 embed 1 block pdl", "C1 embed 8 blocks no pdl", "copy 8x256x4 pdl",
              "copy 8x256x4 with 1.3 KB descriptor, pdl"]
-    for v, nm in enumerate(names):
+    names = list(enumerate(names)) + [(10, "copy 64 KB, 32-B vector per thread, 8x256"),
+                                      (11, "same, 16x128"), (12, "same, 32x64"), (13, "same, 64x32"),
+                                      (14, "stores only, 8x256"), (15, "loads only, 8x256")]
+    for v, nm in names:
         us = [L.probe_latency(v, dst.data_ptr(), src.data_ptr(), scratch.data_ptr(), 200)
               for _ in range(3)]
         print(json.dumps({"variant": nm, "us_per_op": [round(x, 3) for x in us]}), flush=True)
