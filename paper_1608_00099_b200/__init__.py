@@ -8,6 +8,9 @@ step runs in libtriot.so's kernels, see include/triot.h):
     expected_value(p)                                   -> (d,) float64 CUDA tensor
                                                            (triot_expected_value)
 
+    prepare_embed(dst, src) / prepare_apply_binary(a, b, op, out) -> a re-issuable call with its
+                                                           arguments marshalled once
+
 The C-ABI entry points themselves are re-exported with their C names (triot_embed, ...).
 There is no CPU fallback: importing raises if libtriot.so is missing, and the tensor API
 raises for non-CUDA tensors.
@@ -25,7 +28,7 @@ from ._lib import (OP_BINARY, OP_EMBED, OP_EV, TRIOT_ADD, TRIOT_DIV, TRIOT_EMBED
 from .api import (OPS, View, apply_binary, apply_binary_view, embed, embed_view,
                   expected_value, expected_value_view, fused_update, inner_product,
                   naive_convolve, embed_host, apply_binary_host, sum_rows,
-                  expected_value_host)
+                  expected_value_host, Prepared, prepare_embed, prepare_apply_binary)
 from ._lib import (triot_expected_value_offset, triot_sum_rows, triot_expected_value_host)
 from ._lib import (triot_apply_binary_view, triot_embed_view, triot_expected_value_view,
                    triot_fused_update,
@@ -33,6 +36,7 @@ from ._lib import (triot_apply_binary_view, triot_embed_view, triot_expected_val
 
 __all__ = [
     "embed", "apply_binary", "expected_value", "OPS", "TriotError", "View", "embed_view",
+    "Prepared", "prepare_embed", "prepare_apply_binary",
     "apply_binary_view", "triot_embed_view", "triot_apply_binary_view", "inner_product",
     "expected_value_view", "triot_expected_value_view",
     "fused_update", "triot_inner_product", "triot_inner_product_workspace_size",

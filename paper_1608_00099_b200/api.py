@@ -194,6 +194,66 @@ def embed(dst, src, region_only: bool = False):
     return dst
 
 
+class Prepared:
+    """A call with its arguments marshalled once (P:266 calls the dispatch "already a prerequisite
+    cost"; for a 75 KB op the Python-side marshalling is most of the time per call).  Calling the
+    object re-issues the same C-ABI call -- same tensors, same shapes -- on the device's current
+    stream; the tensors are kept alive by it.  Marshalling only, as the plain wrappers."""
+    __slots__ = ("_fn", "_args", "_idx", "_keep", "result")
+
+    def __init__(self, fn, args, idx, keep, result):
+        self._fn, self._args, self._idx, self._keep, self.result = fn, args, idx, keep, result
+
+    def __call__(self):
+        if _GET_DEV is not None and _RAW_STREAM is not None and _GET_DEV() == self._idx:
+            st = self._fn(*self._args, _RAW_STREAM(self._idx))
+        else:
+            with _device(self.result.device):
+                st = self._fn(*self._args, _stream(self.result.device))
+        if st:
+            _lib.check(st)
+        return self.result
+
+
+def prepare_embed(dst, src, region_only: bool = False) -> Prepared:
+    """embed(dst, src, region_only) as a re-issuable call: checks and argument marshalling
+    happen here, once; each call of the result is one triot_embed."""
+    _torch()
+    _check_tensor("dst", dst)
+    _check_tensor("src", src, dst.device)
+    if src.dtype != dst.dtype or src.dim() != dst.dim():
+        raise ValueError("dst and src must have the same dtype and dimension")
+    import ctypes
+    flags = _lib.TRIOT_EMBED_REGION_ONLY if region_only else _lib.TRIOT_EMBED_FULL
+    args = (ctypes.c_void_p(dst.data_ptr()), _lib._shape(tuple(dst.shape)),
+            ctypes.c_void_p(src.data_ptr()), _lib._shape(tuple(src.shape)), dst.dim(),
+            _dtype_code(dst), flags)
+    return Prepared(_lib.lib().triot_embed, args, dst.get_device(), (dst, src), dst)
+
+
+def prepare_apply_binary(a, b, op: str = "mul", out=None, iter_shape=None) -> Prepared:
+    """apply_binary(a, b, op, out, iter_shape) as a re-issuable call (see prepare_embed)."""
+    torch = _torch()
+    _check_tensor("a", a)
+    _check_tensor("b", b, a.device)
+    if a.dtype != b.dtype or a.dim() != b.dim():
+        raise ValueError("a and b must have the same dtype and dimension")
+    if iter_shape is None:
+        iter_shape = tuple(min(x, y) for x, y in zip(a.shape, b.shape))
+    iter_shape = tuple(int(x) for x in iter_shape)
+    if out is None:
+        out = torch.empty(iter_shape, dtype=a.dtype, device=a.device)
+    _check_tensor("out", out, a.device)
+    if out.dtype != a.dtype or out.dim() != a.dim():
+        raise ValueError("out must have the operands' dtype and dimension")
+    import ctypes
+    args = (ctypes.c_void_p(out.data_ptr()), _lib._shape(tuple(out.shape)),
+            ctypes.c_void_p(a.data_ptr()), _lib._shape(tuple(a.shape)),
+            ctypes.c_void_p(b.data_ptr()), _lib._shape(tuple(b.shape)), _lib._shape(iter_shape),
+            a.dim(), _dtype_code(a), OPS[op])
+    return Prepared(_lib.lib().triot_apply_binary, args, a.get_device(), (a, b, out), out)
+
+
 def apply_binary(a, b, op: str = "mul", out=None, iter_shape=None):
     """out[t] = a[t] OP b[t] for t in iter_shape (default: element-wise min of the shapes).
     `out` defaults to a new tensor dense in iter_shape."""

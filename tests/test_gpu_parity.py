@@ -276,6 +276,40 @@ def test_streams_and_repeated_calls():
         assert torch.equal(m, outs[0][1])
 
 
+def test_prepared_calls():
+    """prepare_embed / prepare_apply_binary marshal once; every call of the result issues the same
+    C-ABI call on the current stream (bit-exact, also after the inputs change and on a side
+    stream); the checks of the plain wrappers run at preparation."""
+    inp = make_inputs("C1")
+    src = _dev(inp["src"])
+    dst = _poisoned(inp["dst_shape"], np.float64)
+    call = T.prepare_embed(dst, src)
+    ref = np.empty(inp["dst_shape"]); O.embed(ref, inp["src"])
+    assert call() is dst
+    assert_bits_equal(dst, ref)
+    src.mul_(2.0)
+    dst.fill_(float("nan"))
+    with torch.cuda.stream(torch.cuda.Stream()):
+        call()
+    torch.cuda.synchronize()
+    ref2 = np.empty(inp["dst_shape"]); O.embed(ref2, inp["src"] * 2.0)
+    assert_bits_equal(dst, ref2)
+    rng = np.random.default_rng(12)
+    a, b = rng.standard_normal((9, 14, 6)), rng.standard_normal((12, 10, 8))
+    ad, bd = _dev(a), _dev(b)
+    bcall = T.prepare_apply_binary(ad, bd, "sub")
+    assert_bits_equal(bcall(), O.apply_binary(a, b, "sub"))
+    assert_bits_equal(bcall(), O.apply_binary(a, b, "sub"))
+    reg = T.prepare_embed(torch.full((6, 6), 7.0, dtype=torch.float64, device=DEV),
+                          _dev(np.ones((2, 9))), region_only=True)
+    out = reg().cpu().numpy()
+    assert out[:2].tolist() == [[1.0] * 6] * 2 and np.all(out[2:] == 7.0)
+    with pytest.raises(TypeError):
+        T.prepare_embed(dst.cpu(), src.cpu())
+    with pytest.raises(ValueError):
+        T.prepare_embed(dst, src.float())
+
+
 def test_errors_raise_not_fallback():
     x = torch.zeros(4, 4, dtype=torch.float64, device=DEV)
     with pytest.raises(T.TriotError):

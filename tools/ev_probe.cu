@@ -79,6 +79,12 @@ extern "C" int probe_ev_variant_c3(const double* p, double* means, void* ws, int
     case 3: ev_kernel<6, 8, 4, uint32_t, 3, 4><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
     case 4: ev_kernel<6, 8, 4, uint32_t, 8, 2><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
     case 5: ev_kernel<6, 8, 4, uint32_t, 4, 2><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
+    // register-capped instances that fit more blocks per SM in one wave (48 / 40 / 32 registers)
+    case 6: ev_kernel<6, 8, 4, uint32_t, 2, 5><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
+    case 7: ev_kernel<6, 8, 4, uint32_t, 1, 5><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
+    case 8: ev_kernel<6, 8, 4, uint32_t, 2, 6><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
+    case 9: ev_kernel<6, 8, 4, uint32_t, 1, 6><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
+    case 10: ev_kernel<6, 8, 4, uint32_t, 1, 8><<<grid, TRIOT_BLOCK, 0, s>>>(d); break;
     default: return -200;
   }
   return cudaGetLastError() != cudaSuccess ? -100 : (int)grid;

@@ -54,7 +54,11 @@ def main():
         B = torch.from_numpy(inp["b"]).to(dev)
         probe = lambda p_, m_, w_, t_, n_, s_: L.probe_dot_b2(A.data_ptr(), B.data_ptr(), m_, w_,
                                                                t_, n_, s_)
-    for rep in range(3):
+    dump = []
+    nrep = 3
+    if "--dump" in sys.argv:   # per-block traces of many launches (per-SM statistics offline)
+        nrep = int(sys.argv[sys.argv.index("--dump") + 1])
+    for rep in range(nrep):
         scratch.fill_(1)
         clean.sum()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -65,6 +69,9 @@ def main():
         assert grid > 0, grid
         tr = trace[: grid * 8].view(grid, 8).cpu().numpy().astype(np.int64)
         t0 = tr[:, 0].min()
+        if "--dump" in sys.argv:
+            dump.append(np.concatenate([tr[:, :7] - t0, tr[:, 7:8]], axis=1).astype(np.int32))
+            continue
         rel = (tr[:, :5] - t0) / 1000.0
         pct = lambda col, qs: [round(float(np.percentile(rel[:, col], q)), 2) for q in qs]
         print(json.dumps({
@@ -79,6 +86,10 @@ def main():
             "slowest_blocks_sm": [int(x) for x in tr[np.argsort(-tr[:, 2])[:8], 7]],
             "fastest_blocks_sm": [int(x) for x in tr[np.argsort(tr[:, 2])[:8], 7]],
             "means": means.cpu().tolist()}), flush=True)
+    if dump:
+        out = os.path.join(ROOT, "gpurun_out", "ev_trace_dump.npy")
+        np.save(out, np.stack(dump))
+        print("saved", out, np.stack(dump).shape)
 
 
 if __name__ == "__main__":
