@@ -193,6 +193,10 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The loop-free paths of warps that own a single step (0: off, for A/B measurements)
+#ifndef TRIOT_ONESTEP
+#define TRIOT_ONESTEP 1
+#endif
 // Keeps a value's computation ahead of a following pdl_wait(): volatile asm statements are not
 // reordered among themselves, so the operand must be ready before the wait is issued.
 __device__ __forceinline__ void pin_before_wait(uint32_t x) { asm volatile("" ::"r"(x)); }
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(kBlock) embed_kernel(const __grid_constant__ D
   IDX v = base0 + (IDX)lane;
   odo_start<D, 2, true, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
-  if (!ZR && d.wspan == 32) {
+  if (TRIOT_ONESTEP && !ZR && d.wspan == 32) {
     // One step per warp (small, launch-bound ops: C1): no loop, no odometer step, and the
     // vector's classification is formed before the wait, so that after it only the loads and
     // the store remain (C1: 1.57 -> 1.18 us per op back to back in a CUDA graph,
@@ -684,6 +688,26 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(const __grid_constant__ 
   IDX v = base0 + (IDX)lane;
   odo_start<D, 3, false, IDX>(d, v, u, off, oob);
   const uint32_t lgL = d.lgL;
+  if (TRIOT_ONESTEP && d.wspan == 32) {
+    // one step per warp (small, launch-bound ops): offsets formed before the wait, then two
+    // loads, the op and one store (embed_kernel's one-step path)
+    const bool valid = v < vend;
+    const IDX o0 = off[0], o1 = off[1], o2 = off[2];
+    pin_before_wait(o0);
+    pin_before_wait(o1);
+    pin_before_wait(o2);
+    pin_before_wait((uint32_t)valid);
+    pdl_wait();
+    if (!valid) return;
+    uint32_t wa[NW], wb[NW], r[NW];
+    load_vec<ESZ, V, IDX, false>(d.t[1], o1, lgL, wa);
+    load_vec<ESZ, V, IDX, false>(d.t[2], o2, lgL, wb);
+#pragma unroll
+    for (int e = 0; e < V; ++e)
+      Elem<ESZ>::put(r + e * EW, bop<OP>(Elem<ESZ>::get(wa + e * EW), Elem<ESZ>::get(wb + e * EW)));
+    store_vec<ESZ, V, IDX>(d.t[0], o0, lgL, r);
+    return;
+  }
   pdl_wait();
   for (IDX b = base0; b < vend; b += K * d.dv) {
     uint32_t ba[K][NW], bb[K][NW];

@@ -91,6 +91,20 @@ extern "C" double probe_latency(int variant, void* dst, const void* src, void* s
   memset(&d, 0, sizeof(d));
   fill_desc<uint32_t>(g, d);
   const void* efn = (const void*)&embed_kernel<4, 8, 4, uint32_t, 4, false>;
+  // a small product of two PMFs of different shapes (64 KB out): c (8,16,8,8) = a (9,16,8,8) * b (8,17,8,8)
+  Geom gb;
+  const int64_t ash[4] = {9, 16, 8, 8}, bsh[4] = {8, 17, 8, 8};
+  const char* sc = (const char*)scratch;
+  plan_binary(gb, (void*)dst, dsh, sc, ash, sc + 9 * 16 * 64 * 8, bsh, dsh, 4, 1, 2);
+  set_decomposition(gb, 0, (uint64_t)8 * (TRIOT_BLOCK / 32));
+  Desc<uint32_t> db;
+  memset(&db, 0, sizeof(db));
+  fill_desc<uint32_t>(gb, db);
+  const void* bfn = gb.D == 2   ? (const void*)&binary_kernel<2, 8, 4, uint32_t, 2, 2>
+                    : gb.D == 3 ? (const void*)&binary_kernel<3, 8, 4, uint32_t, 2, 2>
+                                : (const void*)&binary_kernel<4, 8, 4, uint32_t, 2, 2>;
+  void* bargs[1] = {&db};
+  if (variant == 9 && (gb.V != 4 || gb.D < 2 || gb.D > 4)) return -2.0;
   void* eargs[1] = {&d};
   const double* s = (const double*)scratch;
   double* o = (double*)scratch + 8192;
@@ -108,6 +122,7 @@ extern "C" double probe_latency(int variant, void* dst, const void* src, void* s
       case 2: launch((const void*)copy1_pdl, 1, 32, cargs, st, true); break;
       case 3: case 4: launch(efn, grid, eblock, eargs, st, true); break;
       case 6: launch((const void*)copy8_pdl, 8, 256, cargs, st, true); break;
+      case 9: launch(bfn, 8, TRIOT_BLOCK, bargs, st, true); break;
       case 7: launch((const void*)copy8_desc_pdl, 8, 256, eargs, st, true); break;
       case 10: case 11: case 12: case 13: case 14: case 15:
         launch((const void*)copyv_pdl, 2048 / vblock, vblock, vargs, st, true); break;
