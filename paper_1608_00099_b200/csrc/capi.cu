@@ -181,6 +181,10 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   if (kMinSteps < 4 && g_override.bpsm == 0 && grid > (uint64_t)sms * (uint64_t)occ)
     grid = (uint64_t)sms * (uint64_t)occ;
   if (grid > (uint64_t)max_grid) grid = (uint64_t)max_grid;
+  // a reduction of at most four steps per warp of one block (32 KB: two batches of loads) runs
+  // as that one block: its result needs no cross-block hand-off (ev_reduce's single-block path;
+  // in a CUDA graph, per op: 128 B 2.30 -> 1.31 us, 8 KB 2.42 -> 1.56 us; tools/dbg/ev_small.py)
+  if ((g.op == OP_EV || g.op == OP_DOT) && g_override.mode < 0 && g.nsteps <= 4 * wpb) grid = 1;
   if (grid < 1) grid = 1;
   set_decomposition(g, pol.mode, grid * wpb);
   if (pol.mode == 0) {  // drop blocks whose warps would get no chunk

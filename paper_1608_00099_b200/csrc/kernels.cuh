@@ -1535,6 +1535,20 @@ __device__ __forceinline__ void ordered_slot_sum(const double* src, unsigned npa
   __syncthreads();
 }
 
+// out[j] from the slot totals in sm[0][]; a block of a larger PMF adds offset * mass
+template <int NS, int BLOCK, typename IDX>
+__device__ __forceinline__ void ev_write_out(const Desc<IDX>& d,
+                                             const double (&sm)[BLOCK / 32][NS]) {
+  if (threadIdx.x < (unsigned)d.d_out) {
+    const int sl = d.slot_of_axis[threadIdx.x];
+    double v = sl >= 0 ? sm[0][sl] : 0.0;
+    // sum_t (off_j + t_j) p[t] = m_j + off_j * mass (one rounding)
+    if ((int)threadIdx.x < d.nax && d.offd[threadIdx.x] != 0.0)
+      v = fma(d.offd[threadIdx.x], sm[0][d.slot_of_axis[d.nax]], v);
+    ((double*)d.out)[threadIdx.x] = v;
+  }
+}
+
 // Fixed-order block reduction ("each thread computes its own pre-result and these pre-results
 // are amalgamated"): warp reduce-scatter, warps in index order -> one partial per block
 // (slot blockIdx); then every block but the last-launched one *arrives* on a counter with a
@@ -1556,6 +1570,20 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
     if ((lane & (GRP - 1)) == 0 && slot < NS) sm[wib][slot] = v;
   }
   __syncthreads();
+  if (gridDim.x == 1 && !d.split) {
+    // a single block (a small PMF: launch_geometry): its slot sums are the totals -- no partial
+    // in global memory, no counter, no L2 round trips (a 128-byte EV in a CUDA graph: 2.3 ->
+    // 1.x us per op).  The same values as the general path gives for one block.
+    if (threadIdx.x < NS) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
+      sm[0][threadIdx.x] = t;  // each thread reads and writes its own column only
+    }
+    __syncthreads();
+    ev_write_out<NS, BLOCK, IDX>(d, sm);
+    return;
+  }
   unsigned* ctr = (unsigned*)d.ws;
   double* part = (double*)((char*)d.ws + TRIOT_EV_WS_HEADER);
   constexpr int P = ev_slot_pad(NS);
@@ -1593,14 +1621,7 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
   TRIOT_TRACE(5);
   ordered_slot_sum<NS, BLOCK>(part, gridDim.x, sm);
   TRIOT_TRACE(6);
-  if (threadIdx.x < (unsigned)d.d_out) {
-    const int sl = d.slot_of_axis[threadIdx.x];
-    double v = sl >= 0 ? sm[0][sl] : 0.0;
-    // a block of a larger PMF: sum_t (off_j + t_j) p[t] = m_j + off_j * mass (one rounding)
-    if ((int)threadIdx.x < d.nax && d.offd[threadIdx.x] != 0.0)
-      v = fma(d.offd[threadIdx.x], sm[0][d.slot_of_axis[d.nax]], v);
-    ((double*)d.out)[threadIdx.x] = v;
-  }
+  ev_write_out<NS, BLOCK, IDX>(d, sm);
 }
 
 // Amalgamation of pre-results: out[j] = sum_r rows[r][j], rows in order (fixed order:
