@@ -136,6 +136,14 @@ Policy auto_policy(const Geom& g) {
   return Policy{0, 64, 0};
 }
 
+// One-cluster reductions (mid-size expected values): blocks per cluster, and a switch
+// (TRIOT_NO_CLUSTER=1 in the environment: A/B measurements)
+constexpr unsigned kClusterBlocks = 8;
+bool cluster_ok() {
+  static const bool off = [] { const char* e = getenv("TRIOT_NO_CLUSTER"); return e && *e == '1'; }();
+  return !off;
+}
+
 int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -185,9 +193,18 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
   // as that one block: its result needs no cross-block hand-off (ev_reduce's single-block path;
   // in a CUDA graph, per op: 128 B 2.30 -> 1.31 us, 8 KB 2.42 -> 1.56 us; tools/dbg/ev_small.py)
   if ((g.op == OP_EV || g.op == OP_DOT) && g_override.mode < 0 && g.nsteps <= 4 * wpb) grid = 1;
+  // up to four steps per warp of eight blocks (256 KB): ONE thread-block cluster of 8 blocks
+  // whose partials meet in block 0's shared memory (st.shared::cluster + barrier.cluster): no
+  // global partial, no counter, no L2 round trips (ev_reduce's cluster path)
+  g.cluster = 0;
+  if ((g.op == OP_EV || g.op == OP_DOT) && g_override.mode < 0 && !g.split && grid > 1 &&
+      g.nsteps <= 4 * wpb * kClusterBlocks && cluster_ok()) {
+    grid = kClusterBlocks;
+    g.cluster = kClusterBlocks;
+  }
   if (grid < 1) grid = 1;
   set_decomposition(g, pol.mode, grid * wpb);
-  if (pol.mode == 0) {  // drop blocks whose warps would get no chunk
+  if (pol.mode == 0 && !g.cluster) {  // drop blocks whose warps would get no chunk
     uint64_t q = g.wmul / 32;
     grid = (g.nsteps + q * wpb - 1) / (q * wpb);
     if (grid < 1) grid = 1;
@@ -202,18 +219,29 @@ int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
 // back to back in a CUDA graph: C3 5.40 vs 5.25 TB/s, C1 1.75 vs 2.03 us per op with / without;
 // the latency-bound convolution is launched without it, see triot_naive_convolve.)
 int launch_pdl(const void* fn, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-               void** args, bool pdl = true) {
+               void** args, bool pdl = true, unsigned cluster = 0) {
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {  // the grid as thread-block clusters of `cluster` blocks (distributed smem)
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC");
   return TRIOT_OK;
@@ -227,7 +255,7 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
   d.out = out;
   d.ws = ws;
   void* args[1] = {&d};
-  return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args);
+  return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args, true, g.cluster);
 }
 
 // Reductions: workspace bytes a grid needs (the counter header, one P-slot partial per block).

@@ -73,6 +73,8 @@ struct Desc {
   int32_t slot_of_axis[TRIOT_MAXD + 1];  // out[j] = slot >= 0 ? total[slot] : 0 (slot D+1 = mass)
   int32_t op;            // binary op
   int32_t split;         // reductions: 1 = write the block partial only; ev_final_kernel sums
+  uint32_t cluster;      // reductions: > 1 = the grid is ONE thread-block cluster of this many
+                         // blocks; the partials meet in block 0's shared memory (DSMEM)
   // expected value of a block of a larger PMF (slab / chunk / shard): output axis j < nax
   // gets offd[j] * mass added (global coordinate = offset + local), mass = slot_of_axis[nax]
   int32_t nax;
@@ -109,6 +111,7 @@ struct Desc {
 //   [arrival counter u32 | pad to 256 B] [grid x P block partials]   (P = slots per block)
 // Zero-filled once by the caller; every call leaves the counter at 0.
 #define TRIOT_EV_MAX_GRID 8192
+#define TRIOT_CLUSTER_MAX 8   // blocks of a one-cluster reduction (the portable cluster size)
 #define TRIOT_EV_WS_HEADER 256
 // EV bulk-copy pipeline: NSTAGE shared-memory stages of SVEC 32-byte vectors per block
 #define TRIOT_EV_NSTAGE 6

@@ -1584,6 +1584,37 @@ __device__ __forceinline__ void ev_reduce(const Desc<IDX>& d, double (&acc)[NS])
     ev_write_out<NS, BLOCK, IDX>(d, sm);
     return;
   }
+  if (d.cluster > 1 && !d.split) {
+    // The grid is one thread-block cluster (a mid-size PMF: launch_geometry).  Every block
+    // stores its slot sums into block 0's shared memory (distributed shared memory) and
+    // arrives on the cluster barrier with release; block 0 waits with acquire, adds the
+    // partials in block order and writes the result: the same fixed order as the general
+    // path, with no partial in global memory, no counter and no L2 round trip.
+    __shared__ double cl[TRIOT_CLUSTER_MAX][NS];
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    if (threadIdx.x < NS) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < BLOCK / 32; ++w) t += sm[w][threadIdx.x];
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                   : "=r"(remote)
+                   : "r"((uint32_t)__cvta_generic_to_shared(&cl[rank][threadIdx.x])), "r"(0u));
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(t) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+    if (rank != 0) return;
+    if (threadIdx.x < NS) {
+      double t = 0.0;
+      for (unsigned r = 0; r < d.cluster; ++r) t += cl[r][threadIdx.x];
+      sm[0][threadIdx.x] = t;
+    }
+    __syncthreads();
+    ev_write_out<NS, BLOCK, IDX>(d, sm);
+    return;
+  }
   unsigned* ctr = (unsigned*)d.ws;
   double* part = (double*)((char*)d.ws + TRIOT_EV_WS_HEADER);
   constexpr int P = ev_slot_pad(NS);

@@ -61,6 +61,7 @@ struct Geom {
   bool with_mass = false;   // EV: also write sum(p) after the d means
   int nout = -1;            // reduction outputs if not d (+mass): the inner product writes 1
   bool split = false;       // reductions: partials summed by a second (PDL) kernel
+  uint32_t cluster = 0;     // reductions: the grid is one cluster of this many blocks (launch_geometry)
   int nax = 0;              // EV of a block of a larger PMF: per-axis coordinate offsets
   double offd[TRIOT_MAXD] = {};
   bool view = false;        // EV of a view: p is strided (offsets tracked by the odometer)
@@ -150,6 +151,7 @@ void fill_desc(const Geom& g, Desc<IDX>& d) {
   d.d_out = g.nout >= 0 ? g.nout : g.d + (g.with_mass ? 1 : 0);
   d.op = g.binop;
   d.split = g.split ? 1 : 0;
+  d.cluster = g.cluster;
   d.nax = g.nax;
   for (int k = 0; k < TRIOT_MAXD; ++k) d.offd[k] = g.offd[k];
   d.zmask = g.zmask;
