@@ -63,7 +63,7 @@ int vindex(const Geom& g) {
   if (g.evrows) return 5;
   if (g.dshift) return 7;
   if (g.rows) return g.rwarp ? 6 : 5;
-  if (g.flat) return 3;
+  if (g.flat) return g.V * g.esz == 64 ? 6 : 3;  // 6: the expected value's 64-byte flat units
   if (g.V == 32 / g.esz) return 0;
   if (g.V == 16 / g.esz) return 1;
   return 2;

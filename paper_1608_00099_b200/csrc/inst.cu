@@ -125,6 +125,9 @@ const void* kptr_rowsw() {
   return (const void*)&embed_rowsw_kernel<D, ESZ, IDX>;
 #elif TRIOT_INST_OP == 1
   return (const void*)&binary_rowsw_kernel<D, ESZ, IDX, TRIOT_INST_BOP>;
+#elif TRIOT_INST_OP == 2 && TRIOT_INST_BOP == 0
+  // the expected value has no warp-per-row kernel: the slot carries its flat 64-byte units
+  return (const void*)&ev_flat_kernel<D, ESZ, IDX, 1, 64>;
 #else
   return nullptr;
 #endif
@@ -158,7 +161,7 @@ const void* kptr_zero_runs() {
 
 // table index: ((D-1) * NVI + vi) * 2 + idx64, vi: 0 = 32 B, 1 = 16 B, 2 = one element,
 // 3 = flat 32-B vectors, 4 = 32 B with embed zero runs, 5 = row windows, 6 = row windows with
-// a warp per row, 7 = 32 B with shifted stores (embed into a misaligned dense dst)
+// a warp per row (expected value: flat 64-byte units), 7 = 32 B with shifted stores (embed into a misaligned dense dst)
 constexpr int NVI = 8;
 template <int D>
 struct Fill {

@@ -2254,9 +2254,16 @@ __global__ void __launch_bounds__(kBlock) update_kernel(const __grid_constant__ 
 // EV on flat vectors (odd innermost extents): p is the counter itself, so vector v is elements
 // [v*V, v*V + V) of p; the element digits are the weights, walked with the +1 odometer and its
 // deferred-weight events.
-template <int D, int ESZ, typename IDX, int K>
+// VB = 64 (rows longer than a unit, so at most one wrap per unit): two 32-byte loads per lane
+// and unit; the unit's mass and its sum of prefix sums come from one pass of adds and
+// immediate-weight FMAs (no prefix array), the prefix at the wrap from a second pass
+// of block masses plus at most three elements, taken only by the warps in which a lane wraps;
+// the digit bookkeeping is paid once per 64 bytes (rows of 33, 268 MB, ncu cold: f32 65.6 ->
+// 51.5-53.3 us = 5.0-5.2 TB/s, 154 -> 103 warp instructions per 32 bytes; f64 54.2 -> 46.9 us
+// = 5.7 TB/s, 129 -> 78; profiles/r02_evodd_flat*).
+template <int D, int ESZ, typename IDX, int K, int VB = 32>
 __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__ Desc<IDX> d) {
-  constexpr int V = 32 / ESZ;
+  constexpr int V = VB / ESZ;
   constexpr int EW = ESZ / 4;
   constexpr int NW = V * EW;
   constexpr int NS = D + 2;
@@ -2288,6 +2295,8 @@ __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__
         const IDX f0 = vj * (IDX)V;
         if (vj < vend && pvec && f0 + (IDX)V <= d.nelem) {
           Mem<32>::ld(addr<ESZ>(d.t[0].ptr, f0), buf[j]);
+          if constexpr (VB == 64)
+            Mem<32>::ld(addr<ESZ>(d.t[0].ptr, f0 + (IDX)(V / 2)), buf[j] + NW / 2);
         } else {
 #pragma unroll
           for (int e = 0; e < V; ++e) {
@@ -2307,24 +2316,69 @@ __global__ void __launch_bounds__(kBlock) ev_flat_kernel(const __grid_constant__
         // -(V S + sum of the V prefix sums) in total; a wrap (column n-1 -> 0) instead changes
         // it by -(n-1), a correction of +n x (mass at the wrap), and carries into the outer
         // digits with their own events.  Past the end the elements are +0.0.
-        double pfx[V + 1];  // pfx[e] = sum of the vector's first e elements
-        pfx[0] = 0.0;
-        double sumpre = 0.0;
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          pfx[e + 1] = pfx[e] + (double)Elem<ESZ>::get(buf[j] + e * EW);
-          sumpre += pfx[e + 1];
-        }
-        const double pre = pfx[V];
-        // wraps (column n-1 -> 0) follow elements ew - 1 with ew = n - col, ew + n, ... <= V;
-        // the loop trip count is uniform (V / n + 1), so the warp stays converged
         const IDX col = u[D - 1];
         IDX ew = D > 1 ? d.ext[D - 1] - col : (IDX)(V + 1);
+        double pre, sumpre;
+        double pfx[VB == 64 ? 1 : V + 1];  // pfx[e] = sum of the vector's first e elements
+        constexpr int NB = VB == 64 ? V / 4 : 1;  // blocks of four elements (VB = 64)
+        double sb[NB];
+        if constexpr (VB == 64) {
+          // block masses, the unit's mass and the sum of the V prefix sums (= sum_e (V - e) x_e)
+          // in one pass
+          double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const double x0 = (double)Elem<ESZ>::get(buf[j] + (4 * b) * EW);
+            const double x1 = (double)Elem<ESZ>::get(buf[j] + (4 * b + 1) * EW);
+            const double x2 = (double)Elem<ESZ>::get(buf[j] + (4 * b + 2) * EW);
+            const double x3 = (double)Elem<ESZ>::get(buf[j] + (4 * b + 3) * EW);
+            sb[b] = (x0 + x1) + (x2 + x3);
+            q0 = fma((double)(V - 4 * b), x0, q0);
+            q1 = fma((double)(V - 4 * b - 1), x1, q1);
+            q0 = fma((double)(V - 4 * b - 2), x2, q0);
+            q1 = fma((double)(V - 4 * b - 3), x3, q1);
+          }
+          pre = sb[0];
+#pragma unroll
+          for (int b = 1; b < NB; ++b) pre += sb[b];
+          sumpre = q0 + q1;
+        } else {
+          pfx[0] = 0.0;
+          sumpre = 0.0;
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            pfx[e + 1] = pfx[e] + (double)Elem<ESZ>::get(buf[j] + e * EW);
+            sumpre += pfx[e + 1];
+          }
+          pre = pfx[V];
+        }
+        // wraps (column n-1 -> 0) follow elements ew - 1 with ew = n - col, ew + n, ... <= V;
+        // the loop trip count is uniform (V / n + 1), so the warp stays converged
         for (uint32_t w = 0; w < wmax; ++w, ew += d.ext[D - 1]) {
           if (ew > (IDX)V) continue;
-          double pw = 0.0;  // pfx[ew] (a select chain: ew is per lane)
+          double pw = 0.0;  // the sum of the first ew elements (ew is per lane)
+          if constexpr (VB == 64) {
+            // whole blocks before the wrap, then up to three elements of the block it falls in
+            // (its raw words picked by a select chain over the blocks: no dynamic indexing)
+            const uint32_t bw = (uint32_t)ew >> 2, r = (uint32_t)ew & 3u;
 #pragma unroll
-          for (int e = 1; e <= V; ++e) pw = ((IDX)e == ew) ? pfx[e] : pw;
+            for (int b = 0; b < NB; ++b) pw += ((uint32_t)b < bw) ? sb[b] : 0.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              uint32_t raw[EW];
+#pragma unroll
+              for (int q = 0; q < EW; ++q) raw[q] = buf[j][(4 * (NB - 1) + i) * EW + q];
+#pragma unroll
+              for (int b = NB - 2; b >= 0; --b)
+#pragma unroll
+                for (int q = 0; q < EW; ++q)
+                  raw[q] = ((uint32_t)b == bw) ? buf[j][(4 * b + i) * EW + q] : raw[q];
+              pw += ((uint32_t)i < r) ? (double)Elem<ESZ>::get(raw) : 0.0;
+            }
+          } else {
+#pragma unroll
+            for (int e = 1; e <= V; ++e) pw = ((IDX)e == ew) ? pfx[e] : pw;
+          }
           const double sc = a.S + pw;  // the running mass at this wrap
           a.ev[D - 1] = fma(nd, sc, a.ev[D - 1]);
 #pragma unroll

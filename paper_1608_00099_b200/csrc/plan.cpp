@@ -121,7 +121,10 @@ static void finish_geometry(Geom& g, int nt);
 // access iff it is dense with the counter (its strides are the counter's Horner strides) and
 // 32-B aligned.
 static void plan_flat(Geom& g, const Axis* ax, int na, int nt, bool bounds, const uint64_t* n0) {
-  const int V = 32 / g.esz;
+  // 32-byte vectors; the expected value takes 64-byte units (two 32-byte loads per lane) when a
+  // row is longer than a unit, i.e. at most one wrap per unit: the per-unit digit bookkeeping
+  // is then paid once per 64 bytes (ev_flat_kernel, VB = 64)
+  const int V = (g.op == OP_EV && ax[na - 1].n > (uint64_t)(64 / g.esz) ? 64 : 32) / g.esz;
   g.flat = true;
   g.V = V;
   g.R = 1;

@@ -469,6 +469,33 @@ def _odd_shapes_vs_oracle(seed, expect):
     np.testing.assert_array_equal(np.array(got), O.expected_value(p))
 
 
+def test_ev_flat_64_byte_units_plan_and_model():
+    """A dense expected value with an odd innermost extent longer than 64 bytes takes flat units
+    of 64 bytes (at most one wrap per unit); shorter odd rows keep 32-byte flat vectors.  The CPU
+    model of the flat walk (V elements with Alg 3's +1, then the mixed-radix skip) on that plan
+    equals the oracle exactly on integer data."""
+    p = T.triot_plan_describe(2, [(40, 33)], None, 2, F32, 0)
+    assert p["flat"] and p["V"] == 16 and p["nvec"] == (40 * 33 + 15) // 16
+    p = T.triot_plan_describe(2, [(40, 33)], None, 2, F64, 0)
+    assert p["flat"] and p["V"] == 8
+    p = T.triot_plan_describe(2, [(9, 17)], None, 2, F32, 0, [4, 0, 0])   # 17 > 16: 64-byte units
+    assert p["flat"] and p["V"] == 16
+    p = T.triot_plan_describe(2, [(9, 15)], None, 2, F32, 0, [4, 0, 0])   # short odd rows: 32 bytes
+    assert p["flat"] and p["V"] == 8
+    p = T.triot_plan_describe(2, [(9, 9)], None, 2, F64, 0, [8, 0, 0])    # 9 > 8: 64-byte units
+    assert p["flat"] and p["V"] == 8
+    rng = np.random.default_rng(64)
+    for shape, dt, npdt in [((13, 33), F32, np.float32), ((7, 5, 19), F64, np.float64),
+                            ((3, 4, 65), F32, np.float32), ((101,), F64, np.float64),
+                            ((6, 9), F64, np.float64)]:
+        q = rng.integers(0, 50, size=shape).astype(npdt)
+        for warps in (1, 3, 8):
+            desc = T.triot_plan_describe(2, [shape], None, len(shape), dt, 0, [8, 0, 0], 0, warps)
+            assert desc["flat"] and desc["V"] * (4 if dt == F32 else 8) == 64
+            got = kernel_model.run(desc, "ev", [q.reshape(-1)])
+            np.testing.assert_array_equal(np.array(got), O.expected_value(q))
+
+
 def test_flat_geometry_chosen_for_odd_innermost(no_rows):
     p = T.triot_plan_describe(0, [(5, 7), (4, 6)], None, 2, F32, 0)
     assert p["flat"] and p["V"] == 8 and p["D"] == 2 and p["nvec"] == 5
