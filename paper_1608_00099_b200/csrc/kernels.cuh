@@ -1368,6 +1368,18 @@ __device__ __forceinline__ void ev_decode(const Desc<IDX>& d, IDX v, IDX (&u)[D]
   decode_digits<D, IDX>(d, v, u);
 }
 
+// in-vector row / column weighted sums of a collapsed vector with a compile-time row length
+template <int V, int LGL>
+__device__ __forceinline__ void ev_collapsed_weights(const double (&x)[V], double& wr, double& wc) {
+#pragma unroll
+  for (int e = 1; e < V; ++e) {
+    constexpr int L = 1 << LGL;
+    const int r = e / L, c = e % L;
+    if (r) wr = fma((double)r, x[e], wr);
+    if (c) wc = fma((double)c, x[e], wc);
+  }
+}
+
 // One vector: S += sum_e p_e; the in-vector row (e >> lgL) and column (e & (L-1)) weights
 // accumulate into Wr / Wc.  lgL is a runtime value but e is unrolled.
 template <int D, int ESZ, int V, typename IDX>
@@ -1390,12 +1402,21 @@ __device__ __forceinline__ void ev_accumulate(const Desc<IDX>& d, const uint32_t
     for (int e = 1; e < V; ++e) wc = fma((double)e, x[e], wc);
     a.Wc += wc;
   } else if (V > 1) {
+    // rows shorter than a vector (2 or 4 elements): the row / column of element e from lgL.
+    // The usual row lengths get immediate weights (warp-uniform branch); the generic form
+    // converts two integers per element ((8192,8192,4) f32, 268 MB: 3.97 -> 5.35 TB/s).
     double wr = 0.0, wc = 0.0;
+    if (lgL == 2 && V >= 8) {
+      ev_collapsed_weights<V, 2>(x, wr, wc);
+    } else if (lgL == 1 && V >= 4) {
+      ev_collapsed_weights<V, 1>(x, wr, wc);
+    } else {
 #pragma unroll
-    for (int e = 1; e < V; ++e) {
-      const uint32_t r = (uint32_t)e >> lgL, c = (uint32_t)e & ((1u << lgL) - 1u);
-      if (r) wr = fma((double)r, x[e], wr);
-      if (c) wc = fma((double)c, x[e], wc);
+      for (int e = 1; e < V; ++e) {
+        const uint32_t r = (uint32_t)e >> lgL, c = (uint32_t)e & ((1u << lgL) - 1u);
+        if (r) wr = fma((double)r, x[e], wr);
+        if (c) wc = fma((double)c, x[e], wc);
+      }
     }
     a.Wr += wr;
     a.Wc += wc;

@@ -4,6 +4,7 @@
 
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -482,7 +483,17 @@ static void build(Geom& g, const uint64_t* n, const uint64_t (*sig)[TRIOT_MAXD],
       return;
     }
   }
-  if (cc[best].V == 1 && vmax > 1 && g.op == OP_EV && !g.view && g_rows_on && na >= 2 &&
+  // ... and a dense p whose rows would only take 16-byte vectors (n = 12, 20, 28 floats; 6, 10,
+  // 14 ... doubles): half-width loads stream at 3.7-4.4 TB/s, the row tiles at 5.2-5.7 and, past
+  // their 31 elements, the 64-byte flat units at 5.0-5.7 (268 MB, profiles/r02_ev_narrow*.jsonl)
+  const bool narrow = g.op == OP_EV && !g.view && g_rows_on && cc[best].V > 1 &&
+                      cc[best].V * g.esz < 32 && !cc[best].collapsed;
+  if (narrow && g.flat_ok && nl > kEvRowsMax && nl > (uint64_t)(64 / g.esz) &&
+      ((uintptr_t)g.t[0].ptr % 32) == 0) {
+    plan_flat(g, ax, na, nt, bounds, n);
+    return;
+  }
+  if ((cc[best].V == 1 || narrow) && vmax > 1 && g.op == OP_EV && !g.view && g_rows_on && na >= 2 &&
       nl >= 3 && nl <= kEvRowsMax && ((uintptr_t)g.t[0].ptr % 16) == 0) {
     plan_ev_rows(g, ax, na, n);
     return;

@@ -496,6 +496,35 @@ def test_ev_flat_64_byte_units_plan_and_model():
             np.testing.assert_array_equal(np.array(got), O.expected_value(q))
 
 
+def test_ev_rows_that_would_take_16_byte_vectors():
+    """A dense expected value whose rows only admit 16-byte vectors (12, 20, 28 floats; 6, 10, ...
+    doubles) takes the shared-memory row tiles up to 31 elements and the 64-byte flat units beyond
+    (32-byte aligned p), not half-width loads; views and rows of whole 32-byte vectors keep the
+    regular geometry.  The CPU model on those plans equals the oracle."""
+    for shape, dt in [((50, 12), F32), ((50, 20), F32), ((9, 7, 28), F32), ((50, 6), F64),
+                      ((50, 10), F64), ((11, 30), F64)]:
+        p = T.triot_plan_describe(2, [shape], None, len(shape), dt, 0)
+        assert p["evrows"] and not p["flat"] and p["rowlen"] == shape[-1], (shape, p)
+    for shape, dt, v in [((50, 36), F32, 16), ((50, 44), F32, 16), ((50, 34), F64, 8)]:
+        p = T.triot_plan_describe(2, [shape], None, len(shape), dt, 0)
+        assert p["flat"] and p["V"] == v, (shape, p)
+        p = T.triot_plan_describe(2, [shape], None, len(shape), dt, 0, [16, 0, 0])
+        assert not p["flat"] and not p["evrows"] and p["V"] * (4 if dt == F32 else 8) == 16
+    p = T.triot_plan_describe(2, [(50, 16)], None, 2, F32, 0)
+    assert not p["evrows"] and not p["flat"] and p["V"] == 8          # whole 32-byte vectors
+    p = T.triot_plan_describe(2, [(50, 16)], None, 2, F32, 0, [16, 0, 0])
+    assert p["evrows"]                              # 16-byte aligned only: rows of 16 as tiles
+    rng = np.random.default_rng(16)
+    for shape, dt, npdt in [((13, 12), F32, np.float32), ((5, 7, 6), F64, np.float64),
+                            ((9, 36), F32, np.float32), ((3, 5, 34), F64, np.float64)]:
+        q = rng.integers(0, 50, size=shape).astype(npdt)
+        for warps in (1, 5):
+            desc = T.triot_plan_describe(2, [shape], None, len(shape), dt, 0, [0, 0, 0], 0, warps)
+            assert desc["evrows"] or desc["flat"]
+            got = kernel_model.run(desc, "ev", [q.reshape(-1)])
+            np.testing.assert_array_equal(np.array(got), O.expected_value(q))
+
+
 def test_flat_geometry_chosen_for_odd_innermost(no_rows):
     p = T.triot_plan_describe(0, [(5, 7), (4, 6)], None, 2, F32, 0)
     assert p["flat"] and p["V"] == 8 and p["D"] == 2 and p["nvec"] == 5
