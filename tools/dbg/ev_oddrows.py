@@ -7,7 +7,7 @@ DEV = torch.device("cuda:0")
 scratch = torch.empty(512 << 20, dtype=torch.uint8, device=DEV)
 clean = torch.ones(512 << 18, dtype=torch.int32, device=DEV)
 for dt in (torch.float64, torch.float32):
-    for n in (7, 31, 33, 45, 63, 65, 127, 255, 999):
+    for n in (tuple(int(x) for x in os.environ["EVODD_N"].split(",")) if os.environ.get("EVODD_N") else (7, 31, 33, 45, 63, 65, 127, 255, 999)):
         rows = (256 << 20) // (n * (8 if dt == torch.float64 else 4))
         r = int(rows ** 0.5)
         p = torch.rand((r, r, n), dtype=dt, device=DEV)
