@@ -328,6 +328,13 @@ int launch_ev_rows(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) 
   uint64_t rpt = TRIOT_EVROWS_STAGE / ((uint64_t)TRIOT_BLOCK * rb);  // ~16 KB stages
   if (rpt < 1) rpt = 1;
   if (rpt > 8) rpt = 8;
+  // Tiny odd rows (at most 32 bytes): a thread takes rpt CONSECUTIVE rows of a tile, so that
+  // between them the digits advance by Alg 3's +1 (one subtraction in the common case) instead
+  // of a full mixed-radix step per 12-28 bytes; rpt odd keeps the threads' shared-memory
+  // strides (rpt * n words) odd, i.e. conflict-free.  TRIOT_EVROWS_NOGROUP=1: off (A/B).
+  static const bool nogroup = [] { const char* e = getenv("TRIOT_EVROWS_NOGROUP"); return e && *e == '1'; }();
+  const bool grouped = !nogroup && rb <= 32 && (g.rowlen & 1u) && rpt >= 3;
+  if (grouped && (rpt & 1) == 0) --rpt;
   const uint64_t stage = ((uint64_t)TRIOT_BLOCK * rpt * rb + 127) & ~127ull;
   const size_t smem = (size_t)(kEvRowsStages * stage + 8 * kEvRowsStages);
   int dev = 0;
@@ -363,7 +370,9 @@ int launch_ev_rows(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) 
   const uint64_t per = (ntiles + blocks - 1) / blocks;
   const uint64_t grid = (ntiles + per - 1) / per;
   g.mode = 0;
-  g.dv = TRIOT_BLOCK;  // a thread's rows advance by one block's worth
+  // a thread's rows advance by one block's worth; grouped: from the last row of its group to
+  // the first row of its group in the next tile
+  g.dv = grouped ? tr - rpt + 1 : (uint64_t)TRIOT_BLOCK;
   set_step(g);
   g.wmul = tr;
   g.wspan = per;
@@ -379,6 +388,7 @@ int launch_ev_rows(Geom& g, void* stream, void* out, void* ws, size_t ws_bytes) 
     fill_desc<IDX>(g, d);
     d.out = out;
     d.ws = ws;
+    d.rgroup = grouped ? 1u : 0u;
     void* args[1] = {&d};
     return launch_pdl(fn, (unsigned)grid, TRIOT_BLOCK, smem, (cudaStream_t)stream, args);
   };

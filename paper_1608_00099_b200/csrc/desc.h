@@ -92,6 +92,9 @@ struct Desc {
   // lane e % 32, row umulhi(e, rmag) = e / rowlen (rmag = 2^32 / rowlen + 1, exact for
   // e < 2^13); scols = the embed bound of the column.
   uint32_t rowlen, rmag, rwin;
+  // expected value row tiles: 1 = a thread takes rwin consecutive rows of a tile (+1 digit steps
+  // between them, the step dlt to its group in the next tile); 0 = rows t, t + block, ...
+  uint32_t rgroup;
   // rows that are segments of a longer split axis (seglen = rowlen): the embed bound of the
   // unsplit axis is segm, so segment s reads columns [0, clamp(segm - s rowlen, 0, rowlen))
   IDX seglen, segm;

@@ -1909,6 +1909,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // mass s = sum_c x_c and column moment sum_c c x_c by suffix sums (T += x_c; m += T for c
 // from n-1 down to 1), no per-element weight or odometer -- ~4 instructions per element
 // against the flat kernel's ~10.  Bytes = p + d doubles.
+// mass T and column moment m of one row of N elements by suffix sums, N a compile-time constant
+template <int ESZ, int N>
+__device__ __forceinline__ void ev_row_sums(const unsigned char* rp, double& T, double& m) {
+#pragma unroll
+  for (int c = N - 1; c >= 1; --c) {
+    T += (double)Elem<ESZ>::get((const uint32_t*)(rp + c * ESZ));
+    m += T;
+  }
+  T += (double)Elem<ESZ>::get((const uint32_t*)rp);
+}
+
 #ifndef TRIOT_EVROWS_MINB
 #define TRIOT_EVROWS_MINB 2
 #endif
@@ -1954,8 +1965,9 @@ __global__ void __launch_bounds__(kBlock, TRIOT_EVROWS_MINB)
   if (tid == 0)
     for (int s = 0; s < NST - 1; ++s)
       if (t0 + (IDX)s < t1) issue(t0 + (IDX)s, s);
+  const bool grp = d.rgroup != 0;  // a thread's rows of a tile: consecutive, or strided by the block
   IDX u[D];
-  decode_digits<D, IDX>(d, t0 * TR + (IDX)tid, u);
+  decode_digits<D, IDX>(d, t0 * TR + (grp ? (IDX)tid * (IDX)RPT : (IDX)tid), u);
   EvAcc<D> a;
   ev_acc_init<D, IDX>(a);
   for (IDX i = t0; i < t1; ++i) {
@@ -1966,20 +1978,52 @@ __global__ void __launch_bounds__(kBlock, TRIOT_EVROWS_MINB)
     mbar_wait(&full[s], par);
     const unsigned char* st = smem + (size_t)s * stage;
     for (uint32_t r = 0; r < RPT; ++r) {
-      const IDX row = i * TR + (IDX)(r * kBlock + tid);
+      const uint32_t rit = grp ? (uint32_t)tid * RPT + r : r * kBlock + (uint32_t)tid;
+      const IDX row = i * TR + (IDX)rit;
       if (row < d.nvec) {
-        const unsigned char* rp = st + (size_t)(r * kBlock + tid) * row_bytes;
+        const unsigned char* rp = st + (size_t)rit * row_bytes;
         double T = 0.0, m = 0.0;
+        // short rows fully unrolled (a run-time trip count costs more than their data: f32 rows
+        // of 3 ran 79 instructions per row, ncu); longer ones the generic loop
+        switch (n) {
+          case 3: ev_row_sums<ESZ, 3>(rp, T, m); break;
+          case 5: ev_row_sums<ESZ, 5>(rp, T, m); break;
+          case 6: ev_row_sums<ESZ, 6>(rp, T, m); break;
+          case 7: ev_row_sums<ESZ, 7>(rp, T, m); break;
+          case 9: ev_row_sums<ESZ, 9>(rp, T, m); break;
+          case 10: ev_row_sums<ESZ, 10>(rp, T, m); break;
+          case 11: ev_row_sums<ESZ, 11>(rp, T, m); break;
+          case 12: ev_row_sums<ESZ, 12>(rp, T, m); break;
+          case 13: ev_row_sums<ESZ, 13>(rp, T, m); break;
+          case 14: ev_row_sums<ESZ, 14>(rp, T, m); break;
+          case 15: ev_row_sums<ESZ, 15>(rp, T, m); break;
+          default:
 #pragma unroll 4
-        for (int c = (int)n - 1; c >= 1; --c) {
-          T += (double)Elem<ESZ>::get((const uint32_t*)(rp + (size_t)c * ESZ));
-          m += T;
+            for (int c = (int)n - 1; c >= 1; --c) {
+              T += (double)Elem<ESZ>::get((const uint32_t*)(rp + (size_t)c * ESZ));
+              m += T;
+            }
+            T += (double)Elem<ESZ>::get((const uint32_t*)rp);
         }
-        T += (double)Elem<ESZ>::get((const uint32_t*)rp);
         a.S += T;
         a.Wc += m;
       }
-      digits_step_ev<D, IDX>(d, u, a);
+      if (grp && r + 1 < RPT) {
+        // the next row of the group: Alg 3's +1 on the outer digits, each change
+        // with its telescoped weight event -- one subtraction unless a digit wraps
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) {
+          const IDX old = u[k];
+          IDX nu = old + 1;
+          const bool carry = k > 0 && nu >= d.ext[k];
+          if (carry) nu = 0;
+          u[k] = nu;
+          a.ev[k] = carry ? fma((double)old, a.S, a.ev[k]) : a.ev[k] - a.S;
+          if (!carry) break;
+        }
+      } else {
+        digits_step_ev<D, IDX>(d, u, a);
+      }
     }
     __syncthreads();  // every thread is done with stage s before thread 0 refills it
   }
