@@ -1479,8 +1479,11 @@ __device__ __forceinline__ double warp_reduce_scatter(const double (&acc)[NS], i
 }
 
 // 32-byte chunks per thread in flight in the final ordered sum, and the poll's sleep (ns)
+// (6 x 256 threads x 4 doubles cover the 592 x 8 partials of a d <= 6 expected value at 4 blocks
+// per SM in ONE round of loads: C3 back to back 24.94 -> 24.56 us against 4 chunks, which took
+// a second round trip for the last 160 chunks; profiles/r02_ev18_final_chunks*)
 #ifndef TRIOT_EV_FINAL_CHUNKS
-#define TRIOT_EV_FINAL_CHUNKS 4
+#define TRIOT_EV_FINAL_CHUNKS 6
 #endif
 #ifndef TRIOT_EV_POLL_SLEEP
 #define TRIOT_EV_POLL_SLEEP 64
