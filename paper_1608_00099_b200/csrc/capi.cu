@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <utility>
 #include <unordered_map>
@@ -139,9 +140,10 @@ Policy auto_policy(const Geom& g) {
 // One-cluster reductions (mid-size expected values): blocks per cluster, and a switch
 // (TRIOT_NO_CLUSTER=1 in the environment: A/B measurements)
 constexpr unsigned kClusterBlocks = 8;
+std::atomic<bool> g_cluster_refused{false};  // a cluster launch failed once: the counter path from then on
 bool cluster_ok() {
   static const bool off = [] { const char* e = getenv("TRIOT_NO_CLUSTER"); return e && *e == '1'; }();
-  return !off;
+  return !off && !g_cluster_refused.load(std::memory_order_relaxed);
 }
 
 int launch_geometry(const void* fn, Geom& g, int max_grid, unsigned* grid_out) {
@@ -255,7 +257,19 @@ int launch_t(const Geom& g, const void* fn, unsigned grid, cudaStream_t st, void
   d.out = out;
   d.ws = ws;
   void* args[1] = {&d};
-  return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args, true, g.cluster);
+  if (g.cluster > 1) {
+    // A cluster launch can be refused where 8 co-scheduled blocks do not fit (a partitioned
+    // GPU): then the same grid runs the counter path -- same blocks, same fixed order -- and
+    // later calls skip the cluster.
+    if (launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args, true, g.cluster) == TRIOT_OK) return TRIOT_OK;
+    cudaGetLastError();
+    g_cluster_refused.store(true, std::memory_order_relaxed);
+    d.cluster = 0;
+    const int st2 = launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args);
+    if (st2 == TRIOT_OK) clear_error();  // the refused attempt's message
+    return st2;
+  }
+  return launch_pdl(fn, grid, TRIOT_BLOCK, 0, st, args);
 }
 
 // Reductions: workspace bytes a grid needs (the counter header, one P-slot partial per block).
